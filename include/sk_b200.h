@@ -1,0 +1,181 @@
+/*
+ * sk_b200.h -- C ABI of the B200-native sLdG time step (libsk_b200.so).
+ *
+ * Drop-in boundary for the reference solver interface in
+ * /root/reference/proj/core (arXiv 2408.11235). The reference has no FFI: its
+ * "operator API" is a set of free C++ functions over NodalField&. Each entry
+ * point below names the reference function it replaces (file:line); the C++
+ * mirror with the reference's signatures and exception types is
+ * include/solkin_b200.hpp, the ctypes binding is
+ * paper_2408_11235_b200/_native.py, and INTEGRATION.md shows how a maintainer
+ * binds the reference's callers to it.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; device pointers are marked `_dev`.
+ *  - All work is enqueued asynchronously on the context's CUDA stream
+ *    (sk_ctx_set_stream). Functions that return host values synchronise.
+ *  - Every function returns an sk_status; on failure sk_last_error() holds
+ *    the message (thread-local). SK_ERR_RUNTIME mirrors std::runtime_error
+ *    from solkin::require (common.hpp:9-11); SK_ERR_SIMULATION mirrors
+ *    solkin::SimulationError{step} (common.hpp:16-20) and
+ *    sk_last_error_step() gives its step.
+ *  - Errors detected on the device (ghost width, nonfinite values) surface at
+ *    the next synchronising call, or immediately when eager errors are on
+ *    (the default; sk_ctx_set_eager_errors).
+ *  - Field storage is the reference layout ((vc*p+vn)*nx+xc)*p+xn
+ *    (field.hpp:71-73), fp64, double-buffered on the device.
+ */
+#ifndef SK_B200_H
+#define SK_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int sk_status;
+#define SK_OK 0
+#define SK_ERR_RUNTIME 1    /* std::runtime_error (solkin::require)  */
+#define SK_ERR_SIMULATION 2 /* solkin::SimulationError               */
+#define SK_ERR_CUDA 3       /* CUDA runtime failure / no device       */
+
+#define SK_BC_ZERO_INFLOW 0 /* BoundaryRule::ZeroInflow (advection.hpp:35) */
+#define SK_BC_PERIODIC 1    /* BoundaryRule::Periodic (test rule)          */
+
+#define SK_DIR_X 0 /* SweepDirection::X (limiters.hpp:101) */
+#define SK_DIR_V 1
+
+#define SK_SPECIES_ELECTRON 0
+#define SK_SPECIES_ION 1
+
+typedef struct sk_ctx sk_ctx;     /* one GPU: x grid, degree k, Poisson plan, stream */
+typedef struct sk_field sk_field; /* NodalField on the device (field.hpp:21-80)      */
+typedef struct sk_state sk_state; /* SimulationState (stepper.hpp:44-54)             */
+
+/* LimiterConfig (limiters.hpp:19-34). indicator: 0 none, 1 minmod, 2 meanerr;
+ * modifier: 0 none, 1 simple WENO, 2 line WENO. */
+typedef struct {
+    int indicator;
+    int modifier;
+    int inline_sldg;
+    double threshold;
+    double gamma_simple[3];
+    double gamma_line[3];
+    double epsilon;
+} sk_limiter;
+
+/* SweepStats (advection.hpp:37-53) */
+typedef struct {
+    long long outputs;
+    long long inline_troubled;
+    long long inline_clamped;
+    long long inline_mean_outside;
+    long long post_checked;
+    long long post_troubled;
+} sk_stats;
+
+/* VAdjustPolicy (adaptivity.hpp:13-19) */
+typedef struct {
+    double p;
+    double gamma;
+    double tol;
+} sk_vadjust;
+
+/* ShrinkResult (adaptivity.hpp:23-28) */
+typedef struct {
+    double vmax_before;
+    double vmax_after;
+    double mass_before;
+    double mass_after;
+} sk_shrink_result;
+
+/* RunConfig subset that shapes the step (config.hpp:11-41) */
+typedef struct {
+    double L, dt, mu, sigma, vmax_e, vmax_i;
+    int k, fine_block_cells, coarse_block_cells, refinement_ratio, v_cells;
+    sk_limiter limiter;
+    int v_adjust;
+    sk_vadjust policy;
+    double penalty_scale;
+} sk_run_config;
+
+/* ---- errors ---- */
+const char* sk_last_error(void);
+long sk_last_error_step(void);
+const char* sk_version(void);
+
+/* ---- context: Grid1D x (grid.hpp:18-49), degree k, PoissonOperator
+ *      (poisson.hpp:24-57, assembled + reduced once) ---- */
+sk_status sk_ctx_create(int device, int k, int nblocks, const double* block_left,
+                        const int* block_cells, const double* block_dx, double penalty_scale,
+                        sk_ctx** out);
+sk_status sk_ctx_destroy(sk_ctx* ctx);
+sk_status sk_ctx_set_stream(sk_ctx* ctx, void* cuda_stream);
+sk_status sk_ctx_set_eager_errors(sk_ctx* ctx, int on);
+sk_status sk_ctx_synchronize(sk_ctx* ctx); /* also reports device-side errors */
+sk_status sk_stats_get(sk_ctx* ctx, sk_stats* out);
+sk_status sk_stats_reset(sk_ctx* ctx);
+/* Grid1D::three_block (grid.cpp:36-46) with the reference's arithmetic */
+sk_status sk_grid_three_block(double left, double right, int fine_cells, int coarse_cells, int m,
+                              double* block_left, int* block_cells, double* block_dx);
+
+/* ---- fields: NodalField(species, x, v, k) (field.cpp:9-16) ---- */
+sk_status sk_field_create(sk_ctx* ctx, int species, double v_left, double v_right, int v_cells,
+                          sk_field** out);
+sk_status sk_field_destroy(sk_field* f);
+size_t sk_field_size(const sk_field* f);
+double* sk_field_data_dev(sk_field* f); /* current buffer (device) */
+sk_status sk_field_upload(sk_field* f, const double* host, size_t count);
+sk_status sk_field_download(sk_field* f, double* host, size_t count);
+sk_status sk_field_upload_async(sk_field* f, const double* host_pinned, size_t count);
+sk_status sk_field_download_async(sk_field* f, double* host_pinned, size_t count);
+/* v grid: left, dx, cells (synchronises: the cut-off updates it on device) */
+sk_status sk_field_v_grid(sk_field* f, double* left, double* dx, int* cells);
+/* run.cpp:41-46 blob f = (2 pi)^-1/2 exp(-x^2/(2 sigma^2)) exp(-v^2/2) */
+sk_status sk_field_fill_blob(sk_field* f, double sigma);
+
+/* ---- operators ---- */
+/* advect_x (advection.hpp:83; advection.cpp:144-207). max_ghost < 0: unchecked. */
+sk_status sk_advect_x(sk_field* f, double tau, double sqrt_mu, int bc, const sk_limiter* lim,
+                      int max_ghost, long step_index);
+/* advect_v (advection.hpp:87-88; advection.cpp:209-238). E_dev: nx*(k+1) doubles. */
+sk_status sk_advect_v(sk_field* f, double tau, const double* E_dev, double charge_sign,
+                      double sqrt_mu, int bc, const sk_limiter* lim);
+/* apply_post_limiter (limiters.hpp:107-108; limiters.cpp:280-345) */
+sk_status sk_post_limit(sk_field* f, int dir, const sk_limiter* lim, int bc);
+/* charge_density (poisson.hpp:61; poisson.cpp:194-216) -> rho_dev[nx*(k+1)] */
+sk_status sk_charge_density(sk_field* fe, sk_field* fi, double* rho_dev);
+/* PoissonOperator::solve (poisson.cpp:166-192); phi_dev may be NULL */
+sk_status sk_poisson_solve(sk_ctx* ctx, const double* rho_dev, double* E_dev, double* phi_dev);
+/* check_velocity_shrink (adaptivity.hpp:21; adaptivity.cpp:16-38); synchronises */
+sk_status sk_check_velocity_shrink(sk_field* f, const sk_vadjust* policy, int* out_shrink);
+/* shrink_velocity_domain (adaptivity.hpp:33; adaptivity.cpp:94-130); synchronises */
+sk_status sk_shrink_velocity_domain(sk_field* f, const sk_vadjust* policy, sk_shrink_result* out);
+/* mass, l2_norm (field.cpp:52-88), momentum, kinetic energy; synchronises */
+sk_status sk_field_moments(sk_field* f, double* out4);
+/* electric_energy (diagnostics.cpp:71-83) of E_dev; synchronises */
+sk_status sk_electric_energy(sk_ctx* ctx, const double* E_dev, double* out);
+
+/* ---- state + step: build_initial_state (run.cpp:26-58), strang_step
+ *      (stepper.cpp:44-103), run() loop body (run.cpp:124-131) ---- */
+sk_status sk_state_create(sk_ctx* ctx, const sk_run_config* cfg, sk_state** out);
+sk_status sk_state_destroy(sk_state* s);
+sk_field* sk_state_field(sk_state* s, int species);
+double* sk_state_E_dev(sk_state* s);
+sk_status sk_state_download_E(sk_state* s, double* host, size_t count);
+/* one strang_step (no shrink); max_ghost < 0: run()'s rule */
+sk_status sk_strang_step(sk_state* s);
+/* one run() loop body: strang_step + shrink checks with the 10-step cooldown */
+sk_status sk_run_step(sk_state* s);
+/* n loop bodies (CUDA-graph replayed after the first) */
+sk_status sk_run_steps(sk_state* s, int n);
+sk_status sk_state_step_index(sk_state* s, long* step);
+sk_status sk_state_shrinks(sk_state* s, int species, int* count, long* last_step);
+/* drop-in strang_step over HOST NodalFields: upload, step, download */
+sk_status sk_run_step_host(sk_state* s, double* fe_host, double* fi_host, size_t count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

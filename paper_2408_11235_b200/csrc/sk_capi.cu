@@ -1,0 +1,963 @@
+// sk_capi.cu -- C ABI (include/sk_b200.h) and host orchestration.
+//
+// Host C++ above the kernels: owns device memory, the per-context Poisson plan
+// and status block, enqueues the reference's step sequence
+// (stepper.cpp:44-103 + run.cpp:124-131) on one CUDA stream with no host
+// round trip, and maps device-side error flags back onto the reference's two
+// exception classes (common.hpp:9-20) as status codes.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sk_b200.h"
+#include "sk_kernels.cuh"
+
+using namespace sk;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long g_err_step = 0;
+
+sk_status fail(sk_status code, const std::string& msg, long step = 0) {
+    g_err = msg;
+    g_err_step = step;
+    return code;
+}
+
+#define CK(expr)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(SK_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t n) {
+    return cudaMalloc((void**)p, sizeof(T) * (n ? n : 1));
+}
+
+}  // namespace
+
+struct sk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    bool eager = true;
+    int k = 0, P = 1;
+    Basis basis{};
+    Grid grid{};
+    int xtiles[kMaxBlocks + 1] = {};   // x sweep tile prefix (T = kXThreads*2)
+    int ptiles[kMaxBlocks + 1] = {};   // post-limiter tile prefix (T = kXThreads)
+    PoissonPlan plan;
+    PoissonDev pdev{};
+    std::vector<void*> pbufs;
+    DevStatus* st = nullptr;           // device
+    DevStatus* st_host = nullptr;      // pinned mirror
+    double* rho_partial = nullptr;
+    size_t rho_partial_n = 0;
+    double* diag_partial = nullptr;
+    double* diag_out = nullptr;
+    double* pinned = nullptr;          // small pinned readback buffer
+};
+
+struct sk_field {
+    sk_ctx* ctx = nullptr;
+    int species = 0;
+    int nv = 0;
+    size_t n = 0;
+    double* buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    DevVGrid* vg = nullptr;            // device
+    double* xtab = nullptr;            // [nclass][nv*P][xnf]
+    double* vtab = nullptr;            // [vnf][nx*P]
+    double* ttab = nullptr;            // shrink transfer [nv][4][P*P]
+    int* tcell = nullptr;              // [nv][4]
+    double* cur_ptr() { return buf[cur]; }
+    double* other_ptr() { return buf[cur ^ 1]; }
+    void swap() { cur ^= 1; }
+};
+
+struct sk_state {
+    sk_ctx* ctx = nullptr;
+    sk_field* f[2] = {nullptr, nullptr};
+    double* E = nullptr;
+    double* phi = nullptr;
+    double* rho = nullptr;
+    sk_run_config cfg{};
+    double sqrt_mu[2] = {1.0, 1.0};
+    double charge[2] = {-1.0, 1.0};
+    long step_host = 0;
+    cudaGraphExec_t graph2 = nullptr;  // two loop bodies
+    int graph_cur0 = -1, graph_cur1 = -1;
+};
+
+namespace {
+
+// Read the device status block and turn a raised flag into an error code.
+sk_status collect_errors(sk_ctx* c) {
+    CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(DevStatus), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    DevStatus& h = *c->st_host;
+    if (!h.err_code) return SK_OK;
+    std::string msg;
+    sk_status code = h.err_code == 2 ? SK_ERR_SIMULATION : SK_ERR_RUNTIME;
+    long step = (long)h.err_step;
+    switch (h.err_kind) {
+        case 1:
+            msg = "step " + std::to_string(step) + ": insufficient ghost width: sweep requires " +
+                  std::to_string(h.err_need) + " cells, layout provides " + std::to_string(h.err_have);
+            break;
+        case 2:
+            msg = "exchange_block_ghosts: neighbor block cannot supply ghost width " +
+                  std::to_string(h.err_need);
+            break;
+        case 3:
+            msg = "step " + std::to_string(step) + ": nonfinite values in the density function";
+            break;
+        default:
+            msg = "velocity shrink: transfer table overflow";
+    }
+    // clear so the context stays usable (the reference's exception unwinds)
+    int zero[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(&c->st->err_code, zero, sizeof(int) * 4, cudaMemcpyHostToDevice, c->stream));
+    long long z = 0;
+    CK(cudaMemcpyAsync(&c->st->err_step, &z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return fail(code, msg, step);
+}
+
+sk_status after_launch(sk_ctx* c) {
+    CK(cudaGetLastError());
+    if (c->eager) return collect_errors(c);
+    return SK_OK;
+}
+
+PostCfg post_cfg(const sk_limiter* l) {
+    PostCfg p{};
+    p.indicator = l->indicator;
+    p.modifier = l->modifier;
+    p.threshold = l->threshold;
+    for (int i = 0; i < 3; ++i) {
+        p.gamma_simple[i] = l->gamma_simple[i];
+        p.gamma_line[i] = l->gamma_line[i];
+    }
+    p.epsilon = l->epsilon;
+    return p;
+}
+
+sk_status validate_limiter(const sk_limiter* l) {
+    if (!l) return SK_OK;
+    if (l->indicator < 0 || l->indicator > 2 || l->modifier < 0 || l->modifier > 2)
+        return fail(SK_ERR_RUNTIME, "unknown limiter mode");
+    if (l->indicator && !l->modifier) return fail(SK_ERR_RUNTIME, "unknown limiter modifier");
+    if (l->modifier == 2 && l->gamma_line[1] == 0.0)
+        return fail(SK_ERR_RUNTIME, "line WENO: gamma_0 must be nonzero");
+    return SK_OK;
+}
+
+// ---- enqueue helpers (no sync) ----
+sk_status enq_xtab(sk_field** fs, int nspecies, double tau, const double* sqrt_mu, int inline_sldg,
+                   double threshold, int max_ghost, double dt_auto, long long step_index) {
+    sk_ctx* c = fs[0]->ctx;
+    XTabArgs a{};
+    a.basis = c->basis;
+    a.grid = c->grid;
+    a.st = c->st;
+    for (int i = 0; i < nspecies; ++i) {
+        int sp = fs[i]->species;
+        a.vg[sp] = fs[i]->vg;
+        a.tab[sp] = fs[i]->xtab;
+        a.sqrt_mu[sp] = sqrt_mu[i];
+    }
+    a.tau = tau;
+    a.nlines = fs[0]->nv * c->P;
+    a.nspecies = nspecies;
+    a.species0 = nspecies == 2 ? 0 : fs[0]->species;
+    a.inline_sldg = inline_sldg;
+    a.threshold = threshold;
+    a.max_ghost = max_ghost;
+    a.dt_auto = dt_auto;
+    a.step_index = step_index;
+    CK(launch_xtab(a, c->stream));
+    return SK_OK;
+}
+
+sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
+                     int check_finite) {
+    sk_ctx* c = fs[0]->ctx;
+    XSweepArgs a{};
+    a.basis = c->basis;
+    a.grid = c->grid;
+    a.st = c->st;
+    for (int i = 0; i < nspecies; ++i) {
+        int sp = fs[i]->species;
+        a.src[sp] = fs[i]->cur_ptr();
+        a.dst[sp] = fs[i]->other_ptr();
+        a.tab[sp] = fs[i]->xtab;
+    }
+    a.nlines = fs[0]->nv * c->P;
+    a.nspecies = nspecies;
+    a.species0 = nspecies == 2 ? 0 : fs[0]->species;
+    std::memcpy(a.tile_start, c->xtiles, sizeof a.tile_start);
+    a.inline_sldg = inline_sldg;
+    a.periodic = periodic;
+    a.check_finite = check_finite;
+    a.threshold = threshold;
+    CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
+    for (int i = 0; i < nspecies; ++i) fs[i]->swap();
+    return SK_OK;
+}
+
+sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, const double* charge,
+                   const double* sqrt_mu, int inline_sldg, double threshold) {
+    sk_ctx* c = fs[0]->ctx;
+    VTabArgs a{};
+    a.basis = c->basis;
+    for (int i = 0; i < nspecies; ++i) {
+        int sp = fs[i]->species;
+        a.vg[sp] = fs[i]->vg;
+        a.tab[sp] = fs[i]->vtab;
+        a.charge[sp] = charge[i];
+        a.sqrt_mu[sp] = sqrt_mu[i];
+    }
+    a.E = E;
+    a.tau = tau;
+    a.nxd = c->grid.ncells * c->P;
+    a.nspecies = nspecies;
+    a.species0 = nspecies == 2 ? 0 : fs[0]->species;
+    a.inline_sldg = inline_sldg;
+    a.threshold = threshold;
+    CK(launch_vtab(a, c->stream));
+    return SK_OK;
+}
+
+sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
+                     int check_finite) {
+    sk_ctx* c = fs[0]->ctx;
+    VSweepArgs a{};
+    a.basis = c->basis;
+    a.st = c->st;
+    for (int i = 0; i < nspecies; ++i) {
+        int sp = fs[i]->species;
+        a.src[sp] = fs[i]->cur_ptr();
+        a.dst[sp] = fs[i]->other_ptr();
+        a.tab[sp] = fs[i]->vtab;
+    }
+    a.nxd = c->grid.ncells * c->P;
+    a.ld = a.nxd;
+    a.n = fs[0]->nv;
+    a.gl = a.gr = 0;
+    a.nspecies = nspecies;
+    a.species0 = nspecies == 2 ? 0 : fs[0]->species;
+    a.inline_sldg = inline_sldg;
+    a.periodic = periodic;
+    a.check_finite = check_finite;
+    a.threshold = threshold;
+    CK(launch_vsweep(a, c->stream));
+    for (int i = 0; i < nspecies; ++i) fs[i]->swap();
+    return SK_OK;
+}
+
+sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, int periodic) {
+    if (!lim || lim->indicator == 0) return SK_OK;
+    sk_ctx* c = fs[0]->ctx;
+    PostArgs a{};
+    a.basis = c->basis;
+    a.grid = c->grid;
+    a.st = c->st;
+    for (int i = 0; i < nspecies; ++i) {
+        int sp = fs[i]->species;
+        a.src[sp] = fs[i]->cur_ptr();
+        a.dst[sp] = fs[i]->other_ptr();
+    }
+    a.cfg = post_cfg(lim);
+    a.nxd = c->grid.ncells * c->P;
+    a.ld = a.nxd;
+    a.nrows = fs[0]->nv * c->P;
+    a.nv = fs[0]->nv;
+    a.nspecies = nspecies;
+    a.species0 = nspecies == 2 ? 0 : fs[0]->species;
+    a.periodic = periodic;
+    std::memcpy(a.tile_start, c->ptiles, sizeof a.tile_start);
+    if (dir == SK_DIR_X)
+        CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
+    else
+        CK(launch_post_v(a, c->stream));
+    for (int i = 0; i < nspecies; ++i) fs[i]->swap();
+    return SK_OK;
+}
+
+sk_status enq_rho(sk_field* fe, sk_field* fi, double* rho) {
+    sk_ctx* c = fe->ctx;
+    RhoArgs a{};
+    a.basis = c->basis;
+    a.vg[0] = fe->vg;
+    a.vg[1] = fi->vg;
+    a.f[0] = fe->cur_ptr();
+    a.f[1] = fi->cur_ptr();
+    a.nxd = c->grid.ncells * c->P;
+    a.ld = a.nxd;
+    a.nrows = fe->nv * c->P;
+    a.rows_per_chunk = a.nrows <= 256 * 64 ? 64 : (a.nrows + 255) / 256;
+    a.nchunks = (a.nrows + a.rows_per_chunk - 1) / a.rows_per_chunk;
+    size_t need = (size_t)2 * a.nchunks * a.nxd;
+    if (need > c->rho_partial_n) {
+        if (c->rho_partial) cudaFree(c->rho_partial);
+        CK(dalloc(&c->rho_partial, need));
+        c->rho_partial_n = need;
+    }
+    a.partial = c->rho_partial;
+    a.rho = rho;
+    CK(launch_rho(a, 2, c->stream));
+    return SK_OK;
+}
+
+sk_status enq_shrink(sk_field** fs, int nspecies, const sk_vadjust& pol, int force, int v_adjust) {
+    sk_ctx* c = fs[0]->ctx;
+    ShrinkArgs a{};
+    a.basis = c->basis;
+    a.st = c->st;
+    int mask = 0;
+    for (int i = 0; i < nspecies; ++i) {
+        int sp = fs[i]->species;
+        mask |= 1 << sp;
+        a.vg[sp] = fs[i]->vg;
+        a.f[sp] = fs[i]->cur_ptr();
+        a.out[sp] = fs[i]->other_ptr();
+        a.ttab[sp] = fs[i]->ttab;
+        a.tcell[sp] = fs[i]->tcell;
+    }
+    a.nxd = c->grid.ncells * c->P;
+    a.ld = a.nxd;
+    a.nv = fs[0]->nv;
+    a.species_mask = mask;
+    a.v_adjust = v_adjust;
+    a.force = force;
+    a.p = pol.p;
+    a.gamma = pol.gamma;
+    a.tol = pol.tol;
+    a.cooldown = 10;
+    CK(launch_shrink(a, c->stream));
+    return SK_OK;
+}
+
+sk_status validate_policy(const sk_vadjust* p) {
+    if (!(p->p > 0 && p->gamma >= 0 && p->p + p->gamma < 1))
+        return fail(SK_ERR_RUNTIME, "VAdjustPolicy: need 0 < p, 0 <= gamma, p + gamma < 1");
+    if (!(p->tol > 0)) return fail(SK_ERR_RUNTIME, "VAdjustPolicy: tol must be positive");
+    return SK_OK;
+}
+
+sk_status moments(sk_field* f, double* out4) {
+    sk_ctx* c = f->ctx;
+    DiagArgs a{};
+    a.basis = c->basis;
+    a.grid = c->grid;
+    a.vg = f->vg;
+    a.f = f->cur_ptr();
+    a.nxd = c->grid.ncells * c->P;
+    a.ld = a.nxd;
+    a.nrows = f->nv * c->P;
+    CK(launch_diag(a, c->diag_out, c->diag_partial, c->stream));
+    CK(cudaMemcpyAsync(c->pinned, c->diag_out, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(out4, c->pinned, sizeof(double) * 4);
+    return SK_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* sk_last_error(void) { return g_err.c_str(); }
+long sk_last_error_step(void) { return g_err_step; }
+const char* sk_version(void) { return "sk_b200 0.1 (sm_100a, fp64, -fmad=false)"; }
+
+sk_status sk_grid_three_block(double left, double right, int nf, int nc, int m, double* bl, int* bc,
+                              double* bd) {
+    if (!(right > left)) return fail(SK_ERR_RUNTIME, "Grid1D::three_block: invalid extent");
+    if (!(nf >= 1 && nc >= 1 && m >= 1))
+        return fail(SK_ERR_RUNTIME, "Grid1D::three_block: invalid sizes");
+    // grid.cpp:36-46
+    double dxf = (right - left) / (2.0 * nf + static_cast<double>(m) * nc);
+    double dxc = m * dxf;
+    bl[0] = left;
+    bc[0] = nf;
+    bd[0] = dxf;
+    bl[1] = left + nf * dxf;
+    bc[1] = nc;
+    bd[1] = dxc;
+    bl[2] = bl[1] + nc * dxc;
+    bc[2] = nf;
+    bd[2] = dxf;
+    return SK_OK;
+}
+
+sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, const int* cells,
+                        const double* dx, double penalty_scale, sk_ctx** out) {
+    *out = nullptr;
+    if (k < 0 || k > 6) return fail(SK_ERR_RUNTIME, "k must be in 0..6");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(SK_ERR_CUDA, "no CUDA device (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(SK_ERR_CUDA, "invalid device index");
+    CK(cudaSetDevice(device));
+    auto* c = new sk_ctx;
+    c->device = device;
+    c->k = k;
+    c->P = k + 1;
+    c->basis = make_basis(k);
+    std::string e = grid_init(c->grid, nblocks, left, cells, dx);
+    if (!e.empty()) {
+        delete c;
+        return fail(SK_ERR_RUNTIME, e);
+    }
+    const int T = kXThreads * 2, T1 = kXThreads;
+    for (int b = 0; b < nblocks; ++b) {
+        c->xtiles[b + 1] = c->xtiles[b] + (c->grid.cells[b] + T - 1) / T;
+        c->ptiles[b + 1] = c->ptiles[b] + (c->grid.cells[b] + T1 - 1) / T1;
+    }
+    e = poisson_plan_build(c->plan, c->grid, k, penalty_scale);
+    if (!e.empty()) {
+        delete c;
+        return fail(SK_ERR_RUNTIME, e);
+    }
+    // upload the Poisson plan
+    PoissonPlan& P = c->plan;
+    PoissonDev& d = c->pdev;
+    d.k = k;
+    d.ps = P.ps;
+    d.ncells = P.ncells;
+    d.nlevels = P.nlevels;
+    if (P.nlevels > 32) {
+        delete c;
+        return fail(SK_ERR_RUNTIME, "Poisson plan: too many levels");
+    }
+    for (int l = 0; l < P.nlevels; ++l) {
+        d.level_n[l] = P.level_n[l];
+        d.level_off[l] = P.level_off[l];
+    }
+    auto up = [&](const std::vector<double>& v) -> const double* {
+        double* p = nullptr;
+        if (dalloc(&p, v.size()) != cudaSuccess) return nullptr;
+        cudaMemcpy(p, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice);
+        c->pbufs.push_back(p);
+        return p;
+    };
+    d.Dinv = up(P.Dinv);
+    d.Lo = up(P.Lo);
+    d.Up = up(P.Up);
+    d.Alpha = up(P.Alpha);
+    d.Gamma = up(P.Gamma);
+    d.interp = up(P.interp);
+    d.deriv = up(P.deriv);
+    d.h = up(P.h);
+    d.ws = up(P.ws);
+    long total_blocks = 0;
+    for (int l = 0; l < P.nlevels; ++l) total_blocks += P.level_n[l];
+    CK(dalloc(&d.bws, (size_t)total_blocks * P.ps));
+    CK(dalloc(&d.xws, (size_t)total_blocks * P.ps));
+    c->pbufs.push_back(d.bws);
+    c->pbufs.push_back(d.xws);
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(dalloc(&c->st, 1));
+    CK(cudaMemset(c->st, 0, sizeof(DevStatus)));
+    {
+        DevStatus init{};
+        init.last_shrink[0] = init.last_shrink[1] = -10;  // run.cpp:124-125
+        CK(cudaMemcpy(c->st, &init, sizeof init, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMallocHost((void**)&c->st_host, sizeof(DevStatus)));
+    CK(dalloc(&c->diag_partial, 592 * 4));
+    CK(dalloc(&c->diag_out, 4));
+    CK(cudaMallocHost((void**)&c->pinned, sizeof(double) * 64));
+    *out = c;
+    return SK_OK;
+}
+
+sk_status sk_ctx_destroy(sk_ctx* c) {
+    if (!c) return SK_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (void* p : c->pbufs) cudaFree(p);
+    cudaFree(c->st);
+    cudaFreeHost(c->st_host);
+    cudaFree(c->rho_partial);
+    cudaFree(c->diag_partial);
+    cudaFree(c->diag_out);
+    cudaFreeHost(c->pinned);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return SK_OK;
+}
+
+sk_status sk_ctx_set_stream(sk_ctx* c, void* s) {
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (s) {
+        c->stream = (cudaStream_t)s;
+        c->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    return SK_OK;
+}
+
+sk_status sk_ctx_set_eager_errors(sk_ctx* c, int on) {
+    c->eager = on != 0;
+    return SK_OK;
+}
+
+sk_status sk_ctx_synchronize(sk_ctx* c) {
+    CK(cudaSetDevice(c->device));
+    return collect_errors(c);
+}
+
+sk_status sk_stats_get(sk_ctx* c, sk_stats* out) {
+    sk_status rc = collect_errors(c);
+    DevStatus& h = *c->st_host;
+    std::memset(out, 0, sizeof *out);
+    for (int sp = 0; sp < 2; ++sp) {
+        out->inline_troubled += (long long)h.stats[sp][0];
+        out->inline_clamped += (long long)h.stats[sp][1];
+        out->inline_mean_outside += (long long)h.stats[sp][2];
+        out->post_troubled += (long long)h.stats[sp][3];
+        out->post_checked += (long long)h.post_checked[sp];
+    }
+    out->outputs = -1;  // counted on the host by the callers (sk_state / bindings)
+    return rc;
+}
+
+sk_status sk_stats_reset(sk_ctx* c) {
+    CK(cudaMemsetAsync(c->st->stats, 0, sizeof(c->st->stats) + sizeof(c->st->post_checked),
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+// ---------------------------------------------------------------------------
+sk_status sk_field_create(sk_ctx* c, int species, double v_left, double v_right, int v_cells,
+                          sk_field** out) {
+    *out = nullptr;
+    if (species != 0 && species != 1) return fail(SK_ERR_RUNTIME, "species must be 0 or 1");
+    if (!(v_right > v_left && v_cells >= 1))
+        return fail(SK_ERR_RUNTIME, "Grid1D::uniform: invalid extent or cell count");
+    double dv = (v_right - v_left) / v_cells;  // grid.cpp:31-34
+    double right = v_left + v_cells * dv;
+    if (!(std::abs(v_left + right) <= 1e-12 * (right - v_left)))
+        return fail(SK_ERR_RUNTIME, "NodalField: v grid must be symmetric about 0");
+    CK(cudaSetDevice(c->device));
+    auto* f = new sk_field;
+    f->ctx = c;
+    f->species = species;
+    f->nv = v_cells;
+    const int P = c->P;
+    f->n = (size_t)c->grid.ncells * v_cells * P * P;
+    CK(dalloc(&f->buf[0], f->n));
+    CK(dalloc(&f->buf[1], f->n));
+    CK(cudaMemsetAsync(f->buf[0], 0, sizeof(double) * f->n, c->stream));
+    CK(dalloc(&f->vg, 1));
+    DevVGrid vg{v_left, dv, v_cells, 0};
+    CK(cudaMemcpy(f->vg, &vg, sizeof vg, cudaMemcpyHostToDevice));
+    CK(dalloc(&f->xtab, (size_t)c->grid.nclass * v_cells * P * xtab_nf(P)));
+    CK(dalloc(&f->vtab, (size_t)vtab_nf(P) * c->grid.ncells * P));
+    CK(dalloc(&f->ttab, (size_t)v_cells * 4 * P * P));
+    CK(dalloc(&f->tcell, (size_t)v_cells * 4));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = f;
+    return SK_OK;
+}
+
+sk_status sk_field_destroy(sk_field* f) {
+    if (!f) return SK_OK;
+    cudaSetDevice(f->ctx->device);
+    cudaStreamSynchronize(f->ctx->stream);
+    cudaFree(f->buf[0]);
+    cudaFree(f->buf[1]);
+    cudaFree(f->vg);
+    cudaFree(f->xtab);
+    cudaFree(f->vtab);
+    cudaFree(f->ttab);
+    cudaFree(f->tcell);
+    delete f;
+    return SK_OK;
+}
+
+size_t sk_field_size(const sk_field* f) { return f->n; }
+double* sk_field_data_dev(sk_field* f) { return f->cur_ptr(); }
+
+sk_status sk_field_upload(sk_field* f, const double* host, size_t count) {
+    if (count != f->n) return fail(SK_ERR_RUNTIME, "field upload: size mismatch");
+    CK(cudaMemcpyAsync(f->cur_ptr(), host, sizeof(double) * count, cudaMemcpyHostToDevice,
+                       f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    return SK_OK;
+}
+sk_status sk_field_download(sk_field* f, double* host, size_t count) {
+    if (count != f->n) return fail(SK_ERR_RUNTIME, "field download: size mismatch");
+    CK(cudaMemcpyAsync(host, f->cur_ptr(), sizeof(double) * count, cudaMemcpyDeviceToHost,
+                       f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    return SK_OK;
+}
+sk_status sk_field_upload_async(sk_field* f, const double* host, size_t count) {
+    if (count != f->n) return fail(SK_ERR_RUNTIME, "field upload: size mismatch");
+    CK(cudaMemcpyAsync(f->cur_ptr(), host, sizeof(double) * count, cudaMemcpyHostToDevice,
+                       f->ctx->stream));
+    return SK_OK;
+}
+sk_status sk_field_download_async(sk_field* f, double* host, size_t count) {
+    if (count != f->n) return fail(SK_ERR_RUNTIME, "field download: size mismatch");
+    CK(cudaMemcpyAsync(host, f->cur_ptr(), sizeof(double) * count, cudaMemcpyDeviceToHost,
+                       f->ctx->stream));
+    return SK_OK;
+}
+
+sk_status sk_field_v_grid(sk_field* f, double* left, double* dx, int* cells) {
+    DevVGrid h{};
+    CK(cudaMemcpyAsync(f->ctx->pinned, f->vg, sizeof h, cudaMemcpyDeviceToHost, f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    std::memcpy(&h, f->ctx->pinned, sizeof h);
+    if (left) *left = h.left;
+    if (dx) *dx = h.dx;
+    if (cells) *cells = h.cells;
+    return SK_OK;
+}
+
+sk_status sk_field_fill_blob(sk_field* f, double sigma) {
+    sk_ctx* c = f->ctx;
+    const int P = c->P;
+    const Grid& g = c->grid;
+    double vleft, vdx;
+    int vcells;
+    sk_status rc = sk_field_v_grid(f, &vleft, &vdx, &vcells);
+    if (rc) return rc;
+    // run.cpp:19-22 gaussian_blob = (c*exp(x part))*exp(v part); field.cpp:42-50
+    std::vector<double> gx((size_t)g.ncells * P), gv((size_t)vcells * P);
+    const double cst = 1.0 / std::sqrt(2.0 * M_PI);
+    for (int xc = 0; xc < g.ncells; ++xc)
+        for (int xn = 0; xn < P; ++xn) {
+            double x = grid_cell_left(g, xc) + grid_cell_width(g, xc) * c->basis.nodes[xn];
+            gx[(size_t)xc * P + xn] = cst * std::exp(-x * x / (2.0 * sigma * sigma));
+        }
+    for (int vc = 0; vc < vcells; ++vc)
+        for (int vn = 0; vn < P; ++vn) {
+            double v = (vleft + vc * vdx) + vdx * c->basis.nodes[vn];
+            gv[(size_t)vc * P + vn] = std::exp(-v * v / 2.0);
+        }
+    double *dgx, *dgv;
+    CK(dalloc(&dgx, gx.size()));
+    CK(dalloc(&dgv, gv.size()));
+    CK(cudaMemcpy(dgx, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dgv, gv.data(), sizeof(double) * gv.size(), cudaMemcpyHostToDevice));
+    CK(launch_fill_separable(f->cur_ptr(), dgx, dgv, (long long)g.ncells * P, vcells * P, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dgx);
+    cudaFree(dgv);
+    return SK_OK;
+}
+
+// ---------------------------------------------------------------------------
+sk_status sk_advect_x(sk_field* f, double tau, double sqrt_mu, int bc, const sk_limiter* lim,
+                      int max_ghost, long step_index) {
+    sk_ctx* c = f->ctx;
+    CK(cudaSetDevice(c->device));
+    if (sk_status rc = validate_limiter(lim)) return rc;
+    if (c->grid.nblocks > 1 && bc != SK_BC_ZERO_INFLOW)
+        return fail(SK_ERR_RUNTIME, "advect_x: periodic rule is only supported on single-block grids");
+    int inl = lim && lim->inline_sldg;
+    double thr = lim ? lim->threshold : 0.5;
+    sk_field* fs[1] = {f};
+    double sm[1] = {sqrt_mu};
+    if (sk_status rc = enq_xtab(fs, 1, tau, sm, inl, thr, max_ghost < 0 ? -1 : max_ghost, 0.0,
+                                step_index))
+        return rc;
+    if (sk_status rc = enq_xsweep(fs, 1, bc == SK_BC_PERIODIC, inl, thr, 0)) return rc;
+    return after_launch(c);
+}
+
+sk_status sk_advect_v(sk_field* f, double tau, const double* E, double charge_sign, double sqrt_mu,
+                      int bc, const sk_limiter* lim) {
+    sk_ctx* c = f->ctx;
+    CK(cudaSetDevice(c->device));
+    if (sk_status rc = validate_limiter(lim)) return rc;
+    int inl = lim && lim->inline_sldg;
+    double thr = lim ? lim->threshold : 0.5;
+    sk_field* fs[1] = {f};
+    double ch[1] = {charge_sign}, sm[1] = {sqrt_mu};
+    if (sk_status rc = enq_vtab(fs, 1, E, tau, ch, sm, inl, thr)) return rc;
+    if (sk_status rc = enq_vsweep(fs, 1, bc == SK_BC_PERIODIC, inl, thr, 0)) return rc;
+    return after_launch(c);
+}
+
+sk_status sk_post_limit(sk_field* f, int dir, const sk_limiter* lim, int bc) {
+    sk_ctx* c = f->ctx;
+    CK(cudaSetDevice(c->device));
+    if (sk_status rc = validate_limiter(lim)) return rc;
+    if (!lim || lim->indicator == 0) return SK_OK;
+    if (dir == SK_DIR_X && c->grid.nblocks > 1 && bc == SK_BC_PERIODIC)
+        return fail(SK_ERR_RUNTIME, "apply_post_limiter: periodic rule needs a single-block grid");
+    sk_field* fs[1] = {f};
+    if (sk_status rc = enq_post(fs, 1, dir, lim, bc == SK_BC_PERIODIC)) return rc;
+    return after_launch(c);
+}
+
+sk_status sk_charge_density(sk_field* fe, sk_field* fi, double* rho) {
+    if (fe->ctx != fi->ctx) return fail(SK_ERR_RUNTIME, "charge_density: species must share the x grid");
+    if (fe->nv != fi->nv) return fail(SK_ERR_RUNTIME, "charge_density: v cell counts differ");
+    CK(cudaSetDevice(fe->ctx->device));
+    if (sk_status rc = enq_rho(fe, fi, rho)) return rc;
+    return after_launch(fe->ctx);
+}
+
+sk_status sk_poisson_solve(sk_ctx* c, const double* rho, double* E, double* phi) {
+    CK(cudaSetDevice(c->device));
+    CK(launch_poisson(c->pdev, rho, E, phi, c->stream));
+    return after_launch(c);
+}
+
+sk_status sk_check_velocity_shrink(sk_field* f, const sk_vadjust* pol, int* out) {
+    if (sk_status rc = validate_policy(pol)) return rc;
+    sk_ctx* c = f->ctx;
+    CK(cudaSetDevice(c->device));
+    sk_field* fs[1] = {f};
+    if (sk_status rc = enq_shrink(fs, 1, *pol, -1, 1)) return rc;
+    if (sk_status rc = collect_errors(c)) return rc;
+    *out = c->st_host->shrink_flag[f->species];
+    return SK_OK;
+}
+
+sk_status sk_shrink_velocity_domain(sk_field* f, const sk_vadjust* pol, sk_shrink_result* out) {
+    if (sk_status rc = validate_policy(pol)) return rc;
+    sk_ctx* c = f->ctx;
+    CK(cudaSetDevice(c->device));
+    double m0[4], m1[4], left0, left1;
+    if (sk_status rc = moments(f, m0)) return rc;
+    if (sk_status rc = sk_field_v_grid(f, &left0, nullptr, nullptr)) return rc;
+    double dx0;
+    sk_field_v_grid(f, nullptr, &dx0, nullptr);
+    sk_field* fs[1] = {f};
+    if (sk_status rc = enq_shrink(fs, 1, *pol, 1, 1)) return rc;
+    if (sk_status rc = collect_errors(c)) return rc;
+    if (sk_status rc = moments(f, m1)) return rc;
+    double dx1;
+    if (sk_status rc = sk_field_v_grid(f, &left1, &dx1, nullptr)) return rc;
+    if (out) {
+        out->vmax_before = left0 + f->nv * dx0;
+        out->vmax_after = -left1;
+        out->mass_before = m0[0];
+        out->mass_after = m1[0];
+    }
+    return SK_OK;
+}
+
+sk_status sk_field_moments(sk_field* f, double* out4) {
+    CK(cudaSetDevice(f->ctx->device));
+    return moments(f, out4);
+}
+
+sk_status sk_electric_energy(sk_ctx* c, const double* E, double* out) {
+    const int P = c->P;
+    std::vector<double> h((size_t)c->grid.ncells * P);
+    CK(cudaMemcpyAsync(h.data(), E, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    double acc = 0.0;  // diagnostics.cpp:71-83
+    for (int cc = 0; cc < c->grid.ncells; ++cc) {
+        double hh = grid_cell_width(c->grid, cc);
+        for (int q = 0; q < P; ++q) {
+            double e = h[(size_t)cc * P + q];
+            acc += 0.5 * c->basis.weights[q] * hh * e * e;
+        }
+    }
+    *out = acc;
+    return SK_OK;
+}
+
+// ---------------------------------------------------------------------------
+sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
+    *out = nullptr;
+    if (cfg->k != c->k) return fail(SK_ERR_RUNTIME, "state: degree differs from the context");
+    if (!(cfg->dt > 0)) return fail(SK_ERR_RUNTIME, "dt: must be positive");
+    if (!(cfg->mu > 0)) return fail(SK_ERR_RUNTIME, "SpeciesParams::ion: mass ratio must be positive");
+    if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
+    if (cfg->v_adjust)
+        if (sk_status rc = validate_policy(&cfg->policy)) return rc;
+    auto* s = new sk_state;
+    s->ctx = c;
+    s->cfg = *cfg;
+    s->sqrt_mu[0] = 1.0;
+    s->sqrt_mu[1] = std::sqrt(cfg->mu);
+    s->charge[0] = -1.0;
+    s->charge[1] = 1.0;
+    sk_status rc;
+    if ((rc = sk_field_create(c, 0, -cfg->vmax_e, cfg->vmax_e, cfg->v_cells, &s->f[0])) ||
+        (rc = sk_field_create(c, 1, -cfg->vmax_i, cfg->vmax_i, cfg->v_cells, &s->f[1]))) {
+        sk_state_destroy(s);
+        return rc;
+    }
+    double sigma = cfg->sigma < 0 ? 0.1 * cfg->L : cfg->sigma;  // config.cpp resolve()
+    if ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma))) {
+        sk_state_destroy(s);
+        return rc;
+    }
+    const size_t ne = (size_t)c->grid.ncells * c->P;
+    CK(dalloc(&s->E, ne));
+    CK(dalloc(&s->rho, ne));
+    CK(dalloc(&s->phi, (size_t)c->grid.ncells * (c->P + 1)));
+    // run.cpp:56 initial field
+    if ((rc = enq_rho(s->f[0], s->f[1], s->rho))) return rc;
+    CK(launch_poisson(c->pdev, s->rho, s->E, s->phi, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = s;
+    return SK_OK;
+}
+
+sk_status sk_state_destroy(sk_state* s) {
+    if (!s) return SK_OK;
+    cudaSetDevice(s->ctx->device);
+    if (s->graph2) cudaGraphExecDestroy(s->graph2);
+    sk_field_destroy(s->f[0]);
+    sk_field_destroy(s->f[1]);
+    cudaFree(s->E);
+    cudaFree(s->rho);
+    cudaFree(s->phi);
+    delete s;
+    return SK_OK;
+}
+
+sk_field* sk_state_field(sk_state* s, int species) { return s->f[species & 1]; }
+double* sk_state_E_dev(sk_state* s) { return s->E; }
+
+sk_status sk_state_download_E(sk_state* s, double* host, size_t count) {
+    sk_ctx* c = s->ctx;
+    if (count != (size_t)c->grid.ncells * c->P) return fail(SK_ERR_RUNTIME, "E: size mismatch");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(host, s->E, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+namespace {
+
+// stepper.cpp:44-103 (blob: no source term), all on the context stream.
+sk_status enq_strang(sk_state* s) {
+    sk_ctx* c = s->ctx;
+    const sk_limiter* lim = &s->cfg.limiter;
+    const int inl = lim->inline_sldg;
+    const double thr = lim->threshold;
+    const double dt = s->cfg.dt, half = 0.5 * dt;
+    sk_field* fs[2] = {s->f[0], s->f[1]};
+    sk_status rc;
+    // x tables serve both x half-sweeps (same tau, same v grid within a step)
+    if ((rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1))) return rc;
+    if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0))) return rc;
+    if ((rc = enq_post(fs, 2, SK_DIR_X, lim, 0))) return rc;
+    if ((rc = enq_rho(fs[0], fs[1], s->rho))) return rc;
+    CK(launch_poisson(c->pdev, s->rho, s->E, s->phi, c->stream));
+    if ((rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr))) return rc;
+    if ((rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;
+    if ((rc = enq_post(fs, 2, SK_DIR_V, lim, 0))) return rc;
+    if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
+    if ((rc = enq_post(fs, 2, SK_DIR_X, lim, 0))) return rc;
+    return SK_OK;
+}
+
+sk_status enq_run_body(sk_state* s) {
+    sk_ctx* c = s->ctx;
+    if (sk_status rc = enq_strang(s)) return rc;
+    CK(launch_step_end(c->st, s->cfg.v_adjust, 10, 3, c->stream));
+    if (s->cfg.v_adjust) {
+        sk_field* fs[2] = {s->f[0], s->f[1]};
+        if (sk_status rc = enq_shrink(fs, 2, s->cfg.policy, 0, 1)) return rc;
+    }
+    s->step_host += 1;
+    return SK_OK;
+}
+
+}  // namespace
+
+sk_status sk_strang_step(sk_state* s) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    if (sk_status rc = enq_strang(s)) return rc;
+    CK(launch_step_end(c->st, 0, 10, 0, c->stream));
+    s->step_host += 1;
+    return after_launch(c);
+}
+
+sk_status sk_run_step(sk_state* s) {
+    CK(cudaSetDevice(s->ctx->device));
+    if (sk_status rc = enq_run_body(s)) return rc;
+    return after_launch(s->ctx);
+}
+
+sk_status sk_run_steps(sk_state* s, int n) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    // Two loop bodies leave both ping-pong buffers where they started, so a
+    // captured pair replays with fixed pointers.
+    if (n >= 2 && (!s->graph2 || s->graph_cur0 != s->f[0]->cur || s->graph_cur1 != s->f[1]->cur)) {
+        if (s->graph2) {
+            cudaGraphExecDestroy(s->graph2);
+            s->graph2 = nullptr;
+        }
+        int c0 = s->f[0]->cur, c1 = s->f[1]->cur;
+        long h0 = s->step_host;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        sk_status rc = enq_run_body(s);
+        if (!rc) rc = enq_run_body(s);
+        cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+        s->step_host = h0;
+        if (rc) return rc;
+        CK(ce);
+        if (s->f[0]->cur != c0 || s->f[1]->cur != c1)
+            return fail(SK_ERR_RUNTIME, "internal: buffer parity after two steps");
+        CK(cudaGraphInstantiate(&s->graph2, g, 0));
+        cudaGraphDestroy(g);
+        s->graph_cur0 = c0;
+        s->graph_cur1 = c1;
+    }
+    int done = 0;
+    for (; done + 2 <= n; done += 2) {
+        CK(cudaGraphLaunch(s->graph2, c->stream));
+        s->step_host += 2;
+    }
+    for (; done < n; ++done)
+        if (sk_status rc = enq_run_body(s)) return rc;
+    return after_launch(c);
+}
+
+sk_status sk_state_step_index(sk_state* s, long* step) {
+    if (sk_status rc = collect_errors(s->ctx)) return rc;
+    *step = (long)s->ctx->st_host->step;
+    return SK_OK;
+}
+
+sk_status sk_state_shrinks(sk_state* s, int species, int* count, long* last) {
+    if (sk_status rc = collect_errors(s->ctx)) return rc;
+    if (count) *count = s->ctx->st_host->shrink_count[species & 1];
+    if (last) *last = (long)s->ctx->st_host->last_shrink[species & 1];
+    return SK_OK;
+}
+
+sk_status sk_run_step_host(sk_state* s, double* fe, double* fi, size_t count) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    if (sk_status rc = sk_field_upload_async(s->f[0], fe, count)) return rc;
+    if (sk_status rc = sk_field_upload_async(s->f[1], fi, count)) return rc;
+    if (sk_status rc = enq_run_body(s)) return rc;
+    if (sk_status rc = sk_field_download_async(s->f[0], fe, count)) return rc;
+    if (sk_status rc = sk_field_download_async(s->f[1], fi, count)) return rc;
+    return collect_errors(c);
+}
+
+}  // extern "C"

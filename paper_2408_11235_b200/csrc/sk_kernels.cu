@@ -1,0 +1,1005 @@
+// sk_kernels.cu -- sm_100a kernels of the sLdG time step.
+//
+// Data layout in HBM is the reference's NodalField layout
+// ((vc*P+vn)*nx+xc)*P+xn (core/include/solkin/field.hpp:71-73): an x line is a
+// contiguous row of nx*P doubles, a v line is a column with row stride nx*P.
+//
+//   xtab_kernel     per (species, dx class, v row): i*, alpha, A, B, limiter
+//                   moments (make_plan, advection.cpp:132-140) + ghost checks
+//   xsweep_kernel   K1: one CTA per (x-row, tile of a block): coalesced window
+//                   load (with 3-block ghost transfer, adaptivity.cpp:169-207)
+//                   -> SoA smem -> per-cell projection + inline limiter in
+//                   registers -> SoA smem -> coalesced store
+//   vtab_kernel     per (species, x dof): tables from E (advect_v, :209-238)
+//   vsweep_kernel   K2: one thread per x dof over a chunk of v cells, sliding
+//                   2-cell register window; loads/stores coalesced across x
+//   rho_*           K4: deterministic two-pass charge-density moment
+//   poisson_kernel  block-cyclic-reduction replay of the SIPG solve + E=-phi'
+//   shrink_*        K5/K6: velocity cut-off check, transfer tables, projection
+//   diag_*          K8: mass / L2 / momentum / kinetic-energy reductions
+//   post_*          K3: minmod / mean-error indicators + simple / line WENO
+// All arithmetic is fp64 with -fmad=false so per-cell results are bitwise the
+// reference's.
+#include <cuda_runtime.h>
+
+#include "sk_kernels.cuh"
+
+namespace sk {
+
+namespace {
+
+template <int P>
+__host__ __device__ constexpr int xs_pad() {
+    return P == 2 ? 8 : P == 3 ? 5 : P == 4 ? 4 : P >= 5 ? 3 : 0;
+}
+template <int P, int T>
+__host__ __device__ constexpr int xs_stride() {
+    return ((T + 2 + 15) / 16) * 16 + xs_pad<P>();
+}
+template <int P>
+__host__ __device__ constexpr int xnf() {
+    return ((2 + 2 * P * P + 2 * P) + 1) & ~1;
+}
+template <int P>
+__host__ __device__ constexpr int vnf() {
+    return 2 + 2 * P * P + 2 * P;
+}
+
+__device__ __forceinline__ void raise_error(DevStatus* st, int code, int kind, int need, int have,
+                                            long long step) {
+    if (atomicCAS(&st->err_code, 0, code) == 0) {
+        st->err_kind = kind;
+        st->err_need = need;
+        st->err_have = have;
+        st->err_step = step;
+    }
+}
+
+__device__ __forceinline__ void count_flags(unsigned long long* dst, unsigned t, unsigned c,
+                                            unsigned o) {
+    const unsigned full = 0xffffffffu;
+    t = __reduce_add_sync(full, t);
+    c = __reduce_add_sync(full, c);
+    o = __reduce_add_sync(full, o);
+    if ((threadIdx.x & 31) == 0) {
+        if (t) atomicAdd(&dst[0], (unsigned long long)t);
+        if (c) atomicAdd(&dst[1], (unsigned long long)c);
+        if (o) atomicAdd(&dst[2], (unsigned long long)o);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// x tables
+// ---------------------------------------------------------------------------
+template <int P>
+__global__ void xtab_kernel(const __grid_constant__ XTabArgs a) {
+    const int line = blockIdx.x * blockDim.x + threadIdx.x;
+    if (line >= a.nlines) return;
+    const int sp = a.species0 + blockIdx.y;
+    const Grid& g = a.grid;
+    const DevVGrid vg = *a.vg[sp];
+    const int vc = line / P, vn = line - (line / P) * P;
+    // field.cpp:37-40 v_node = cell_left + cell_width * node
+    const double vnode = (vg.left + vc * vg.dx) + vg.dx * a.basis.nodes[vn];
+    const double speed = vnode / a.sqrt_mu[sp];  // advection.cpp:164
+    constexpr int NF = xnf<P>();
+    int istar_c[kMaxBlocks];
+    for (int c = 0; c < g.nclass; ++c) {
+        int istar;
+        double alpha;
+        decompose_shift(speed, a.tau, g.class_dx[c], istar, alpha);
+        istar_c[c] = istar;
+        double A[P * P], B[P * P];
+        shift_matrices<P>(a.basis, alpha, A, B);
+        double* row = a.tab[sp] + ((long long)c * a.nlines + line) * NF;
+        row[0] = (double)istar;
+        row[1] = alpha;
+#pragma unroll
+        for (int i = 0; i < P * P; ++i) {
+            row[2 + i] = A[i];
+            row[2 + P * P + i] = B[i];
+        }
+        if (a.inline_sldg) {  // limiters.cpp:167-173
+            double el[P], er[P];
+            interval_moments<P>(a.basis, -alpha, 1.0 - alpha, el);
+            interval_moments<P>(a.basis, 1.0 - alpha, 2.0 - alpha, er);
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                row[2 + 2 * P * P + i] = el[i];
+                row[2 + 2 * P * P + P + i] = er[i];
+            }
+        }
+    }
+    if (g.nblocks == 1) return;
+    // ghost-width checks (advection.cpp:181-190) and neighbour capacity
+    // (adaptivity.cpp:179-183)
+    int max_ghost = a.max_ghost;
+    if (max_ghost == -2) {  // run.cpp:125-128
+        const DevVGrid v0 = *a.vg[0], v1 = *a.vg[1];
+        double r0 = v0.left + v0.cells * v0.dx, r1 = v1.left + v1.cells * v1.dx;
+        double vmax_now = dmax2(r0, r1);
+        double smm = dmin2(a.sqrt_mu[0], a.sqrt_mu[1]);
+        max_ghost = (int)ceil(vmax_now * a.dt_auto / (smm * g.dx[0])) + 1;
+    }
+    const DevStatus* stc = a.st;
+    long long step = a.step_index >= 0 ? a.step_index : stc->step;
+    for (int b = 0; b < g.nblocks; ++b) {
+        int istar = istar_c[g.cls[b]];
+        int gl = b > 0 ? max(0, -istar) : 0;
+        int gr = b + 1 < g.nblocks ? max(0, istar + 1) : 0;
+        int need = max(gl, gr);
+        if (max_ghost >= 0 && need > max_ghost) {
+            raise_error(a.st, 2, 1, need, max_ghost, step);
+            return;
+        }
+        for (int side = 0; side < 2; ++side) {
+            int j = side == 0 ? gl : gr;
+            if (j == 0) continue;
+            bool left = side == 0;
+            int nb = left ? b - 1 : b + 1;
+            int iface = left ? g.start[b] : g.start[b] + g.cells[b];
+            int lo, hi;
+            if (g.dx[nb] == g.dx[b]) {
+                lo = left ? iface - j : iface + (j - 1);
+                hi = lo + 1;
+            } else if (g.dx[nb] > g.dx[b]) {
+                int m = (int)llround(g.dx[nb] / g.dx[b]);
+                lo = left ? iface - 1 - (j - 1) / m : iface + (j - 1) / m;
+                hi = lo + 1;
+            } else {
+                int m = (int)llround(g.dx[b] / g.dx[nb]);
+                lo = left ? iface - j * m : iface + (j - 1) * m;
+                hi = lo + m;
+            }
+            if (!(lo >= g.start[nb] && hi <= g.start[nb] + g.cells[nb])) {
+                raise_error(a.st, 1, 2, j, 0, step);
+                return;
+            }
+        }
+    }
+}
+
+// ghost cell value for block-local cell s outside [0, cells_b) (fill_ghost,
+// adaptivity.cpp:169-207): copy / coarse_to_fine piece / fine_to_coarse.
+template <int P>
+__device__ double x_fetch_outside(const Basis& basis, const Grid& g, const double* line, int b,
+                                  int s, int n) {
+    const bool left = s < 0;
+    int nb, j;
+    if (left) {
+        if (b == 0) return 0.0;
+        nb = b - 1;
+        j = -s;
+    } else {
+        if (b == g.nblocks - 1) return 0.0;
+        nb = b + 1;
+        j = s - g.cells[b] + 1;
+    }
+    const int iface = left ? g.start[b] : g.start[b] + g.cells[b];
+    const int nb_begin = g.start[nb], nb_end = nb_begin + g.cells[nb];
+    if (g.dx[nb] == g.dx[b]) {
+        int src = left ? iface - j : iface + (j - 1);
+        if (src < nb_begin || src >= nb_end) return 0.0;
+        return line[(long long)src * P + n];
+    }
+    if (g.dx[nb] > g.dx[b]) {
+        int m = (int)llround(g.dx[nb] / g.dx[b]);
+        int coarse = left ? iface - 1 - (j - 1) / m : iface + (j - 1) / m;
+        if (coarse < nb_begin || coarse >= nb_end) return 0.0;
+        int piece = left ? m - 1 - (j - 1) % m : (j - 1) % m;
+        double u[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) u[q] = line[(long long)coarse * P + q];
+        return coarse_to_fine_node<P>(basis, u, m, piece, n);
+    }
+    int m = (int)llround(g.dx[b] / g.dx[nb]);
+    int lo = left ? iface - j * m : iface + (j - 1) * m;
+    if (lo < nb_begin || lo + m > nb_end) return 0.0;
+    return fine_to_coarse_node<P>(basis, line + (long long)lo * P, m, n);
+}
+
+// ---------------------------------------------------------------------------
+// K1: x sweep
+// ---------------------------------------------------------------------------
+template <int P, int CPT>
+__global__ void __launch_bounds__(kXThreads, 2) xsweep_kernel(const __grid_constant__ XSweepArgs a) {
+    constexpr int T = kXThreads * CPT;
+    constexpr int W = xs_stride<P, T>();
+    constexpr int NF = xnf<P>();
+    extern __shared__ double smem[];
+    double* win = smem;           // [P][W] input window, SoA
+    double* outs = smem + P * W;  // [P][W] output tile, SoA
+
+    const int line = blockIdx.x;
+    const int sp = a.species0 + blockIdx.z;
+    const int tile = blockIdx.y;
+    const Grid& g = a.grid;
+    int b = 0;
+    while (tile >= a.tile_start[b + 1]) ++b;
+    const int cells_b = g.cells[b];
+    const int c0 = (tile - a.tile_start[b]) * T;
+    const int nt = min(T, cells_b - c0);
+
+    const double* row = a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * NF;
+    const int istar = (int)row[0];
+    const double alpha = row[1];
+    double A[P * P], B[P * P];
+#pragma unroll
+    for (int i = 0; i < P * P; ++i) {
+        A[i] = row[2 + i];
+        B[i] = row[2 + P * P + i];
+    }
+
+    const long long lb = (long long)line * g.ncells * P;
+    const double* src = a.src[sp] + lb;
+    const int s0 = c0 + istar;
+    const int nwin = (nt + 1) * P;
+    const long long gbase = (long long)g.start[b] * P;
+    for (int e = threadIdx.x; e < nwin; e += kXThreads) {
+        const int wc = e / P, n = e - (e / P) * P;
+        const int s = s0 + wc;
+        double v;
+        if (s >= 0 && s < cells_b) {
+            v = __ldg(src + gbase + (long long)s * P + n);
+        } else if (a.periodic) {  // advection.cpp:86-88 (single block only)
+            int ss = ((s % cells_b) + cells_b) % cells_b;
+            v = src[gbase + (long long)ss * P + n];
+        } else {
+            v = x_fetch_outside<P>(a.basis, g, src, b, s, n);
+        }
+        win[n * W + wc] = v;
+    }
+    __syncthreads();
+
+    unsigned nt_t = 0, nt_c = 0, nt_o = 0;
+    bool bad = false;
+    double el[P], er[P];
+    if (a.inline_sldg) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            el[i] = row[2 + 2 * P * P + i];
+            er[i] = row[2 + 2 * P * P + P + i];
+        }
+    }
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+        const int c = threadIdx.x + cc * kXThreads;
+        if (c < nt) {
+            double ul[P], ur[P], o[P];
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                ul[n] = win[n * W + c];
+                ur[n] = win[n * W + c + 1];
+            }
+            project_cell<P>(A, B, ul, ur, o);
+            if (a.inline_sldg) {
+                int fl = inline_limit<P>(a.basis, alpha, a.threshold, el, er, ul, ur, o);
+                nt_t += fl & 1;
+                nt_c += (fl >> 1) & 1;
+                nt_o += (fl >> 2) & 1;
+            }
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                bad |= !isfinite(o[m]);
+                outs[m * W + c] = o[m];
+            }
+        }
+    }
+    __syncthreads();
+    double* dst = a.dst[sp] + lb + gbase + (long long)c0 * P;
+    for (int e = threadIdx.x; e < nt * P; e += kXThreads) {
+        const int c = e / P, m = e - (e / P) * P;
+        dst[e] = outs[m * W + c];
+    }
+    if (a.inline_sldg) count_flags(a.st->stats[sp], nt_t, nt_c, nt_o);
+    if (a.check_finite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(&a.st->nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------
+// v tables and K2: v sweep
+// ---------------------------------------------------------------------------
+template <int P>
+__global__ void vtab_kernel(const __grid_constant__ VTabArgs a) {
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xd >= a.nxd) return;
+    const int sp = a.species0 + blockIdx.y;
+    const double speed = a.charge[sp] * a.E[xd] / a.sqrt_mu[sp];  // advection.cpp:226
+    const double dv = a.vg[sp]->dx;
+    int istar;
+    double alpha;
+    decompose_shift(speed, a.tau, dv, istar, alpha);
+    double A[P * P], B[P * P];
+    shift_matrices<P>(a.basis, alpha, A, B);
+    double* t = a.tab[sp];
+    const int n = a.nxd;
+    t[xd] = (double)istar;
+    t[n + xd] = alpha;
+#pragma unroll
+    for (int i = 0; i < P * P; ++i) {
+        t[(long long)(2 + i) * n + xd] = A[i];
+        t[(long long)(2 + P * P + i) * n + xd] = B[i];
+    }
+    if (a.inline_sldg) {
+        double el[P], er[P];
+        interval_moments<P>(a.basis, -alpha, 1.0 - alpha, el);
+        interval_moments<P>(a.basis, 1.0 - alpha, 2.0 - alpha, er);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            t[(long long)(2 + 2 * P * P + i) * n + xd] = el[i];
+            t[(long long)(2 + 2 * P * P + P + i) * n + xd] = er[i];
+        }
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void vload(const double* f, long long ld, int xd, int s, int lo, int hi,
+                                      int periodic, int ncell, double* u) {
+    if (periodic) s = ((s % ncell) + ncell) % ncell;
+    if (s >= lo && s < hi) {
+        const double* p = f + (long long)s * P * ld + xd;
+#pragma unroll
+        for (int n = 0; n < P; ++n) u[n] = __ldg(p + n * ld);
+    } else {
+#pragma unroll
+        for (int n = 0; n < P; ++n) u[n] = 0.0;
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant__ VSweepArgs a) {
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    const int sp = a.species0 + blockIdx.z;
+    const int j0 = blockIdx.y * kVChunk;
+    const int j1 = min(j0 + kVChunk, a.n);
+    unsigned nt_t = 0, nt_c = 0, nt_o = 0;
+    bool bad = false;
+    if (xd < a.nxd) {
+        const double* t = a.tab[sp];
+        const int nx = a.nxd;
+        const int istar = (int)t[xd];
+        const double alpha = t[nx + xd];
+        double A[P * P], B[P * P], el[P], er[P];
+#pragma unroll
+        for (int i = 0; i < P * P; ++i) {
+            A[i] = t[(long long)(2 + i) * nx + xd];
+            B[i] = t[(long long)(2 + P * P + i) * nx + xd];
+        }
+        if (a.inline_sldg) {
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+                el[i] = t[(long long)(2 + 2 * P * P + i) * nx + xd];
+                er[i] = t[(long long)(2 + 2 * P * P + P + i) * nx + xd];
+            }
+        }
+        const double* f = a.src[sp];
+        double* out = a.dst[sp];
+        const long long ld = a.ld;
+        const int lo = -a.gl, hi = a.n + a.gr;
+        double ul[P], ur[P], nx1[P];
+        vload<P>(f, ld, xd, j0 + istar, lo, hi, a.periodic, a.n, ul);
+        vload<P>(f, ld, xd, j0 + istar + 1, lo, hi, a.periodic, a.n, ur);
+        for (int j = j0; j < j1; ++j) {
+            vload<P>(f, ld, xd, j + istar + 2, lo, hi, a.periodic, a.n, nx1);  // prefetch
+            double o[P];
+            project_cell<P>(A, B, ul, ur, o);
+            if (a.inline_sldg) {
+                int fl = inline_limit<P>(a.basis, alpha, a.threshold, el, er, ul, ur, o);
+                nt_t += fl & 1;
+                nt_c += (fl >> 1) & 1;
+                nt_o += (fl >> 2) & 1;
+            }
+            double* op = out + (long long)j * P * ld + xd;
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                bad |= !isfinite(o[m]);
+                op[m * ld] = o[m];
+            }
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                ul[n] = ur[n];
+                ur[n] = nx1[n];
+            }
+        }
+    }
+    if (a.inline_sldg) count_flags(a.st->stats[sp], nt_t, nt_c, nt_o);
+    if (a.check_finite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+        atomicOr(&a.st->nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------
+// K4: charge density (poisson.cpp:194-216), deterministic two-pass
+// ---------------------------------------------------------------------------
+template <int P>
+__global__ void rho_partial_kernel(const __grid_constant__ RhoArgs a) {
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xd >= a.nxd) return;
+    const int sp = blockIdx.z;
+    const int chunk = blockIdx.y;
+    const double dv = a.vg[sp]->dx;
+    const int r0 = chunk * a.rows_per_chunk, r1 = min(r0 + a.rows_per_chunk, a.nrows);
+    const double* f = a.f[sp] + xd;
+    double acc = 0.0;
+    for (int r = r0; r < r1; ++r) {
+        const int vn = r - (r / P) * P;
+        acc += a.basis.weights[vn] * dv * __ldg(f + (long long)r * a.ld);
+    }
+    a.partial[((long long)sp * a.nchunks + chunk) * a.nxd + xd] = acc;
+}
+
+__global__ void rho_reduce_kernel(const __grid_constant__ RhoArgs a) {
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xd >= a.nxd) return;
+    double acc = 0.0;
+    for (int c = 0; c < a.nchunks; ++c) acc += a.partial[((long long)1 * a.nchunks + c) * a.nxd + xd];
+    for (int c = 0; c < a.nchunks; ++c) acc -= a.partial[((long long)0 * a.nchunks + c) * a.nxd + xd];
+    a.rho[xd] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Poisson: replay of the host block-cyclic-reduction plan (single CTA)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ PoissonDev pd,
+                                                       const double* __restrict__ rho,
+                                                       double* __restrict__ E,
+                                                       double* __restrict__ phi) {
+    const int ps = pd.ps, k = pd.k, N = pd.ncells, pp = ps * ps;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    double* b0 = pd.bws;
+    // load vector (poisson.cpp:135-149)
+    for (int i = tid; i < N * ps; i += nth) {
+        const int c = i / ps, m = i - (i / ps) * ps;
+        double val = 0.0;
+        for (int n = 0; n <= k; ++n) val += pd.interp[m * (k + 1) + n] * rho[c * (k + 1) + n];
+        b0[i] = pd.ws[m] * pd.h[c] * val;
+    }
+    __syncthreads();
+    for (int l = 0; l + 1 < pd.nlevels; ++l) {
+        const int Nl = pd.level_n[l], Nn = pd.level_n[l + 1];
+        const double* bl = pd.bws + pd.level_off[l] * ps;
+        double* bn = pd.bws + pd.level_off[l + 1] * ps;
+        const double* Al = pd.Alpha + pd.level_off[l] * pp;
+        const double* Gl = pd.Gamma + pd.level_off[l] * pp;
+        for (int i = tid; i < Nn * ps; i += nth) {
+            const int r = i / ps, m = i - (i / ps) * ps, q = 2 * r;
+            double v = bl[q * ps + m];
+            if (q - 1 >= 0)
+                for (int n = 0; n < ps; ++n) v += Al[(long long)q * pp + m * ps + n] * bl[(q - 1) * ps + n];
+            if (q + 1 < Nl)
+                for (int n = 0; n < ps; ++n) v += Gl[(long long)q * pp + m * ps + n] * bl[(q + 1) * ps + n];
+            bn[i] = v;
+        }
+        __syncthreads();
+    }
+    {
+        const int L = pd.nlevels - 1;
+        const double* bt = pd.bws + pd.level_off[L] * ps;
+        double* xt = pd.xws + pd.level_off[L] * ps;
+        const double* Di = pd.Dinv + pd.level_off[L] * pp;
+        for (int m = tid; m < ps; m += nth) {
+            double v = 0.0;
+            for (int n = 0; n < ps; ++n) v += Di[m * ps + n] * bt[n];
+            xt[m] = v;
+        }
+        __syncthreads();
+    }
+    for (int l = pd.nlevels - 2; l >= 0; --l) {
+        const int Nl = pd.level_n[l];
+        double* bl = pd.bws + pd.level_off[l] * ps;
+        double* xl = pd.xws + pd.level_off[l] * ps;
+        const double* xn = pd.xws + pd.level_off[l + 1] * ps;
+        const double* Lo = pd.Lo + pd.level_off[l] * pp;
+        const double* Up = pd.Up + pd.level_off[l] * pp;
+        const double* Di = pd.Dinv + pd.level_off[l] * pp;
+        for (int i = tid; i < Nl * ps; i += nth) {
+            const int q = i / ps, m = i - (i / ps) * ps;
+            if ((q & 1) == 0) {
+                xl[i] = xn[(q / 2) * ps + m];
+            } else {
+                double t = bl[i];
+                const double* xm = xn + ((q - 1) / 2) * ps;
+                for (int j = 0; j < ps; ++j) t -= Lo[(long long)q * pp + m * ps + j] * xm[j];
+                if (q + 1 < Nl) {
+                    const double* xp = xn + ((q + 1) / 2) * ps;
+                    for (int j = 0; j < ps; ++j) t -= Up[(long long)q * pp + m * ps + j] * xp[j];
+                }
+                bl[i] = t;
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < Nl * ps; i += nth) {
+            const int q = i / ps, m = i - (i / ps) * ps;
+            if (q & 1) {
+                double v = 0.0;
+                for (int n = 0; n < ps; ++n) v += Di[(long long)q * pp + m * ps + n] * bl[q * ps + n];
+                xl[i] = v;
+            }
+        }
+        __syncthreads();
+    }
+    const double* x0 = pd.xws;
+    if (phi)
+        for (int i = tid; i < N * ps; i += nth) phi[i] = x0[i];
+    // E = -phi' at the degree-k nodes (poisson.cpp:176-192)
+    for (int i = tid; i < N * (k + 1); i += nth) {
+        const int c = i / (k + 1), m = i - (i / (k + 1)) * (k + 1);
+        double dphi = 0.0;
+        for (int n = 0; n < ps; ++n) dphi += pd.deriv[m * ps + n] * x0[c * ps + n];
+        E[i] = -dphi / pd.h[c];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// step end: step counter, nonfinite -> SimulationError (stepper.cpp:99-102),
+// shrink cooldown gate (run.cpp:98-101)
+// ---------------------------------------------------------------------------
+__global__ void step_end_kernel(DevStatus* st, int v_adjust, long long cooldown, int mask) {
+    st->step += 1;
+    if (st->nonfinite) raise_error(st, 2, 3, 0, 0, st->step);
+    for (int sp = 0; sp < 2; ++sp)
+        st->shrink_flag[sp] =
+            ((mask >> sp) & 1) && v_adjust && (st->step - st->last_shrink[sp] >= cooldown) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// K5/K6: velocity cut-off (adaptivity.cpp:16-130)
+// ---------------------------------------------------------------------------
+template <int P>
+__global__ void shrink_check_kernel(const __grid_constant__ ShrinkArgs a) {
+    const int sp = blockIdx.y;
+    if (!((a.species_mask >> sp) & 1)) return;
+    if (a.st->shrink_flag[sp] == 0) return;
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xd >= a.nxd) return;
+    const DevVGrid vg = *a.vg[sp];
+    const double dv = vg.dx;
+    const double right = vg.left + vg.cells * vg.dx;
+    const double probe = right * (1.0 - a.p - a.gamma);
+    const double* f = a.f[sp];
+    bool fail = false;
+    for (int s = 0; s < 2; ++s) {
+        double vp = (s == 0 ? 1.0 : -1.0) * probe;
+        int vc = (int)floor((vp - vg.left) / dv);
+        vc = min(max(vc, 0), vg.cells - 1);
+        double xi = (vp - (vg.left + vc * vg.dx)) / dv;
+        double val = 0.0;
+#pragma unroll
+        for (int vn = 0; vn < P; ++vn)
+            val += lagrange<P>(a.basis, vn, xi) * f[((long long)vc * P + vn) * a.ld + xd];
+        if (fabs(val) >= a.tol) fail = true;
+    }
+    if (fail) a.st->shrink_flag[sp] = 0;
+}
+
+// build_v_transfer (adaptivity.cpp:52-90): one thread per new cell
+template <int P>
+__global__ void shrink_table_kernel(const __grid_constant__ ShrinkArgs a) {
+    const int sp = blockIdx.y;
+    if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= a.nv) return;
+    const DevVGrid ov = *a.vg[sp];
+    const double vmax_before = ov.left + ov.cells * ov.dx;
+    const double new_vmax = vmax_before * (1.0 - a.p);
+    const double nleft = -new_vmax;
+    const double ndx = (new_vmax - (-new_vmax)) / a.nv;  // Grid1D::uniform (grid.cpp:31-34)
+    const double old_dx = ov.dx;
+    const double aa = nleft + j * ndx;
+    const double h = ndx;
+    const double bb = aa + h;
+    int i0 = (int)floor((aa - ov.left) / old_dx);
+    i0 = min(max(i0, 0), ov.cells - 1);
+    int np = 0;
+    double* T = a.ttab[sp] + (long long)j * 4 * P * P;
+    int* cellv = a.tcell[sp] + (long long)j * 4;
+    for (int i = i0; i < ov.cells; ++i) {
+        double oa = ov.left + i * ov.dx, ob = oa + old_dx;
+        double s0 = dmax2(aa, oa), s1 = dmin2(bb, ob);
+        if (s1 <= s0) {
+            if (oa >= bb) break;
+            continue;
+        }
+        if (np >= 4) {
+            raise_error(a.st, 1, 4, np, 4, a.st->step);
+            break;
+        }
+        double Tm[P * P];
+#pragma unroll
+        for (int t = 0; t < P * P; ++t) Tm[t] = 0.0;
+        const double len = s1 - s0;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            double x = s0 + len * a.basis.nodes[q];
+            double xi_src = (x - oa) / old_dx;
+            double xi_tgt = (x - aa) / h;
+            double wq = a.basis.weights[q] * len;
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                double lm = lagrange<P>(a.basis, m, xi_tgt) / (a.basis.weights[m] * h);
+#pragma unroll
+                for (int n = 0; n < P; ++n) Tm[m * P + n] += wq * lm * lagrange<P>(a.basis, n, xi_src);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < P * P; ++t) T[np * P * P + t] = Tm[t];
+        cellv[np] = i;
+        ++np;
+    }
+    for (int q = np; q < 4; ++q) cellv[q] = -1;
+}
+
+// per x dof, new cell j: dst[m] = sum_pieces (sum_n T[m][n] src[n]) (adaptivity.cpp:109-124)
+template <int P>
+__global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
+    const int sp = blockIdx.z;
+    if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xd >= a.nxd) return;
+    const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
+    const double* f = a.f[sp];
+    double* out = a.out[sp];
+    for (int j = j0; j < j1; ++j) {
+        double dst[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) dst[m] = 0.0;
+        const double* T = a.ttab[sp] + (long long)j * 4 * P * P;
+        const int* cellv = a.tcell[sp] + (long long)j * 4;
+        for (int pc = 0; pc < 4; ++pc) {
+            const int oc = cellv[pc];
+            if (oc < 0) break;
+            double src[P];
+#pragma unroll
+            for (int n = 0; n < P; ++n) src[n] = f[((long long)oc * P + n) * a.ld + xd];
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < P; ++n) acc += T[pc * P * P + m * P + n] * src[n];
+                dst[m] += acc;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = dst[m];
+    }
+}
+
+// copy the projection back and commit the new v grid (field.cpp:96-101)
+__global__ void shrink_commit_kernel(const __grid_constant__ ShrinkArgs a, long long total) {
+    const int sp = blockIdx.y;
+    if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const double2* s2 = reinterpret_cast<const double2*>(a.out[sp]);
+    double2* d2 = reinterpret_cast<double2*>(a.f[sp]);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total / 2; i += stride)
+        d2[i] = s2[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (total & 1) a.f[sp][total - 1] = a.out[sp][total - 1];
+    }
+}
+
+__global__ void shrink_finalize_kernel(const __grid_constant__ ShrinkArgs a) {
+    const int sp = threadIdx.x;
+    if (sp >= 2 || !((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
+    DevVGrid ov = *a.vg[sp];
+    const double vmax_before = ov.left + ov.cells * ov.dx;
+    const double new_vmax = vmax_before * (1.0 - a.p);
+    a.vg[sp]->left = -new_vmax;
+    a.vg[sp]->dx = (new_vmax - (-new_vmax)) / a.nv;
+    a.st->vmax_before[sp] = vmax_before;
+    a.st->last_shrink[sp] = a.st->step;
+    a.st->shrink_count[sp] += 1;
+}
+
+__global__ void shrink_force_kernel(DevStatus* st, int mask) {
+    for (int sp = 0; sp < 2; ++sp) st->shrink_flag[sp] = (mask >> sp) & 1;
+}
+
+// ---------------------------------------------------------------------------
+// K8: diagnostics (field.cpp:52-88 + harness moments), deterministic
+// ---------------------------------------------------------------------------
+constexpr int kDiagBlocks = 592;
+constexpr int kDiagThreads = 256;
+
+template <int P>
+__global__ void __launch_bounds__(kDiagThreads) diag_partial_kernel(const __grid_constant__ DiagArgs a) {
+    const DevVGrid vg = a.vg[0];
+    const long long total = (long long)a.nrows * a.nxd;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int r = (int)(i / a.nxd);
+        const int xd = (int)(i - (long long)r * a.nxd);
+        const int vc = r / P, vn = r - (r / P) * P;
+        const int xc = xd / P, xn = xd - (xd / P) * P;
+        int b = 0;
+        while (xc >= a.grid.start[b + 1]) ++b;
+        const double wv = a.basis.weights[vn] * vg.dx;
+        const double w = wv * a.basis.weights[xn] * a.grid.dx[b];
+        const double v = (vg.left + vc * vg.dx) + vg.dx * a.basis.nodes[vn];
+        const double f = a.f[(long long)r * a.ld + xd];
+        s[0] += w * f;
+        s[1] += w * f * f;
+        s[2] += w * (v * f);
+        s[3] += w * ((0.5 * v * v) * f);
+    }
+    __shared__ double red[4][kDiagThreads];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = s[q];
+    __syncthreads();
+    for (int w = kDiagThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) a.partial[blockIdx.x * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void diag_final_kernel(const double* partial, int nblk, double* out) {
+    const int q = threadIdx.x;
+    if (q >= 4) return;
+    double acc = 0.0;
+    for (int b = 0; b < nblk; ++b) acc += partial[b * 4 + q];
+    out[q] = q == 1 ? sqrt(acc) : acc;
+}
+
+__global__ void fill_separable_kernel(double* f, const double* gx, const double* gv, long long ld,
+                                      long long total) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const long long r = i / ld;
+        const long long xd = i - r * ld;
+        f[i] = gx[xd] * gv[r];  // run.cpp:19-22: (c*exp(x-part))*exp(v-part)
+    }
+}
+
+__global__ void copy_kernel(double* dst, const double* src, long long n) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// K3: literature post-limiters (limiters.cpp:254-345). Flags from pre-pass data
+// (out of place). X: tiles with a 1-cell halo (block ghosts via fill_ghost j=1).
+// ---------------------------------------------------------------------------
+template <int P>
+__device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, const double* um,
+                                          const double* u0, const double* up) {
+    return cfg.indicator == 1 ? indicator_minmod<P>(b, um, u0, up)
+                              : indicator_meanerr<P>(b, um, u0, up, cfg.threshold);
+}
+
+template <int P>
+__device__ __forceinline__ void post_modify(const PostCfg& cfg, const Basis& b, const double* um,
+                                            const double* u0, const double* up, double* out) {
+    if (cfg.modifier == 1)
+        modify_simple_weno<P>(b, um, u0, up, cfg, out);
+    else
+        modify_line_weno<P>(b, um, u0, up, cfg, out);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant__ PostArgs a) {
+    constexpr int T = kXThreads;
+    constexpr int W = xs_stride<P, T>();
+    __shared__ double win[P * W];
+    const int line = blockIdx.x;
+    const int sp = a.species0 + blockIdx.z;
+    const int tile = blockIdx.y;
+    const Grid& g = a.grid;
+    int b = 0;
+    while (tile >= a.tile_start[b + 1]) ++b;
+    const int cells_b = g.cells[b];
+    const int c0 = (tile - a.tile_start[b]) * T;
+    const int nt = min(T, cells_b - c0);
+    const long long lb = (long long)line * g.ncells * P;
+    const double* src = a.src[sp] + lb;
+    const long long gbase = (long long)g.start[b] * P;
+    for (int e = threadIdx.x; e < (nt + 2) * P; e += T) {
+        const int wc = e / P, n = e - (e / P) * P;
+        const int s = c0 - 1 + wc;
+        double v;
+        if (s >= 0 && s < cells_b) {
+            v = src[gbase + (long long)s * P + n];
+        } else if (a.periodic) {
+            int ss = ((s % cells_b) + cells_b) % cells_b;
+            v = src[gbase + (long long)ss * P + n];
+        } else {
+            v = x_fetch_outside<P>(a.basis, g, src, b, s, n);
+        }
+        win[n * W + wc] = v;
+    }
+    __syncthreads();
+    const int c = threadIdx.x;
+    unsigned flagged = 0;
+    if (c < nt) {
+        double um[P], u0[P], up[P], o[P];
+#pragma unroll
+        for (int n = 0; n < P; ++n) {
+            um[n] = win[n * W + c];
+            u0[n] = win[n * W + c + 1];
+            up[n] = win[n * W + c + 2];
+        }
+        if (post_flag<P>(a.cfg, a.basis, um, u0, up)) {
+            flagged = 1;
+            post_modify<P>(a.cfg, a.basis, um, u0, up, o);
+        } else {
+#pragma unroll
+            for (int n = 0; n < P; ++n) o[n] = u0[n];
+        }
+        double* dst = a.dst[sp] + lb + gbase + (long long)(c0 + c) * P;
+#pragma unroll
+        for (int n = 0; n < P; ++n) dst[n] = o[n];
+    }
+    unsigned tot = __reduce_add_sync(0xffffffffu, flagged);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&a.st->stats[sp][3], (unsigned long long)tot);
+    if (threadIdx.x == 0) atomicAdd(&a.st->post_checked[sp], (unsigned long long)nt);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant__ PostArgs a) {
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    const int sp = a.species0 + blockIdx.z;
+    const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
+    unsigned flagged = 0;
+    if (xd < a.nxd) {
+        const double* f = a.src[sp];
+        double* out = a.dst[sp];
+        double um[P], u0[P], up[P];
+        vload<P>(f, a.ld, xd, j0 - 1, 0, a.nv, a.periodic, a.nv, um);
+        vload<P>(f, a.ld, xd, j0, 0, a.nv, a.periodic, a.nv, u0);
+        for (int j = j0; j < j1; ++j) {
+            vload<P>(f, a.ld, xd, j + 1, 0, a.nv, a.periodic, a.nv, up);
+            double o[P];
+            if (post_flag<P>(a.cfg, a.basis, um, u0, up)) {
+                ++flagged;
+                post_modify<P>(a.cfg, a.basis, um, u0, up, o);
+            } else {
+#pragma unroll
+                for (int n = 0; n < P; ++n) o[n] = u0[n];
+            }
+#pragma unroll
+            for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = o[m];
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                um[n] = u0[n];
+                u0[n] = up[n];
+            }
+        }
+    }
+    unsigned tot = __reduce_add_sync(0xffffffffu, flagged);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&a.st->stats[sp][3], (unsigned long long)tot);
+}
+
+__global__ void post_v_count_kernel(DevStatus* st, int mask, unsigned long long per_species) {
+    for (int sp = 0; sp < 2; ++sp)
+        if ((mask >> sp) & 1) st->post_checked[sp] += per_species;
+}
+
+}  // namespace
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+#define SK_DISPATCH_P(P_, CALL)                               \
+    switch (P_) {                                             \
+        case 1: { constexpr int PP = 1; CALL; } break;        \
+        case 2: { constexpr int PP = 2; CALL; } break;        \
+        case 3: { constexpr int PP = 3; CALL; } break;        \
+        case 4: { constexpr int PP = 4; CALL; } break;        \
+        case 5: { constexpr int PP = 5; CALL; } break;        \
+        case 6: { constexpr int PP = 6; CALL; } break;        \
+        case 7: { constexpr int PP = 7; CALL; } break;        \
+        default: return cudaErrorInvalidValue;                \
+    }
+
+cudaError_t launch_xtab(const XTabArgs& a, cudaStream_t s) {
+    dim3 grid((a.nlines + 127) / 128, a.nspecies);
+    SK_DISPATCH_P(a.basis.p, (xtab_kernel<PP><<<grid, 128, 0, s>>>(a)));
+    return cudaGetLastError();
+}
+
+template <int P, int CPT>
+static cudaError_t launch_xsweep_t(const XSweepArgs& a, int ntiles, cudaStream_t s) {
+    constexpr int T = kXThreads * CPT;
+    const size_t smem = sizeof(double) * 2 * P * xs_stride<P, T>();
+    static unsigned configured = 0;  // per-device bit
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(configured & (1u << (dev & 31)))) {
+        cudaFuncSetAttribute(xsweep_kernel<P, CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        configured |= 1u << (dev & 31);
+    }
+    dim3 grid(a.nlines, ntiles, a.nspecies);
+    xsweep_kernel<P, CPT><<<grid, kXThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xsweep(const XSweepArgs& a, int ntiles, cudaStream_t s) {
+    SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, 2>(a, ntiles, s)));
+    return cudaSuccess;
+}
+
+cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s) {
+    dim3 grid((a.nxd + 127) / 128, a.nspecies);
+    SK_DISPATCH_P(a.basis.p, (vtab_kernel<PP><<<grid, 128, 0, s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
+    dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.n + kVChunk - 1) / kVChunk, a.nspecies);
+    SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP><<<grid, kVThreads, 0, s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rho(const RhoArgs& a, int nspecies, cudaStream_t s) {
+    dim3 grid((a.nxd + 127) / 128, a.nchunks, nspecies);
+    SK_DISPATCH_P(a.basis.p, (rho_partial_kernel<PP><<<grid, 128, 0, s>>>(a)));
+    rho_reduce_kernel<<<(a.nxd + 127) / 128, 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
+                           cudaStream_t s) {
+    poisson_kernel<<<1, 1024, 0, s>>>(pd, rho, E, phi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_step_end(DevStatus* st, int v_adjust, long long cooldown, int mask,
+                            cudaStream_t s) {
+    step_end_kernel<<<1, 1, 0, s>>>(st, v_adjust, cooldown, mask);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s) {
+    const int P = a.basis.p;
+    // force: 0 = run() cadence (flags from step_end), -1 = check only, 1 = shrink unchecked
+    if (a.force) shrink_force_kernel<<<1, 1, 0, s>>>(a.st, a.species_mask);
+    if (a.force != 1)
+        SK_DISPATCH_P(P, (shrink_check_kernel<PP><<<dim3((a.nxd + 255) / 256, 2), 256, 0, s>>>(a)));
+    if (a.force < 0) return cudaGetLastError();
+    SK_DISPATCH_P(P, (shrink_table_kernel<PP><<<dim3((a.nv + 127) / 128, 2), 128, 0, s>>>(a)));
+    SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3((a.nxd + 127) / 128, (a.nv + kVChunk - 1) / kVChunk, 2), 128, 0, s>>>(a)));
+    const long long total = (long long)a.nv * P * a.nxd;
+    shrink_commit_kernel<<<dim3(1184, 2), 256, 0, s>>>(a, total);
+    shrink_finalize_kernel<<<1, 32, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_diag(const DiagArgs& a, double* out4, double* partial, cudaStream_t s) {
+    DiagArgs b = a;
+    b.partial = partial;
+    SK_DISPATCH_P(a.basis.p, (diag_partial_kernel<PP><<<kDiagBlocks, kDiagThreads, 0, s>>>(b)));
+    diag_final_kernel<<<1, 32, 0, s>>>(partial, kDiagBlocks, out4);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_separable(double* f, const double* gx, const double* gv, long long ld,
+                                  int nrows, cudaStream_t s) {
+    fill_separable_kernel<<<1184, 256, 0, s>>>(f, gx, gv, ld, (long long)nrows * ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s) {
+    dim3 grid(a.nrows, ntiles, a.nspecies);
+    SK_DISPATCH_P(a.basis.p, (post_x_kernel<PP><<<grid, kXThreads, 0, s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s) {
+    dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
+    SK_DISPATCH_P(a.basis.p, (post_v_kernel<PP><<<grid, kVThreads, 0, s>>>(a)));
+    int mask = 0;
+    for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
+    post_v_count_kernel<<<1, 1, 0, s>>>(a.st, mask, (unsigned long long)a.nv * a.nxd);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale_copy(double* dst, const double* src, size_t n, cudaStream_t s) {
+    copy_kernel<<<1184, 256, 0, s>>>(dst, src, (long long)n);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

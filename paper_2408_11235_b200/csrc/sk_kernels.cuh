@@ -1,0 +1,169 @@
+// sk_kernels.cuh -- kernel parameter blocks and launchers (sk_kernels.cu).
+#pragma once
+
+#include "sk_internal.hpp"
+
+namespace sk {
+
+constexpr int kXThreads = 256;  // x sweep CTA
+constexpr int kVThreads = 128;  // v sweep CTA (one thread per x dof)
+constexpr int kVChunk = 32;     // v cells per v-sweep thread
+
+inline int xtab_nf(int P) { return ((2 + 2 * P * P + 2 * P) + 1) & ~1; }  // AoS row, 16B aligned
+inline int vtab_nf(int P) { return 2 + 2 * P * P + 2 * P; }
+
+// Per-line shift tables (make_plan, advection.cpp:132-140) for the x sweep.
+struct XTabArgs {
+    Basis basis;
+    Grid grid;
+    const DevVGrid* vg[2];  // per species
+    DevStatus* st;
+    double* tab[2];      // [nclass][nlines][nf]
+    double sqrt_mu[2];
+    double tau;
+    int nlines;          // nv * P
+    int nspecies;
+    int species0;        // first species index handled
+    int inline_sldg;
+    double threshold;
+    int max_ghost;       // >=0 explicit, -1 no check, -2 run() rule from dt_auto
+    double dt_auto;
+    long long step_index;  // <0: use st->step
+};
+
+struct XSweepArgs {
+    Basis basis;
+    Grid grid;
+    DevStatus* st;
+    const double* src[2];
+    double* dst[2];
+    const double* tab[2];
+    int nlines;
+    int nspecies;
+    int species0;
+    int tile_start[kMaxBlocks + 1];  // tiles per block (prefix)
+    int inline_sldg;
+    int periodic;
+    int check_finite;
+    double threshold;
+};
+
+struct VTabArgs {
+    Basis basis;
+    const DevVGrid* vg[2];
+    double* tab[2];      // SoA [nf][nxd]
+    const double* E;
+    double charge[2];
+    double sqrt_mu[2];
+    double tau;
+    int nxd;
+    int nspecies;
+    int species0;
+    int inline_sldg;
+    double threshold;
+};
+
+struct VSweepArgs {
+    Basis basis;
+    DevStatus* st;
+    const double* src[2];  // points at local cell 0 (halo rows before/after)
+    double* dst[2];
+    const double* tab[2];
+    long long ld;          // row stride (nx * P)
+    int nxd;
+    int n;                 // local v cells written
+    int gl, gr;            // halo cells readable below / above
+    int nspecies;
+    int species0;
+    int inline_sldg;
+    int periodic;
+    int check_finite;
+    double threshold;
+};
+
+struct RhoArgs {
+    Basis basis;
+    const DevVGrid* vg[2];
+    const double* f[2];
+    double* partial;       // [2][nchunks][nxd]
+    double* rho;
+    long long ld;
+    int nxd;
+    int nrows;             // local v rows (cells*P)
+    int nchunks;
+    int rows_per_chunk;
+};
+
+struct PoissonDev {
+    int k, ps, ncells, nlevels;
+    int level_n[32];
+    long long level_off[32];
+    const double *Dinv, *Lo, *Up, *Alpha, *Gamma, *interp, *deriv, *h, *ws;
+    double *bws, *xws;     // [sum level_n * ps]
+};
+
+struct ShrinkArgs {
+    Basis basis;
+    DevStatus* st;
+    DevVGrid* vg[2];
+    double* f[2];
+    double* out[2];
+    double* ttab[2];       // [nv][4 pieces][P*P]
+    int* tcell[2];         // [nv][4]
+    long long ld;
+    int nxd;
+    int nv;
+    int species_mask;      // which species to consider
+    int v_adjust;
+    int force;             // 1: bypass check/cooldown (standalone shrink)
+    double p, gamma, tol;
+    long long cooldown;
+};
+
+struct DiagArgs {
+    Basis basis;
+    Grid grid;
+    const DevVGrid* vg;
+    const double* f;
+    double* partial;       // [nblk][4]
+    long long ld;
+    int nxd;
+    int nrows;
+};
+
+struct PostArgs {
+    Basis basis;
+    Grid grid;
+    DevStatus* st;
+    const double* src[2];
+    double* dst[2];
+    PostCfg cfg;
+    long long ld;
+    int nxd;
+    int nrows;             // v rows
+    int nv;
+    int nspecies;
+    int species0;
+    int periodic;
+    int tile_start[kMaxBlocks + 1];
+};
+
+// launchers (P = k+1 dispatch inside)
+cudaError_t launch_xtab(const XTabArgs& a, cudaStream_t s);
+cudaError_t launch_xsweep(const XSweepArgs& a, int ntiles, cudaStream_t s);
+cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s);
+cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s);
+cudaError_t launch_rho(const RhoArgs& a, int nspecies_mask, cudaStream_t s);
+cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
+                           cudaStream_t s);
+cudaError_t launch_step_end(DevStatus* st, int v_adjust, long long cooldown, int species_mask,
+                            cudaStream_t s);
+cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s);
+cudaError_t launch_diag(const DiagArgs& a, double* out4, double* partial, cudaStream_t s);
+cudaError_t launch_fill_separable(double* f, const double* gx, const double* gv, long long ld,
+                                  int nrows, cudaStream_t s);
+cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s);
+cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s);
+cudaError_t launch_scale_copy(double* dst, const double* src, size_t n, cudaStream_t s);
+
+}  // namespace sk

@@ -1,0 +1,416 @@
+// sk_numerics.cuh -- per-cell sLdG arithmetic for sm_100a (device + host).
+//
+// Every function keeps the reference's floating-point operation order so the
+// kernels (compiled with -fmad=false, see build.py) reproduce the reference
+// bit for bit given the same inputs:
+//   lagrange / evaluate / mean / moments / extrema   core/src/basis.cpp:102-225
+//   decompose_shift / shift matrices                 core/src/advection.cpp:14-66
+//   inline sLdG limiter                              core/src/limiters.cpp:167-222
+//   post-limiter indicators / WENO modifiers         core/src/limiters.cpp:47-165
+//   coarse<->fine transfer                           core/src/adaptivity.cpp:132-156
+// P = k+1 is a template parameter so every loop unrolls into registers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+
+#define SK_HD __host__ __device__ __forceinline__
+#define SK_MAXP 8
+
+namespace sk {
+
+// Reference-cell constants, computed once on the host with the reference's
+// formulas (sk_host.cpp) and passed by value in kernel parameter space.
+struct Basis {
+    int k, p;
+    double nodes[SK_MAXP];
+    double weights[SK_MAXP];
+    double bary[SK_MAXP];
+    double mono[SK_MAXP * SK_MAXP];  // nodal -> monomial, row-major [d][n]
+    double diff[SK_MAXP * SK_MAXP];  // nodal differentiation [m][n]
+    double cheb[33];                 // cos(pi(2j+1)/66), basis.cpp:211 (k > 3)
+};
+
+SK_HD double dmax2(double a, double b) { return (a < b) ? b : a; }  // std::max
+SK_HD double dmin2(double a, double b) { return (b < a) ? b : a; }  // std::min
+
+// basis.cpp:102-108
+template <int P>
+SK_HD double lagrange(const Basis& b, int n, double xi) {
+    double v = b.bary[n];
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+        if (j != n) v *= (xi - b.nodes[j]);
+    return v;
+}
+
+// basis.cpp:123-134 (second barycentric form, exact at nodes)
+template <int P>
+SK_HD double evaluate(const Basis& b, const double* u, double xi) {
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        if (xi == b.nodes[n]) return u[n];
+        double t = b.bary[n] / (xi - b.nodes[n]);
+        num += t * u[n];
+        den += t;
+    }
+    return num / den;
+}
+
+// basis.cpp:136-140
+template <int P>
+SK_HD double mean(const Basis& b, const double* u) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) acc += b.weights[j] * u[j];
+    return acc;
+}
+
+// basis.cpp:142-150
+template <int P>
+SK_HD double integrate(const Basis& b, const double* u, double a, double bb) {
+    double acc = 0.0;
+    const double len = bb - a;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        double xi = a + len * b.nodes[q];
+        acc += b.weights[q] * evaluate<P>(b, u, xi);
+    }
+    return acc * len;
+}
+
+// basis.cpp:152-161
+template <int P>
+SK_HD void interval_moments(const Basis& b, double a, double bb, double* m) {
+    const double len = bb - a;
+#pragma unroll
+    for (int n = 0; n < P; ++n) m[n] = 0.0;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        double xi = a + len * b.nodes[q];
+#pragma unroll
+        for (int n = 0; n < P; ++n) m[n] += b.weights[q] * len * lagrange<P>(b, n, xi);
+    }
+}
+
+// basis.cpp:172-215 extremum_on; IS_MAX selects the comparison.
+template <int P, bool IS_MAX>
+SK_HD bool better(double x, double y) { return IS_MAX ? (x > y) : (x < y); }
+
+template <int P, bool IS_MAX>
+SK_HD double extremum_on(const Basis& b, const double* u, double a, double bb) {
+    double best = evaluate<P>(b, u, a);
+    if (bb == a) return best;
+    double vb = evaluate<P>(b, u, bb);
+    if (better<P, IS_MAX>(vb, best)) best = vb;
+    if constexpr (P <= 2) {
+        return best;
+    } else if constexpr (P <= 4) {
+        double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int d = 0; d < P; ++d) {  // basis.cpp:163-170 to_monomial
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < P; ++n) acc += b.mono[d * P + n] * u[n];
+            c[d] = acc;
+        }
+        double qa = 3.0 * c[3], qb = 2.0 * c[2], qc = c[1];
+        double x0 = 0.0, x1 = 0.0;
+        int nc = 0;
+        if (fabs(qa) > 0.0) {
+            double disc = qb * qb - 4.0 * qa * qc;
+            if (disc >= 0.0) {
+                double r = sqrt(disc);
+                x0 = (-qb + r) / (2.0 * qa);
+                x1 = (-qb - r) / (2.0 * qa);
+                nc = 2;
+            }
+        } else if (fabs(qb) > 0.0) {
+            x0 = -qc / qb;
+            nc = 1;
+        }
+        if (nc >= 1 && x0 > a && x0 < bb) {
+            double v = evaluate<P>(b, u, x0);
+            if (better<P, IS_MAX>(v, best)) best = v;
+        }
+        if (nc >= 2 && x1 > a && x1 < bb) {
+            double v = evaluate<P>(b, u, x1);
+            if (better<P, IS_MAX>(v, best)) best = v;
+        }
+        return best;
+    } else {
+        for (int j = 0; j < 33; ++j) {
+            double x = 0.5 * (a + bb) + 0.5 * (bb - a) * b.cheb[j];
+            double v = evaluate<P>(b, u, x);
+            if (better<P, IS_MAX>(v, best)) best = v;
+        }
+        return best;
+    }
+}
+
+// advection.cpp:14-25
+SK_HD void decompose_shift(double speed, double dt, double dx, int& istar, double& alpha) {
+    double s = -speed * dt / dx;
+    double fl = floor(s);
+    double al = s - fl;
+    int is = (int)fl;
+    if (al >= 1.0) {
+        al -= 1.0;
+        is += 1;
+    }
+    istar = is;
+    alpha = al;
+}
+
+// advection.cpp:27-66 (alpha in [0,1) by construction of decompose_shift)
+template <int P>
+SK_HD void shift_matrices(const Basis& b, double alpha, double* A, double* B) {
+#pragma unroll
+    for (int i = 0; i < P * P; ++i) {
+        A[i] = 0.0;
+        B[i] = 0.0;
+    }
+    const double len_a = 1.0 - alpha;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        double xi = len_a * b.nodes[q];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            double lm = lagrange<P>(b, m, xi);
+#pragma unroll
+            for (int n = 0; n < P; ++n)
+                A[m * P + n] += b.weights[q] * len_a * lagrange<P>(b, n, xi + alpha) * lm;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        double xi = 1.0 - alpha + alpha * b.nodes[q];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            double lm = lagrange<P>(b, m, xi);
+#pragma unroll
+            for (int n = 0; n < P; ++n)
+                B[m * P + n] += b.weights[q] * alpha * lagrange<P>(b, n, alpha * b.nodes[q]) * lm;
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        double inv_w = 1.0 / b.weights[m];
+#pragma unroll
+        for (int n = 0; n < P; ++n) {
+            A[m * P + n] *= inv_w;
+            B[m * P + n] *= inv_w;
+        }
+    }
+}
+
+// advection.cpp:95-101: acc += A*ul + B*ur, j ascending
+template <int P>
+SK_HD void project_cell(const double* A, const double* B, const double* ul, const double* ur,
+                        double* o) {
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) acc += A[m * P + j] * ul[j] + B[m * P + j] * ur[j];
+        o[m] = acc;
+    }
+}
+
+// Inline sLdG limiter, limiters.cpp:175-222. Returns flags:
+// bit0 troubled, bit1 clamped, bit2 mean_outside. `up` is modified in place.
+template <int P>
+SK_HD int inline_limit(const Basis& b, double alpha, double threshold, const double* ext_l,
+                       const double* ext_r, const double* ul, const double* ur, double* up) {
+    double mean_l = mean<P>(b, ul);
+    double mean_r = mean<P>(b, ur);
+    double denom = dmax2(fabs(mean_l), fabs(mean_r));
+    if (denom <= 0.0) return 0;
+    double el = 0.0, er = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        el += ext_l[n] * up[n];
+        er += ext_r[n] * up[n];
+    }
+    double ind = (fabs(el - mean_l) + fabs(er - mean_r)) / denom;
+    if (!(ind > threshold)) return 0;
+    // clamp (limiters.cpp:191-215)
+    int flags = 1;
+    double mean_p = mean<P>(b, up);
+    double wmax = dmax2(extremum_on<P, true>(b, ul, alpha, 1.0), extremum_on<P, true>(b, ur, 0.0, alpha));
+    double wmin = dmin2(extremum_on<P, false>(b, ul, alpha, 1.0), extremum_on<P, false>(b, ur, 0.0, alpha));
+    double pmax = extremum_on<P, true>(b, up, 0.0, 1.0);
+    double pmin = extremum_on<P, false>(b, up, 0.0, 1.0);
+    if ((mean_p > wmax) || (mean_p < wmin)) flags |= 4;
+    double theta = 1.0;
+    double dmx = pmax - mean_p;
+    if (dmx != 0.0) theta = dmin2(theta, fabs((wmax - mean_p) / dmx));
+    double dmn = pmin - mean_p;
+    if (dmn != 0.0) theta = dmin2(theta, fabs((wmin - mean_p) / dmn));
+    if (theta < 1.0) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) up[j] = theta * (up[j] - mean_p) + mean_p;
+        flags |= 2;
+    }
+    return flags;
+}
+
+// ---------------- post limiters (limiters.cpp:47-165) ----------------
+SK_HD double minmod(double a, double b, double c) {
+    if (a > 0 && b > 0 && c > 0) return dmin2(a, dmin2(b, c));
+    if (a < 0 && b < 0 && c < 0) return -dmin2(-a, dmin2(-b, -c));
+    return 0.0;
+}
+
+template <int P>
+SK_HD bool indicator_minmod(const Basis& b, const double* um, const double* u0, const double* up) {
+    double mean_m = mean<P>(b, um);
+    double mean_0 = mean<P>(b, u0);
+    double mean_p = mean<P>(b, up);
+    double u0_plus = evaluate<P>(b, u0, 1.0) - mean_0;
+    double u0_minus = mean_0 - evaluate<P>(b, u0, 0.0);
+    double d_plus = mean_p - mean_0;
+    double d_minus = mean_0 - mean_m;
+    double scale = fabs(mean_m);
+    double v;
+    v = fabs(mean_0); if (scale < v) scale = v;
+    v = fabs(mean_p); if (scale < v) scale = v;
+    v = fabs(u0_plus); if (scale < v) scale = v;
+    v = fabs(u0_minus); if (scale < v) scale = v;
+    v = fabs(d_plus); if (scale < v) scale = v;
+    v = fabs(d_minus); if (scale < v) scale = v;
+    double guard = 1e-13 * scale;
+    return fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard ||
+           fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard;
+}
+
+template <int P>
+SK_HD bool indicator_meanerr(const Basis& b, const double* um, const double* u0, const double* up,
+                             double threshold) {
+    double mean_m = mean<P>(b, um);
+    double mean_0 = mean<P>(b, u0);
+    double mean_p = mean<P>(b, up);
+    double denom = dmax2(fabs(mean_m), dmax2(fabs(mean_0), fabs(mean_p)));
+    if (denom <= 0.0) return false;
+    double ext_m = integrate<P>(b, um, 1.0, 2.0);
+    double ext_p = integrate<P>(b, up, -1.0, 0.0);
+    double ind = (fabs(ext_m - mean_0) + fabs(ext_p - mean_0)) / denom;
+    return ind > threshold;
+}
+
+template <int P>
+SK_HD double smoothness_beta(const Basis& b, const double* u) {
+    double cur[P], nxt[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) cur[i] = u[i];
+    double total = 0.0;
+#pragma unroll
+    for (int s = 1; s < P; ++s) {
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < P; ++n) acc += b.diff[m * P + n] * cur[n];
+            nxt[m] = acc;
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) total += b.weights[q] * nxt[q] * nxt[q];
+#pragma unroll
+        for (int i = 0; i < P; ++i) cur[i] = nxt[i];
+    }
+    return total;
+}
+
+struct PostCfg {
+    int indicator;  // 1 minmod, 2 meanerr
+    int modifier;   // 1 simple WENO, 2 line WENO
+    double threshold;
+    double gamma_simple[3];
+    double gamma_line[3];
+    double epsilon;
+};
+
+template <int P>
+SK_HD void modify_simple_weno(const Basis& b, const double* um, const double* u0, const double* up,
+                              const PostCfg& cfg, double* out) {
+    double beta_m = smoothness_beta<P>(b, um);
+    double beta_0 = smoothness_beta<P>(b, u0);
+    double beta_p = smoothness_beta<P>(b, up);
+    const double eps = cfg.epsilon;
+    double wm = cfg.gamma_simple[0] / ((eps + beta_m) * (eps + beta_m));
+    double w0 = cfg.gamma_simple[1] / ((eps + beta_0) * (eps + beta_0));
+    double wp = cfg.gamma_simple[2] / ((eps + beta_p) * (eps + beta_p));
+    double sum = wm + w0 + wp;
+    wm /= sum;
+    w0 /= sum;
+    wp /= sum;
+    double mean_0 = mean<P>(b, u0);
+    double ext_mean_m = integrate<P>(b, um, 1.0, 2.0);
+    double ext_mean_p = integrate<P>(b, up, -1.0, 0.0);
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        double xi = b.nodes[m];
+        double cand_m = evaluate<P>(b, um, 1.0 + xi) - ext_mean_m + mean_0;
+        double cand_p = evaluate<P>(b, up, xi - 1.0) - ext_mean_p + mean_0;
+        out[m] = wm * cand_m + w0 * u0[m] + wp * cand_p;
+    }
+}
+
+template <int P>
+SK_HD void modify_line_weno(const Basis& b, const double* um, const double* u0, const double* up,
+                            const PostCfg& cfg, double* out) {
+    double mean_m = mean<P>(b, um);
+    double mean_0 = mean<P>(b, u0);
+    double mean_p = mean<P>(b, up);
+    double bm = mean_0 - mean_m, am = mean_0 - 0.5 * bm;
+    double bp = mean_p - mean_0, ap = mean_0 - 0.5 * bp;
+    const double gm = cfg.gamma_line[0], g0 = cfg.gamma_line[1], gp = cfg.gamma_line[2];
+    double pm[P], pp[P], p0[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        double xi = b.nodes[m];
+        pm[m] = am + bm * xi;
+        pp[m] = ap + bp * xi;
+        p0[m] = (u0[m] - gm * pm[m] - gp * pp[m]) / g0;
+    }
+    double beta_m = smoothness_beta<P>(b, um);
+    double beta_0 = smoothness_beta<P>(b, u0);
+    double beta_p = smoothness_beta<P>(b, up);
+    double tau = 0.5 * (fabs(beta_0 - beta_m) + fabs(beta_0 - beta_p));
+    tau *= tau;
+    const double eps = cfg.epsilon;
+    double wm = gm * (1.0 + tau / (eps + beta_m));
+    double w0 = g0 * (1.0 + tau / (eps + beta_0));
+    double wp = gp * (1.0 + tau / (eps + beta_p));
+    double sum = wm + w0 + wp;
+    wm /= sum;
+    w0 /= sum;
+    wp /= sum;
+#pragma unroll
+    for (int m = 0; m < P; ++m) out[m] = wm * pm[m] + w0 * p0[m] + wp * pp[m];
+}
+
+// ---------------- sheath-mesh transfer (adaptivity.cpp:132-156) ----------------
+// coarse_to_fine, one piece, one node: evaluate(coarse, (piece + x_q)/m)
+template <int P>
+SK_HD double coarse_to_fine_node(const Basis& b, const double* coarse, int m, int piece, int q) {
+    return evaluate<P>(b, coarse, (piece + b.nodes[q]) / m);
+}
+
+// fine_to_coarse, output node mm, from m consecutive fine cells (stride P)
+template <int P>
+SK_HD double fine_to_coarse_node(const Basis& b, const double* fine, int m, int mm) {
+    double acc = 0.0;
+    for (int j = 0; j < m; ++j) {
+        const double* cell = fine + j * P;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            double xi_c = (j + b.nodes[q]) / m;
+            acc += b.weights[q] / m * cell[q] * lagrange<P>(b, mm, xi_c);
+        }
+    }
+    return acc / b.weights[mm];
+}
+
+}  // namespace sk
