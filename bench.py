@@ -1,0 +1,280 @@
+#!/usr/bin/env python
+"""Benchmark: phase-space DoF updates/s of the full sLdG run() loop body.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl b200|reference]
+
+One "step" = one run() loop body (core/src/run.cpp:124-131): x half-sweep
+(+inline sLdG limiter, + 3-block transfer), charge density, Poisson solve, v
+sweep, x half-sweep, nonfinite check, velocity cut-off check (and shrink when
+it fires) for BOTH species. value = 2*(nx*p)*(nv*p)*K / device time.
+
+N == 1: the whole state on one B200. N > 1 (torchrun): the phase space is
+sharded along v (paper_2408_11235_b200.sharding), max-over-ranks device time.
+--impl reference: the reference itself (oracle/_ref, compiled from
+/root/reference) on this host's cores, same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "phase-space DoF updates/s per step (e+ion)"
+UNIT = "DoF/s"
+BYTES_PER_DOF_SWEEP = 16.0  # fp64 read + write per directional sweep
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_reference_run(cfg, steps: int, warmup: int, budget_s: float):
+    """Time the reference (oracle/_ref) on this host: returns (DoF/s, info)."""
+    import oracle
+
+    if not oracle.ref_available():
+        raise RuntimeError("oracle/_ref/libsolkin_ref.so not built")
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    t0 = time.perf_counter()
+    st = oracle.Ref().state(threads=threads, **cfg.oracle_kwargs())
+    t_init = time.perf_counter() - t0
+    tw = st.run(max(warmup, 1))
+    per_step = tw / max(warmup, 1)
+    k = max(1, min(steps, int(budget_s / max(per_step, 1e-9))))
+    t = st.run(k)
+    rate = cfg.dof_total * k / t
+    sample = (f"{cfg.nx}x{cfg.v_cells} k={cfg.k} {cfg.limiter}: {k} timed run() loop bodies "
+              f"after {max(warmup, 1)} warm-up (init {t_init:.1f}s), {threads} threads, "
+              f"{t:.2f}s timed")
+    return rate, dict(threads=threads, steps=k, seconds=t, sample=sample, timers=st.timers())
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rate, info = cpu_reference_run(cfg, args.steps, args.warmup, budget_s=args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": info["steps"],
+        "warmup": args.warmup, "ms_per_step": 1e3 * info["seconds"] / info["steps"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (blob initial condition, run.cpp:41-46)", "impl": "reference",
+        "config": config_dict(args, cfg),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": info["threads"],
+                         "kind": "reference", "sample": info["sample"]},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, cfg):
+    p = cfg.k + 1
+    return {
+        "workload": f"{args.config}: {cfg.nx}x{cfg.v_cells} cells/species, k={cfg.k}, "
+                    f"mu={cfg.mu:g}, limiter={cfg.limiter}, refinement m={cfg.refinement_ratio}, "
+                    f"v cut-off {'on' if cfg.v_adjust else 'off'}",
+        "nx": cfg.nx, "nv": cfg.v_cells, "k": cfg.k, "dof_total": cfg.dof_total,
+        "field_bytes_per_species": 8 * cfg.nx * p * cfg.v_cells * p,
+        "parallelism": f"v-shard x{args.gpus}" if args.gpus > 1 else "single GPU",
+        "l2": "inputs larger than L2 (no flush needed)"
+              if 8 * cfg.dof_total > 126e6 else "state fits in L2 (parity config)",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--limiter", default=None)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+
+    import paper_2408_11235_b200 as sk
+
+    over = {"limiter": args.limiter} if args.limiter else {}
+    cfg = sk.named_config(args.config, **over)
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_2408_11235_b200 import sharding
+
+        sharding.bench_sharded(args, cfg, METRIC, UNIT, config_dict(args, cfg))
+        return
+
+    import numpy as np
+    import torch
+
+    dev = 0
+    torch.cuda.set_device(dev)
+    st = sk.SimulationState(cfg, device=dev)
+    st.ctx.set_eager_errors(False)
+    st.run_steps(args.warmup)
+    st.ctx.synchronize()
+
+    # ---- timed region: K run() loop bodies, CUDA events on the step stream ----
+    stream = st.ctx.stream  # the library's stream: events bracket exactly its work
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.set_phase_timing(True)
+    st.phase_times()
+    launches0 = st.launches()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    st.run_steps(args.steps)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    st.ctx.synchronize()  # raises on device-side errors
+    launches = st.launches() - launches0
+    ms = t0.elapsed_time(t1)
+    phases = st.phase_times()
+    st.set_phase_timing(False)
+    value = cfg.dof_total * args.steps / (ms / 1e3)
+
+    # roofline: dominant kernel = longest phase; algorithmic bytes = 16 B per DoF
+    # swept (both species) per launch, divided by its mean event-timed duration
+    peak, peak_kind = peaks()
+    sweep_phases = {"x_sweep_1", "x_sweep_2", "v_sweep"}
+    dom = max(phases, key=lambda k: phases[k][0])
+    dom_ms, dom_n = phases[dom]
+    per_launch_ms = dom_ms / max(dom_n, 1)
+    if dom in sweep_phases or dom.startswith("post"):
+        alg_bytes = BYTES_PER_DOF_SWEEP * cfg.dof_total
+    else:
+        alg_bytes = None
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9 if alg_bytes else None
+    step_bytes = 3 * BYTES_PER_DOF_SWEEP * cfg.dof_total
+    step_gbs = step_bytes * args.steps / (ms / 1e3) / 1e9
+    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic = None
+    try:
+        with open(prof_path) as f:
+            traffic = json.load(f).get(args.config, {}).get(dom)
+    except Exception:
+        pass
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (blob initial condition, run.cpp:41-46)",
+        "config": config_dict(args, cfg),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "alg_bytes_per_launch": alg_bytes, "ms_per_launch": per_launch_ms,
+                     "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
+        "gpu_launches": launches,
+        "limiter_stats": st.stats(),
+        "clocks": clk,
+    }
+
+    # ---- e2e: the drop-in C-ABI call over pinned HOST buffers ----
+    if not args.no_e2e:
+        n = st.f_e.size
+        fe = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        fi = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        fe_np, fi_np = fe.numpy(), fi.numpy()
+        fe_np[:] = st.f_e.download()
+        fi_np[:] = st.f_i.download()
+        st.run_step_host(fe_np, fi_np)  # warm-up
+        k2 = args.e2e_steps
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(k2):
+            st.run_step_host(fe_np, fi_np)
+        w = time.perf_counter() - w0
+        line["e2e"] = {"value": cfg.dof_total * k2 / w, "unit": UNIT,
+                       "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n,
+                       "steps": k2, "api": "sk_run_step_host (include/sk_b200.h)"}
+        del fe, fi
+
+    # ---- CPU baseline: the reference on this host, bounded sample ----
+    if not args.no_cpu:
+        try:
+            rate, info = cpu_reference_run(cfg, 3, 1, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["threads"],
+                                    "kind": "reference", "sample": info["sample"]}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"not run: {e}"}
+    print(json.dumps(line), flush=True)
+    del np
+
+
+if __name__ == "__main__":
+    main()

@@ -89,7 +89,13 @@ SIGNATURES = {
     "sk_state_step_index": (_i, [_vp, _lp]),
     "sk_state_shrinks": (_i, [_vp, _i, _ip, _lp]),
     "sk_run_step_host": (_i, [_vp, _dp, _dp, _sz]),
+    "sk_state_set_phase_timing": (_i, [_vp, _i]),
+    "sk_state_phase_times": (_i, [_vp, _dp, _lp, _i]),
+    "sk_ctx_launch_count": (C.c_longlong, [_vp]),
 }
+
+PHASES = ("x_tables", "x_sweep_1", "post_x_1", "charge_density", "poisson", "v_tables",
+          "v_sweep", "post_v", "x_sweep_2", "post_x_2", "step_end_cutoff")
 
 
 def header_symbols() -> list[str]:

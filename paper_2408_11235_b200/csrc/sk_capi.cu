@@ -63,6 +63,10 @@ struct sk_ctx {
     double* diag_partial = nullptr;
     double* diag_out = nullptr;
     double* pinned = nullptr;          // small pinned readback buffer
+    long long launches = 0;            // kernels enqueued (bench gpu_launches)
+    unsigned long long* fix_list = nullptr;  // deferred limiter clamps
+    unsigned int* fix_count = nullptr;
+    unsigned int fix_cap = 0;
 };
 
 struct sk_field {
@@ -94,6 +98,13 @@ struct sk_state {
     long step_host = 0;
     cudaGraphExec_t graph2 = nullptr;  // two loop bodies
     int graph_cur0 = -1, graph_cur1 = -1;
+    long long graph_launches = 0;      // kernels per graph replay
+    // optional per-phase CUDA-event timing (sk_state_set_phase_timing)
+    bool timing = false;
+    std::vector<std::pair<int, cudaEvent_t>> marks;
+    std::vector<cudaEvent_t> pool;
+    double phase_ms[16] = {};
+    long phase_count[16] = {};
 };
 
 namespace {
@@ -184,6 +195,7 @@ sk_status enq_xtab(sk_field** fs, int nspecies, double tau, const double* sqrt_m
     a.dt_auto = dt_auto;
     a.step_index = step_index;
     CK(launch_xtab(a, c->stream));
+    c->launches += 1;
     return SK_OK;
 }
 
@@ -208,7 +220,16 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.periodic = periodic;
     a.check_finite = check_finite;
     a.threshold = threshold;
+    a.fix_list = c->fix_list;
+    a.fix_count = c->fix_count;
+    a.fix_cap = c->fix_cap;
+    if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
+    c->launches += 1;
+    if (inline_sldg) {
+        CK(launch_xfix(a, c->stream));
+        c->launches += 1;
+    }
     for (int i = 0; i < nspecies; ++i) fs[i]->swap();
     return SK_OK;
 }
@@ -233,6 +254,7 @@ sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, con
     a.inline_sldg = inline_sldg;
     a.threshold = threshold;
     CK(launch_vtab(a, c->stream));
+    c->launches += 1;
     return SK_OK;
 }
 
@@ -258,7 +280,16 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.periodic = periodic;
     a.check_finite = check_finite;
     a.threshold = threshold;
+    a.fix_list = c->fix_list;
+    a.fix_count = c->fix_count;
+    a.fix_cap = c->fix_cap;
+    if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_vsweep(a, c->stream));
+    c->launches += 1;
+    if (inline_sldg) {
+        CK(launch_vfix(a, c->stream));
+        c->launches += 1;
+    }
     for (int i = 0; i < nspecies; ++i) fs[i]->swap();
     return SK_OK;
 }
@@ -284,10 +315,13 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     a.species0 = nspecies == 2 ? 0 : fs[0]->species;
     a.periodic = periodic;
     std::memcpy(a.tile_start, c->ptiles, sizeof a.tile_start);
-    if (dir == SK_DIR_X)
+    if (dir == SK_DIR_X) {
         CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
-    else
+        c->launches += 1;
+    } else {
         CK(launch_post_v(a, c->stream));
+        c->launches += 2;
+    }
     for (int i = 0; i < nspecies; ++i) fs[i]->swap();
     return SK_OK;
 }
@@ -314,6 +348,7 @@ sk_status enq_rho(sk_field* fe, sk_field* fi, double* rho) {
     a.partial = c->rho_partial;
     a.rho = rho;
     CK(launch_rho(a, 2, c->stream));
+    c->launches += 2;
     return SK_OK;
 }
 
@@ -343,6 +378,7 @@ sk_status enq_shrink(sk_field** fs, int nspecies, const sk_vadjust& pol, int for
     a.tol = pol.tol;
     a.cooldown = 10;
     CK(launch_shrink(a, c->stream));
+    c->launches += (force != 0) + (force != 1) + (force >= 0 ? 4 : 0);
     return SK_OK;
 }
 
@@ -477,6 +513,10 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
     CK(dalloc(&c->diag_partial, 592 * 4));
     CK(dalloc(&c->diag_out, 4));
     CK(cudaMallocHost((void**)&c->pinned, sizeof(double) * 64));
+    c->fix_cap = 1u << 22;  // 4 Mi queued cells (32 MiB); overflow clamps inline
+    CK(dalloc(&c->fix_list, c->fix_cap));
+    CK(dalloc(&c->fix_count, 1));
+    CK(cudaMemset(c->fix_count, 0, sizeof(unsigned int)));
     *out = c;
     return SK_OK;
 }
@@ -491,6 +531,8 @@ sk_status sk_ctx_destroy(sk_ctx* c) {
     cudaFree(c->rho_partial);
     cudaFree(c->diag_partial);
     cudaFree(c->diag_out);
+    cudaFree(c->fix_list);
+    cudaFree(c->fix_count);
     cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -824,6 +866,9 @@ sk_status sk_state_destroy(sk_state* s) {
     if (!s) return SK_OK;
     cudaSetDevice(s->ctx->device);
     if (s->graph2) cudaGraphExecDestroy(s->graph2);
+    cudaStreamSynchronize(s->ctx->stream);
+    for (auto& m : s->marks) cudaEventDestroy(m.second);
+    for (auto e : s->pool) cudaEventDestroy(e);
     sk_field_destroy(s->f[0]);
     sk_field_destroy(s->f[1]);
     cudaFree(s->E);
@@ -848,6 +893,23 @@ sk_status sk_state_download_E(sk_state* s, double* host, size_t count) {
 namespace {
 
 // stepper.cpp:44-103 (blob: no source term), all on the context stream.
+enum Phase { PH_XTAB, PH_X1, PH_POST_X1, PH_RHO, PH_POISSON, PH_VTAB, PH_V, PH_POST_V, PH_X2,
+             PH_POST_X2, PH_SHRINK, PH_END, PH_N };
+
+sk_status mark(sk_state* s, int phase) {
+    if (!s->timing) return SK_OK;
+    cudaEvent_t e;
+    if (!s->pool.empty()) {
+        e = s->pool.back();
+        s->pool.pop_back();
+    } else {
+        CK(cudaEventCreate(&e));
+    }
+    CK(cudaEventRecord(e, s->ctx->stream));
+    s->marks.emplace_back(phase, e);
+    return SK_OK;
+}
+
 sk_status enq_strang(sk_state* s) {
     sk_ctx* c = s->ctx;
     const sk_limiter* lim = &s->cfg.limiter;
@@ -857,27 +919,35 @@ sk_status enq_strang(sk_state* s) {
     sk_field* fs[2] = {s->f[0], s->f[1]};
     sk_status rc;
     // x tables serve both x half-sweeps (same tau, same v grid within a step)
-    if ((rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1))) return rc;
-    if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0))) return rc;
-    if ((rc = enq_post(fs, 2, SK_DIR_X, lim, 0))) return rc;
-    if ((rc = enq_rho(fs[0], fs[1], s->rho))) return rc;
+    const bool post = lim->indicator != 0;
+    if ((rc = mark(s, PH_XTAB)) || (rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1)))
+        return rc;
+    if ((rc = mark(s, PH_X1)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 0))) return rc;
+    if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
+    if ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho))) return rc;
+    if ((rc = mark(s, PH_POISSON))) return rc;
     CK(launch_poisson(c->pdev, s->rho, s->E, s->phi, c->stream));
-    if ((rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr))) return rc;
-    if ((rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;
-    if ((rc = enq_post(fs, 2, SK_DIR_V, lim, 0))) return rc;
-    if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
-    if ((rc = enq_post(fs, 2, SK_DIR_X, lim, 0))) return rc;
+    c->launches += 1;
+    if ((rc = mark(s, PH_VTAB)) || (rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr)))
+        return rc;
+    if ((rc = mark(s, PH_V)) || (rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;
+    if (post && ((rc = mark(s, PH_POST_V)) || (rc = enq_post(fs, 2, SK_DIR_V, lim, 0)))) return rc;
+    if ((rc = mark(s, PH_X2)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
+    if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     return SK_OK;
 }
 
 sk_status enq_run_body(sk_state* s) {
     sk_ctx* c = s->ctx;
     if (sk_status rc = enq_strang(s)) return rc;
+    if (sk_status rc = mark(s, PH_SHRINK)) return rc;
     CK(launch_step_end(c->st, s->cfg.v_adjust, 10, 3, c->stream));
+    c->launches += 1;
     if (s->cfg.v_adjust) {
         sk_field* fs[2] = {s->f[0], s->f[1]};
         if (sk_status rc = enq_shrink(fs, 2, s->cfg.policy, 0, 1)) return rc;
     }
+    if (sk_status rc = mark(s, PH_END)) return rc;
     s->step_host += 1;
     return SK_OK;
 }
@@ -904,6 +974,11 @@ sk_status sk_run_steps(sk_state* s, int n) {
     CK(cudaSetDevice(c->device));
     // Two loop bodies leave both ping-pong buffers where they started, so a
     // captured pair replays with fixed pointers.
+    if (s->timing) {  // per-phase events: plain enqueue, no graph
+        for (int i = 0; i < n; ++i)
+            if (sk_status rc = enq_run_body(s)) return rc;
+        return after_launch(c);
+    }
     if (n >= 2 && (!s->graph2 || s->graph_cur0 != s->f[0]->cur || s->graph_cur1 != s->f[1]->cur)) {
         if (s->graph2) {
             cudaGraphExecDestroy(s->graph2);
@@ -911,12 +986,15 @@ sk_status sk_run_steps(sk_state* s, int n) {
         }
         int c0 = s->f[0]->cur, c1 = s->f[1]->cur;
         long h0 = s->step_host;
+        long long l0 = c->launches;
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         sk_status rc = enq_run_body(s);
         if (!rc) rc = enq_run_body(s);
         cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
         s->step_host = h0;
+        s->graph_launches = c->launches - l0;
+        c->launches = l0;
         if (rc) return rc;
         CK(ce);
         if (s->f[0]->cur != c0 || s->f[1]->cur != c1)
@@ -930,11 +1008,40 @@ sk_status sk_run_steps(sk_state* s, int n) {
     for (; done + 2 <= n; done += 2) {
         CK(cudaGraphLaunch(s->graph2, c->stream));
         s->step_host += 2;
+        c->launches += s->graph_launches;
     }
     for (; done < n; ++done)
         if (sk_status rc = enq_run_body(s)) return rc;
     return after_launch(c);
 }
+
+sk_status sk_state_set_phase_timing(sk_state* s, int on) {
+    s->timing = on != 0;
+    return SK_OK;
+}
+
+sk_status sk_state_phase_times(sk_state* s, double* ms, long* count, int n) {
+    CK(cudaStreamSynchronize(s->ctx->stream));
+    for (size_t i = 0; i + 1 < s->marks.size(); ++i) {
+        int ph = s->marks[i].first;
+        if (ph == PH_END) continue;
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, s->marks[i].second, s->marks[i + 1].second));
+        s->phase_ms[ph] += t;
+        s->phase_count[ph] += 1;
+    }
+    for (auto& m : s->marks) s->pool.push_back(m.second);
+    s->marks.clear();
+    for (int i = 0; i < n && i < PH_N; ++i) {
+        ms[i] = s->phase_ms[i];
+        if (count) count[i] = s->phase_count[i];
+        s->phase_ms[i] = 0.0;
+        s->phase_count[i] = 0;
+    }
+    return SK_OK;
+}
+
+long long sk_ctx_launch_count(sk_ctx* c) { return c->launches; }
 
 sk_status sk_state_step_index(sk_state* s, long* step) {
     if (sk_status rc = collect_errors(s->ctx)) return rc;

@@ -68,6 +68,42 @@ __device__ __forceinline__ void count_flags(unsigned long long* dst, unsigned t,
     }
 }
 
+// Out-of-line clamp for the (rare) list-overflow path: keeps the clamp's
+// register demand out of the streaming sweeps. Values travel by value.
+template <int P>
+struct ClampIO {
+    double v[P];
+    int flags;
+};
+template <int P>
+__device__ __noinline__ ClampIO<P> clamp_cell_slow(const Basis& b, double alpha, ClampIO<P> ul,
+                                                   ClampIO<P> ur, ClampIO<P> up) {
+    up.flags = inline_clamp<P>(b, alpha, ul.v, ur.v, up.v);
+    return up;
+}
+
+// Warp-aggregated append of a troubled cell to the deferred-clamp list.
+// Returns false when the list is full: the caller then clamps inline.
+__device__ __forceinline__ bool defer_push(unsigned int* count, unsigned int cap,
+                                           unsigned long long* list, bool want,
+                                           unsigned long long entry) {
+    const unsigned act = __activemask();
+    const unsigned m = __ballot_sync(act, want);
+    if (!m) return false;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned)__popc(m));
+    base = __shfl_sync(act, base, leader);
+    if (!want) return false;
+    const unsigned slot = base + __popc(m & ((1u << lane) - 1u));
+    if (slot < cap) {
+        list[slot] = entry;
+        return true;
+    }
+    return false;
+}
+
 // ---------------------------------------------------------------------------
 // x tables
 // ---------------------------------------------------------------------------
@@ -199,101 +235,330 @@ __device__ double x_fetch_outside(const Basis& basis, const Grid& g, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// K1: x sweep
+// cp.async helpers (LDGSTS: global -> shared without a register round trip)
 // ---------------------------------------------------------------------------
-template <int P, int CPT>
-__global__ void __launch_bounds__(kXThreads, 2) xsweep_kernel(const __grid_constant__ XSweepArgs a) {
-    constexpr int T = kXThreads * CPT;
-    constexpr int W = xs_stride<P, T>();
-    constexpr int NF = xnf<P>();
-    extern __shared__ double smem[];
-    double* win = smem;           // [P][W] input window, SoA
-    double* outs = smem + P * W;  // [P][W] output tile, SoA
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+// 8-byte async copy; valid == false zero-fills the destination (no global read)
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(sdst)),
+                 "l"(gsrc), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
-    const int line = blockIdx.x;
-    const int sp = a.species0 + blockIdx.z;
-    const int tile = blockIdx.y;
-    const Grid& g = a.grid;
+// ---------------------------------------------------------------------------
+// TMA bulk copy / mbarrier helpers (sm_90+; SASS UBLKCP / SYNCS)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SK_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SK_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, unsigned bytes,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+    asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// K1: x sweep -- warp-specialised TMA pipeline over tiles
+//   tile = (species, x row, block, T cells); its source window is T+1 cells
+//   that are contiguous in HBM. One producer warp streams windows (and the
+//   tile's table row) into an S-stage smem ring with cp.async.bulk + mbarrier
+//   transaction counts; NC consumer warps compute two cells each (projection
+//   + inline indicator in registers, matrices as smem broadcasts), write the
+//   tile AoS into a triple-buffered output stage and one thread bulk-stores it.
+//   Window cells outside the contiguous valid range (walls, 3-block ghosts,
+//   periodic wrap) are filled by the consumers after the copy lands.
+// ---------------------------------------------------------------------------
+template <int P>
+struct XCfg {
+    static constexpr int NC = 8;                    // consumer warps
+    static constexpr int NT = NC * 32;
+    static constexpr int CPT = P <= 4 ? 2 : 1;
+    static constexpr int T = CPT * NT;              // output cells per tile
+    static constexpr int WIN = (((T + 1) * P + 4) + 1) / 2 * 2;  // window doubles (+ slack), even
+    static constexpr int NF = xnf<P>();
+    static constexpr int STAGE = ((WIN + NF + 1) / 2) * 2;
+    static constexpr int S = 3;                     // input stages
+    static constexpr int SO = 3;                    // output stages
+    static constexpr int OUT = T * P;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + SO * OUT) + 8 * 2 * S;
+};
+
+struct XTile {
+    int sp, line, b, c0, nt;
+};
+
+__device__ __forceinline__ XTile decode_xtile(const XSweepArgs& a, int t, int T) {
+    const int ntl = a.tile_start[a.grid.nblocks];
+    XTile x;
+    const int tl = t % ntl;
+    const int rest = t / ntl;
+    x.line = rest % a.nlines;
+    x.sp = a.species0 + rest / a.nlines;
     int b = 0;
-    while (tile >= a.tile_start[b + 1]) ++b;
-    const int cells_b = g.cells[b];
-    const int c0 = (tile - a.tile_start[b]) * T;
-    const int nt = min(T, cells_b - c0);
+    while (tl >= a.tile_start[b + 1]) ++b;
+    x.b = b;
+    x.c0 = (tl - a.tile_start[b]) * T;
+    x.nt = min(T, a.grid.cells[b] - x.c0);
+    return x;
+}
 
-    const double* row = a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * NF;
-    const int istar = (int)row[0];
-    const double alpha = row[1];
-    double A[P * P], B[P * P];
+// valid contiguous block-local cell range that a bulk copy may fetch
+__device__ __forceinline__ void xvalid_range(const XSweepArgs& a, int b, int& vlo, int& vhi) {
+    const Grid& g = a.grid;
+    vlo = 0;
+    vhi = g.cells[b];
+    if (a.periodic) return;
+    if (b > 0 && g.dx[b - 1] == g.dx[b]) vlo = -g.cells[b - 1];
+    if (b + 1 < g.nblocks && g.dx[b + 1] == g.dx[b]) vhi = g.cells[b] + g.cells[b + 1];
+}
+
+// P doubles of one cell from shared memory (16-byte vector loads for even P;
+// the window origin is 16B-aligned whenever P is even)
+template <int P>
+__device__ __forceinline__ void lds_cell(const double* p, double* u) {
+    if constexpr (P % 2 == 0) {
 #pragma unroll
-    for (int i = 0; i < P * P; ++i) {
-        A[i] = row[2 + i];
-        B[i] = row[2 + P * P + i];
-    }
-
-    const long long lb = (long long)line * g.ncells * P;
-    const double* src = a.src[sp] + lb;
-    const int s0 = c0 + istar;
-    const int nwin = (nt + 1) * P;
-    const long long gbase = (long long)g.start[b] * P;
-    for (int e = threadIdx.x; e < nwin; e += kXThreads) {
-        const int wc = e / P, n = e - (e / P) * P;
-        const int s = s0 + wc;
-        double v;
-        if (s >= 0 && s < cells_b) {
-            v = __ldg(src + gbase + (long long)s * P + n);
-        } else if (a.periodic) {  // advection.cpp:86-88 (single block only)
-            int ss = ((s % cells_b) + cells_b) % cells_b;
-            v = src[gbase + (long long)ss * P + n];
-        } else {
-            v = x_fetch_outside<P>(a.basis, g, src, b, s, n);
+        for (int i = 0; i < P / 2; ++i) {
+            const double2 v = reinterpret_cast<const double2*>(p)[i];
+            u[2 * i] = v.x;
+            u[2 * i + 1] = v.y;
         }
-        win[n * W + wc] = v;
+    } else {
+#pragma unroll
+        for (int n = 0; n < P; ++n) u[n] = p[n];
+    }
+}
+template <int P>
+__device__ __forceinline__ void sts_cell(double* p, const double* u) {
+    if constexpr (P % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < P / 2; ++i)
+            reinterpret_cast<double2*>(p)[i] = make_double2(u[2 * i], u[2 * i + 1]);
+    } else {
+#pragma unroll
+        for (int n = 0; n < P; ++n) p[n] = u[n];
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
+    xsweep_kernel(const __grid_constant__ XSweepArgs a) {
+    using C = XCfg<P>;
+    extern __shared__ __align__(128) double smem[];
+    double* stages = smem;                                   // S x STAGE
+    double* outs = smem + C::S * C::STAGE;                   // SO x OUT
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(outs + C::SO * C::OUT);
+    unsigned long long* empty = full + C::S;
+    const Grid& g = a.grid;
+    const int ntot = a.nspecies * a.nlines * a.tile_start[g.nblocks];
+    const int G = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < C::S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], C::NC);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
+    if (warp == C::NC) {
+        // ---------------- producer warp ----------------
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < ntot; t += G, ++it) {
+                const int stg = it % C::S;
+                mbar_wait(&empty[stg], ((it / C::S) & 1) ^ 1);
+                const XTile x = decode_xtile(a, t, C::T);
+                const double* row = a.tab[x.sp] + ((long long)g.cls[x.b] * a.nlines + x.line) * C::NF;
+                const int istar = (int)__ldg(row);
+                const int s0 = x.c0 + istar;
+                int vlo, vhi;
+                xvalid_range(a, x.b, vlo, vhi);
+                const int clo = max(s0, vlo), chi = min(s0 + x.nt + 1, vhi);
+                double* st = stages + stg * C::STAGE;
+                // element parity of window cell s0 in HBM decides the smem origin
+                const long long eg = ((long long)x.line * g.ncells + g.start[x.b] + s0) * P;
+                const int woff = (int)(eg & 1);
+                unsigned bytes = C::NF * 8;
+                long long g0 = 0, g1 = 0;
+                if (chi > clo) {
+                    g0 = eg + (long long)(clo - s0) * P;
+                    g1 = eg + (long long)(chi - s0) * P;
+                    g0 &= ~1LL;
+                    g1 = (g1 + 1) & ~1LL;
+                    bytes += (unsigned)(g1 - g0) * 8;
+                }
+                mbar_expect_tx(&full[stg], bytes);
+                tma_load_1d(st + C::WIN, row, C::NF * 8, &full[stg]);
+                if (chi > clo) {
+                    double* dst = st + 2 + woff + (g0 - eg);
+                    tma_load_1d(dst, a.src[x.sp] + g0, (unsigned)(g1 - g0) * 8, &full[stg]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int tid = threadIdx.x;
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
-    double el[P], er[P];
-    if (a.inline_sldg) {
+    int it = 0;
+    for (int t = blockIdx.x; t < ntot; t += G, ++it) {
+        const int stg = it % C::S;
+        mbar_wait(&full[stg], (it / C::S) & 1);
+        const XTile x = decode_xtile(a, t, C::T);
+        const int b = x.b, cells_b = g.cells[b];
+        double* st = stages + stg * C::STAGE;
+        const double* row = st + C::WIN;
+        const int istar = (int)row[0];
+        const int s0 = x.c0 + istar;
+        const long long lbase = (long long)x.line * g.ncells * P;
+        const long long eg = lbase + ((long long)g.start[b] + s0) * P;
+        const double* win = st + 2 + (int)(eg & 1);  // window cell w, node n at win[w*P+n]
+        int vlo, vhi;
+        xvalid_range(a, b, vlo, vhi);
+        const int clo = max(s0, vlo), chi = min(s0 + x.nt + 1, vhi);
+        if (clo > s0 || chi < s0 + x.nt + 1) {
+            // walls (zero inflow), 3-block ghosts, periodic wrap
+            const double* src = a.src[x.sp] + lbase;
+            double* w = const_cast<double*>(win);
+            for (int e = tid; e < (x.nt + 1) * P; e += C::NT) {
+                const int wc = e / P, n = e - (e / P) * P;
+                const int s = s0 + wc;
+                if (s >= clo && s < chi) continue;
+                double v;
+                if (a.periodic) {
+                    const int ss = ((s % cells_b) + cells_b) % cells_b;
+                    v = src[(long long)(g.start[b] + ss) * P + n];
+                } else {
+                    v = x_fetch_outside<P>(a.basis, g, src, b, s, n);
+                }
+                w[e] = v;
+            }
+            consumer_sync(C::NT);
+        }
+        double* ob = outs + (it % C::SO) * C::OUT;
+        const double alpha = row[1];
+        double ul[C::CPT][P], ur[C::CPT][P], o[C::CPT][P];
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
-            el[i] = row[2 + 2 * P * P + i];
-            er[i] = row[2 + 2 * P * P + P + i];
+        for (int cc = 0; cc < C::CPT; ++cc) {
+            const int c = min(tid + cc * C::NT, x.nt - 1);
+            lds_cell<P>(win + c * P, ul[cc]);
+            lds_cell<P>(win + (c + 1) * P, ur[cc]);
+        }
+        // advection.cpp:95-101, both cells share each broadcast matrix load
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+            double acc[C::CPT];
+#pragma unroll
+            for (int cc = 0; cc < C::CPT; ++cc) acc[cc] = 0.0;
+            double am[P], bm[P];
+            lds_cell<P>(row + 2 + m * P, am);
+            lds_cell<P>(row + 2 + P * P + m * P, bm);
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+#pragma unroll
+                for (int cc = 0; cc < C::CPT; ++cc) acc[cc] += am[j] * ul[cc][j] + bm[j] * ur[cc][j];
+            }
+#pragma unroll
+            for (int cc = 0; cc < C::CPT; ++cc) o[cc][m] = acc[cc];
+        }
+#pragma unroll
+        for (int cc = 0; cc < C::CPT; ++cc) {
+            const int c = tid + cc * C::NT;
+            if (c < x.nt) {
+                if (a.inline_sldg) {
+                    const bool tr = inline_indicator<P>(a.basis, a.threshold, row + 2 + 2 * P * P,
+                                                        row + 2 + 2 * P * P + P, ul[cc], ur[cc], o[cc]);
+                    const unsigned long long entry =
+                        ((unsigned long long)(x.sp & 1) << 63) | ((unsigned long long)x.line << 32) |
+                        (unsigned)(g.start[b] + x.c0 + c);
+                    if (tr && !defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry)) {
+                        ClampIO<P> L, R, U;
+#pragma unroll
+                        for (int q = 0; q < P; ++q) {
+                            L.v[q] = ul[cc][q];
+                            R.v[q] = ur[cc][q];
+                            U.v[q] = o[cc][q];
+                        }
+                        U = clamp_cell_slow<P>(a.basis, alpha, L, R, U);
+#pragma unroll
+                        for (int q = 0; q < P; ++q) o[cc][q] = U.v[q];
+                        nt_t += U.flags & 1;
+                        nt_c += (U.flags >> 1) & 1;
+                        nt_o += (U.flags >> 2) & 1;
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < P; ++m) bad |= !isfinite(o[cc][m]);
+                sts_cell<P>(ob + c * P, o[cc]);
+            }
+        }
+        // window stage consumed
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stg]);
+        fence_proxy_async();
+        if (tid == 0) bulk_wait_read<C::SO - 2>();  // out stage of tile it+1 is free
+        consumer_sync(C::NT);
+        if (tid == 0) {
+            double* dst = a.dst[x.sp] + lbase + (long long)(g.start[b] + x.c0) * P;
+            tma_store_1d(dst, ob, (unsigned)(x.nt * P * 8));
+            bulk_commit();
         }
     }
-#pragma unroll
-    for (int cc = 0; cc < CPT; ++cc) {
-        const int c = threadIdx.x + cc * kXThreads;
-        if (c < nt) {
-            double ul[P], ur[P], o[P];
-#pragma unroll
-            for (int n = 0; n < P; ++n) {
-                ul[n] = win[n * W + c];
-                ur[n] = win[n * W + c + 1];
-            }
-            project_cell<P>(A, B, ul, ur, o);
-            if (a.inline_sldg) {
-                int fl = inline_limit<P>(a.basis, alpha, a.threshold, el, er, ul, ur, o);
-                nt_t += fl & 1;
-                nt_c += (fl >> 1) & 1;
-                nt_o += (fl >> 2) & 1;
-            }
-#pragma unroll
-            for (int m = 0; m < P; ++m) {
-                bad |= !isfinite(o[m]);
-                outs[m * W + c] = o[m];
-            }
-        }
-    }
-    __syncthreads();
-    double* dst = a.dst[sp] + lb + gbase + (long long)c0 * P;
-    for (int e = threadIdx.x; e < nt * P; e += kXThreads) {
-        const int c = e / P, m = e - (e / P) * P;
-        dst[e] = outs[m * W + c];
-    }
-    if (a.inline_sldg) count_flags(a.st->stats[sp], nt_t, nt_c, nt_o);
-    if (a.check_finite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
-        atomicOr(&a.st->nonfinite, 1);
+    if (tid == 0) bulk_wait<0>();
+    if (a.inline_sldg) count_flags(a.st->stats[a.nspecies == 1 ? a.species0 : 0], nt_t, nt_c, nt_o);
+    if (a.check_finite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.st->nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -346,18 +611,50 @@ __device__ __forceinline__ void vload(const double* f, long long ld, int xd, int
     }
 }
 
+// One thread per x dof walks kVChunk v cells. Source cells stream through a
+// per-thread R-deep cp.async ring in shared memory ([slot][node][thread], so
+// consecutive threads hit consecutive banks), keeping R*P loads in flight per
+// thread without spending registers on them.
+template <int P>
+__host__ __device__ constexpr int vring() { return P <= 4 ? 8 : 4; }
+
+template <int P>
+__device__ __forceinline__ void vissue(const double* f, long long ld, int xd, int s, int lo, int hi,
+                                       int periodic, int ncell, double* slot) {
+    if (periodic) s = ((s % ncell) + ncell) % ncell;
+    const bool valid = s >= lo && s < hi;
+    const double* p = valid ? f + (long long)s * P * ld + xd : f;
+#pragma unroll
+    for (int n = 0; n < P; ++n) cp_async8(slot + n * kVThreads, valid ? p + n * ld : f, valid);
+}
+
 template <int P>
 __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant__ VSweepArgs a) {
+    constexpr int kVRing = vring<P>();
+    __shared__ double ring[kVRing * P * kVThreads];
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
     const int j0 = blockIdx.y * kVChunk;
     const int j1 = min(j0 + kVChunk, a.n);
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
+    double* my = ring + threadIdx.x;
     if (xd < a.nxd) {
         const double* t = a.tab[sp];
         const int nx = a.nxd;
         const int istar = (int)t[xd];
+        const double* f = a.src[sp];
+        double* out = a.dst[sp];
+        const long long ld = a.ld;
+        const int lo = -a.gl, hi = a.n + a.gr;
+        const int sfirst = j0 + istar;  // source cell of ul for j0
+        const int ncells = (j1 - j0) + 1;
+        // prologue: cells 0..R-2 of this thread's source run
+#pragma unroll
+        for (int c = 0; c < kVRing - 1; ++c) {
+            if (c < ncells) vissue<P>(f, ld, xd, sfirst + c, lo, hi, a.periodic, a.n, my + (c % kVRing) * P * kVThreads);
+            cp_commit();
+        }
         const double alpha = t[nx + xd];
         double A[P * P], B[P * P], el[P], er[P];
 #pragma unroll
@@ -372,22 +669,43 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
                 er[i] = t[(long long)(2 + 2 * P * P + P + i) * nx + xd];
             }
         }
-        const double* f = a.src[sp];
-        double* out = a.dst[sp];
-        const long long ld = a.ld;
-        const int lo = -a.gl, hi = a.n + a.gr;
-        double ul[P], ur[P], nx1[P];
-        vload<P>(f, ld, xd, j0 + istar, lo, hi, a.periodic, a.n, ul);
-        vload<P>(f, ld, xd, j0 + istar + 1, lo, hi, a.periodic, a.n, ur);
+        double ul[P], ur[P];
+        cp_wait<kVRing - 2>();
+#pragma unroll
+        for (int n = 0; n < P; ++n) ul[n] = my[n * kVThreads];
+        if (kVRing - 1 < ncells) vissue<P>(f, ld, xd, sfirst + kVRing - 1, lo, hi, a.periodic, a.n, my + ((kVRing - 1) % kVRing) * P * kVThreads);
+        cp_commit();
         for (int j = j0; j < j1; ++j) {
-            vload<P>(f, ld, xd, j + istar + 2, lo, hi, a.periodic, a.n, nx1);  // prefetch
+            const int c = j - j0 + 1;  // ring index of ur
+            cp_wait<kVRing - 2>();
+            const double* sl = my + (c % kVRing) * P * kVThreads;
+#pragma unroll
+            for (int n = 0; n < P; ++n) ur[n] = sl[n * kVThreads];
+            const int cn = c + kVRing - 1;
+            if (cn < ncells) vissue<P>(f, ld, xd, sfirst + cn, lo, hi, a.periodic, a.n, my + (cn % kVRing) * P * kVThreads);
+            cp_commit();
             double o[P];
             project_cell<P>(A, B, ul, ur, o);
             if (a.inline_sldg) {
-                int fl = inline_limit<P>(a.basis, alpha, a.threshold, el, er, ul, ur, o);
-                nt_t += fl & 1;
-                nt_c += (fl >> 1) & 1;
-                nt_o += (fl >> 2) & 1;
+                const bool tr = inline_indicator<P>(a.basis, a.threshold, el, er, ul, ur, o);
+                const unsigned long long entry = ((unsigned long long)(sp & 1) << 63) |
+                                                 ((unsigned long long)j << 32) | (unsigned)xd;
+                if (tr && !defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry)) {
+                    ClampIO<P> L, R, U;
+#pragma unroll
+                    for (int q = 0; q < P; ++q) {
+                        L.v[q] = ul[q];
+                        R.v[q] = ur[q];
+                        U.v[q] = o[q];
+                    }
+                    U = clamp_cell_slow<P>(a.basis, alpha, L, R, U);
+#pragma unroll
+                    for (int q = 0; q < P; ++q) o[q] = U.v[q];
+                    const int fl = U.flags;
+                    nt_t += fl & 1;
+                    nt_c += (fl >> 1) & 1;
+                    nt_o += (fl >> 2) & 1;
+                }
             }
             double* op = out + (long long)j * P * ld + xd;
 #pragma unroll
@@ -396,15 +714,96 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
                 op[m * ld] = o[m];
             }
 #pragma unroll
-            for (int n = 0; n < P; ++n) {
-                ul[n] = ur[n];
-                ur[n] = nx1[n];
-            }
+            for (int n = 0; n < P; ++n) ul[n] = ur[n];
         }
+        cp_wait<0>();
     }
     if (a.inline_sldg) count_flags(a.st->stats[sp], nt_t, nt_c, nt_o);
     if (a.check_finite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
         atomicOr(&a.st->nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------
+// deferred theta clamp of troubled cells (limiters.cpp:191-215), one thread per
+// queued cell. The sweep's source buffer is intact (ping-pong), so ul/ur are
+// re-read exactly as the sweep saw them and the result is bitwise the same.
+// ---------------------------------------------------------------------------
+template <int P>
+__global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSweepArgs a) {
+    constexpr int NF = xnf<P>();
+    const unsigned n = min(*a.fix_count, a.fix_cap);
+    const Grid& g = a.grid;
+    unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned long long e = a.fix_list[i];
+        const int sp = (int)(e >> 63);
+        const int line = (int)((e >> 32) & 0x7fffffffu);
+        const int cell = (int)(e & 0xffffffffu);
+        int b = 0;
+        while (cell >= g.start[b + 1]) ++b;
+        const int local = cell - g.start[b];
+        const double* row = a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * NF;
+        const int istar = (int)row[0];
+        const double alpha = row[1];
+        const long long lbase = (long long)line * g.ncells * P;
+        const double* src = a.src[sp] + lbase;
+        double uu[2][P];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            int s = local + istar + h;
+            for (int q = 0; q < P; ++q) {
+                double v;
+                if (a.periodic) {
+                    int ss = ((s % g.cells[b]) + g.cells[b]) % g.cells[b];
+                    v = src[(long long)(g.start[b] + ss) * P + q];
+                } else if (s >= 0 && s < g.cells[b]) {
+                    v = src[(long long)(g.start[b] + s) * P + q];
+                } else {
+                    v = x_fetch_outside<P>(a.basis, g, src, b, s, q);
+                }
+                uu[h][q] = v;
+            }
+        }
+        double* up = a.dst[sp] + lbase + (long long)cell * P;
+        double o[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) o[q] = up[q];
+        const int fl = inline_clamp<P>(a.basis, alpha, uu[0], uu[1], o);
+#pragma unroll
+        for (int q = 0; q < P; ++q) up[q] = o[q];
+        ct[sp] += fl & 1;
+        cc[sp] += (fl >> 1) & 1;
+        co[sp] += (fl >> 2) & 1;
+    }
+    for (int sp = 0; sp < 2; ++sp) count_flags(a.st->stats[sp], ct[sp], cc[sp], co[sp]);
+}
+
+template <int P>
+__global__ void __launch_bounds__(128) vfix_kernel(const __grid_constant__ VSweepArgs a) {
+    const unsigned n = min(*a.fix_count, a.fix_cap);
+    unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned long long e = a.fix_list[i];
+        const int sp = (int)(e >> 63);
+        const int j = (int)((e >> 32) & 0x7fffffffu);
+        const int xd = (int)(e & 0xffffffffu);
+        const double* t = a.tab[sp];
+        const int istar = (int)t[xd];
+        const double alpha = t[a.nxd + xd];
+        double ul[P], ur[P], o[P];
+        vload<P>(a.src[sp], a.ld, xd, j + istar, -a.gl, a.n + a.gr, a.periodic, a.n, ul);
+        vload<P>(a.src[sp], a.ld, xd, j + istar + 1, -a.gl, a.n + a.gr, a.periodic, a.n, ur);
+        double* op = a.dst[sp] + (long long)j * P * a.ld + xd;
+#pragma unroll
+        for (int m = 0; m < P; ++m) o[m] = op[m * a.ld];
+        const int fl = inline_clamp<P>(a.basis, alpha, ul, ur, o);
+#pragma unroll
+        for (int m = 0; m < P; ++m) op[m * a.ld] = o[m];
+        ct[sp] += fl & 1;
+        cc[sp] += (fl >> 1) & 1;
+        co[sp] += (fl >> 2) & 1;
+    }
+    for (int sp = 0; sp < 2; ++sp) count_flags(a.st->stats[sp], ct[sp], cc[sp], co[sp]);
 }
 
 // ---------------------------------------------------------------------------
@@ -900,26 +1299,54 @@ cudaError_t launch_xtab(const XTabArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int P, int CPT>
-static cudaError_t launch_xsweep_t(const XSweepArgs& a, int ntiles, cudaStream_t s) {
-    constexpr int T = kXThreads * CPT;
-    const size_t smem = sizeof(double) * 2 * P * xs_stride<P, T>();
+static int sm_count() {
+    static int n[32] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!n[dev & 31]) cudaDeviceGetAttribute(&n[dev & 31], cudaDevAttrMultiProcessorCount, dev);
+    return n[dev & 31];
+}
+
+template <int P>
+static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
+    using Cf = XCfg<P>;
+    const size_t smem = Cf::SMEM;
     static unsigned configured = 0;  // per-device bit
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured & (1u << (dev & 31)))) {
-        cudaFuncSetAttribute(xsweep_kernel<P, CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
         configured |= 1u << (dev & 31);
     }
-    dim3 grid(a.nlines, ntiles, a.nspecies);
-    xsweep_kernel<P, CPT><<<grid, kXThreads, smem, s>>>(a);
+    XSweepArgs b = a;
+    b.tile_start[0] = 0;
+    for (int i = 0; i < a.grid.nblocks; ++i)
+        b.tile_start[i + 1] = b.tile_start[i] + (a.grid.cells[i] + Cf::T - 1) / Cf::T;
+    const long long ntot = (long long)a.nspecies * a.nlines * b.tile_start[a.grid.nblocks];
+    const int nthreads = (Cf::NC + 1) * 32;
+    int blocks_per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P>, nthreads, smem);
+    long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
+    if (grid > ntot) grid = ntot;
+    xsweep_kernel<P><<<(int)grid, nthreads, smem, s>>>(b);
     return cudaGetLastError();
 }
 
-cudaError_t launch_xsweep(const XSweepArgs& a, int ntiles, cudaStream_t s) {
-    SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, 2>(a, ntiles, s)));
+cudaError_t launch_xsweep(const XSweepArgs& a, int /*ntiles*/, cudaStream_t s) {
+    SK_DISPATCH_P(a.basis.p, return launch_xsweep_t<PP>(a, s));
     return cudaSuccess;
+}
+
+cudaError_t launch_xfix(const XSweepArgs& a, cudaStream_t s) {
+    SK_DISPATCH_P(a.basis.p, (xfix_kernel<PP><<<sm_count() * 8, 128, 0, s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s) {
+    SK_DISPATCH_P(a.basis.p, (vfix_kernel<PP><<<sm_count() * 8, 128, 0, s>>>(a)));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s) {

@@ -46,6 +46,11 @@ struct XSweepArgs {
     int periodic;
     int check_finite;
     double threshold;
+    // deferred limiter clamp: troubled cells are queued here and clamped by
+    // the fixup kernel so one slow cell never stalls a whole CTA
+    unsigned long long* fix_list;
+    unsigned int* fix_count;
+    unsigned int fix_cap;
 };
 
 struct VTabArgs {
@@ -79,6 +84,9 @@ struct VSweepArgs {
     int periodic;
     int check_finite;
     double threshold;
+    unsigned long long* fix_list;
+    unsigned int* fix_count;
+    unsigned int fix_cap;
 };
 
 struct RhoArgs {
@@ -153,6 +161,8 @@ cudaError_t launch_xtab(const XTabArgs& a, cudaStream_t s);
 cudaError_t launch_xsweep(const XSweepArgs& a, int ntiles, cudaStream_t s);
 cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s);
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s);
+cudaError_t launch_xfix(const XSweepArgs& a, cudaStream_t s);
+cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_rho(const RhoArgs& a, int nspecies_mask, cudaStream_t s);
 cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
                            cudaStream_t s);

@@ -218,15 +218,15 @@ SK_HD void project_cell(const double* A, const double* B, const double* ul, cons
     }
 }
 
-// Inline sLdG limiter, limiters.cpp:175-222. Returns flags:
-// bit0 troubled, bit1 clamped, bit2 mean_outside. `up` is modified in place.
+// Inline sLdG limiter indicator, limiters.cpp:175-189 (cheap: runs on every cell).
 template <int P>
-SK_HD int inline_limit(const Basis& b, double alpha, double threshold, const double* ext_l,
-                       const double* ext_r, const double* ul, const double* ur, double* up) {
+SK_HD bool inline_indicator(const Basis& b, double threshold, const double* ext_l,
+                            const double* ext_r, const double* ul, const double* ur,
+                            const double* up) {
     double mean_l = mean<P>(b, ul);
     double mean_r = mean<P>(b, ur);
     double denom = dmax2(fabs(mean_l), fabs(mean_r));
-    if (denom <= 0.0) return 0;
+    if (denom <= 0.0) return false;
     double el = 0.0, er = 0.0;
 #pragma unroll
     for (int n = 0; n < P; ++n) {
@@ -234,8 +234,14 @@ SK_HD int inline_limit(const Basis& b, double alpha, double threshold, const dou
         er += ext_r[n] * up[n];
     }
     double ind = (fabs(el - mean_l) + fabs(er - mean_r)) / denom;
-    if (!(ind > threshold)) return 0;
-    // clamp (limiters.cpp:191-215)
+    return ind > threshold;
+}
+
+// theta clamp of a troubled cell, limiters.cpp:191-215. Returns flags:
+// bit0 troubled, bit1 clamped, bit2 mean_outside; `up` modified in place.
+template <int P>
+SK_HD int inline_clamp(const Basis& b, double alpha, const double* ul, const double* ur,
+                       double* up) {
     int flags = 1;
     double mean_p = mean<P>(b, up);
     double wmax = dmax2(extremum_on<P, true>(b, ul, alpha, 1.0), extremum_on<P, true>(b, ur, 0.0, alpha));
@@ -254,6 +260,14 @@ SK_HD int inline_limit(const Basis& b, double alpha, double threshold, const dou
         flags |= 2;
     }
     return flags;
+}
+
+// Inline sLdG limiter, limiters.cpp:217-222 (indicator, then clamp).
+template <int P>
+SK_HD int inline_limit(const Basis& b, double alpha, double threshold, const double* ext_l,
+                       const double* ext_r, const double* ul, const double* ur, double* up) {
+    if (!inline_indicator<P>(b, threshold, ext_l, ext_r, ul, ur, up)) return 0;
+    return inline_clamp<P>(b, alpha, ul, ur, up);
 }
 
 // ---------------- post limiters (limiters.cpp:47-165) ----------------

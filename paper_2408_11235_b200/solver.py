@@ -283,11 +283,29 @@ class Context:
         self.h = h
         self.grid, self.k, self.p, self.device = grid, k, k + 1, device
         self.nx = grid.ncells
+        self.stream = None
         if use_torch_stream:
+            # the library runs on a dedicated (non-default, capturable) torch
+            # stream; fence() orders it against torch's current stream
             import torch
 
             torch.cuda.set_device(device)
-            _check(L.sk_ctx_set_stream(h, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            self.stream = torch.cuda.Stream(device=device)
+            _check(L.sk_ctx_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
+
+    def enter(self):
+        """library work must see torch work already queued on the current stream"""
+        if self.stream is not None:
+            import torch
+
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+
+    def leave(self):
+        """torch work queued after this point must see the library's results"""
+        if self.stream is not None:
+            import torch
+
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def close(self):
         if getattr(self, "h", None):
@@ -431,8 +449,10 @@ def advect_v(f: NodalField, tau: float, E_nodes, sp: SpeciesParams,
     if E.numel() != f.ctx.nx * f.ctx.p:
         raise RuntimeError("advect_v: E node array size mismatch")
     lim = opt.limiter.to_c()
+    f.ctx.enter()
     _check(N.lib().sk_advect_v(f.h, tau, C.c_void_p(_dptr(E)), sp.charge_sign, sp.sqrt_mu, opt.bc,
                                C.byref(lim)))
+    f.ctx.leave()
 
 
 def apply_post_limiter(f: NodalField, direction: int, cfg: LimiterConfig, bc: int = 0):
@@ -444,7 +464,9 @@ def apply_post_limiter(f: NodalField, direction: int, cfg: LimiterConfig, bc: in
 def charge_density(fe: NodalField, fi: NodalField, out=None):
     """charge_density (poisson.cpp:194-216) -> CUDA tensor nx*(k+1)."""
     rho = out if out is not None else fe.ctx.dev_zeros(fe.ctx.nx * fe.ctx.p)
+    fe.ctx.enter()
     _check(N.lib().sk_charge_density(fe.h, fi.h, C.c_void_p(_dptr(rho))))
+    fe.ctx.leave()
     return rho
 
 
@@ -464,8 +486,10 @@ class PoissonOperator:
         rho = _device_array(self.ctx, rho)
         E = self.ctx.dev_zeros(self.ctx.nx * self.ctx.p)
         phi = self.ctx.dev_zeros(self.ctx.nx * (self.ctx.p + 1))
+        self.ctx.enter()
         _check(N.lib().sk_poisson_solve(self.ctx.h, C.c_void_p(_dptr(rho)), C.c_void_p(_dptr(E)),
                                         C.c_void_p(_dptr(phi))))
+        self.ctx.leave()
         return FieldPair(E, phi)
 
 
@@ -488,6 +512,7 @@ def shrink_velocity_domain(f: NodalField, policy: VAdjustPolicy = VAdjustPolicy(
 
 def electric_energy(ctx: Context, E) -> float:
     out = C.c_double()
+    ctx.enter()
     _check(N.lib().sk_electric_energy(ctx.h, C.c_void_p(_dptr(E)), C.byref(out)))
     return out.value
 
@@ -557,6 +582,20 @@ class SimulationState:
         _check(N.lib().sk_run_step_host(self.h, fe.ctypes.data_as(pd), fi.ctypes.data_as(pd),
                                         fe.size))
         self.steps_enqueued += 1
+
+    def set_phase_timing(self, on: bool):
+        _check(N.lib().sk_state_set_phase_timing(self.h, int(on)))
+
+    def phase_times(self) -> dict:
+        """accumulated ms per phase since the last call (CUDA events on the step stream)"""
+        n = len(N.PHASES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_long * n)()
+        _check(N.lib().sk_state_phase_times(self.h, ms, cnt, n))
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(N.PHASES)}
+
+    def launches(self) -> int:
+        return int(N.lib().sk_ctx_launch_count(self.ctx.h))
 
     def step_index(self) -> int:
         s = C.c_long()
