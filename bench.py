@@ -138,6 +138,8 @@ def config_dict(args, cfg):
         "nx": cfg.nx, "nv": cfg.v_cells, "k": cfg.k, "dof_total": cfg.dof_total,
         "field_bytes_per_species": 8 * cfg.nx * p * cfg.v_cells * p,
         "parallelism": f"v-shard x{args.gpus}" if args.gpus > 1 else "single GPU",
+        "reductions": "exact (reference order)" if getattr(args, "exact", False)
+                      else "parallel (two-pass moment, cyclic-reduction Poisson)",
         "l2": "inputs larger than L2 (no flush needed)"
               if 8 * cfg.dof_total > 126e6 else "state fits in L2 (parity config)",
     }
@@ -155,6 +157,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--exact", action="store_true",
+                    help="exact-reduction (bitwise parity) mode for rho and Poisson")
     args = ap.parse_args()
 
     import paper_2408_11235_b200 as sk
@@ -178,7 +182,7 @@ def main():
 
     dev = 0
     torch.cuda.set_device(dev)
-    st = sk.SimulationState(cfg, device=dev)
+    st = sk.SimulationState(cfg, device=dev, exact=args.exact)
     st.ctx.set_eager_errors(False)
     st.run_steps(args.warmup)
     st.ctx.synchronize()

@@ -113,6 +113,11 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* block_left
 sk_status sk_ctx_destroy(sk_ctx* ctx);
 sk_status sk_ctx_set_stream(sk_ctx* ctx, void* cuda_stream);
 sk_status sk_ctx_set_eager_errors(sk_ctx* ctx, int on);
+/* Exact-reduction (parity) mode: charge density summed in the reference's
+ * serial order and the Poisson solve replayed as dpbtrs in reference-BLAS order
+ * (poisson.cpp:166-216), so whole trajectories are bitwise the reference's.
+ * Off (default): parallel two-pass moment + block-cyclic-reduction solve. */
+sk_status sk_ctx_set_exact_reductions(sk_ctx* ctx, int on);
 sk_status sk_ctx_synchronize(sk_ctx* ctx); /* also reports device-side errors */
 sk_status sk_stats_get(sk_ctx* ctx, sk_stats* out);
 sk_status sk_stats_reset(sk_ctx* ctx);

@@ -220,6 +220,26 @@ class Oracle(_Lib):
             raise RuntimeError(self.last_error())
         return out
 
+    def advect_x_line(self, k, grid_left, grid_cells, grid_dx, speed, tau, line,
+                      inline_sldg=False, threshold=0.5, max_ghost=-1):
+        nb = len(grid_cells)
+        line = np.ascontiguousarray(line, dtype=np.float64)
+        out = np.zeros_like(line)
+        self.lib.sko_advect_x_line.argtypes = [C.c_int, C.c_int, _dp, C.POINTER(C.c_int), _dp,
+                                               C.c_double, C.c_double, C.c_int, C.c_double,
+                                               C.c_int, _dp, _dp]
+        rc = self.lib.sko_advect_x_line(k, nb, (C.c_double * nb)(*grid_left),
+                                        (C.c_int * nb)(*grid_cells), (C.c_double * nb)(*grid_dx),
+                                        speed, tau, int(inline_sldg), threshold, max_ghost,
+                                        line.ctypes.data_as(_dp), out.ctypes.data_as(_dp))
+        if rc:
+            raise RuntimeError(self.last_error())
+        return out
+
+    def set_rho_order(self, mode: int):
+        """0 = reference order; 1 = electrons first (rounding-noise envelope)"""
+        self.lib.sko_set_rho_order(int(mode))
+
     def state(self, **cfg) -> "OracleState":
         return OracleState(self, **cfg)
 

@@ -1314,6 +1314,11 @@ int sko_poisson_solve(const sko_poisson* P, const double* rho, double* phi, doub
     return SKO_OK;
 }
 
+/* Noise-envelope knob (tests only): 1 = sum electrons before ions in the
+ * charge density, a rounding-level perturbation of the reference's order. */
+static int g_rho_order = 0;
+void sko_set_rho_order(int mode) { g_rho_order = mode; }
+
 /* poisson.cpp:194-216 (ions first, then electrons) */
 void sko_charge_density(const sko_field* fe, const sko_field* fi, double* rho) {
     const sko_basis* b = basis_of(fe->k);
@@ -1321,7 +1326,13 @@ void sko_charge_density(const sko_field* fe, const sko_field* fi, double* rho) {
     const int nx = fe->x.ncells;
     for (int i = 0; i < nx * p; ++i) rho[i] = 0.0;
     const sko_field* fs[2] = {fi, fe};
-    const double signs[2] = {+1.0, -1.0};
+    double signs[2] = {+1.0, -1.0};
+    if (g_rho_order == 1) {
+        fs[0] = fe;
+        fs[1] = fi;
+        signs[0] = -1.0;
+        signs[1] = +1.0;
+    }
     for (int s = 0; s < 2; ++s) {
         const sko_field* f = fs[s];
         for (int vc = 0; vc < f->v.ncells; ++vc) {
@@ -1600,4 +1611,37 @@ void sko_state_summary(sko_state* S, double* out) {
     out[8] = sko_momentum(&S->fi);
     out[9] = sko_kinetic_energy(&S->fe);
     out[10] = sko_kinetic_energy(&S->fi);
+}
+
+/* One x line of advect_x (advection.cpp:160-201) for a given speed: used to
+ * check sampled lines of full-size GPU sweeps without a full CPU field. */
+int sko_advect_x_line(int k, int nblocks, const double* left, const int* cells, const double* dx,
+                      double speed, double tau, int inline_sldg, double threshold, int max_ghost,
+                      const double* line, double* out) {
+    const sko_basis* b = basis_of(k);
+    const int p = k + 1;
+    sko_grid g;
+    int rc = sko_grid_init(&g, nblocks, left, cells, dx);
+    if (rc) return rc;
+    sko_limiter lim;
+    sko_limiter_parse(inline_sldg ? "sldg" : "none", &lim);
+    lim.threshold = threshold;
+    sko_stats st = {0};
+    for (int bl = 0; bl < g.nblocks; ++bl) {
+        line_plan P;
+        make_plan(b, speed, tau, g.dx[bl], &lim, &P);
+        int gl = bl > 0 ? imax2(0, -P.istar) : 0;
+        int gr = bl + 1 < g.nblocks ? imax2(0, P.istar + 1) : 0;
+        if (g.nblocks == 1) gl = gr = 0;
+        if (max_ghost >= 0 && imax2(gl, gr) > max_ghost)
+            return fail(SKO_ERR_SIMULATION, "insufficient ghost width");
+        double* e2 = (double*)malloc(sizeof(double) * (size_t)(gl + g.cells[bl] + gr) * p);
+        rc = sko_exchange_block_ghosts(b, &g, bl, line, gl, gr, e2);
+        if (rc == SKO_OK)
+            rc = sko_advect_line(b, P.A, P.B, P.istar, SKO_BC_ZERO, e2, gl, g.cells[bl], gr,
+                                 out + (size_t)g.start[bl] * p, P.has_lim ? &P.lim : NULL, &st);
+        free(e2);
+        if (rc) return rc;
+    }
+    return SKO_OK;
 }

@@ -148,6 +148,10 @@ int sko_advect_v_lines(const sko_basis* b, int nlines, int line_stride, const do
                        double sqrt_mu, double tau, double dv, const sko_limiter* lim,
                        sko_stats* stats);
 int sko_post_limiter(sko_field* f, int dir, const sko_limiter* cfg, int bc, sko_stats* stats);
+/* one x line of advect_x for a given speed (multi-block ghosts included) */
+int sko_advect_x_line(int k, int nblocks, const double* left, const int* cells, const double* dx,
+                      double speed, double tau, int inline_sldg, double threshold, int max_ghost,
+                      const double* line, double* out);
 
 /* ---- adaptivity (adaptivity.cpp) ---- */
 void sko_fine_to_coarse(const sko_basis* b, const double* fine, int m, double* coarse);
@@ -174,6 +178,8 @@ void sko_poisson_free(sko_poisson* P);
 int sko_poisson_build_load(const sko_poisson* P, const double* rho, double* load);
 int sko_poisson_solve(const sko_poisson* P, const double* rho, double* phi, double* E);
 void sko_charge_density(const sko_field* fe, const sko_field* fi, double* rho);
+/* tests only: 0 = reference order, 1 = electrons first (noise envelope) */
+void sko_set_rho_order(int mode);
 double sko_electric_energy(const sko_grid* g, int k, const double* E);
 
 /* LAPACK restatement (lapack_band.c): reference-LAPACK dpbtf2 + dtbsv order */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "sk_ctx_destroy": (_i, [_vp]),
     "sk_ctx_set_stream": (_i, [_vp, _vp]),
     "sk_ctx_set_eager_errors": (_i, [_vp, _i]),
+    "sk_ctx_set_exact_reductions": (_i, [_vp, _i]),
     "sk_ctx_synchronize": (_i, [_vp]),
     "sk_stats_get": (_i, [_vp, C.POINTER(sk_stats)]),
     "sk_stats_reset": (_i, [_vp]),
@@ -101,7 +102,7 @@ PHASES = ("x_tables", "x_sweep_1", "post_x_1", "charge_density", "poisson", "v_t
 def header_symbols() -> list[str]:
     """Function names declared in include/sk_b200.h."""
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(sk_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(sk_[A-Za-z0-9_]+)\s*\(", text)))
 
 
 _lib = None

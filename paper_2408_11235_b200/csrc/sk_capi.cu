@@ -64,6 +64,7 @@ struct sk_ctx {
     double* diag_out = nullptr;
     double* pinned = nullptr;          // small pinned readback buffer
     long long launches = 0;            // kernels enqueued (bench gpu_launches)
+    bool exact = false;                // exact-reduction (bitwise parity) mode
     unsigned long long* fix_list = nullptr;  // deferred limiter clamps
     unsigned int* fix_count = nullptr;
     unsigned int fix_cap = 0;
@@ -347,6 +348,11 @@ sk_status enq_rho(sk_field* fe, sk_field* fi, double* rho) {
     }
     a.partial = c->rho_partial;
     a.rho = rho;
+    if (c->exact) {
+        CK(launch_rho_exact(a, c->stream));
+        c->launches += 1;
+        return SK_OK;
+    }
     CK(launch_rho(a, 2, c->stream));
     c->launches += 2;
     return SK_OK;
@@ -379,6 +385,15 @@ sk_status enq_shrink(sk_field** fs, int nspecies, const sk_vadjust& pol, int for
     a.cooldown = 10;
     CK(launch_shrink(a, c->stream));
     c->launches += (force != 0) + (force != 1) + (force >= 0 ? 4 : 0);
+    return SK_OK;
+}
+
+sk_status enq_poisson(sk_ctx* c, const double* rho, double* E, double* phi) {
+    if (c->exact)
+        CK(launch_poisson_exact(c->pdev, rho, E, phi, c->stream));
+    else
+        CK(launch_poisson(c->pdev, rho, E, phi, c->stream));
+    c->launches += 1;
     return SK_OK;
 }
 
@@ -468,6 +483,7 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
     PoissonPlan& P = c->plan;
     PoissonDev& d = c->pdev;
     d.k = k;
+    d.kd = P.kd;
     d.ps = P.ps;
     d.ncells = P.ncells;
     d.nlevels = P.nlevels;
@@ -495,6 +511,7 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
     d.deriv = up(P.deriv);
     d.h = up(P.h);
     d.ws = up(P.ws);
+    d.chol = up(P.chol);
     long total_blocks = 0;
     for (int l = 0; l < P.nlevels; ++l) total_blocks += P.level_n[l];
     CK(dalloc(&d.bws, (size_t)total_blocks * P.ps));
@@ -550,6 +567,11 @@ sk_status sk_ctx_set_stream(sk_ctx* c, void* s) {
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
     }
+    return SK_OK;
+}
+
+sk_status sk_ctx_set_exact_reductions(sk_ctx* c, int on) {
+    c->exact = on != 0;
     return SK_OK;
 }
 
@@ -762,7 +784,7 @@ sk_status sk_charge_density(sk_field* fe, sk_field* fi, double* rho) {
 
 sk_status sk_poisson_solve(sk_ctx* c, const double* rho, double* E, double* phi) {
     CK(cudaSetDevice(c->device));
-    CK(launch_poisson(c->pdev, rho, E, phi, c->stream));
+    if (sk_status rc = enq_poisson(c, rho, E, phi)) return rc;
     return after_launch(c);
 }
 
@@ -856,7 +878,7 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
     CK(dalloc(&s->phi, (size_t)c->grid.ncells * (c->P + 1)));
     // run.cpp:56 initial field
     if ((rc = enq_rho(s->f[0], s->f[1], s->rho))) return rc;
-    CK(launch_poisson(c->pdev, s->rho, s->E, s->phi, c->stream));
+    if ((rc = enq_poisson(c, s->rho, s->E, s->phi))) return rc;
     CK(cudaStreamSynchronize(c->stream));
     *out = s;
     return SK_OK;
@@ -925,9 +947,7 @@ sk_status enq_strang(sk_state* s) {
     if ((rc = mark(s, PH_X1)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 0))) return rc;
     if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     if ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho))) return rc;
-    if ((rc = mark(s, PH_POISSON))) return rc;
-    CK(launch_poisson(c->pdev, s->rho, s->E, s->phi, c->stream));
-    c->launches += 1;
+    if ((rc = mark(s, PH_POISSON)) || (rc = enq_poisson(c, s->rho, s->E, s->phi))) return rc;
     if ((rc = mark(s, PH_VTAB)) || (rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr)))
         return rc;
     if ((rc = mark(s, PH_V)) || (rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;

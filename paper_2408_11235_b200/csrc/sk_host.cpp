@@ -292,6 +292,31 @@ std::string poisson_plan_build(PoissonPlan& P, const Grid& g, int k, double pena
                     sigma * t1[a] * t1[b2] - d1[a] / h * t1[b2] - t1[a] * d1[b2] / h);
     }
 
+    // --- reference-LAPACK dpbtf2 factor (poisson.cpp:124-133), for the
+    //     exact-reduction mode that replays dpbtrs on the device ---
+    P.kd = kd;
+    P.chol = band;
+    for (int j = 0; j < n; ++j) {
+        double* col = P.chol.data() + (size_t)j * ldab;
+        double ajj = col[0];
+        if (ajj <= 0.0) return "Poisson factorization failed (matrix not positive definite)";
+        ajj = std::sqrt(ajj);
+        col[0] = ajj;
+        const int kn = kd < n - 1 - j ? kd : n - 1 - j;
+        if (kn > 0) {
+            const double r = 1.0 / ajj;
+            for (int i = 1; i <= kn; ++i) col[i] = r * col[i];
+            for (int jj = 0; jj < kn; ++jj) {
+                const double xj = col[1 + jj];
+                if (xj != 0.0) {
+                    const double temp = -1.0 * xj;
+                    double* c2 = P.chol.data() + (size_t)(j + 1 + jj) * ldab;
+                    for (int ii = jj; ii < kn; ++ii) c2[ii - jj] = c2[ii - jj] + col[1 + ii] * temp;
+                }
+            }
+        }
+    }
+
     // --- block tridiagonal view of the band ---
     auto full = [&](int r, int c) -> double {
         if (r < c) std::swap(r, c);

@@ -79,6 +79,8 @@ struct PoissonPlan {
     std::vector<double> h;           // cell widths
     std::vector<double> ws;          // weights of degree k+1
     std::vector<double> band;        // reference band (for residual checks)
+    std::vector<double> chol;        // dpbtf2 factor of band (exact-reduction mode)
+    int kd = 0;
     double symmetry_defect = 0.0;
 };
 std::string poisson_plan_build(PoissonPlan& P, const Grid& g, int k, double penalty_scale);

@@ -929,6 +929,76 @@ __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ P
 }
 
 // ---------------------------------------------------------------------------
+// exact-reduction mode: the reference's serial orders, so that a whole
+// trajectory is bitwise the reference's (parity mode, not the fast path)
+// ---------------------------------------------------------------------------
+// charge_density (poisson.cpp:194-216): per x dof, ions then electrons,
+// rows ascending, rho += ((sign*w_vn)*dv) * f
+template <int P>
+__global__ void rho_exact_kernel(const __grid_constant__ RhoArgs a) {
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xd >= a.nxd) return;
+    double acc = 0.0;
+    for (int s = 0; s < 2; ++s) {
+        const int sp = s == 0 ? 1 : 0;
+        const double sign = s == 0 ? 1.0 : -1.0;
+        const double dv = a.vg[sp]->dx;
+        const double* f = a.f[sp] + xd;
+        for (int r = 0; r < a.nrows; ++r) {
+            const int vn = r - (r / P) * P;
+            const double w = sign * a.basis.weights[vn] * dv;
+            acc += w * __ldg(f + (long long)r * a.ld);
+        }
+    }
+    a.rho[xd] = acc;
+}
+
+// PoissonOperator::solve with dpbtrs('L') = dtbsv('L','N') + dtbsv('L','T')
+// replayed in reference-BLAS order by one thread (poisson.cpp:135-192)
+__global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constant__ PoissonDev pd,
+                                                            const double* __restrict__ rho,
+                                                            double* __restrict__ E,
+                                                            double* __restrict__ phi) {
+    const int ps = pd.ps, k = pd.k, N = pd.ncells, n = N * ps, kd = pd.kd, ldab = kd + 1;
+    double* x = pd.xws;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int c = i / ps, m = i - (i / ps) * ps;
+        double val = 0.0;
+        for (int q = 0; q <= k; ++q) val += pd.interp[m * (k + 1) + q] * rho[c * (k + 1) + q];
+        x[i] = pd.ws[m] * pd.h[c] * val;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < n; ++j) {
+            if (x[j] != 0.0) {
+                const double* col = pd.chol + (long long)j * ldab;
+                x[j] = x[j] / col[0];
+                const double temp = x[j];
+                const int imax = n - 1 < j + kd ? n - 1 : j + kd;
+                for (int i = j + 1; i <= imax; ++i) x[i] = x[i] - temp * col[i - j];
+            }
+        }
+        for (int j = n - 1; j >= 0; --j) {
+            const double* col = pd.chol + (long long)j * ldab;
+            double temp = x[j];
+            const int imax = n - 1 < j + kd ? n - 1 : j + kd;
+            for (int i = imax; i >= j + 1; --i) temp = temp - col[i - j] * x[i];
+            temp = temp / col[0];
+            x[j] = temp;
+        }
+    }
+    __syncthreads();
+    if (phi)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) phi[i] = x[i];
+    for (int i = threadIdx.x; i < N * (k + 1); i += blockDim.x) {
+        const int c = i / (k + 1), m = i - (i / (k + 1)) * (k + 1);
+        double dphi = 0.0;
+        for (int q = 0; q < ps; ++q) dphi += pd.deriv[m * ps + q] * x[c * ps + q];
+        E[i] = -dphi / pd.h[c];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // step end: step counter, nonfinite -> SimulationError (stepper.cpp:99-102),
 // shrink cooldown gate (run.cpp:98-101)
 // ---------------------------------------------------------------------------
@@ -1371,6 +1441,17 @@ cudaError_t launch_rho(const RhoArgs& a, int nspecies, cudaStream_t s) {
 cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
                            cudaStream_t s) {
     poisson_kernel<<<1, 1024, 0, s>>>(pd, rho, E, phi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s) {
+    SK_DISPATCH_P(a.basis.p, (rho_exact_kernel<PP><<<(a.nxd + 63) / 64, 64, 0, s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double* E, double* phi,
+                                 cudaStream_t s) {
+    poisson_exact_kernel<<<1, 256, 0, s>>>(pd, rho, E, phi);
     return cudaGetLastError();
 }
 

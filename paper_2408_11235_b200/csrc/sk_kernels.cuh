@@ -104,6 +104,8 @@ struct RhoArgs {
 
 struct PoissonDev {
     int k, ps, ncells, nlevels;
+    int kd;
+    const double* chol;    // banded Cholesky factor (ldab = kd+1), exact mode
     int level_n[32];
     long long level_off[32];
     const double *Dinv, *Lo, *Up, *Alpha, *Gamma, *interp, *deriv, *h, *ws;
@@ -166,6 +168,10 @@ cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_rho(const RhoArgs& a, int nspecies_mask, cudaStream_t s);
 cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
                            cudaStream_t s);
+// exact-reduction mode: reference summation order / sequential dpbtrs
+cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s);
+cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double* E, double* phi,
+                                 cudaStream_t s);
 cudaError_t launch_step_end(DevStatus* st, int v_adjust, long long cooldown, int species_mask,
                             cudaStream_t s);
 cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s);

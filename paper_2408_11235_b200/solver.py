@@ -321,6 +321,10 @@ class Context:
     def set_eager_errors(self, on: bool):
         _check(N.lib().sk_ctx_set_eager_errors(self.h, int(on)))
 
+    def set_exact_reductions(self, on: bool):
+        """parity mode: reference-order charge density + sequential dpbtrs solve"""
+        _check(N.lib().sk_ctx_set_exact_reductions(self.h, int(on)))
+
     def synchronize(self):
         _check(N.lib().sk_ctx_synchronize(self.h))
 
@@ -524,12 +528,15 @@ class SimulationState:
     """build_initial_state (run.cpp:26-58) on the device; the step API of
     stepper.cpp:44-103 and the run() loop body of run.cpp:124-131."""
 
-    def __init__(self, cfg: RunConfig, device: int = 0, ctx: Context | None = None):
+    def __init__(self, cfg: RunConfig, device: int = 0, ctx: Context | None = None,
+                 exact: bool = False):
         self.cfg = cfg
         if ctx is None:
             grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
                                       cfg.refinement_ratio)
             ctx = Context(grid, cfg.k, cfg.penalty_scale, device)
+        if exact:
+            ctx.set_exact_reductions(True)
         self.ctx = ctx
         h = C.c_void_p()
         ccfg = cfg.to_c()
