@@ -118,6 +118,10 @@ sk_status sk_ctx_set_eager_errors(sk_ctx* ctx, int on);
  * (poisson.cpp:166-216), so whole trajectories are bitwise the reference's.
  * Off (default): parallel two-pass moment + block-cyclic-reduction solve. */
 sk_status sk_ctx_set_exact_reductions(sk_ctx* ctx, int on);
+/* Capacity of the deferred limiter-clamp list (troubled cells queued by the
+ * sweeps, clamped by a fixup kernel); above it the fixup rescans the sweep.
+ * Default and maximum 4 Mi cells; exposed for testing the rescan path. */
+sk_status sk_ctx_set_fix_capacity(sk_ctx* ctx, unsigned int cap);
 sk_status sk_ctx_synchronize(sk_ctx* ctx); /* also reports device-side errors */
 sk_status sk_stats_get(sk_ctx* ctx, sk_stats* out);
 sk_status sk_stats_reset(sk_ctx* ctx);

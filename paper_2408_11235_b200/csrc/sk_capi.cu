@@ -570,6 +570,12 @@ sk_status sk_ctx_set_stream(sk_ctx* c, void* s) {
     return SK_OK;
 }
 
+sk_status sk_ctx_set_fix_capacity(sk_ctx* c, unsigned int cap) {
+    if (cap > (1u << 22)) return fail(SK_ERR_RUNTIME, "fix capacity above the allocation");
+    c->fix_cap = cap;
+    return SK_OK;
+}
+
 sk_status sk_ctx_set_exact_reductions(sk_ctx* c, int on) {
     c->exact = on != 0;
     return SK_OK;

@@ -68,22 +68,9 @@ __device__ __forceinline__ void count_flags(unsigned long long* dst, unsigned t,
     }
 }
 
-// Out-of-line clamp for the (rare) list-overflow path: keeps the clamp's
-// register demand out of the streaming sweeps. Values travel by value.
-template <int P>
-struct ClampIO {
-    double v[P];
-    int flags;
-};
-template <int P>
-__device__ __noinline__ ClampIO<P> clamp_cell_slow(const Basis& b, double alpha, ClampIO<P> ul,
-                                                   ClampIO<P> ur, ClampIO<P> up) {
-    up.flags = inline_clamp<P>(b, alpha, ul.v, ur.v, up.v);
-    return up;
-}
-
-// Warp-aggregated append of a troubled cell to the deferred-clamp list.
-// Returns false when the list is full: the caller then clamps inline.
+// Warp-aggregated append of a troubled cell to the deferred-clamp list. The
+// counter keeps counting past the capacity so the fixup kernel can tell that
+// the list overflowed (it then rescans the whole sweep).
 __device__ __forceinline__ bool defer_push(unsigned int* count, unsigned int cap,
                                            unsigned long long* list, bool want,
                                            unsigned long long entry) {
@@ -323,7 +310,8 @@ struct XCfg {
     static constexpr int T = CPT * NT;              // output cells per tile
     static constexpr int WIN = (((T + 1) * P + 4) + 1) / 2 * 2;  // window doubles (+ slack), even
     static constexpr int NF = xnf<P>();
-    static constexpr int STAGE = ((WIN + NF + 1) / 2) * 2;
+    static constexpr int HDR = 4;                   // tile header (8 ints) written by the producer
+    static constexpr int STAGE = ((WIN + NF + HDR + 1) / 2) * 2;
     static constexpr int S = 3;                     // input stages
     static constexpr int SO = 3;                    // output stages
     static constexpr int OUT = T * P;
@@ -387,7 +375,7 @@ __device__ __forceinline__ void sts_cell(double* p, const double* u) {
     }
 }
 
-template <int P>
+template <int P, bool INLINE>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
@@ -413,18 +401,36 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
     if (warp == C::NC) {
         // ---------------- producer warp ----------------
         if (lane == 0) {
+            auto row_of = [&](const XTile& x) -> const double* {
+                return a.tab[x.sp] + ((long long)g.cls[x.b] * a.nlines + x.line) * C::NF;
+            };
+            XTile xn = decode_xtile(a, blockIdx.x, C::T);
+            int istar_next = blockIdx.x < ntot ? (int)__ldg(row_of(xn)) : 0;
             int it = 0;
             for (int t = blockIdx.x; t < ntot; t += G, ++it) {
                 const int stg = it % C::S;
+                const XTile x = xn;
+                const int istar = istar_next;
+                if (t + G < ntot) {  // hide the table latency behind this tile
+                    xn = decode_xtile(a, t + G, C::T);
+                    istar_next = (int)__ldg(row_of(xn));
+                }
                 mbar_wait(&empty[stg], ((it / C::S) & 1) ^ 1);
-                const XTile x = decode_xtile(a, t, C::T);
-                const double* row = a.tab[x.sp] + ((long long)g.cls[x.b] * a.nlines + x.line) * C::NF;
-                const int istar = (int)__ldg(row);
                 const int s0 = x.c0 + istar;
                 int vlo, vhi;
                 xvalid_range(a, x.b, vlo, vhi);
                 const int clo = max(s0, vlo), chi = min(s0 + x.nt + 1, vhi);
                 double* st = stages + stg * C::STAGE;
+                // decoded tile for the consumers (released by the arrive below)
+                int* hdr = reinterpret_cast<int*>(st + C::WIN + C::NF);
+                hdr[0] = x.sp;
+                hdr[1] = x.line;
+                hdr[2] = x.b;
+                hdr[3] = x.c0;
+                hdr[4] = x.nt;
+                hdr[5] = s0;
+                hdr[6] = clo;
+                hdr[7] = chi;
                 // element parity of window cell s0 in HBM decides the smem origin
                 const long long eg = ((long long)x.line * g.ncells + g.start[x.b] + s0) * P;
                 const int woff = (int)(eg & 1);
@@ -438,7 +444,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
                     bytes += (unsigned)(g1 - g0) * 8;
                 }
                 mbar_expect_tx(&full[stg], bytes);
-                tma_load_1d(st + C::WIN, row, C::NF * 8, &full[stg]);
+                tma_load_1d(st + C::WIN, row_of(x), C::NF * 8, &full[stg]);
                 if (chi > clo) {
                     double* dst = st + 2 + woff + (g0 - eg);
                     tma_load_1d(dst, a.src[x.sp] + g0, (unsigned)(g1 - g0) * 8, &full[stg]);
@@ -456,23 +462,20 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
     for (int t = blockIdx.x; t < ntot; t += G, ++it) {
         const int stg = it % C::S;
         mbar_wait(&full[stg], (it / C::S) & 1);
-        const XTile x = decode_xtile(a, t, C::T);
-        const int b = x.b, cells_b = g.cells[b];
         double* st = stages + stg * C::STAGE;
         const double* row = st + C::WIN;
-        const int istar = (int)row[0];
-        const int s0 = x.c0 + istar;
-        const long long lbase = (long long)x.line * g.ncells * P;
+        const int* hdr = reinterpret_cast<const int*>(st + C::WIN + C::NF);
+        const int sp = hdr[0], line = hdr[1], b = hdr[2], c0 = hdr[3], nt = hdr[4];
+        const int s0 = hdr[5], clo = hdr[6], chi = hdr[7];
+        const int cells_b = g.cells[b];
+        const long long lbase = (long long)line * g.ncells * P;
         const long long eg = lbase + ((long long)g.start[b] + s0) * P;
         const double* win = st + 2 + (int)(eg & 1);  // window cell w, node n at win[w*P+n]
-        int vlo, vhi;
-        xvalid_range(a, b, vlo, vhi);
-        const int clo = max(s0, vlo), chi = min(s0 + x.nt + 1, vhi);
-        if (clo > s0 || chi < s0 + x.nt + 1) {
+        if (clo > s0 || chi < s0 + nt + 1) {
             // walls (zero inflow), 3-block ghosts, periodic wrap
-            const double* src = a.src[x.sp] + lbase;
+            const double* src = a.src[sp] + lbase;
             double* w = const_cast<double*>(win);
-            for (int e = tid; e < (x.nt + 1) * P; e += C::NT) {
+            for (int e = tid; e < (nt + 1) * P; e += C::NT) {
                 const int wc = e / P, n = e - (e / P) * P;
                 const int s = s0 + wc;
                 if (s >= clo && s < chi) continue;
@@ -488,11 +491,10 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
             consumer_sync(C::NT);
         }
         double* ob = outs + (it % C::SO) * C::OUT;
-        const double alpha = row[1];
         double ul[C::CPT][P], ur[C::CPT][P], o[C::CPT][P];
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
-            const int c = min(tid + cc * C::NT, x.nt - 1);
+            const int c = min(tid + cc * C::NT, nt - 1);
             lds_cell<P>(win + c * P, ul[cc]);
             lds_cell<P>(win + (c + 1) * P, ur[cc]);
         }
@@ -516,28 +518,15 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
             const int c = tid + cc * C::NT;
-            if (c < x.nt) {
-                if (a.inline_sldg) {
+            if (c < nt) {
+                if constexpr (INLINE) {
                     const bool tr = inline_indicator<P>(a.basis, a.threshold, row + 2 + 2 * P * P,
                                                         row + 2 + 2 * P * P + P, ul[cc], ur[cc], o[cc]);
                     const unsigned long long entry =
-                        ((unsigned long long)(x.sp & 1) << 63) | ((unsigned long long)x.line << 32) |
-                        (unsigned)(g.start[b] + x.c0 + c);
-                    if (tr && !defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry)) {
-                        ClampIO<P> L, R, U;
-#pragma unroll
-                        for (int q = 0; q < P; ++q) {
-                            L.v[q] = ul[cc][q];
-                            R.v[q] = ur[cc][q];
-                            U.v[q] = o[cc][q];
-                        }
-                        U = clamp_cell_slow<P>(a.basis, alpha, L, R, U);
-#pragma unroll
-                        for (int q = 0; q < P; ++q) o[cc][q] = U.v[q];
-                        nt_t += U.flags & 1;
-                        nt_c += (U.flags >> 1) & 1;
-                        nt_o += (U.flags >> 2) & 1;
-                    }
+                        ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
+                        (unsigned)(g.start[b] + c0 + c);
+                    // queued for the fixup kernel; on overflow it rescans everything
+                    defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
                 }
 #pragma unroll
                 for (int m = 0; m < P; ++m) bad |= !isfinite(o[cc][m]);
@@ -551,13 +540,22 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
         if (tid == 0) bulk_wait_read<C::SO - 2>();  // out stage of tile it+1 is free
         consumer_sync(C::NT);
         if (tid == 0) {
-            double* dst = a.dst[x.sp] + lbase + (long long)(g.start[b] + x.c0) * P;
-            tma_store_1d(dst, ob, (unsigned)(x.nt * P * 8));
-            bulk_commit();
+            double* dst = a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P;
+            const unsigned bytes = (unsigned)(nt * P * 8);
+            if ((((unsigned long long)dst | bytes) & 15) == 0) {
+                tma_store_1d(dst, ob, bytes);
+                bulk_commit();
+            }
+        }
+        if ((((unsigned long long)(a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P) |
+              (unsigned)(nt * P * 8)) & 15) != 0) {
+            // odd P with an odd cell offset: plain coalesced stores of the tile
+            double* dst = a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P;
+            for (int e = tid; e < nt * P; e += C::NT) dst[e] = ob[e];
         }
     }
     if (tid == 0) bulk_wait<0>();
-    if (a.inline_sldg) count_flags(a.st->stats[a.nspecies == 1 ? a.species0 : 0], nt_t, nt_c, nt_o);
+    if constexpr (INLINE) count_flags(a.st->stats[a.nspecies == 1 ? a.species0 : 0], nt_t, nt_c, nt_o);
     if (a.check_finite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.st->nonfinite, 1);
 }
 
@@ -690,22 +688,7 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
                 const bool tr = inline_indicator<P>(a.basis, a.threshold, el, er, ul, ur, o);
                 const unsigned long long entry = ((unsigned long long)(sp & 1) << 63) |
                                                  ((unsigned long long)j << 32) | (unsigned)xd;
-                if (tr && !defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry)) {
-                    ClampIO<P> L, R, U;
-#pragma unroll
-                    for (int q = 0; q < P; ++q) {
-                        L.v[q] = ul[q];
-                        R.v[q] = ur[q];
-                        U.v[q] = o[q];
-                    }
-                    U = clamp_cell_slow<P>(a.basis, alpha, L, R, U);
-#pragma unroll
-                    for (int q = 0; q < P; ++q) o[q] = U.v[q];
-                    const int fl = U.flags;
-                    nt_t += fl & 1;
-                    nt_c += (fl >> 1) & 1;
-                    nt_o += (fl >> 2) & 1;
-                }
+                defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
             }
             double* op = out + (long long)j * P * ld + xd;
 #pragma unroll
@@ -729,79 +712,122 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
 // re-read exactly as the sweep saw them and the result is bitwise the same.
 // ---------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSweepArgs a) {
+__device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line, int cell, bool rescan,
+                                          unsigned* ct, unsigned* cc, unsigned* co) {
     constexpr int NF = xnf<P>();
-    const unsigned n = min(*a.fix_count, a.fix_cap);
     const Grid& g = a.grid;
-    unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned long long e = a.fix_list[i];
-        const int sp = (int)(e >> 63);
-        const int line = (int)((e >> 32) & 0x7fffffffu);
-        const int cell = (int)(e & 0xffffffffu);
-        int b = 0;
-        while (cell >= g.start[b + 1]) ++b;
-        const int local = cell - g.start[b];
-        const double* row = a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * NF;
-        const int istar = (int)row[0];
-        const double alpha = row[1];
-        const long long lbase = (long long)line * g.ncells * P;
-        const double* src = a.src[sp] + lbase;
-        double uu[2][P];
+    int b = 0;
+    while (cell >= g.start[b + 1]) ++b;
+    const int local = cell - g.start[b];
+    const double* row = a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * NF;
+    const int istar = (int)row[0];
+    const double alpha = row[1];
+    const long long lbase = (long long)line * g.ncells * P;
+    const double* src = a.src[sp] + lbase;
+    double uu[2][P];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            int s = local + istar + h;
-            for (int q = 0; q < P; ++q) {
-                double v;
-                if (a.periodic) {
-                    int ss = ((s % g.cells[b]) + g.cells[b]) % g.cells[b];
-                    v = src[(long long)(g.start[b] + ss) * P + q];
-                } else if (s >= 0 && s < g.cells[b]) {
-                    v = src[(long long)(g.start[b] + s) * P + q];
-                } else {
-                    v = x_fetch_outside<P>(a.basis, g, src, b, s, q);
-                }
-                uu[h][q] = v;
+    for (int h = 0; h < 2; ++h) {
+        const int s = local + istar + h;
+        for (int q = 0; q < P; ++q) {
+            double v;
+            if (a.periodic) {
+                const int ss = ((s % g.cells[b]) + g.cells[b]) % g.cells[b];
+                v = src[(long long)(g.start[b] + ss) * P + q];
+            } else if (s >= 0 && s < g.cells[b]) {
+                v = src[(long long)(g.start[b] + s) * P + q];
+            } else {
+                v = x_fetch_outside<P>(a.basis, g, src, b, s, q);
             }
+            uu[h][q] = v;
         }
-        double* up = a.dst[sp] + lbase + (long long)cell * P;
-        double o[P];
+    }
+    double* up = a.dst[sp] + lbase + (long long)cell * P;
+    double o[P];
 #pragma unroll
-        for (int q = 0; q < P; ++q) o[q] = up[q];
-        const int fl = inline_clamp<P>(a.basis, alpha, uu[0], uu[1], o);
+    for (int q = 0; q < P; ++q) o[q] = up[q];
+    if (rescan && !inline_indicator<P>(a.basis, a.threshold, row + 2 + 2 * P * P,
+                                       row + 2 + 2 * P * P + P, uu[0], uu[1], o))
+        return;
+    const int fl = inline_clamp<P>(a.basis, alpha, uu[0], uu[1], o);
 #pragma unroll
-        for (int q = 0; q < P; ++q) up[q] = o[q];
-        ct[sp] += fl & 1;
-        cc[sp] += (fl >> 1) & 1;
-        co[sp] += (fl >> 2) & 1;
+    for (int q = 0; q < P; ++q) up[q] = o[q];
+    ct[sp] += fl & 1;
+    cc[sp] += (fl >> 1) & 1;
+    co[sp] += (fl >> 2) & 1;
+}
+
+template <int P>
+__global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSweepArgs a) {
+    const unsigned cnt = *a.fix_count;
+    unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cnt <= a.fix_cap) {
+        for (long long i = i0; i < cnt; i += stride) {
+            const unsigned long long e = a.fix_list[i];
+            xfix_cell<P>(a, (int)(e >> 63), (int)((e >> 32) & 0x7fffffffu), (int)(e & 0xffffffffu),
+                         false, ct, cc, co);
+        }
+    } else {  // list overflowed: rescan every cell of the sweep
+        const long long ncell = (long long)a.nspecies * a.nlines * a.grid.ncells;
+        for (long long i = i0; i < ncell; i += stride) {
+            const int cell = (int)(i % a.grid.ncells);
+            const long long r = i / a.grid.ncells;
+            xfix_cell<P>(a, a.species0 + (int)(r / a.nlines), (int)(r % a.nlines), cell, true, ct, cc, co);
+        }
     }
     for (int sp = 0; sp < 2; ++sp) count_flags(a.st->stats[sp], ct[sp], cc[sp], co[sp]);
 }
 
 template <int P>
+__device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, int xd, bool rescan,
+                                          unsigned* ct, unsigned* cc, unsigned* co) {
+    const double* t = a.tab[sp];
+    const int nx = a.nxd;
+    const int istar = (int)t[xd];
+    const double alpha = t[nx + xd];
+    double ul[P], ur[P], o[P];
+    vload<P>(a.src[sp], a.ld, xd, j + istar, -a.gl, a.n + a.gr, a.periodic, a.n, ul);
+    vload<P>(a.src[sp], a.ld, xd, j + istar + 1, -a.gl, a.n + a.gr, a.periodic, a.n, ur);
+    double* op = a.dst[sp] + (long long)j * P * a.ld + xd;
+#pragma unroll
+    for (int m = 0; m < P; ++m) o[m] = op[m * a.ld];
+    if (rescan) {
+        double el[P], er[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            el[i] = t[(long long)(2 + 2 * P * P + i) * nx + xd];
+            er[i] = t[(long long)(2 + 2 * P * P + P + i) * nx + xd];
+        }
+        if (!inline_indicator<P>(a.basis, a.threshold, el, er, ul, ur, o)) return;
+    }
+    const int fl = inline_clamp<P>(a.basis, alpha, ul, ur, o);
+#pragma unroll
+    for (int m = 0; m < P; ++m) op[m * a.ld] = o[m];
+    ct[sp] += fl & 1;
+    cc[sp] += (fl >> 1) & 1;
+    co[sp] += (fl >> 2) & 1;
+}
+
+template <int P>
 __global__ void __launch_bounds__(128) vfix_kernel(const __grid_constant__ VSweepArgs a) {
-    const unsigned n = min(*a.fix_count, a.fix_cap);
+    const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned long long e = a.fix_list[i];
-        const int sp = (int)(e >> 63);
-        const int j = (int)((e >> 32) & 0x7fffffffu);
-        const int xd = (int)(e & 0xffffffffu);
-        const double* t = a.tab[sp];
-        const int istar = (int)t[xd];
-        const double alpha = t[a.nxd + xd];
-        double ul[P], ur[P], o[P];
-        vload<P>(a.src[sp], a.ld, xd, j + istar, -a.gl, a.n + a.gr, a.periodic, a.n, ul);
-        vload<P>(a.src[sp], a.ld, xd, j + istar + 1, -a.gl, a.n + a.gr, a.periodic, a.n, ur);
-        double* op = a.dst[sp] + (long long)j * P * a.ld + xd;
-#pragma unroll
-        for (int m = 0; m < P; ++m) o[m] = op[m * a.ld];
-        const int fl = inline_clamp<P>(a.basis, alpha, ul, ur, o);
-#pragma unroll
-        for (int m = 0; m < P; ++m) op[m * a.ld] = o[m];
-        ct[sp] += fl & 1;
-        cc[sp] += (fl >> 1) & 1;
-        co[sp] += (fl >> 2) & 1;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (cnt <= a.fix_cap) {
+        for (long long i = i0; i < cnt; i += stride) {
+            const unsigned long long e = a.fix_list[i];
+            vfix_cell<P>(a, (int)(e >> 63), (int)((e >> 32) & 0x7fffffffu), (int)(e & 0xffffffffu),
+                         false, ct, cc, co);
+        }
+    } else {  // list overflowed: rescan every cell
+        const long long ncell = (long long)a.nspecies * a.n * a.nxd;
+        for (long long i = i0; i < ncell; i += stride) {
+            const int xd = (int)(i % a.nxd);
+            const long long r = i / a.nxd;
+            vfix_cell<P>(a, a.species0 + (int)(r / a.n), (int)(r % a.n), xd, true, ct, cc, co);
+        }
     }
     for (int sp = 0; sp < 2; ++sp) count_flags(a.st->stats[sp], ct[sp], cc[sp], co[sp]);
 }
@@ -1377,7 +1403,7 @@ static int sm_count() {
     return n[dev & 31];
 }
 
-template <int P>
+template <int P, bool INLINE>
 static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     using Cf = XCfg<P>;
     const size_t smem = Cf::SMEM;
@@ -1385,8 +1411,11 @@ static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured & (1u << (dev & 31)))) {
-        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
+        if (e != cudaSuccess) return e;
+        // full shared-memory carveout so two pipelines share each SM
+        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         configured |= 1u << (dev & 31);
     }
@@ -1397,15 +1426,18 @@ static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     const long long ntot = (long long)a.nspecies * a.nlines * b.tile_start[a.grid.nblocks];
     const int nthreads = (Cf::NC + 1) * 32;
     int blocks_per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P>, nthreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE>, nthreads, smem);
     long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
     if (grid > ntot) grid = ntot;
-    xsweep_kernel<P><<<(int)grid, nthreads, smem, s>>>(b);
+    xsweep_kernel<P, INLINE><<<(int)grid, nthreads, smem, s>>>(b);
     return cudaGetLastError();
 }
 
 cudaError_t launch_xsweep(const XSweepArgs& a, int /*ntiles*/, cudaStream_t s) {
-    SK_DISPATCH_P(a.basis.p, return launch_xsweep_t<PP>(a, s));
+    if (a.inline_sldg)
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, true>(a, s)))
+    else
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, false>(a, s)))
     return cudaSuccess;
 }
 
