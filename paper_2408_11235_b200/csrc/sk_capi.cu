@@ -65,6 +65,9 @@ struct sk_ctx {
     double* pinned = nullptr;          // small pinned readback buffer
     long long launches = 0;            // kernels enqueued (bench gpu_launches)
     bool exact = false;                // exact-reduction (bitwise parity) mode
+    double* rho_fpart = nullptr;       // fused charge-density partials
+    size_t rho_fpart_n = 0;
+    unsigned long long* rho_corr = nullptr;
     unsigned long long* fix_list = nullptr;  // deferred limiter clamps
     unsigned int* fix_count = nullptr;
     unsigned int fix_cap = 0;
@@ -201,7 +204,7 @@ sk_status enq_xtab(sk_field** fs, int nspecies, double tau, const double* sqrt_m
 }
 
 sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
-                     int check_finite) {
+                     int check_finite, double* rho_out = nullptr) {
     sk_ctx* c = fs[0]->ctx;
     XSweepArgs a{};
     a.basis = c->basis;
@@ -224,11 +227,29 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;
+    if (rho_out) {  // fused charge density (both species in this launch)
+        a.rho_fuse = 1;
+        for (int i = 0; i < nspecies; ++i) {
+            a.vg[fs[i]->species] = fs[i]->vg;
+            a.charge_w[fs[i]->species] = fs[i]->species == 1 ? 1.0 : -1.0;
+        }
+        const size_t nxd = (size_t)c->grid.ncells * c->P;
+        const size_t need = (size_t)xsweep_rho_groups(a) * nxd;
+        if (need > c->rho_fpart_n || !c->rho_corr)  // sized in sk_state_create (no
+            return fail(SK_ERR_RUNTIME, "internal: fused rho buffers not sized");  // mallocs in capture)
+        a.rho_partial = c->rho_fpart;
+        a.rho_corr = c->rho_corr;
+        CK(cudaMemsetAsync(c->rho_corr, 0, sizeof(unsigned long long) * nxd, c->stream));
+    }
     if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
     c->launches += 1;
     if (inline_sldg) {
         CK(launch_xfix(a, c->stream));
+        c->launches += 1;
+    }
+    if (rho_out) {
+        CK(launch_rho_fused_reduce(a, rho_out, c->stream));
         c->launches += 1;
     }
     for (int i = 0; i < nspecies; ++i) fs[i]->swap();
@@ -550,6 +571,8 @@ sk_status sk_ctx_destroy(sk_ctx* c) {
     cudaFree(c->diag_out);
     cudaFree(c->fix_list);
     cudaFree(c->fix_count);
+    cudaFree(c->rho_fpart);
+    cudaFree(c->rho_corr);
     cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -879,6 +902,21 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         return rc;
     }
     const size_t ne = (size_t)c->grid.ncells * c->P;
+    {  // fused charge-density buffers, sized once (graph capture cannot malloc)
+        XSweepArgs a{};
+        a.basis = c->basis;
+        a.grid = c->grid;
+        a.nlines = cfg->v_cells * c->P;
+        a.nspecies = 2;
+        a.inline_sldg = cfg->limiter.inline_sldg;
+        const size_t need = (size_t)xsweep_rho_groups(a) * ne;
+        if (need > c->rho_fpart_n) {
+            if (c->rho_fpart) cudaFree(c->rho_fpart);
+            CK(dalloc(&c->rho_fpart, need));
+            c->rho_fpart_n = need;
+        }
+        if (!c->rho_corr) CK(dalloc(&c->rho_corr, ne));
+    }
     CK(dalloc(&s->E, ne));
     CK(dalloc(&s->rho, ne));
     CK(dalloc(&s->phi, (size_t)c->grid.ncells * (c->P + 1)));
@@ -950,9 +988,13 @@ sk_status enq_strang(sk_state* s) {
     const bool post = lim->indicator != 0;
     if ((rc = mark(s, PH_XTAB)) || (rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1)))
         return rc;
-    if ((rc = mark(s, PH_X1)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 0))) return rc;
+    // the charge-density moment rides along the first x sweep unless a post
+    // limiter still has to modify f (or the parity mode wants the serial order)
+    const bool fuse = !post && !c->exact;
+    if ((rc = mark(s, PH_X1)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr)))
+        return rc;
     if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
-    if ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho))) return rc;
+    if (!fuse && ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho)))) return rc;
     if ((rc = mark(s, PH_POISSON)) || (rc = enq_poisson(c, s->rho, s->E, s->phi))) return rc;
     if ((rc = mark(s, PH_VTAB)) || (rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr)))
         return rc;

@@ -310,7 +310,7 @@ struct XCfg {
     static constexpr int T = CPT * NT;              // output cells per tile
     static constexpr int WIN = (((T + 1) * P + 4) + 1) / 2 * 2;  // window doubles (+ slack), even
     static constexpr int NF = xnf<P>();
-    static constexpr int HDR = 4;                   // tile header (8 ints) written by the producer
+    static constexpr int HDR = 6;                   // tile header (8 ints + weight) from the producer
     static constexpr int STAGE = ((WIN + NF + HDR + 1) / 2) * 2;
     static constexpr int S = 3;                     // input stages
     static constexpr int SO = 3;                    // output stages
@@ -375,7 +375,7 @@ __device__ __forceinline__ void sts_cell(double* p, const double* u) {
     }
 }
 
-template <int P, bool INLINE>
+template <int P, bool INLINE, bool RHO>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
@@ -431,6 +431,10 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
                 hdr[5] = s0;
                 hdr[6] = clo;
                 hdr[7] = chi;
+                if (RHO) {  // (sign * w_vn) * dv of this v row (poisson.cpp:207)
+                    const int vn = x.line - (x.line / P) * P;
+                    reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * a.vg[x.sp]->dx;
+                }
                 // element parity of window cell s0 in HBM decides the smem origin
                 const long long eg = ((long long)x.line * g.ncells + g.start[x.b] + s0) * P;
                 const int woff = (int)(eg & 1);
@@ -458,6 +462,12 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
     const int tid = threadIdx.x;
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
+    double racc[RHO ? C::CPT : 1][P];  // fused charge-density partials of this thread's x dofs
+#pragma unroll
+    for (int cc = 0; cc < (RHO ? C::CPT : 1); ++cc)
+#pragma unroll
+        for (int n = 0; n < P; ++n) racc[cc][n] = 0.0;
+    int rcol_nt = 0, rcol_base = 0;
     int it = 0;
     for (int t = blockIdx.x; t < ntot; t += G, ++it) {
         const int stg = it % C::S;
@@ -468,6 +478,10 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
         const int sp = hdr[0], line = hdr[1], b = hdr[2], c0 = hdr[3], nt = hdr[4];
         const int s0 = hdr[5], clo = hdr[6], chi = hdr[7];
         const int cells_b = g.cells[b];
+        if constexpr (RHO) {
+            rcol_nt = nt;
+            rcol_base = g.start[b] + c0;
+        }
         const long long lbase = (long long)line * g.ncells * P;
         const long long eg = lbase + ((long long)g.start[b] + s0) * P;
         const double* win = st + 2 + (int)(eg & 1);  // window cell w, node n at win[w*P+n]
@@ -530,6 +544,11 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
                 }
 #pragma unroll
                 for (int m = 0; m < P; ++m) bad |= !isfinite(o[cc][m]);
+                if constexpr (RHO) {
+                    const double wdv = reinterpret_cast<const double*>(hdr)[4];
+#pragma unroll
+                    for (int m = 0; m < P; ++m) racc[cc][m] += wdv * o[cc][m];
+                }
                 sts_cell<P>(ob + c * P, o[cc]);
             }
         }
@@ -555,6 +574,20 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
         }
     }
     if (tid == 0) bulk_wait<0>();
+    if (RHO && rcol_nt > 0) {
+        // this CTA always saw the same tile column (grid is a multiple of the
+        // tiles per line): one partial row per (column, CTA group)
+        const int ntl = a.tile_start[g.nblocks];
+        double* prow = a.rho_partial + (long long)(blockIdx.x / ntl) * g.ncells * P;
+#pragma unroll
+        for (int cc = 0; cc < (RHO ? C::CPT : 1); ++cc) {
+            const int c = tid + cc * C::NT;
+            if (c < rcol_nt) {
+#pragma unroll
+                for (int n = 0; n < P; ++n) prow[(long long)(rcol_base + c) * P + n] = racc[cc][n];
+            }
+        }
+    }
     if constexpr (INLINE) count_flags(a.st->stats[a.nspecies == 1 ? a.species0 : 0], nt_t, nt_c, nt_o);
     if (a.check_finite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.st->nonfinite, 1);
 }
@@ -748,9 +781,22 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
     if (rescan && !inline_indicator<P>(a.basis, a.threshold, row + 2 + 2 * P * P,
                                        row + 2 + 2 * P * P + P, uu[0], uu[1], o))
         return;
+    double o0[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) o0[q] = o[q];
     const int fl = inline_clamp<P>(a.basis, alpha, uu[0], uu[1], o);
 #pragma unroll
     for (int q = 0; q < P; ++q) up[q] = o[q];
+    if (a.rho_fuse && (fl & 2)) {  // the fused moment summed the unclamped values
+        const int vn = line - (line / P) * P;
+        const double wdv = a.charge_w[sp] * a.basis.weights[vn] * a.vg[sp]->dx;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const double d = wdv * o[q] - wdv * o0[q];
+            atomicAdd(&a.rho_corr[(long long)cell * P + q],
+                      (unsigned long long)__double2ll_rn(d * 0x1p60));
+        }
+    }
     ct[sp] += fl & 1;
     cc[sp] += (fl >> 1) & 1;
     co[sp] += (fl >> 2) & 1;
@@ -1403,22 +1449,30 @@ static int sm_count() {
     return n[dev & 31];
 }
 
-template <int P, bool INLINE>
-static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
+template <int P, bool INLINE, bool RHO>
+static cudaError_t configure_xsweep() {
     using Cf = XCfg<P>;
-    const size_t smem = Cf::SMEM;
     static unsigned configured = 0;  // per-device bit
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured & (1u << (dev & 31)))) {
-        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
         if (e != cudaSuccess) return e;
         // full shared-memory carveout so two pipelines share each SM
-        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         configured |= 1u << (dev & 31);
     }
+    return cudaSuccess;
+}
+
+template <int P, bool INLINE, bool RHO>
+static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
+    using Cf = XCfg<P>;
+    const size_t smem = Cf::SMEM;
+    if (cudaError_t e = configure_xsweep<P, INLINE, RHO>()) return e;
     XSweepArgs b = a;
     b.tile_start[0] = 0;
     for (int i = 0; i < a.grid.nblocks; ++i)
@@ -1426,18 +1480,74 @@ static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     const long long ntot = (long long)a.nspecies * a.nlines * b.tile_start[a.grid.nblocks];
     const int nthreads = (Cf::NC + 1) * 32;
     int blocks_per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE>, nthreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO>, nthreads, smem);
     long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
+    if (a.rho_fuse) {
+        const int ntl = b.tile_start[a.grid.nblocks];
+        grid = grid >= ntl ? (grid / ntl) * ntl : ntl;
+        const long long lines = (long long)a.nspecies * a.nlines;
+        if (grid > lines * ntl) grid = lines * ntl;
+    }
     if (grid > ntot) grid = ntot;
-    xsweep_kernel<P, INLINE><<<(int)grid, nthreads, smem, s>>>(b);
+    xsweep_kernel<P, INLINE, RHO><<<(int)grid, nthreads, smem, s>>>(b);
+    return cudaGetLastError();
+}
+
+template <int P, bool INLINE>
+static int rho_groups_t(const XSweepArgs& a) {
+    using Cf = XCfg<P>;
+    configure_xsweep<P, INLINE, true>();
+    int ntl = 0;
+    for (int i = 0; i < a.grid.nblocks; ++i) ntl += (a.grid.cells[i] + Cf::T - 1) / Cf::T;
+    const long long ntot = (long long)a.nspecies * a.nlines * ntl;
+    int blocks_per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, true>,
+                                                  (Cf::NC + 1) * 32, Cf::SMEM);
+    long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
+    grid = grid >= ntl ? (grid / ntl) * ntl : ntl;
+    const long long lines = (long long)a.nspecies * a.nlines;
+    if (grid > lines * ntl) grid = lines * ntl;
+    if (grid > ntot) grid = ntot;
+    return (int)(grid / ntl);
+}
+
+int xsweep_rho_groups(const XSweepArgs& a) {
+    if (a.inline_sldg) {
+        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, true>(a)))
+    } else {
+        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, false>(a)))
+    }
+    return 0;
+}
+
+__global__ void rho_fused_reduce_kernel(const double* partial, const unsigned long long* corr,
+                                        int groups, int nxd, double* rho) {
+    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xd >= nxd) return;
+    double acc = 0.0;
+    for (int k = 0; k < groups; ++k) acc += partial[(long long)k * nxd + xd];
+    // fixed-point (2^-60) corrections from clamped cells
+    acc += (double)(long long)corr[xd] * 0x1p-60;
+    rho[xd] = acc;
+}
+
+cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s) {
+    const int nxd = a.grid.ncells * a.basis.p;
+    const int groups = xsweep_rho_groups(a);
+    rho_fused_reduce_kernel<<<(nxd + 127) / 128, 128, 0, s>>>(a.rho_partial, a.rho_corr, groups,
+                                                             nxd, rho);
     return cudaGetLastError();
 }
 
 cudaError_t launch_xsweep(const XSweepArgs& a, int /*ntiles*/, cudaStream_t s) {
-    if (a.inline_sldg)
-        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, true>(a, s)))
+    if (a.inline_sldg && a.rho_fuse)
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, true, true>(a, s)))
+    else if (a.inline_sldg)
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, true, false>(a, s)))
+    else if (a.rho_fuse)
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, false, true>(a, s)))
     else
-        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, false>(a, s)))
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, false, false>(a, s)))
     return cudaSuccess;
 }
 

@@ -51,6 +51,13 @@ struct XSweepArgs {
     unsigned long long* fix_list;
     unsigned int* fix_count;
     unsigned int fix_cap;
+    // fused charge-density moment (first x sweep, no post limiter): per-CTA
+    // partial sums [G/ntl][nx*P] + int64 fixed-point corrections of clamped cells
+    int rho_fuse;
+    double* rho_partial;
+    unsigned long long* rho_corr;
+    const DevVGrid* vg[2];
+    double charge_w[2];   // +1 ions, -1 electrons (poisson.cpp:202-214)
 };
 
 struct VTabArgs {
@@ -164,6 +171,9 @@ cudaError_t launch_xsweep(const XSweepArgs& a, int ntiles, cudaStream_t s);
 cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s);
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_xfix(const XSweepArgs& a, cudaStream_t s);
+// rho = sum of the fused partials + fixed-point corrections; returns #partials
+cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s);
+int xsweep_rho_groups(const XSweepArgs& a);
 cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_rho(const RhoArgs& a, int nspecies_mask, cudaStream_t s);
 cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
