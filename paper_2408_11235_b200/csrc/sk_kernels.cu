@@ -307,15 +307,14 @@ struct XCfg {
     static constexpr int NC = 8;                    // consumer warps
     static constexpr int NT = NC * 32;
     static constexpr int CPT = P <= 4 ? 2 : 1;
+    static constexpr int MINB = 2;                  // CTAs per SM the registers must allow
     static constexpr int T = CPT * NT;              // output cells per tile
     static constexpr int WIN = (((T + 1) * P + 4) + 1) / 2 * 2;  // window doubles (+ slack), even
     static constexpr int NF = xnf<P>();
     static constexpr int HDR = 6;                   // tile header (8 ints + weight) from the producer
     static constexpr int STAGE = ((WIN + NF + HDR + 1) / 2) * 2;
-    static constexpr int S = 3;                     // input stages
-    static constexpr int SO = 3;                    // output stages
-    static constexpr int OUT = T * P;
-    static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + SO * OUT) + 8 * 2 * S;
+    static constexpr int S = 5;                     // input stages (outputs go straight to HBM)
+    static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE) + 8 * 2 * S;
 };
 
 struct XTile {
@@ -376,13 +375,12 @@ __device__ __forceinline__ void sts_cell(double* p, const double* u) {
 }
 
 template <int P, bool INLINE, bool RHO>
-__global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
+__global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;                                   // S x STAGE
-    double* outs = smem + C::S * C::STAGE;                   // SO x OUT
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(outs + C::SO * C::OUT);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + C::S * C::STAGE);
     unsigned long long* empty = full + C::S;
     const Grid& g = a.grid;
     const int ntot = a.nspecies * a.nlines * a.tile_start[g.nblocks];
@@ -486,13 +484,17 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
         const long long eg = lbase + ((long long)g.start[b] + s0) * P;
         const double* win = st + 2 + (int)(eg & 1);  // window cell w, node n at win[w*P+n]
         if (clo > s0 || chi < s0 + nt + 1) {
-            // walls (zero inflow), 3-block ghosts, periodic wrap
+            // walls (zero inflow), 3-block ghosts, periodic wrap: only the
+            // window cells outside [clo, chi) -- usually |i*|+1 of them
             const double* src = a.src[sp] + lbase;
             double* w = const_cast<double*>(win);
-            for (int e = tid; e < (nt + 1) * P; e += C::NT) {
+            const int nlo = (max(clo, s0) - s0) * P;                 // [0, nlo)
+            const int nhi0 = (min(max(chi, s0), s0 + nt + 1) - s0) * P;  // [nhi0, (nt+1)P)
+            const int nfill = nlo + ((nt + 1) * P - nhi0);
+            for (int f = tid; f < nfill; f += C::NT) {
+                const int e = f < nlo ? f : nhi0 + (f - nlo);
                 const int wc = e / P, n = e - (e / P) * P;
                 const int s = s0 + wc;
-                if (s >= clo && s < chi) continue;
                 double v;
                 if (a.periodic) {
                     const int ss = ((s % cells_b) + cells_b) % cells_b;
@@ -504,7 +506,6 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
             }
             consumer_sync(C::NT);
         }
-        double* ob = outs + (it % C::SO) * C::OUT;
         double ul[C::CPT][P], ur[C::CPT][P], o[C::CPT][P];
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
@@ -529,6 +530,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
 #pragma unroll
             for (int cc = 0; cc < C::CPT; ++cc) o[cc][m] = acc[cc];
         }
+        double wdv = 0.0;
+        if constexpr (RHO) wdv = reinterpret_cast<const double*>(hdr)[4];
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
             const int c = tid + cc * C::NT;
@@ -545,35 +548,37 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, 2)
 #pragma unroll
                 for (int m = 0; m < P; ++m) bad |= !isfinite(o[cc][m]);
                 if constexpr (RHO) {
-                    const double wdv = reinterpret_cast<const double*>(hdr)[4];
 #pragma unroll
                     for (int m = 0; m < P; ++m) racc[cc][m] += wdv * o[cc][m];
                 }
-                sts_cell<P>(ob + c * P, o[cc]);
             }
         }
-        // window stage consumed
+        // the window stage is consumed: hand it back before the stores
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stg]);
-        fence_proxy_async();
-        if (tid == 0) bulk_wait_read<C::SO - 2>();  // out stage of tile it+1 is free
-        consumer_sync(C::NT);
-        if (tid == 0) {
-            double* dst = a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P;
-            const unsigned bytes = (unsigned)(nt * P * 8);
-            if ((((unsigned long long)dst | bytes) & 15) == 0) {
-                tma_store_1d(dst, ob, bytes);
-                bulk_commit();
+        double* dline = a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P;
+#pragma unroll
+        for (int cc = 0; cc < C::CPT; ++cc) {
+            const int c = tid + cc * C::NT;
+            if (c < nt) {
+                // straight to HBM: the warp's lanes cover 32 contiguous cells
+                double* dp = dline + (long long)c * P;
+                if constexpr (P % 2 == 0) {
+                    if ((((unsigned long long)dp) & 15) == 0) {
+#pragma unroll
+                        for (int i = 0; i < P / 2; ++i)
+                            reinterpret_cast<double2*>(dp)[i] = make_double2(o[cc][2 * i], o[cc][2 * i + 1]);
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
+                }
             }
         }
-        if ((((unsigned long long)(a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P) |
-              (unsigned)(nt * P * 8)) & 15) != 0) {
-            // odd P with an odd cell offset: plain coalesced stores of the tile
-            double* dst = a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P;
-            for (int e = tid; e < nt * P; e += C::NT) dst[e] = ob[e];
-        }
     }
-    if (tid == 0) bulk_wait<0>();
     if (RHO && rcol_nt > 0) {
         // this CTA always saw the same tile column (grid is a multiple of the
         // tiles per line): one partial row per (column, CTA group)
