@@ -515,6 +515,8 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
     for (int l = 0; l < P.nlevels; ++l) {
         d.level_n[l] = P.level_n[l];
         d.level_off[l] = P.level_off[l];
+        d.keep_off[l] = P.keep_off[l];
+        d.odd_off[l] = P.odd_off[l];
     }
     auto up = [&](const std::vector<double>& v) -> const double* {
         double* p = nullptr;
@@ -523,11 +525,12 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
         c->pbufs.push_back(p);
         return p;
     };
-    d.Dinv = up(P.Dinv);
-    d.Lo = up(P.Lo);
-    d.Up = up(P.Up);
-    d.Alpha = up(P.Alpha);
-    d.Gamma = up(P.Gamma);
+    d.AlphaT = up(P.AlphaT);
+    d.GammaT = up(P.GammaT);
+    d.LoT = up(P.LoT);
+    d.UpT = up(P.UpT);
+    d.DinvT = up(P.DinvT);
+    d.DinvTop = up(P.DinvTop);
     d.interp = up(P.interp);
     d.deriv = up(P.deriv);
     d.h = up(P.h);

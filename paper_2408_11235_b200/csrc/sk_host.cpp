@@ -335,55 +335,68 @@ std::string poisson_plan_build(PoissonPlan& P, const Grid& g, int k, double pena
 
     // --- block cyclic reduction (even positions survive each level) ---
     int Nl = N;
-    long off = 0;
+    long off = 0, koff = 0, ooff = 0;
+    auto put_t = [&](std::vector<double>& dst, long base, int rows, int r, const Mat& M) {
+        // [ps*ps][rows] block starting at base*pp
+        for (int e = 0; e < pp; ++e) dst[(size_t)base * pp + (size_t)e * rows + r] = M[e];
+    };
     while (true) {
+        const int Nn = (Nl + 1) / 2, No = Nl / 2;
         P.level_n.push_back(Nl);
         P.level_off.push_back(off);
+        P.keep_off.push_back(koff);
+        P.odd_off.push_back(ooff);
         std::vector<Mat> Dinv(Nl);
         for (int q = 0; q < Nl; ++q)
             if (!invert(D[q], Dinv[q], ps))
                 return "Poisson factorization failed (singular block in cyclic reduction)";
-        for (int q = 0; q < Nl; ++q) {
-            P.Dinv.insert(P.Dinv.end(), Dinv[q].begin(), Dinv[q].end());
-            P.Lo.insert(P.Lo.end(), Lo[q].begin(), Lo[q].end());
-            P.Up.insert(P.Up.end(), Up[q].begin(), Up[q].end());
+        if (Nl == 1) {
+            P.DinvTop = Dinv[0];
+            break;
         }
-        std::vector<Mat> alpha(Nl, Mat(pp, 0.0)), gamma(Nl, Mat(pp, 0.0));
-        const int Nn = (Nl + 1) / 2;
+        P.LoT.resize((size_t)(ooff + No) * pp);
+        P.UpT.resize((size_t)(ooff + No) * pp);
+        P.DinvT.resize((size_t)(ooff + No) * pp);
+        for (int o = 0; o < No; ++o) {
+            const int q = 2 * o + 1;
+            put_t(P.LoT, ooff, No, o, Lo[q]);
+            put_t(P.UpT, ooff, No, o, Up[q]);
+            put_t(P.DinvT, ooff, No, o, Dinv[q]);
+        }
+        P.AlphaT.resize((size_t)(koff + Nn) * pp, 0.0);
+        P.GammaT.resize((size_t)(koff + Nn) * pp, 0.0);
         std::vector<Mat> D2(Nn), Lo2(Nn, Mat(pp, 0.0)), Up2(Nn, Mat(pp, 0.0));
-        for (int r = 0; r < Nn && Nl > 1; ++r) {
+        for (int r = 0; r < Nn; ++r) {
             int q = 2 * r;
             Mat Dn = D[q];
+            Mat alpha(pp, 0.0), gamma(pp, 0.0);
             if (q - 1 >= 0) {
-                Mat a = matmul(Lo[q], Dinv[q - 1], ps);
-                for (auto& v : a) v = -v;
-                alpha[q] = a;
-                Mat t = matmul(a, Up[q - 1], ps);
+                alpha = matmul(Lo[q], Dinv[q - 1], ps);
+                for (auto& v : alpha) v = -v;
+                Mat t = matmul(alpha, Up[q - 1], ps);
                 for (int i = 0; i < pp; ++i) Dn[i] += t[i];
-                Lo2[r] = matmul(a, Lo[q - 1], ps);
+                Lo2[r] = matmul(alpha, Lo[q - 1], ps);
             }
             if (q + 1 < Nl) {
-                Mat gm = matmul(Up[q], Dinv[q + 1], ps);
-                for (auto& v : gm) v = -v;
-                gamma[q] = gm;
-                Mat t = matmul(gm, Lo[q + 1], ps);
+                gamma = matmul(Up[q], Dinv[q + 1], ps);
+                for (auto& v : gamma) v = -v;
+                Mat t = matmul(gamma, Lo[q + 1], ps);
                 for (int i = 0; i < pp; ++i) Dn[i] += t[i];
-                Up2[r] = matmul(gm, Up[q + 1], ps);
+                Up2[r] = matmul(gamma, Up[q + 1], ps);
             }
             // symmetrise the Schur complement against roundoff drift
             for (int a = 0; a < ps; ++a)
                 for (int b2 = a + 1; b2 < ps; ++b2) {
-                    double s = 0.5 * (Dn[a * ps + b2] + Dn[b2 * ps + a]);
-                    Dn[a * ps + b2] = Dn[b2 * ps + a] = s;
+                    double sm = 0.5 * (Dn[a * ps + b2] + Dn[b2 * ps + a]);
+                    Dn[a * ps + b2] = Dn[b2 * ps + a] = sm;
                 }
             D2[r] = Dn;
-        }
-        for (int q = 0; q < Nl; ++q) {
-            P.Alpha.insert(P.Alpha.end(), alpha[q].begin(), alpha[q].end());
-            P.Gamma.insert(P.Gamma.end(), gamma[q].begin(), gamma[q].end());
+            put_t(P.AlphaT, koff, Nn, r, alpha);
+            put_t(P.GammaT, koff, Nn, r, gamma);
         }
         off += Nl;
-        if (Nl == 1) break;
+        koff += Nn;
+        ooff += No;
         D.swap(D2);
         Lo.swap(Lo2);
         Up.swap(Up2);

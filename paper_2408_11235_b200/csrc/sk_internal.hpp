@@ -72,8 +72,12 @@ std::string grid_init(Grid& g, int nblocks, const double* left, const int* cells
 struct PoissonPlan {
     int k = 0, ps = 0, ncells = 0, nlevels = 0;
     std::vector<int> level_n;        // block rows per level
-    std::vector<long> level_off;     // offset (in blocks) of each level
-    std::vector<double> Dinv, Lo, Up, Alpha, Gamma;  // [sum level_n][ps*ps]
+    std::vector<long> level_off;     // offset (in blocks) of each level (vectors)
+    std::vector<long> keep_off;      // offset of the level's even rows (alpha/gamma)
+    std::vector<long> odd_off;       // offset of the level's odd rows (Lo/Up/Dinv)
+    // transposed + compacted for coalesced device reads: entry (m,n) of all
+    // rows of a level is contiguous, [level block][ps*ps][rows]
+    std::vector<double> AlphaT, GammaT, LoT, UpT, DinvT, DinvTop;
     std::vector<double> interp;      // (k+2)x(k+1)
     std::vector<double> deriv;       // (k+1)x(k+2)
     std::vector<double> h;           // cell widths

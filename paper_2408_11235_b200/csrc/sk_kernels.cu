@@ -314,7 +314,8 @@ struct XCfg {
     static constexpr int HDR = 6;                   // tile header (8 ints + weight) from the producer
     static constexpr int STAGE = ((WIN + NF + HDR + 1) / 2) * 2;
     static constexpr int S = 5;                     // input stages (outputs go straight to HBM)
-    static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE) + 8 * 2 * S;
+    static constexpr int RACC = T * P;              // fused charge-density accumulators (RHO)
+    static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + RACC) + 8 * 2 * S;
 };
 
 struct XTile {
@@ -380,7 +381,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     using C = XCfg<P>;
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;                                   // S x STAGE
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + C::S * C::STAGE);
+    double* racc = smem + C::S * C::STAGE;                   // [T][P] this CTA's column (RHO)
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(racc + C::RACC);
     unsigned long long* empty = full + C::S;
     const Grid& g = a.grid;
     const int ntot = a.nspecies * a.nlines * a.tile_start[g.nblocks];
@@ -460,11 +462,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     const int tid = threadIdx.x;
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
-    double racc[RHO ? C::CPT : 1][P];  // fused charge-density partials of this thread's x dofs
-#pragma unroll
-    for (int cc = 0; cc < (RHO ? C::CPT : 1); ++cc)
-#pragma unroll
-        for (int n = 0; n < P; ++n) racc[cc][n] = 0.0;
+    if constexpr (RHO)  // each thread owns its cells' x dofs: no sharing, no sync
+        for (int e = tid; e < C::RACC; e += C::NT) racc[e] = 0.0;
     int rcol_nt = 0, rcol_base = 0;
     int it = 0;
     for (int t = blockIdx.x; t < ntot; t += G, ++it) {
@@ -549,7 +548,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 for (int m = 0; m < P; ++m) bad |= !isfinite(o[cc][m]);
                 if constexpr (RHO) {
 #pragma unroll
-                    for (int m = 0; m < P; ++m) racc[cc][m] += wdv * o[cc][m];
+                    for (int m = 0; m < P; ++m) racc[c * P + m] += wdv * o[cc][m];
                 }
             }
         }
@@ -585,11 +584,11 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         const int ntl = a.tile_start[g.nblocks];
         double* prow = a.rho_partial + (long long)(blockIdx.x / ntl) * g.ncells * P;
 #pragma unroll
-        for (int cc = 0; cc < (RHO ? C::CPT : 1); ++cc) {
+        for (int cc = 0; cc < C::CPT; ++cc) {
             const int c = tid + cc * C::NT;
             if (c < rcol_nt) {
 #pragma unroll
-                for (int n = 0; n < P; ++n) prow[(long long)(rcol_base + c) * P + n] = racc[cc][n];
+                for (int n = 0; n < P; ++n) prow[(long long)(rcol_base + c) * P + n] = racc[c * P + n];
             }
         }
     }
@@ -913,94 +912,132 @@ __global__ void rho_reduce_kernel(const __grid_constant__ RhoArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Poisson: replay of the host block-cyclic-reduction plan (single CTA)
+// Poisson: replay of the host block-cyclic-reduction plan (single CTA, one
+// thread per block row per level, PS = k+2 compile-time)
 // ---------------------------------------------------------------------------
+// M is stored transposed over rows: entry (m,n) of row r at M[(m*PS+n)*rows + r]
+template <int PS>
+__device__ __forceinline__ void matvec_t(const double* __restrict__ M, int rows, int r,
+                                         const double* x, double* v, double sign) {
+#pragma unroll
+    for (int m = 0; m < PS; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int n = 0; n < PS; ++n) acc += M[(long long)(m * PS + n) * rows + r] * x[n];
+        v[m] += sign * acc;
+    }
+}
+
+template <int PS>
 __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ PoissonDev pd,
                                                        const double* __restrict__ rho,
                                                        double* __restrict__ E,
                                                        double* __restrict__ phi) {
-    const int ps = pd.ps, k = pd.k, N = pd.ncells, pp = ps * ps;
+    constexpr int pp = PS * PS;
+    const int k = PS - 2, N = pd.ncells;
     const int tid = threadIdx.x, nth = blockDim.x;
+    // vectors are SoA per level: b_l[m*Nl + q]
     double* b0 = pd.bws;
-    // load vector (poisson.cpp:135-149)
-    for (int i = tid; i < N * ps; i += nth) {
-        const int c = i / ps, m = i - (i / ps) * ps;
+    for (int i = tid; i < N * PS; i += nth) {  // load vector (poisson.cpp:135-149)
+        const int m = i / N, c = i - (i / N) * N;
         double val = 0.0;
+#pragma unroll
         for (int n = 0; n <= k; ++n) val += pd.interp[m * (k + 1) + n] * rho[c * (k + 1) + n];
         b0[i] = pd.ws[m] * pd.h[c] * val;
     }
     __syncthreads();
+    // reduction: b'_r = b_q + alpha_q b_{q-1} + gamma_q b_{q+1}, q = 2r;
+    // one thread per (row, component): coalesced over rows, short chains
     for (int l = 0; l + 1 < pd.nlevels; ++l) {
         const int Nl = pd.level_n[l], Nn = pd.level_n[l + 1];
-        const double* bl = pd.bws + pd.level_off[l] * ps;
-        double* bn = pd.bws + pd.level_off[l + 1] * ps;
-        const double* Al = pd.Alpha + pd.level_off[l] * pp;
-        const double* Gl = pd.Gamma + pd.level_off[l] * pp;
-        for (int i = tid; i < Nn * ps; i += nth) {
-            const int r = i / ps, m = i - (i / ps) * ps, q = 2 * r;
-            double v = bl[q * ps + m];
-            if (q - 1 >= 0)
-                for (int n = 0; n < ps; ++n) v += Al[(long long)q * pp + m * ps + n] * bl[(q - 1) * ps + n];
-            if (q + 1 < Nl)
-                for (int n = 0; n < ps; ++n) v += Gl[(long long)q * pp + m * ps + n] * bl[(q + 1) * ps + n];
-            bn[i] = v;
+        const double* bl = pd.bws + pd.level_off[l] * PS;
+        double* bn = pd.bws + pd.level_off[l + 1] * PS;
+        const double* Al = pd.AlphaT + pd.keep_off[l] * pp;
+        const double* Gl = pd.GammaT + pd.keep_off[l] * pp;
+        for (int i = tid; i < Nn * PS; i += nth) {
+            const int m = i / Nn, r = i - (i / Nn) * Nn, q = 2 * r;
+            double v = bl[m * Nl + q];
+            if (q - 1 >= 0) {
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < PS; ++n) acc += Al[(long long)(m * PS + n) * Nn + r] * bl[n * Nl + q - 1];
+                v += acc;
+            }
+            if (q + 1 < Nl) {
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < PS; ++n) acc += Gl[(long long)(m * PS + n) * Nn + r] * bl[n * Nl + q + 1];
+                v += acc;
+            }
+            bn[m * Nn + r] = v;
         }
         __syncthreads();
     }
     {
         const int L = pd.nlevels - 1;
-        const double* bt = pd.bws + pd.level_off[L] * ps;
-        double* xt = pd.xws + pd.level_off[L] * ps;
-        const double* Di = pd.Dinv + pd.level_off[L] * pp;
-        for (int m = tid; m < ps; m += nth) {
-            double v = 0.0;
-            for (int n = 0; n < ps; ++n) v += Di[m * ps + n] * bt[n];
-            xt[m] = v;
+        const double* bt = pd.bws + pd.level_off[L] * PS;
+        double* xt = pd.xws + pd.level_off[L] * PS;
+        if (tid < PS) {
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < PS; ++n) acc += pd.DinvTop[tid * PS + n] * bt[n];
+            xt[tid] = acc;
         }
         __syncthreads();
     }
+    // back substitution: even rows inherit, odd rows x = Dinv (b - Lo x_{q-1} - Up x_{q+1})
     for (int l = pd.nlevels - 2; l >= 0; --l) {
-        const int Nl = pd.level_n[l];
-        double* bl = pd.bws + pd.level_off[l] * ps;
-        double* xl = pd.xws + pd.level_off[l] * ps;
-        const double* xn = pd.xws + pd.level_off[l + 1] * ps;
-        const double* Lo = pd.Lo + pd.level_off[l] * pp;
-        const double* Up = pd.Up + pd.level_off[l] * pp;
-        const double* Di = pd.Dinv + pd.level_off[l] * pp;
-        for (int i = tid; i < Nl * ps; i += nth) {
-            const int q = i / ps, m = i - (i / ps) * ps;
+        const int Nl = pd.level_n[l], Nn = pd.level_n[l + 1], No = Nl / 2;
+        double* bl = pd.bws + pd.level_off[l] * PS;
+        double* xl = pd.xws + pd.level_off[l] * PS;
+        const double* xn = pd.xws + pd.level_off[l + 1] * PS;
+        const double* Lo = pd.LoT + pd.odd_off[l] * pp;
+        const double* Up = pd.UpT + pd.odd_off[l] * pp;
+        const double* Di = pd.DinvT + pd.odd_off[l] * pp;
+        // residual t = b - Lo x_{q-1} - Up x_{q+1} of odd rows, in place in b;
+        // even rows copy from the coarser level
+        for (int i = tid; i < Nl * PS; i += nth) {
+            const int m = i / Nl, q = i - (i / Nl) * Nl;
             if ((q & 1) == 0) {
-                xl[i] = xn[(q / 2) * ps + m];
+                xl[m * Nl + q] = xn[m * Nn + q / 2];
             } else {
-                double t = bl[i];
-                const double* xm = xn + ((q - 1) / 2) * ps;
-                for (int j = 0; j < ps; ++j) t -= Lo[(long long)q * pp + m * ps + j] * xm[j];
+                const int o = q >> 1;
+                double t = bl[m * Nl + q];
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < PS; ++n) acc += Lo[(long long)(m * PS + n) * No + o] * xn[n * Nn + o];
+                t -= acc;
                 if (q + 1 < Nl) {
-                    const double* xp = xn + ((q + 1) / 2) * ps;
-                    for (int j = 0; j < ps; ++j) t -= Up[(long long)q * pp + m * ps + j] * xp[j];
+                    acc = 0.0;
+#pragma unroll
+                    for (int n = 0; n < PS; ++n) acc += Up[(long long)(m * PS + n) * No + o] * xn[n * Nn + o + 1];
+                    t -= acc;
                 }
-                bl[i] = t;
+                bl[m * Nl + q] = t;
             }
         }
         __syncthreads();
-        for (int i = tid; i < Nl * ps; i += nth) {
-            const int q = i / ps, m = i - (i / ps) * ps;
-            if (q & 1) {
-                double v = 0.0;
-                for (int n = 0; n < ps; ++n) v += Di[(long long)q * pp + m * ps + n] * bl[q * ps + n];
-                xl[i] = v;
-            }
+        for (int i = tid; i < No * PS; i += nth) {
+            const int m = i / No, o = i - (i / No) * No, q = 2 * o + 1;
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < PS; ++n) acc += Di[(long long)(m * PS + n) * No + o] * bl[n * Nl + q];
+            xl[m * Nl + q] = acc;
         }
         __syncthreads();
     }
     const double* x0 = pd.xws;
     if (phi)
-        for (int i = tid; i < N * ps; i += nth) phi[i] = x0[i];
+        for (int i = tid; i < N * PS; i += nth) {
+            const int c = i / PS, m = i - (i / PS) * PS;
+            phi[i] = x0[m * N + c];
+        }
     // E = -phi' at the degree-k nodes (poisson.cpp:176-192)
     for (int i = tid; i < N * (k + 1); i += nth) {
         const int c = i / (k + 1), m = i - (i / (k + 1)) * (k + 1);
         double dphi = 0.0;
-        for (int n = 0; n < ps; ++n) dphi += pd.deriv[m * ps + n] * x0[c * ps + n];
+#pragma unroll
+        for (int n = 0; n < PS; ++n) dphi += pd.deriv[m * PS + n] * x0[n * N + c];
         E[i] = -dphi / pd.h[c];
     }
 }
@@ -1587,7 +1624,7 @@ cudaError_t launch_rho(const RhoArgs& a, int nspecies, cudaStream_t s) {
 
 cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
                            cudaStream_t s) {
-    poisson_kernel<<<1, 1024, 0, s>>>(pd, rho, E, phi);
+    SK_DISPATCH_P(pd.ps - 1, (poisson_kernel<PP + 1><<<1, 1024, 0, s>>>(pd, rho, E, phi)));
     return cudaGetLastError();
 }
 

@@ -114,9 +114,10 @@ struct PoissonDev {
     int kd;
     const double* chol;    // banded Cholesky factor (ldab = kd+1), exact mode
     int level_n[32];
-    long long level_off[32];
-    const double *Dinv, *Lo, *Up, *Alpha, *Gamma, *interp, *deriv, *h, *ws;
-    double *bws, *xws;     // [sum level_n * ps]
+    long long level_off[32], keep_off[32], odd_off[32];
+    const double *AlphaT, *GammaT, *LoT, *UpT, *DinvT, *DinvTop;  // see PoissonPlan
+    const double *interp, *deriv, *h, *ws;
+    double *bws, *xws;     // per level SoA [ps][rows]
 };
 
 struct ShrinkArgs {
