@@ -653,92 +653,111 @@ __device__ __forceinline__ void vload(const double* f, long long ld, int xd, int
 template <int P>
 __host__ __device__ constexpr int vring() { return P <= 4 ? 8 : 4; }
 
+// issue the P node rows of source cell s (pointer gp = its row-0 address) into
+// a ring slot; cells outside [lo, hi) are zero-filled without a global read
 template <int P>
-__device__ __forceinline__ void vissue(const double* f, long long ld, int xd, int s, int lo, int hi,
-                                       int periodic, int ncell, double* slot) {
-    if (periodic) s = ((s % ncell) + ncell) % ncell;
-    const bool valid = s >= lo && s < hi;
-    const double* p = valid ? f + (long long)s * P * ld + xd : f;
+__device__ __forceinline__ void vissue(const double* gp, long long ld, bool valid, double* slot) {
 #pragma unroll
-    for (int n = 0; n < P; ++n) cp_async8(slot + n * kVThreads, valid ? p + n * ld : f, valid);
+    for (int n = 0; n < P; ++n) cp_async8(slot + n * kVThreads, valid ? gp + n * ld : gp, valid);
 }
 
-template <int P>
+template <int P, bool INLINE, bool PERIODIC>
 __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant__ VSweepArgs a) {
-    constexpr int kVRing = vring<P>();
-    __shared__ double ring[kVRing * P * kVThreads];
+    constexpr int R = vring<P>();
+    static_assert(kVChunk % R == 0, "chunk must be a multiple of the ring depth");
+    __shared__ double ring[R * P * kVThreads];
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
     const int j0 = blockIdx.y * kVChunk;
     const int j1 = min(j0 + kVChunk, a.n);
-    unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
     double* my = ring + threadIdx.x;
     if (xd < a.nxd) {
         const double* t = a.tab[sp];
         const int nx = a.nxd;
         const int istar = (int)t[xd];
-        const double* f = a.src[sp];
-        double* out = a.dst[sp];
+        const double* f = a.src[sp] + xd;
         const long long ld = a.ld;
+        const long long cstride = (long long)P * ld;  // one v cell
         const int lo = -a.gl, hi = a.n + a.gr;
-        const int sfirst = j0 + istar;  // source cell of ul for j0
-        const int ncells = (j1 - j0) + 1;
-        // prologue: cells 0..R-2 of this thread's source run
+        const int ncells = (j1 - j0) + 1;              // source cells of this run
+        // next source cell to issue and its row pointer (non-periodic: linear walk)
+        int s_iss = j0 + istar;
+        auto src_of = [&](int s) -> const double* {
+            if constexpr (PERIODIC) s = ((s % a.n) + a.n) % a.n;
+            return f + (long long)s * cstride;
+        };
+        auto ok = [&](int s) -> bool {
+            if constexpr (PERIODIC) return true;
+            return (unsigned)(s - lo) < (unsigned)(hi - lo);
+        };
+        const double* g_iss = src_of(s_iss);
 #pragma unroll
-        for (int c = 0; c < kVRing - 1; ++c) {
-            if (c < ncells) vissue<P>(f, ld, xd, sfirst + c, lo, hi, a.periodic, a.n, my + (c % kVRing) * P * kVThreads);
+        for (int c = 0; c < R - 1; ++c) {  // prologue: cells 0..R-2
+            if (c < ncells) vissue<P>(g_iss, ld, ok(s_iss), my + c * P * kVThreads);
             cp_commit();
+            ++s_iss;
+            g_iss = PERIODIC ? src_of(s_iss) : g_iss + cstride;
         }
         const double alpha = t[nx + xd];
-        double A[P * P], B[P * P], el[P], er[P];
+        double A[P * P], B[P * P], el[INLINE ? P : 1], er[INLINE ? P : 1];
 #pragma unroll
         for (int i = 0; i < P * P; ++i) {
             A[i] = t[(long long)(2 + i) * nx + xd];
             B[i] = t[(long long)(2 + P * P + i) * nx + xd];
         }
-        if (a.inline_sldg) {
+        if constexpr (INLINE) {
 #pragma unroll
             for (int i = 0; i < P; ++i) {
                 el[i] = t[(long long)(2 + 2 * P * P + i) * nx + xd];
                 er[i] = t[(long long)(2 + 2 * P * P + P + i) * nx + xd];
             }
         }
+        (void)alpha;
         double ul[P], ur[P];
-        cp_wait<kVRing - 2>();
+        cp_wait<R - 2>();
 #pragma unroll
         for (int n = 0; n < P; ++n) ul[n] = my[n * kVThreads];
-        if (kVRing - 1 < ncells) vissue<P>(f, ld, xd, sfirst + kVRing - 1, lo, hi, a.periodic, a.n, my + ((kVRing - 1) % kVRing) * P * kVThreads);
+        if (R - 1 < ncells) vissue<P>(g_iss, ld, ok(s_iss), my + (R - 1) * P * kVThreads);
         cp_commit();
-        for (int j = j0; j < j1; ++j) {
-            const int c = j - j0 + 1;  // ring index of ur
-            cp_wait<kVRing - 2>();
-            const double* sl = my + (c % kVRing) * P * kVThreads;
+        ++s_iss;
+        g_iss = PERIODIC ? src_of(s_iss) : g_iss + cstride;
+        double* op = a.dst[sp] + xd + (long long)j0 * cstride;
+        for (int jb = 0; jb < kVChunk; jb += R) {
 #pragma unroll
-            for (int n = 0; n < P; ++n) ur[n] = sl[n * kVThreads];
-            const int cn = c + kVRing - 1;
-            if (cn < ncells) vissue<P>(f, ld, xd, sfirst + cn, lo, hi, a.periodic, a.n, my + (cn % kVRing) * P * kVThreads);
-            cp_commit();
-            double o[P];
-            project_cell<P>(A, B, ul, ur, o);
-            if (a.inline_sldg) {
-                const bool tr = inline_indicator<P>(a.basis, a.threshold, el, er, ul, ur, o);
-                const unsigned long long entry = ((unsigned long long)(sp & 1) << 63) |
-                                                 ((unsigned long long)j << 32) | (unsigned)xd;
-                defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+            for (int u = 0; u < R; ++u) {
+                const int jj = jb + u;  // output cell j0 + jj; ur = ring cell jj+1
+                if (j0 + jj < j1) {
+                    cp_wait<R - 2>();
+                    const double* sl = my + ((u + 1) % R) * P * kVThreads;
+#pragma unroll
+                    for (int n = 0; n < P; ++n) ur[n] = sl[n * kVThreads];
+                    if (jj + R < ncells) vissue<P>(g_iss, ld, ok(s_iss), my + u * P * kVThreads);
+                    cp_commit();
+                    ++s_iss;
+                    g_iss = PERIODIC ? src_of(s_iss) : g_iss + cstride;
+                    double o[P];
+                    project_cell<P>(A, B, ul, ur, o);
+                    if constexpr (INLINE) {
+                        const bool tr = inline_indicator<P>(a.basis, a.threshold, el, er, ul, ur, o);
+                        const unsigned long long entry = ((unsigned long long)(sp & 1) << 63) |
+                                                         ((unsigned long long)(j0 + jj) << 32) |
+                                                         (unsigned)xd;
+                        defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+                    }
+#pragma unroll
+                    for (int m = 0; m < P; ++m) {
+                        bad |= !isfinite(o[m]);
+                        op[m * ld] = o[m];
+                    }
+                    op += cstride;
+#pragma unroll
+                    for (int n = 0; n < P; ++n) ul[n] = ur[n];
+                }
             }
-            double* op = out + (long long)j * P * ld + xd;
-#pragma unroll
-            for (int m = 0; m < P; ++m) {
-                bad |= !isfinite(o[m]);
-                op[m * ld] = o[m];
-            }
-#pragma unroll
-            for (int n = 0; n < P; ++n) ul[n] = ur[n];
         }
         cp_wait<0>();
     }
-    if (a.inline_sldg) count_flags(a.st->stats[sp], nt_t, nt_c, nt_o);
     if (a.check_finite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
         atomicOr(&a.st->nonfinite, 1);
 }
@@ -1611,7 +1630,12 @@ cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s) {
 
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.n + kVChunk - 1) / kVChunk, a.nspecies);
-    SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP><<<grid, kVThreads, 0, s>>>(a)));
+    if (a.periodic)
+        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, true><<<grid, kVThreads, 0, s>>>(a)))
+    else if (a.inline_sldg)
+        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, false><<<grid, kVThreads, 0, s>>>(a)))
+    else
+        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, false, false><<<grid, kVThreads, 0, s>>>(a)))
     return cudaGetLastError();
 }
 
