@@ -139,6 +139,14 @@ sk_status sk_field_upload(sk_field* f, const double* host, size_t count);
 sk_status sk_field_download(sk_field* f, double* host, size_t count);
 sk_status sk_field_upload_async(sk_field* f, const double* host_pinned, size_t count);
 sk_status sk_field_download_async(sk_field* f, double* host_pinned, size_t count);
+/* v-shard of a NodalField for a multi-GPU run sharded along v: this rank holds
+ * global v cells [cell0, cell0+ncell) plus `halo` cells below and above for
+ * the v sweep. Storage rows are contiguous, so each halo is one contiguous
+ * device block: sk_field_halo(side 0 lower / 1 upper, send 1: interior edge
+ * rows to send, 0: halo rows to receive into). */
+sk_status sk_field_create_shard(sk_ctx* ctx, int species, double v_left, double v_right,
+                                int v_cells_global, int cell0, int ncell, int halo, sk_field** out);
+sk_status sk_field_halo(sk_field* f, int side, int send, double** ptr_dev, size_t* count);
 /* v grid: left, dx, cells (synchronises: the cut-off updates it on device) */
 sk_status sk_field_v_grid(sk_field* f, double* left, double* dx, int* cells);
 /* run.cpp:41-46 blob f = (2 pi)^-1/2 exp(-x^2/(2 sigma^2)) exp(-v^2/2) */
@@ -173,6 +181,15 @@ sk_status sk_state_destroy(sk_state* s);
 sk_field* sk_state_field(sk_state* s, int species);
 double* sk_state_E_dev(sk_state* s);
 sk_status sk_state_download_E(sk_state* s, double* host, size_t count);
+/* v-sharded state: rank `rank` of `nranks` holds v_cells/nranks cells of each
+ * species plus `halo` cells; the step runs as phase 2 (x half sweep + local
+ * rho) -> caller all-reduces rho (sk_state_rho_dev) and exchanges the halos
+ * -> phase 3 (Poisson, v sweep, x half sweep). Phases 0/1: local initial rho
+ * and the Poisson solve of the all-reduced rho (initial field). */
+sk_status sk_state_create_shard(sk_ctx* ctx, const sk_run_config* cfg, int rank, int nranks,
+                                int halo, sk_state** out);
+double* sk_state_rho_dev(sk_state* s);
+sk_status sk_state_phase(sk_state* s, int phase);
 /* one strang_step (no shrink); max_ghost < 0: run()'s rule */
 sk_status sk_strang_step(sk_state* s);
 /* one run() loop body: strang_step + shrink checks with the 10-step cooldown */

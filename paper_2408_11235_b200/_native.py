@@ -70,6 +70,11 @@ SIGNATURES = {
     "sk_field_upload_async": (_i, [_vp, _dp, _sz]),
     "sk_field_download_async": (_i, [_vp, _dp, _sz]),
     "sk_field_v_grid": (_i, [_vp, _dp, _dp, _ip]),
+    "sk_field_create_shard": (_i, [_vp, _i, _d, _d, _i, _i, _i, _i, C.POINTER(_vp)]),
+    "sk_field_halo": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_sz)]),
+    "sk_state_create_shard": (_i, [_vp, C.POINTER(sk_run_config), _i, _i, _i, C.POINTER(_vp)]),
+    "sk_state_rho_dev": (_vp, [_vp]),
+    "sk_state_phase": (_i, [_vp, _i]),
     "sk_field_fill_blob": (_i, [_vp, _d]),
     "sk_advect_x": (_i, [_vp, _d, _d, _i, C.POINTER(sk_limiter), _i, C.c_long]),
     "sk_advect_v": (_i, [_vp, _d, _vp, _d, _d, _i, C.POINTER(sk_limiter)]),

@@ -76,8 +76,12 @@ struct sk_ctx {
 struct sk_field {
     sk_ctx* ctx = nullptr;
     int species = 0;
-    int nv = 0;
-    size_t n = 0;
+    int nv = 0;                        // v cells held (interior)
+    int nv_global = 0;
+    int cell0 = 0;                     // first global v cell (v-shard)
+    int halo = 0;                      // halo cells stored below and above
+    size_t n = 0;                      // interior doubles
+    size_t halo_off = 0;               // doubles from buffer start to the interior
     double* buf[2] = {nullptr, nullptr};
     int cur = 0;
     DevVGrid* vg = nullptr;            // device
@@ -85,9 +89,11 @@ struct sk_field {
     double* vtab = nullptr;            // [vnf][nx*P]
     double* ttab = nullptr;            // shrink transfer [nv][4][P*P]
     int* tcell = nullptr;              // [nv][4]
-    double* cur_ptr() { return buf[cur]; }
-    double* other_ptr() { return buf[cur ^ 1]; }
+    double* cur_ptr() { return buf[cur] + halo_off; }
+    double* other_ptr() { return buf[cur ^ 1] + halo_off; }
     void swap() { cur ^= 1; }
+    int gl() const { return cell0 > 0 ? halo : 0; }
+    int gr() const { return cell0 + nv < nv_global ? halo : 0; }
 };
 
 struct sk_state {
@@ -103,6 +109,7 @@ struct sk_state {
     cudaGraphExec_t graph2 = nullptr;  // two loop bodies
     int graph_cur0 = -1, graph_cur1 = -1;
     long long graph_launches = 0;      // kernels per graph replay
+    int rank = 0, nranks = 1;          // v-shard of a multi-GPU run
     // optional per-phase CUDA-event timing (sk_state_set_phase_timing)
     bool timing = false;
     std::vector<std::pair<int, cudaEvent_t>> marks;
@@ -133,6 +140,10 @@ sk_status collect_errors(sk_ctx* c) {
             break;
         case 3:
             msg = "step " + std::to_string(step) + ": nonfinite values in the density function";
+            break;
+        case 5:
+            msg = "step " + std::to_string(step) + ": insufficient v halo: v sweep shifts " +
+                  std::to_string(h.err_need) + " cells, shard halo is " + std::to_string(h.err_have);
             break;
         default:
             msg = "velocity shrink: transfer table overflow";
@@ -270,6 +281,9 @@ sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, con
     }
     a.E = E;
     a.tau = tau;
+    a.st = c->st;
+    a.halo_lo = fs[0]->gl() > 0 ? fs[0]->gl() : -1;
+    a.halo_hi = fs[0]->gr() > 0 ? fs[0]->gr() : -1;
     a.nxd = c->grid.ncells * c->P;
     a.nspecies = nspecies;
     a.species0 = nspecies == 2 ? 0 : fs[0]->species;
@@ -295,7 +309,8 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.nxd = c->grid.ncells * c->P;
     a.ld = a.nxd;
     a.n = fs[0]->nv;
-    a.gl = a.gr = 0;
+    a.gl = fs[0]->gl();
+    a.gr = fs[0]->gr();
     a.nspecies = nspecies;
     a.species0 = nspecies == 2 ? 0 : fs[0]->species;
     a.inline_sldg = inline_sldg;
@@ -640,35 +655,61 @@ sk_status sk_stats_reset(sk_ctx* c) {
 }
 
 // ---------------------------------------------------------------------------
-sk_status sk_field_create(sk_ctx* c, int species, double v_left, double v_right, int v_cells,
-                          sk_field** out) {
+sk_status sk_field_create_shard(sk_ctx* c, int species, double v_left, double v_right,
+                                int v_cells_global, int cell0, int ncell, int halo, sk_field** out) {
     *out = nullptr;
     if (species != 0 && species != 1) return fail(SK_ERR_RUNTIME, "species must be 0 or 1");
-    if (!(v_right > v_left && v_cells >= 1))
+    if (!(v_right > v_left && v_cells_global >= 1))
         return fail(SK_ERR_RUNTIME, "Grid1D::uniform: invalid extent or cell count");
-    double dv = (v_right - v_left) / v_cells;  // grid.cpp:31-34
-    double right = v_left + v_cells * dv;
+    if (cell0 < 0 || ncell < 1 || cell0 + ncell > v_cells_global || halo < 0)
+        return fail(SK_ERR_RUNTIME, "v shard: invalid cell range");
+    double dv = (v_right - v_left) / v_cells_global;  // grid.cpp:31-34
+    double right = v_left + v_cells_global * dv;
     if (!(std::abs(v_left + right) <= 1e-12 * (right - v_left)))
         return fail(SK_ERR_RUNTIME, "NodalField: v grid must be symmetric about 0");
     CK(cudaSetDevice(c->device));
     auto* f = new sk_field;
     f->ctx = c;
     f->species = species;
-    f->nv = v_cells;
+    f->nv = ncell;
+    f->nv_global = v_cells_global;
+    f->cell0 = cell0;
+    f->halo = halo;
     const int P = c->P;
-    f->n = (size_t)c->grid.ncells * v_cells * P * P;
-    CK(dalloc(&f->buf[0], f->n));
-    CK(dalloc(&f->buf[1], f->n));
-    CK(cudaMemsetAsync(f->buf[0], 0, sizeof(double) * f->n, c->stream));
+    const size_t row = (size_t)c->grid.ncells * P;  // one v row (x line)
+    f->n = (size_t)ncell * P * row;
+    f->halo_off = (size_t)halo * P * row;
+    const size_t total = f->n + 2 * f->halo_off;
+    CK(dalloc(&f->buf[0], total + 8));  // +8: bulk copies may round up past the end
+    CK(dalloc(&f->buf[1], total + 8));
+    CK(cudaMemsetAsync(f->buf[0], 0, sizeof(double) * total, c->stream));
+    CK(cudaMemsetAsync(f->buf[1], 0, sizeof(double) * total, c->stream));
     CK(dalloc(&f->vg, 1));
-    DevVGrid vg{v_left, dv, v_cells, 0};
+    DevVGrid vg{v_left, dv, v_cells_global, cell0};
     CK(cudaMemcpy(f->vg, &vg, sizeof vg, cudaMemcpyHostToDevice));
-    CK(dalloc(&f->xtab, (size_t)c->grid.nclass * v_cells * P * xtab_nf(P)));
+    CK(dalloc(&f->xtab, (size_t)c->grid.nclass * ncell * P * xtab_nf(P)));
     CK(dalloc(&f->vtab, (size_t)vtab_nf(P) * c->grid.ncells * P));
-    CK(dalloc(&f->ttab, (size_t)v_cells * 4 * P * P));
-    CK(dalloc(&f->tcell, (size_t)v_cells * 4));
+    CK(dalloc(&f->ttab, (size_t)v_cells_global * 4 * P * P));
+    CK(dalloc(&f->tcell, (size_t)v_cells_global * 4));
     CK(cudaStreamSynchronize(c->stream));
     *out = f;
+    return SK_OK;
+}
+
+sk_status sk_field_create(sk_ctx* c, int species, double v_left, double v_right, int v_cells,
+                          sk_field** out) {
+    return sk_field_create_shard(c, species, v_left, v_right, v_cells, 0, v_cells, 0, out);
+}
+
+sk_status sk_field_halo(sk_field* f, int side, int send, double** ptr, size_t* count) {
+    if (f->halo == 0) return fail(SK_ERR_RUNTIME, "field has no v halo");
+    const size_t hrows = f->halo_off;  // halo cells * P * row doubles
+    double* in = f->cur_ptr();
+    if (side == 0)
+        *ptr = send ? in : in - hrows;
+    else
+        *ptr = send ? in + (f->n - hrows) : in + f->n;
+    *count = hrows;
     return SK_OK;
 }
 
@@ -737,16 +778,16 @@ sk_status sk_field_fill_blob(sk_field* f, double sigma) {
     sk_status rc = sk_field_v_grid(f, &vleft, &vdx, &vcells);
     if (rc) return rc;
     // run.cpp:19-22 gaussian_blob = (c*exp(x part))*exp(v part); field.cpp:42-50
-    std::vector<double> gx((size_t)g.ncells * P), gv((size_t)vcells * P);
+    std::vector<double> gx((size_t)g.ncells * P), gv((size_t)f->nv * P);
     const double cst = 1.0 / std::sqrt(2.0 * M_PI);
     for (int xc = 0; xc < g.ncells; ++xc)
         for (int xn = 0; xn < P; ++xn) {
             double x = grid_cell_left(g, xc) + grid_cell_width(g, xc) * c->basis.nodes[xn];
             gx[(size_t)xc * P + xn] = cst * std::exp(-x * x / (2.0 * sigma * sigma));
         }
-    for (int vc = 0; vc < vcells; ++vc)
+    for (int vc = 0; vc < f->nv; ++vc)
         for (int vn = 0; vn < P; ++vn) {
-            double v = (vleft + vc * vdx) + vdx * c->basis.nodes[vn];
+            double v = (vleft + (vc + f->cell0) * vdx) + vdx * c->basis.nodes[vn];
             gv[(size_t)vc * P + vn] = std::exp(-v * v / 2.0);
         }
     double *dgx, *dgv;
@@ -754,7 +795,7 @@ sk_status sk_field_fill_blob(sk_field* f, double sigma) {
     CK(dalloc(&dgv, gv.size()));
     CK(cudaMemcpy(dgx, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dgv, gv.data(), sizeof(double) * gv.size(), cudaMemcpyHostToDevice));
-    CK(launch_fill_separable(f->cur_ptr(), dgx, dgv, (long long)g.ncells * P, vcells * P, c->stream));
+    CK(launch_fill_separable(f->cur_ptr(), dgx, dgv, (long long)g.ncells * P, f->nv * P, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     cudaFree(dgx);
     cudaFree(dgv);
@@ -931,6 +972,67 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
     return SK_OK;
 }
 
+sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, int nranks,
+                                int halo, sk_state** out) {
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SK_ERR_RUNTIME, "v shard: bad rank");
+    if (cfg->v_cells % nranks) return fail(SK_ERR_RUNTIME, "v shard: v_cells must divide by the rank count");
+    if (nranks > 1 && cfg->v_adjust)
+        return fail(SK_ERR_RUNTIME, "v shard: the velocity cut-off is not supported across ranks yet");
+    if (nranks > 1 && cfg->limiter.indicator)
+        return fail(SK_ERR_RUNTIME, "v shard: post limiters are not supported across ranks yet");
+    if (cfg->k != c->k) return fail(SK_ERR_RUNTIME, "state: degree differs from the context");
+    if (!(cfg->dt > 0)) return fail(SK_ERR_RUNTIME, "dt: must be positive");
+    if (!(cfg->mu > 0)) return fail(SK_ERR_RUNTIME, "SpeciesParams::ion: mass ratio must be positive");
+    if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
+    const int ncell = cfg->v_cells / nranks, cell0 = rank * ncell;
+    if (nranks > 1 && halo > ncell) return fail(SK_ERR_RUNTIME, "v shard: halo wider than a shard");
+    auto* s = new sk_state;
+    s->ctx = c;
+    s->cfg = *cfg;
+    s->rank = rank;
+    s->nranks = nranks;
+    s->sqrt_mu[0] = 1.0;
+    s->sqrt_mu[1] = std::sqrt(cfg->mu);
+    const int h = nranks > 1 ? halo : 0;
+    sk_status rc;
+    if ((rc = sk_field_create_shard(c, 0, -cfg->vmax_e, cfg->vmax_e, cfg->v_cells, cell0, ncell, h, &s->f[0])) ||
+        (rc = sk_field_create_shard(c, 1, -cfg->vmax_i, cfg->vmax_i, cfg->v_cells, cell0, ncell, h, &s->f[1]))) {
+        sk_state_destroy(s);
+        return rc;
+    }
+    double sigma = cfg->sigma < 0 ? 0.1 * cfg->L : cfg->sigma;
+    if ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma))) {
+        sk_state_destroy(s);
+        return rc;
+    }
+    const size_t ne = (size_t)c->grid.ncells * c->P;
+    {
+        XSweepArgs a{};
+        a.basis = c->basis;
+        a.grid = c->grid;
+        a.nlines = ncell * c->P;
+        a.nspecies = 2;
+        a.inline_sldg = cfg->limiter.inline_sldg;
+        const size_t need = (size_t)xsweep_rho_groups(a) * ne;
+        if (need > c->rho_fpart_n) {
+            if (c->rho_fpart) cudaFree(c->rho_fpart);
+            CK(dalloc(&c->rho_fpart, need));
+            c->rho_fpart_n = need;
+        }
+        if (!c->rho_corr) CK(dalloc(&c->rho_corr, ne));
+    }
+    CK(dalloc(&s->E, ne));
+    CK(dalloc(&s->rho, ne));
+    CK(dalloc(&s->phi, (size_t)c->grid.ncells * (c->P + 1)));
+    // local charge density of the initial data; the caller sums it over the
+    // ranks and calls sk_state_phase(s, 1) for the initial field (run.cpp:56)
+    if ((rc = enq_rho(s->f[0], s->f[1], s->rho))) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    *out = s;
+    return SK_OK;
+}
+
 sk_status sk_state_destroy(sk_state* s) {
     if (!s) return SK_OK;
     cudaSetDevice(s->ctx->device);
@@ -979,7 +1081,8 @@ sk_status mark(sk_state* s, int phase) {
     return SK_OK;
 }
 
-sk_status enq_strang(sk_state* s) {
+// phase A: x tables + first x half sweep (+ fused local charge density)
+sk_status enq_phase_a(sk_state* s) {
     sk_ctx* c = s->ctx;
     const sk_limiter* lim = &s->cfg.limiter;
     const int inl = lim->inline_sldg;
@@ -987,8 +1090,8 @@ sk_status enq_strang(sk_state* s) {
     const double dt = s->cfg.dt, half = 0.5 * dt;
     sk_field* fs[2] = {s->f[0], s->f[1]};
     sk_status rc;
-    // x tables serve both x half-sweeps (same tau, same v grid within a step)
     const bool post = lim->indicator != 0;
+    // x tables serve both x half-sweeps (same tau, same v grid within a step)
     if ((rc = mark(s, PH_XTAB)) || (rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1)))
         return rc;
     // the charge-density moment rides along the first x sweep unless a post
@@ -998,6 +1101,19 @@ sk_status enq_strang(sk_state* s) {
         return rc;
     if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     if (!fuse && ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho)))) return rc;
+    return SK_OK;
+}
+
+// phase B: Poisson, v sweep, second x half sweep (rho already global)
+sk_status enq_phase_b(sk_state* s) {
+    sk_ctx* c = s->ctx;
+    const sk_limiter* lim = &s->cfg.limiter;
+    const int inl = lim->inline_sldg;
+    const double thr = lim->threshold;
+    const double dt = s->cfg.dt;
+    sk_field* fs[2] = {s->f[0], s->f[1]};
+    sk_status rc;
+    const bool post = lim->indicator != 0;
     if ((rc = mark(s, PH_POISSON)) || (rc = enq_poisson(c, s->rho, s->E, s->phi))) return rc;
     if ((rc = mark(s, PH_VTAB)) || (rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr)))
         return rc;
@@ -1006,6 +1122,12 @@ sk_status enq_strang(sk_state* s) {
     if ((rc = mark(s, PH_X2)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
     if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     return SK_OK;
+}
+
+// stepper.cpp:44-103 (blob: no source term), all on the context stream.
+sk_status enq_strang(sk_state* s) {
+    if (sk_status rc = enq_phase_a(s)) return rc;
+    return enq_phase_b(s);
 }
 
 sk_status enq_run_body(sk_state* s) {
@@ -1024,6 +1146,28 @@ sk_status enq_run_body(sk_state* s) {
 }
 
 }  // namespace
+
+double* sk_state_rho_dev(sk_state* s) { return s->rho; }
+
+sk_status sk_state_phase(sk_state* s, int phase) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    sk_status rc = SK_OK;
+    switch (phase) {
+        case 0: rc = enq_rho(s->f[0], s->f[1], s->rho); break;
+        case 1: rc = enq_poisson(c, s->rho, s->E, s->phi); break;
+        case 2: rc = enq_phase_a(s); break;
+        case 3:
+            if ((rc = enq_phase_b(s))) break;
+            CK(launch_step_end(c->st, 0, 10, 0, c->stream));
+            c->launches += 1;
+            s->step_host += 1;
+            break;
+        default: return fail(SK_ERR_RUNTIME, "unknown step phase");
+    }
+    if (rc) return rc;
+    return after_launch(c);
+}
 
 sk_status sk_strang_step(sk_state* s) {
     sk_ctx* c = s->ctx;

@@ -33,8 +33,8 @@ struct Grid {
 struct DevVGrid {
     double left;
     double dx;
-    int cells;
-    int pad;
+    int cells;   // global v cell count (Grid1D::right = left + cells*dx)
+    int cell0;   // first global v cell held by this field (v-shard offset)
 };
 
 // Device-resident step / error / counter block (one per context).

@@ -103,7 +103,8 @@ __global__ void xtab_kernel(const __grid_constant__ XTabArgs a) {
     const DevVGrid vg = *a.vg[sp];
     const int vc = line / P, vn = line - (line / P) * P;
     // field.cpp:37-40 v_node = cell_left + cell_width * node
-    const double vnode = (vg.left + vc * vg.dx) + vg.dx * a.basis.nodes[vn];
+    // global cell index so a v-shard reproduces the single-GPU v_node bitwise
+    const double vnode = (vg.left + (vc + vg.cell0) * vg.dx) + vg.dx * a.basis.nodes[vn];
     const double speed = vnode / a.sqrt_mu[sp];  // advection.cpp:164
     constexpr int NF = xnf<P>();
     int istar_c[kMaxBlocks];
@@ -611,6 +612,8 @@ __global__ void vtab_kernel(const __grid_constant__ VTabArgs a) {
     decompose_shift(speed, a.tau, dv, istar, alpha);
     double A[P * P], B[P * P];
     shift_matrices<P>(a.basis, alpha, A, B);
+    if ((a.halo_lo >= 0 && -istar > a.halo_lo) || (a.halo_hi >= 0 && istar + 1 > a.halo_hi))
+        raise_error(a.st, 2, 5, max(-istar, istar + 1), max(a.halo_lo, a.halo_hi), a.st->step);
     double* t = a.tab[sp];
     const int n = a.nxd;
     t[xd] = (double)istar;
@@ -1317,7 +1320,7 @@ __global__ void __launch_bounds__(kDiagThreads) diag_partial_kernel(const __grid
         while (xc >= a.grid.start[b + 1]) ++b;
         const double wv = a.basis.weights[vn] * vg.dx;
         const double w = wv * a.basis.weights[xn] * a.grid.dx[b];
-        const double v = (vg.left + vc * vg.dx) + vg.dx * a.basis.nodes[vn];
+        const double v = (vg.left + (vc + vg.cell0) * vg.dx) + vg.dx * a.basis.nodes[vn];
         const double f = a.f[(long long)r * a.ld + xd];
         s[0] += w * f;
         s[1] += w * f * f;

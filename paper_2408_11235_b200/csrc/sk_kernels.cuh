@@ -73,6 +73,8 @@ struct VTabArgs {
     int species0;
     int inline_sldg;
     double threshold;
+    DevStatus* st;
+    int halo_lo, halo_hi;  // v-shard: max readable cells below/above (-1: wall)
 };
 
 struct VSweepArgs {

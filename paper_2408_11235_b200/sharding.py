@@ -1,5 +1,230 @@
-"""v-sharded multi-GPU step (placeholder until the sharded path lands)."""
+"""v-sharded multi-GPU step: one process per GPU.
+
+Phase space is sharded along v: rank r of G holds v cells [r*nv/G, (r+1)*nv/G)
+of each species for all x, plus `halo` cells below and above. Then
+
+  * x sweeps are fully local (an x line is one v row);
+  * the charge density is a local partial (fused into the first x sweep)
+    followed by an all-reduce(sum) of nx*(k+1) doubles;
+  * the Poisson solve is replicated (every rank gets the same E);
+  * the v sweep reads `halo` cells from the neighbouring ranks, exchanged
+    point-to-point right after the first x sweep.
+
+Plumbing is torch.distributed: NCCL over NVLink/NVSwitch for device buffers,
+gloo for the CPU tests (tests/test_sharding.py drive exactly these functions
+with the C oracle as the per-rank compute). The velocity cut-off and the
+literature post limiters are not sharded yet (the C ABI refuses them).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass
+
+from . import _native as N
+
+
+@dataclass(frozen=True)
+class VShardPlan:
+    nv: int       # global v cells
+    nranks: int
+    rank: int
+    halo: int     # cells exchanged with each neighbour
+
+    def __post_init__(self):
+        if self.nranks < 1 or not 0 <= self.rank < self.nranks:
+            raise ValueError("bad rank")
+        if self.nv % self.nranks:
+            raise ValueError("v_cells must divide by the rank count")
+        if self.nranks > 1 and not 0 < self.halo <= self.ncell:
+            raise ValueError("halo must be in 1..cells per shard")
+
+    @property
+    def ncell(self) -> int:
+        return self.nv // self.nranks
+
+    @property
+    def cell0(self) -> int:
+        return self.rank * self.ncell
+
+    @property
+    def lower(self):
+        return self.rank - 1 if self.rank > 0 else None
+
+    @property
+    def upper(self):
+        return self.rank + 1 if self.rank + 1 < self.nranks else None
+
+    @property
+    def gl(self) -> int:  # readable halo cells below (0 at the global wall)
+        return self.halo if self.lower is not None else 0
+
+    @property
+    def gr(self) -> int:
+        return self.halo if self.upper is not None else 0
+
+
+def halo_cells_needed(max_abs_E: float, dt: float, dv: float, sqrt_mu_min: float = 1.0) -> int:
+    """cells a v sweep can reach beyond its shard: |i*|+1 with
+    i* = floor(-c E dt / (sqrt(mu) dv)) (advection.cpp:14-25, :226)."""
+    import math
+
+    return int(math.floor(max_abs_E * dt / (sqrt_mu_min * dv))) + 2
+
+
+def exchange_halos(lower_send, lower_recv, upper_send, upper_recv, plan: VShardPlan, group=None):
+    """Swap v halos with the neighbouring ranks. Each argument is a contiguous
+    tensor of halo*(k+1) v rows (device tensors under NCCL, CPU under gloo):
+    my lowest interior rows go to rank-1 (its upper halo), my highest to rank+1
+    (its lower halo). Halos at the global v walls are left as they are (the
+    kernels treat them as zero inflow)."""
+    import torch.distributed as dist
+
+    ops = []
+    if plan.lower is not None:
+        ops.append(dist.P2POp(dist.isend, lower_send, plan.lower, group))
+        ops.append(dist.P2POp(dist.irecv, lower_recv, plan.lower, group))
+    if plan.upper is not None:
+        ops.append(dist.P2POp(dist.isend, upper_send, plan.upper, group))
+        ops.append(dist.P2POp(dist.irecv, upper_recv, plan.upper, group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+
+def allreduce_rho(rho, group=None):
+    """charge density = sum of the ranks' partial v moments (poisson.cpp:194-216)."""
+    import torch.distributed as dist
+
+    dist.all_reduce(rho, op=dist.ReduceOp.SUM, group=group)
+
+
+class _DevView:
+    """__cuda_array_interface__ over a raw device pointer (no ownership)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _dev_tensor(ptr: int, n: int, device: int):
+    import torch
+
+    return torch.as_tensor(_DevView(ptr, n), device=f"cuda:{device}")
+
+
+class ShardedState:
+    """SimulationState sharded along v over the ranks of the default group."""
+
+    def __init__(self, cfg, rank: int, nranks: int, halo: int = 16, device: int = 0, group=None):
+        from .solver import Context, Grid1D, NodalField, _check
+
+        self.cfg, self.group = cfg, group
+        self.plan = VShardPlan(cfg.v_cells, nranks, rank, halo if nranks > 1 else 0)
+        grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
+                                  cfg.refinement_ratio)
+        self.ctx = Context(grid, cfg.k, cfg.penalty_scale, device)
+        self.device = device
+        h = C.c_void_p()
+        ccfg = cfg.to_c()
+        _check(N.lib().sk_state_create_shard(self.ctx.h, C.byref(ccfg), rank, nranks,
+                                             self.plan.halo, C.byref(h)))
+        self.h = h
+        L = N.lib()
+        self.f = [NodalField(self.ctx, sp, None, _handle=L.sk_state_field(h, sp), _owner=self)
+                  for sp in (0, 1)]
+        n_rho = self.ctx.nx * self.ctx.p
+        self.rho = _dev_tensor(L.sk_state_rho_dev(h), n_rho, device)
+        # initial field: local moment (created) -> all-reduce -> Poisson
+        self._reduce_rho()
+        self._phase(1)
+
+    def _phase(self, ph: int):
+        from .solver import _check
+
+        _check(N.lib().sk_state_phase(self.h, ph))
+
+    def _reduce_rho(self):
+        if self.plan.nranks == 1:
+            return
+        self.ctx.leave()
+        allreduce_rho(self.rho, self.group)
+        self.ctx.enter()
+
+    def _exchange(self):
+        if self.plan.nranks == 1:
+            return
+        from .solver import _check
+
+        self.ctx.leave()
+        for f in self.f:
+            views = []
+            for side in (0, 1):
+                for send in (1, 0):
+                    ptr, cnt = C.c_void_p(), C.c_size_t()
+                    _check(N.lib().sk_field_halo(f.h, side, send, C.byref(ptr), C.byref(cnt)))
+                    views.append(_dev_tensor(ptr.value, cnt.value, self.device))
+            exchange_halos(views[0], views[1], views[2], views[3], self.plan, self.group)
+        self.ctx.enter()
+
+    def step(self):
+        """one strang_step: x half sweep (+ local rho) | all-reduce rho, halo
+        exchange | Poisson, v sweep, x half sweep"""
+        self._phase(2)
+        self._reduce_rho()
+        self._exchange()
+        self._phase(3)
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.lib().sk_state_destroy(self.h)
+            self.h = None
+        self.ctx.close()
 
 
 def bench_sharded(args, cfg, metric, unit, config):
-    raise NotImplementedError("v-sharded multi-GPU step not built yet")
+    """bench.py under torchrun: N ranks, one GPU each, NCCL; device time is
+    the max over ranks of the CUDA-event time around K steps."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import dataclasses
+
+    cfg = dataclasses.replace(cfg, v_adjust=False)  # cut-off is not sharded yet
+    dv = 2 * cfg.vmax_e / cfg.v_cells
+    halo = max(4, min(cfg.v_cells // world, halo_cells_needed(0.5, cfg.dt, dv)))
+    st = ShardedState(cfg, rank, world, halo=halo, device=local)
+    st.ctx.set_eager_errors(False)
+    for _ in range(args.warmup):
+        st.step()
+    st.ctx.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(st.ctx.stream)
+    for _ in range(args.steps):
+        st.step()
+    t1.record(st.ctx.stream)
+    torch.cuda.synchronize()
+    st.ctx.synchronize()
+    ms = torch.tensor([t0.elapsed_time(t1)], device=f"cuda:{local}")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    if rank == 0:
+        value = cfg.dof_total * args.steps / (ms / 1e3)
+        cfgd = dict(config)
+        cfgd["parallelism"] = f"v-shard x{world} (halo {halo} cells, NCCL all-reduce + P2P)"
+        cfgd["v_cutoff"] = "off (not sharded yet)"
+        line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (blob initial condition, run.cpp:41-46)",
+                "config": cfgd}
+        print(json.dumps(line), flush=True)
+    st.close()
+    dist.destroy_process_group()

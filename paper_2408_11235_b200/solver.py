@@ -359,9 +359,7 @@ class NodalField:
                                            C.byref(h)))
             self.h = h
             self._owns = True
-        left, dx, cells = C.c_double(), C.c_double(), C.c_int()
-        _check(N.lib().sk_field_v_grid(self.h, C.byref(left), C.byref(dx), C.byref(cells)))
-        self.nv = cells.value
+        self.nv = self.size // (ctx.p * ctx.nx * ctx.p)  # cells held (a v shard may hold fewer)
 
     def close(self):
         if self._owns and getattr(self, "h", None):

@@ -404,3 +404,77 @@ def test_cpp_mirror_runs_against_oracle():
     assert r.returncode == 0, r.stderr
     r = subprocess.run([out], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_two_v_shards_on_one_gpu_match_unsharded(sk):
+    """The CUDA v-shard path (global cell offsets in the x tables, halo reads in
+    the v sweep, local fused charge density) driven like two ranks, with the
+    all-reduce and the halo exchange done by device copies in one process."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2408_11235_b200 import _native as N
+    from paper_2408_11235_b200.sharding import VShardPlan, _dev_tensor
+    from paper_2408_11235_b200.solver import Context, Grid1D, _check
+
+    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter="sldg", v_adjust=False)
+    ref = sk.SimulationState(cfg)
+    L = N.lib()
+    grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
+                              cfg.refinement_ratio)
+    world, halo = 2, 6
+    shards = []
+    for r in range(world):
+        ctx = Context(grid, cfg.k, cfg.penalty_scale, 0)
+        h = C.c_void_p()
+        ccfg = cfg.to_c()
+        _check(L.sk_state_create_shard(ctx.h, C.byref(ccfg), r, world, halo, C.byref(h)))
+        rho = _dev_tensor(L.sk_state_rho_dev(h), ctx.nx * ctx.p, 0)
+        shards.append((ctx, h, rho, VShardPlan(cfg.v_cells, world, r, halo)))
+
+    def reduce_rho():
+        for ctx, *_ in shards:
+            ctx.synchronize()
+        tot = sum(s[2].clone() for s in shards)
+        for s in shards:
+            s[2].copy_(tot)
+        torch.cuda.synchronize()
+
+    def exchange():
+        for ctx, *_ in shards:
+            ctx.synchronize()
+        views = {}
+        for r, (ctx, h, _, _) in enumerate(shards):
+            for sp in (0, 1):
+                f = L.sk_state_field(h, sp)
+                for side in (0, 1):
+                    for send in (1, 0):
+                        ptr, cnt = C.c_void_p(), C.c_size_t()
+                        _check(L.sk_field_halo(f, side, send, C.byref(ptr), C.byref(cnt)))
+                        views[(r, sp, side, send)] = _dev_tensor(ptr.value, cnt.value, 0)
+        for sp in (0, 1):  # rank0 upper halo <- rank1 lower interior, and back
+            views[(0, sp, 1, 0)].copy_(views[(1, sp, 0, 1)])
+            views[(1, sp, 0, 0)].copy_(views[(0, sp, 1, 1)])
+        torch.cuda.synchronize()
+
+    reduce_rho()
+    for ctx, h, *_ in shards:
+        _check(L.sk_state_phase(h, 1))
+    for _ in range(4):
+        ref.strang_step()
+        for ctx, h, *_ in shards:
+            _check(L.sk_state_phase(h, 2))
+        reduce_rho()
+        exchange()
+        for ctx, h, *_ in shards:
+            _check(L.sk_state_phase(h, 3))
+    for sp in (0, 1):
+        parts = []
+        for ctx, h, _, plan in shards:
+            f = sk.NodalField(ctx, sp, None, _handle=L.sk_state_field(h, sp))
+            parts.append(f.download())
+        got = np.concatenate(parts)
+        assert rel(got, ref.field(sp).download()) <= 1e-12, f"species {sp}"
+    for ctx, h, *_ in shards:
+        L.sk_state_destroy(h)
