@@ -57,7 +57,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -100,10 +100,13 @@ def cpu_reference_run(cfg, steps: int, warmup: int, budget_s: float):
     t0 = time.perf_counter()
     st = oracle.Ref().state(threads=threads, **cfg.oracle_kwargs())
     t_init = time.perf_counter() - t0
-    tw = st.run(max(warmup, 1))
-    per_step = tw / max(warmup, 1)
-    k = max(1, min(steps, int(budget_s / max(per_step, 1e-9))))
-    t = st.run(k)
+    st.run(max(warmup, 1))
+    # time single loop bodies until the budget is spent (a shrink event, 10x a
+    # plain step on the CPU, must not size the sample)
+    k, t = 0, 0.0
+    while k < max(steps, 1) and (k == 0 or t < budget_s):
+        t += st.run(1)
+        k += 1
     rate = cfg.dof_total * k / t
     sample = (f"{cfg.nx}x{cfg.v_cells} k={cfg.k} {cfg.limiter}: {k} timed run() loop bodies "
               f"after {max(warmup, 1)} warm-up (init {t_init:.1f}s), {threads} threads, "
@@ -187,11 +190,10 @@ def main():
     st.run_steps(args.warmup)
     st.ctx.synchronize()
 
-    # ---- timed region: K run() loop bodies, CUDA events on the step stream ----
-    stream = st.ctx.stream  # the library's stream: events bracket exactly its work
+    # ---- timed region: K run() loop bodies (graph replay), CUDA events on the
+    # library's stream, which carries exactly the step's work ----
+    stream = st.ctx.stream
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st.set_phase_timing(True)
-    st.phase_times()
     launches0 = st.launches()
     clocks = ClockSampler(dev)
     clocks.start()
@@ -200,10 +202,21 @@ def main():
     st.run_steps(args.steps)
     t1.record(stream)
     torch.cuda.synchronize()
-    clk = clocks.stop()
     st.ctx.synchronize()  # raises on device-side errors
     launches = st.launches() - launches0
     ms = t0.elapsed_time(t1)
+    # ---- second K-step window with per-phase events (eager enqueue): the
+    # per-kernel durations behind the roofline ----
+    st.set_phase_timing(True)
+    st.phase_times()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    st.run_steps(args.steps)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    st.ctx.synchronize()
+    ms_phased = t0.elapsed_time(t1)
     phases = st.phase_times()
     st.set_phase_timing(False)
     value = cfg.dof_total * args.steps / (ms / 1e3)
@@ -213,6 +226,7 @@ def main():
     peak, peak_kind = peaks()
     sweep_phases = {"x_sweep_1", "x_sweep_2", "v_sweep"}
     dom = max(phases, key=lambda k: phases[k][0])
+    dom_share = phases[dom][0] / ms_phased
     dom_ms, dom_n = phases[dom]
     per_launch_ms = dom_ms / max(dom_n, 1)
     if dom in sweep_phases or dom.startswith("post"):
@@ -240,7 +254,11 @@ def main():
                      "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes, "ms_per_launch": per_launch_ms,
-                     "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak},
+                     "share_of_step": dom_share,
+                     "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak,
+                     "timing": "kernel ms from per-phase CUDA events over a second K-step "
+                               "window (eager enqueue, %.3f ms/step vs %.3f graphed)"
+                               % (ms_phased / args.steps, ms / args.steps)},
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
         "gpu_launches": launches,
         "limiter_stats": st.stats(),
@@ -270,7 +288,7 @@ def main():
     # ---- CPU baseline: the reference on this host, bounded sample ----
     if not args.no_cpu:
         try:
-            rate, info = cpu_reference_run(cfg, 3, 1, budget_s=args.cpu_budget)
+            rate, info = cpu_reference_run(cfg, 50, 1, budget_s=args.cpu_budget)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": info["threads"],
                                     "kind": "reference", "sample": info["sample"]}
         except Exception as e:  # noqa: BLE001

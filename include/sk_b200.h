@@ -201,7 +201,10 @@ sk_status sk_state_shrinks(sk_state* s, int species, int* count, long* last_step
 /* per-phase CUDA-event timing of the step (disables graph replay while on).
  * Phases: 0 x tables, 1 x sweep 1, 2 post X 1, 3 charge density, 4 Poisson,
  * 5 v tables, 6 v sweep, 7 post V, 8 x sweep 2, 9 post X 2, 10 step end +
- * cut-off. sk_state_phase_times returns and clears the accumulated ms. */
+ * cut-off, 11/12/13 the launches after the main kernel of x sweep 1 / v sweep /
+ * x sweep 2 (limiter fixup, fused-moment reduction). Phases 1, 6, 8 then time
+ * the sweep kernel alone. sk_state_phase_times returns and clears the
+ * accumulated ms. */
 sk_status sk_state_set_phase_timing(sk_state* s, int on);
 sk_status sk_state_phase_times(sk_state* s, double* ms, long* count, int n);
 /* kernels this context has enqueued (graph replays included) */

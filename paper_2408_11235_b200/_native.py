@@ -102,7 +102,8 @@ SIGNATURES = {
 }
 
 PHASES = ("x_tables", "x_sweep_1", "post_x_1", "charge_density", "poisson", "v_tables",
-          "v_sweep", "post_v", "x_sweep_2", "post_x_2", "step_end_cutoff")
+          "v_sweep", "post_v", "x_sweep_2", "post_x_2", "step_end_cutoff",
+          "x_fix_1", "v_fix", "x_fix_2")
 
 
 def header_symbols() -> list[str]:

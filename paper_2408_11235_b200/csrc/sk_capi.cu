@@ -64,6 +64,8 @@ struct sk_ctx {
     double* diag_out = nullptr;
     double* pinned = nullptr;          // small pinned readback buffer
     long long launches = 0;            // kernels enqueued (bench gpu_launches)
+    sk_state* fix_timer = nullptr;     // phase timing: mark the fixup launches of
+    int fix_phase = -1;                // the next sweep as their own phase
     bool exact = false;                // exact-reduction (bitwise parity) mode
     double* rho_fpart = nullptr;       // fused charge-density partials
     size_t rho_fpart_n = 0;
@@ -119,6 +121,20 @@ struct sk_state {
 };
 
 namespace {
+
+sk_status mark(sk_state* s, int phase) {
+    if (!s->timing) return SK_OK;
+    cudaEvent_t e;
+    if (!s->pool.empty()) {
+        e = s->pool.back();
+        s->pool.pop_back();
+    } else {
+        CK(cudaEventCreate(&e));
+    }
+    CK(cudaEventRecord(e, s->ctx->stream));
+    s->marks.emplace_back(phase, e);
+    return SK_OK;
+}
 
 // Read the device status block and turn a raised flag into an error code.
 sk_status collect_errors(sk_ctx* c) {
@@ -255,6 +271,8 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
     c->launches += 1;
+    if (c->fix_timer)
+        if (sk_status rc = mark(c->fix_timer, c->fix_phase)) return rc;
     if (inline_sldg) {
         CK(launch_xfix(a, c->stream));
         c->launches += 1;
@@ -323,6 +341,8 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_vsweep(a, c->stream));
     c->launches += 1;
+    if (c->fix_timer)
+        if (sk_status rc = mark(c->fix_timer, c->fix_phase)) return rc;
     if (inline_sldg) {
         CK(launch_vfix(a, c->stream));
         c->launches += 1;
@@ -1065,21 +1085,21 @@ namespace {
 
 // stepper.cpp:44-103 (blob: no source term), all on the context stream.
 enum Phase { PH_XTAB, PH_X1, PH_POST_X1, PH_RHO, PH_POISSON, PH_VTAB, PH_V, PH_POST_V, PH_X2,
-             PH_POST_X2, PH_SHRINK, PH_END, PH_N };
+             PH_POST_X2, PH_SHRINK, PH_X1_FIX, PH_V_FIX, PH_X2_FIX, PH_END, PH_N };
 
-sk_status mark(sk_state* s, int phase) {
-    if (!s->timing) return SK_OK;
-    cudaEvent_t e;
-    if (!s->pool.empty()) {
-        e = s->pool.back();
-        s->pool.pop_back();
-    } else {
-        CK(cudaEventCreate(&e));
+// while timing, the launches a sweep issues after its main kernel (limiter
+// fixup, fused-moment reduction) are timed as their own phase
+struct FixTimer {
+    sk_ctx* c;
+    FixTimer(sk_state* s, int ph) : c(s->ctx) {
+        if (s->timing) {
+            c->fix_timer = s;
+            c->fix_phase = ph;
+        }
     }
-    CK(cudaEventRecord(e, s->ctx->stream));
-    s->marks.emplace_back(phase, e);
-    return SK_OK;
-}
+    ~FixTimer() { c->fix_timer = nullptr; }
+};
+
 
 // phase A: x tables + first x half sweep (+ fused local charge density)
 sk_status enq_phase_a(sk_state* s) {
@@ -1097,8 +1117,12 @@ sk_status enq_phase_a(sk_state* s) {
     // the charge-density moment rides along the first x sweep unless a post
     // limiter still has to modify f (or the parity mode wants the serial order)
     const bool fuse = !post && !c->exact;
-    if ((rc = mark(s, PH_X1)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr)))
-        return rc;
+    {
+        FixTimer ft(s, PH_X1_FIX);
+        if ((rc = mark(s, PH_X1)) ||
+            (rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr)))
+            return rc;
+    }
     if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     if (!fuse && ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho)))) return rc;
     return SK_OK;
@@ -1117,9 +1141,15 @@ sk_status enq_phase_b(sk_state* s) {
     if ((rc = mark(s, PH_POISSON)) || (rc = enq_poisson(c, s->rho, s->E, s->phi))) return rc;
     if ((rc = mark(s, PH_VTAB)) || (rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr)))
         return rc;
-    if ((rc = mark(s, PH_V)) || (rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;
+    {
+        FixTimer ft(s, PH_V_FIX);
+        if ((rc = mark(s, PH_V)) || (rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;
+    }
     if (post && ((rc = mark(s, PH_POST_V)) || (rc = enq_post(fs, 2, SK_DIR_V, lim, 0)))) return rc;
-    if ((rc = mark(s, PH_X2)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
+    {
+        FixTimer ft(s, PH_X2_FIX);
+        if ((rc = mark(s, PH_X2)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
+    }
     if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     return SK_OK;
 }
