@@ -266,7 +266,7 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
             return fail(SK_ERR_RUNTIME, "internal: fused rho buffers not sized");  // mallocs in capture)
         a.rho_partial = c->rho_fpart;
         a.rho_corr = c->rho_corr;
-        CK(cudaMemsetAsync(c->rho_corr, 0, sizeof(unsigned long long) * nxd, c->stream));
+        CK(cudaMemsetAsync(c->rho_corr, 0, sizeof(unsigned long long) * nxd * 2 * kRhoCorrCopies, c->stream));
     }
     if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
@@ -979,7 +979,7 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
             CK(dalloc(&c->rho_fpart, need));
             c->rho_fpart_n = need;
         }
-        if (!c->rho_corr) CK(dalloc(&c->rho_corr, ne));
+        if (!c->rho_corr) CK(dalloc(&c->rho_corr, 2 * ne * kRhoCorrCopies));
     }
     CK(dalloc(&s->E, ne));
     CK(dalloc(&s->rho, ne));
@@ -1040,7 +1040,7 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
             CK(dalloc(&c->rho_fpart, need));
             c->rho_fpart_n = need;
         }
-        if (!c->rho_corr) CK(dalloc(&c->rho_corr, ne));
+        if (!c->rho_corr) CK(dalloc(&c->rho_corr, 2 * ne * kRhoCorrCopies));
     }
     CK(dalloc(&s->E, ne));
     CK(dalloc(&s->rho, ne));

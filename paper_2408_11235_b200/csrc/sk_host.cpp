@@ -86,6 +86,18 @@ Basis make_basis(int k) {  // basis.cpp:29-91
         for (int d = 0; d < p; ++d) b.mono[d * p + n2] = c[d];
     }
     for (int j = 0; j < 33; ++j) b.cheb[j] = std::cos(M_PI * (2 * j + 1) / 66.0);
+    // evaluate() terms at the cell ends (sk_numerics.cuh EvalPt): same
+    // division and ordered sum as evaluate() performs at run time
+    b.ev0den = 0.0;
+    b.ev1den = 0.0;
+    for (int n = 0; n < p; ++n) {
+        b.ev0[n] = b.bary[n] / (0.0 - b.nodes[n]);
+        b.ev1[n] = b.bary[n] / (1.0 - b.nodes[n]);
+    }
+    for (int n = 0; n < p; ++n) {
+        b.ev0den += b.ev0[n];
+        b.ev1den += b.ev1[n];
+    }
     return b;
 }
 

@@ -68,27 +68,61 @@ __device__ __forceinline__ void count_flags(unsigned long long* dst, unsigned t,
     }
 }
 
-// Warp-aggregated append of a troubled cell to the deferred-clamp list. The
+// Warp-aggregated append of troubled cells to the deferred-clamp list. The
 // counter keeps counting past the capacity so the fixup kernel can tell that
-// the list overflowed (it then rescans the whole sweep).
-__device__ __forceinline__ bool defer_push(unsigned int* count, unsigned int cap,
-                                           unsigned long long* list, bool want,
-                                           unsigned long long entry) {
-    const unsigned act = __activemask();
-    const unsigned m = __ballot_sync(act, want);
-    if (!m) return false;
+// the list overflowed (it then rescans the whole sweep). Called by the whole
+// (converged) warp; the common no-troubled-cell case is one vote.
+template <int N>
+__device__ __forceinline__ void defer_push_n(unsigned int* count, unsigned int cap,
+                                             unsigned long long* list, const bool (&want)[N],
+                                             const unsigned long long (&entry)[N],
+                                             unsigned members = 0xffffffffu) {
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < N; ++i) any |= want[i];
+    if (!__any_sync(members, any)) return;
     const int lane = threadIdx.x & 31;
-    const int leader = __ffs(m) - 1;
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(count, (unsigned)__popc(m));
-    base = __shfl_sync(act, base, leader);
-    if (!want) return false;
-    const unsigned slot = base + __popc(m & ((1u << lane) - 1u));
-    if (slot < cap) {
-        list[slot] = entry;
-        return true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const unsigned m = __ballot_sync(members, want[i]);
+        if (!m) continue;
+        const int leader = __ffs(m) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(count, (unsigned)__popc(m));
+        base = __shfl_sync(members, base, leader);
+        const unsigned slot = base + __popc(m & ((1u << lane) - 1u));
+        if (want[i] && slot < cap) list[slot] = entry[i];
     }
-    return false;
+}
+
+// per-species limiter counters of a whole block: warp reduce -> shared ->
+// one global atomic per nonzero counter per block (the fixup kernels' per-warp
+// atomics all hit the same six words)
+__device__ __forceinline__ void block_count_flags(DevStatus* st, const unsigned (&ct)[2],
+                                                  const unsigned (&cc)[2], const unsigned (&co)[2]) {
+    __shared__ unsigned acc[6];
+    if (threadIdx.x < 6) acc[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned full = 0xffffffffu;
+    unsigned v[6] = {ct[0], cc[0], co[0], ct[1], cc[1], co[1]};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        v[i] = __reduce_add_sync(full, v[i]);
+        if ((threadIdx.x & 31) == 0 && v[i]) atomicAdd(&acc[i], v[i]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 6 && acc[threadIdx.x])
+        atomicAdd(&st->stats[threadIdx.x / 3][threadIdx.x % 3], (unsigned long long)acc[threadIdx.x]);
+}
+
+// true when none of the P values is inf/NaN: one test on the OR of the
+// exponent fields' all-ones patterns instead of P separate isfinite()
+template <int P>
+__device__ __forceinline__ bool all_finite(const double* o) {
+    unsigned nf = 0;
+#pragma unroll
+    for (int m = 0; m < P; ++m) nf |= (unsigned)((((unsigned)__double2hiint(o[m]) & 0x7ff00000u) == 0x7ff00000u));
+    return nf == 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -255,12 +289,15 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    // the suspend-time hint lets a waiting warp sleep until the phase flips
+    // instead of spinning on try_wait (a spinning producer warp stole ~8 % of
+    // the x sweep's issue slots)
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "SK_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra SK_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "n"(1000000)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, unsigned bytes,
@@ -461,6 +498,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 
     // ---------------- consumer warps ----------------
     const int tid = threadIdx.x;
+    [[maybe_unused]] const ThrCut cut = make_thr_cut(a.threshold);
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
     if constexpr (RHO)  // each thread owns its cells' x dofs: no sharing, no sync
@@ -532,26 +570,31 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         }
         double wdv = 0.0;
         if constexpr (RHO) wdv = reinterpret_cast<const double*>(hdr)[4];
+        [[maybe_unused]] bool tr[C::CPT];
+        [[maybe_unused]] unsigned long long entry[C::CPT];
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
             const int c = tid + cc * C::NT;
+            if constexpr (INLINE) {
+                const double* ext = row + 2 + 2 * P * P;
+                tr[cc] = c < nt && inline_indicator_m<P>(cut, ext, ext + P, mean<P>(a.basis, ul[cc]),
+                                                         mean<P>(a.basis, ur[cc]), o[cc]);
+                entry[cc] = ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
+                            (unsigned)(g.start[b] + c0 + c);
+            }
             if (c < nt) {
-                if constexpr (INLINE) {
-                    const bool tr = inline_indicator<P>(a.basis, a.threshold, row + 2 + 2 * P * P,
-                                                        row + 2 + 2 * P * P + P, ul[cc], ur[cc], o[cc]);
-                    const unsigned long long entry =
-                        ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
-                        (unsigned)(g.start[b] + c0 + c);
-                    // queued for the fixup kernel; on overflow it rescans everything
-                    defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
-                }
-#pragma unroll
-                for (int m = 0; m < P; ++m) bad |= !isfinite(o[cc][m]);
                 if constexpr (RHO) {
 #pragma unroll
                     for (int m = 0; m < P; ++m) racc[c * P + m] += wdv * o[cc][m];
                 }
             }
+        }
+        // troubled cells are queued for the fixup kernel (on overflow it rescans)
+        if constexpr (INLINE) defer_push_n<C::CPT>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+        if (a.check_finite) {  // stepper.cpp:99-102, only on the step's last sweep
+#pragma unroll
+            for (int cc = 0; cc < C::CPT; ++cc)
+                if (tid + cc * C::NT < nt) bad |= !all_finite<P>(o[cc]);
         }
         // the window stage is consumed: hand it back before the stores
         __syncwarp();
@@ -675,6 +718,7 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
     const int j1 = min(j0 + kVChunk, a.n);
     bool bad = false;
     double* my = ring + threadIdx.x;
+    [[maybe_unused]] const unsigned members = __ballot_sync(0xffffffffu, xd < a.nxd);
     if (xd < a.nxd) {
         const double* t = a.tab[sp];
         const int nx = a.nxd;
@@ -721,6 +765,9 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
         cp_wait<R - 2>();
 #pragma unroll
         for (int n = 0; n < P; ++n) ul[n] = my[n * kVThreads];
+        [[maybe_unused]] const ThrCut cut = make_thr_cut(a.threshold);
+        [[maybe_unused]] double mean_l = INLINE ? mean<P>(a.basis, ul) : 0.0;  // carried along the walk
+        const bool check = a.check_finite;
         if (R - 1 < ncells) vissue<P>(g_iss, ld, ok(s_iss), my + (R - 1) * P * kVThreads);
         cp_commit();
         ++s_iss;
@@ -742,17 +789,17 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
                     double o[P];
                     project_cell<P>(A, B, ul, ur, o);
                     if constexpr (INLINE) {
-                        const bool tr = inline_indicator<P>(a.basis, a.threshold, el, er, ul, ur, o);
-                        const unsigned long long entry = ((unsigned long long)(sp & 1) << 63) |
-                                                         ((unsigned long long)(j0 + jj) << 32) |
-                                                         (unsigned)xd;
-                        defer_push(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+                        const double mean_r = mean<P>(a.basis, ur);
+                        const bool tr[1] = {inline_indicator_m<P>(cut, el, er, mean_l, mean_r, o)};
+                        const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
+                                                             ((unsigned long long)(j0 + jj) << 32) |
+                                                             (unsigned)xd};
+                        defer_push_n<1>(a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
+                        mean_l = mean_r;
                     }
+                    if (check) bad |= !all_finite<P>(o);
 #pragma unroll
-                    for (int m = 0; m < P; ++m) {
-                        bad |= !isfinite(o[m]);
-                        op[m * ld] = o[m];
-                    }
+                    for (int m = 0; m < P; ++m) op[m * ld] = o[m];
                     op += cstride;
 #pragma unroll
                     for (int n = 0; n < P; ++n) ul[n] = ur[n];
@@ -770,6 +817,21 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
 // queued cell. The sweep's source buffer is intact (ping-pong), so ul/ur are
 // re-read exactly as the sweep saw them and the result is bitwise the same.
 // ---------------------------------------------------------------------------
+// Clamp corrections of the fused charge density as exact integers: d splits
+// exactly into hi = RN(d 2^30) 2^-30 and lo = d - hi (|lo| <= 2^-31), summed
+// as int64 at scales 2^30 and 2^76. Integer sums do not depend on the order
+// of the atomics, so rho is deterministic; the range is |sum| < 2^33 per x
+// dof and the dropped part of lo is < 2^-77 per correction.
+__device__ __forceinline__ void rho_corr_add(unsigned long long* base, long long lo_off, long long i, double d) {
+    const double hi = rint(d * 0x1p30) * 0x1p-30;
+    const double lo = d - hi;
+    atomicAdd(base + i, (unsigned long long)__double2ll_rn(hi * 0x1p30));
+    atomicAdd(base + lo_off + i, (unsigned long long)__double2ll_rn(lo * 0x1p76));
+}
+__device__ __forceinline__ double rho_corr_value(unsigned long long hi, unsigned long long lo) {
+    return (double)(long long)hi * 0x1p-30 + (double)(long long)lo * 0x1p-76;
+}
+
 template <int P>
 __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line, int cell, bool rescan,
                                           unsigned* ct, unsigned* cc, unsigned* co) {
@@ -819,8 +881,9 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const double d = wdv * o[q] - wdv * o0[q];
-            atomicAdd(&a.rho_corr[(long long)cell * P + q],
-                      (unsigned long long)__double2ll_rn(d * 0x1p60));
+            // spread over copies by v row: clamped cells of many rows share an x dof
+            rho_corr_add(a.rho_corr + (long long)(line % kRhoCorrCopies) * a.grid.ncells * P,
+                         (long long)kRhoCorrCopies * a.grid.ncells * P, (long long)cell * P + q, d);
         }
     }
     ct[sp] += fl & 1;
@@ -848,7 +911,7 @@ __global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSwee
             xfix_cell<P>(a, a.species0 + (int)(r / a.nlines), (int)(r % a.nlines), cell, true, ct, cc, co);
         }
     }
-    for (int sp = 0; sp < 2; ++sp) count_flags(a.st->stats[sp], ct[sp], cc[sp], co[sp]);
+    block_count_flags(a.st, ct, cc, co);
 }
 
 template <int P>
@@ -901,7 +964,7 @@ __global__ void __launch_bounds__(128) vfix_kernel(const __grid_constant__ VSwee
             vfix_cell<P>(a, a.species0 + (int)(r / a.n), (int)(r % a.n), xd, true, ct, cc, co);
         }
     }
-    for (int sp = 0; sp < 2; ++sp) count_flags(a.st->stats[sp], ct[sp], cc[sp], co[sp]);
+    block_count_flags(a.st, ct, cc, co);
 }
 
 // ---------------------------------------------------------------------------
@@ -1589,9 +1652,17 @@ __global__ void rho_fused_reduce_kernel(const double* partial, const unsigned lo
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= nxd) return;
     double acc = 0.0;
-    for (int k = 0; k < groups; ++k) acc += partial[(long long)k * nxd + xd];
-    // fixed-point (2^-60) corrections from clamped cells
-    acc += (double)(long long)corr[xd] * 0x1p-60;
+#pragma unroll 8
+    for (int k = 0; k < groups; ++k) acc += __ldg(partial + (long long)k * nxd + xd);  // loads overlap
+    // clamp corrections (rho_corr_add): integer sums are exact, so neither the
+    // atomics' order nor the copy split changes rho
+    unsigned long long ih = 0, il = 0;
+#pragma unroll 8
+    for (int k = 0; k < kRhoCorrCopies; ++k) {
+        ih += __ldg(corr + (long long)k * nxd + xd);
+        il += __ldg(corr + (long long)(kRhoCorrCopies + k) * nxd + xd);
+    }
+    acc += rho_corr_value(ih, il);
     rho[xd] = acc;
 }
 

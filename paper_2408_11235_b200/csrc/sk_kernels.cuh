@@ -8,6 +8,7 @@ namespace sk {
 constexpr int kXThreads = 256;  // x sweep CTA
 constexpr int kVThreads = 128;  // v sweep CTA (one thread per x dof)
 constexpr int kVChunk = 32;     // v cells per v-sweep thread
+constexpr int kRhoCorrCopies = 64;  // fused-moment clamp corrections: copies keyed by v row
 
 inline int xtab_nf(int P) { return ((2 + 2 * P * P + 2 * P) + 1) & ~1; }  // AoS row, 16B aligned
 inline int vtab_nf(int P) { return 2 + 2 * P * P + 2 * P; }

@@ -29,6 +29,10 @@ struct Basis {
     double mono[SK_MAXP * SK_MAXP];  // nodal -> monomial, row-major [d][n]
     double diff[SK_MAXP * SK_MAXP];  // nodal differentiation [m][n]
     double cheb[33];                 // cos(pi(2j+1)/66), basis.cpp:211 (k > 3)
+    // evaluate() at xi = 0 and xi = 1 (basis.cpp:123-134): the barycentric
+    // terms t_n = bary[n] / (xi - x_n) and their ordered sum, computed once
+    double ev0[SK_MAXP], ev0den;
+    double ev1[SK_MAXP], ev1den;
 };
 
 SK_HD double dmax2(double a, double b) { return (a < b) ? b : a; }  // std::max
@@ -149,6 +153,108 @@ SK_HD double extremum_on(const Basis& b, const double* u, double a, double bb) {
     }
 }
 
+// evaluate(u, xi) at a point fixed for many u: the barycentric terms are
+// computed once; same operations in the same order as evaluate(), so the
+// value is bitwise evaluate()'s. hit >= 0: xi is node `hit` (exact return).
+template <int P>
+struct EvalPt {
+    double t[P];
+    double den;
+    int hit;
+};
+template <int P>
+SK_HD EvalPt<P> make_evalpt(const Basis& b, double xi) {
+    EvalPt<P> e;
+    e.hit = -1;
+    e.den = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        if (e.hit < 0 && xi == b.nodes[n]) e.hit = n;
+        e.t[n] = b.bary[n] / (xi - b.nodes[n]);
+    }
+    if (e.hit < 0) {
+#pragma unroll
+        for (int n = 0; n < P; ++n) e.den += e.t[n];
+    }
+    return e;
+}
+template <int P>
+SK_HD EvalPt<P> basis_evalpt(const Basis& b, int one) {  // xi = 0 or 1 (never a GL node)
+    EvalPt<P> e;
+    e.hit = -1;
+#pragma unroll
+    for (int n = 0; n < P; ++n) e.t[n] = one ? b.ev1[n] : b.ev0[n];
+    e.den = one ? b.ev1den : b.ev0den;
+    return e;
+}
+template <int P>
+SK_HD double eval_at(const EvalPt<P>& e, const double* u) {
+    if (e.hit >= 0) return u[e.hit];
+    double num = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) num += e.t[n] * u[n];
+    return num / e.den;
+}
+
+// extremum_on<P,true> and extremum_on<P,false> of the same (u, [a, bb]) in one
+// pass: both visit the same candidate points with the same values and differ
+// only in the comparison, so (mx, mn) are bitwise the two separate results.
+template <int P>
+SK_HD void extremum_minmax(const Basis& b, const double* u, double a, double bb, const EvalPt<P>& pa,
+                           const EvalPt<P>& pb, double& mx, double& mn) {
+    const double va = eval_at<P>(pa, u);
+    mx = va;
+    mn = va;
+    if (bb == a) return;
+    const double vb = eval_at<P>(pb, u);
+    if (vb > mx) mx = vb;
+    if (vb < mn) mn = vb;
+    if constexpr (P <= 2) {
+        return;
+    } else if constexpr (P <= 4) {
+        double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int d = 0; d < P; ++d) {  // basis.cpp:163-170 to_monomial
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < P; ++n) acc += b.mono[d * P + n] * u[n];
+            c[d] = acc;
+        }
+        double qa = 3.0 * c[3], qb = 2.0 * c[2], qc = c[1];
+        double x0 = 0.0, x1 = 0.0;
+        int nc = 0;
+        if (fabs(qa) > 0.0) {
+            double disc = qb * qb - 4.0 * qa * qc;
+            if (disc >= 0.0) {
+                double r = sqrt(disc);
+                x0 = (-qb + r) / (2.0 * qa);
+                x1 = (-qb - r) / (2.0 * qa);
+                nc = 2;
+            }
+        } else if (fabs(qb) > 0.0) {
+            x0 = -qc / qb;
+            nc = 1;
+        }
+        if (nc >= 1 && x0 > a && x0 < bb) {
+            const double v = evaluate<P>(b, u, x0);
+            if (v > mx) mx = v;
+            if (v < mn) mn = v;
+        }
+        if (nc >= 2 && x1 > a && x1 < bb) {
+            const double v = evaluate<P>(b, u, x1);
+            if (v > mx) mx = v;
+            if (v < mn) mn = v;
+        }
+    } else {
+        for (int j = 0; j < 33; ++j) {
+            const double x = 0.5 * (a + bb) + 0.5 * (bb - a) * b.cheb[j];
+            const double v = evaluate<P>(b, u, x);
+            if (v > mx) mx = v;
+            if (v < mn) mn = v;
+        }
+    }
+}
+
 // advection.cpp:14-25
 SK_HD void decompose_shift(double speed, double dt, double dx, int& istar, double& alpha) {
     double s = -speed * dt / dx;
@@ -237,6 +343,51 @@ SK_HD bool inline_indicator(const Basis& b, double threshold, const double* ext_
     return ind > threshold;
 }
 
+// `num / den > thr` (limiters.cpp:178-188) decided without the division when
+// that is provably the same answer. With thr in [2^-60, 2^60], den in
+// [2^-900, 2^900) and hi = RN(thr(1+2^-50)), lo = RN(thr(1-2^-50)):
+//   num > RN(hi*den)  =>  num/den > thr(1+2^-51)  =>  RN(num/den) > thr,
+//   num < RN(lo*den)  =>  num/den < thr           =>  RN(num/den) <= thr,
+// so only the ~2^-50-wide band around the threshold (and NaN, zero or
+// out-of-range operands) pays for the correctly rounded quotient.
+struct ThrCut {
+    double thr, hi, lo;
+};
+SK_HD ThrCut make_thr_cut(double thr) {
+    ThrCut t{thr, HUGE_VAL, -HUGE_VAL};  // +-inf: always the exact path
+    if (thr >= 0x1p-60 && thr <= 0x1p60) {
+        t.hi = thr * (1.0 + 0x1p-50);
+        t.lo = thr * (1.0 - 0x1p-50);
+    }
+    return t;
+}
+SK_HD bool over_threshold(double num, double den, const ThrCut& t) {
+#ifdef __CUDA_ARCH__
+    const unsigned e = (unsigned)__double2hiint(den) - 0x07b00000u;  // den in [2^-900, 2^900)
+    if (e < 0x78300000u - 0x07b00000u) {
+        const bool up = num > t.hi * den;
+        if (up || num < t.lo * den) return up;
+    }
+#endif
+    if (!(den > 0.0)) return false;
+    return num / den > t.thr;
+}
+
+// inline_indicator with the source-cell means supplied by the caller (a sweep
+// that walks cells in order reuses the right mean as the next left one)
+template <int P>
+SK_HD bool inline_indicator_m(const ThrCut& t, const double* ext_l, const double* ext_r,
+                              double mean_l, double mean_r, const double* up) {
+    double denom = dmax2(fabs(mean_l), fabs(mean_r));
+    double el = 0.0, er = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        el += ext_l[n] * up[n];
+        er += ext_r[n] * up[n];
+    }
+    return over_threshold(fabs(el - mean_l) + fabs(er - mean_r), denom, t);
+}
+
 // theta clamp of a troubled cell, limiters.cpp:191-215. Returns flags:
 // bit0 troubled, bit1 clamped, bit2 mean_outside; `up` modified in place.
 template <int P>
@@ -244,10 +395,14 @@ SK_HD int inline_clamp(const Basis& b, double alpha, const double* ul, const dou
                        double* up) {
     int flags = 1;
     double mean_p = mean<P>(b, up);
-    double wmax = dmax2(extremum_on<P, true>(b, ul, alpha, 1.0), extremum_on<P, true>(b, ur, 0.0, alpha));
-    double wmin = dmin2(extremum_on<P, false>(b, ul, alpha, 1.0), extremum_on<P, false>(b, ur, 0.0, alpha));
-    double pmax = extremum_on<P, true>(b, up, 0.0, 1.0);
-    double pmin = extremum_on<P, false>(b, up, 0.0, 1.0);
+    // the six extremum_on calls of limiters.cpp:196-201 as three min/max pairs
+    const EvalPt<P> pa = make_evalpt<P>(b, alpha), p0 = basis_evalpt<P>(b, 0), p1 = basis_evalpt<P>(b, 1);
+    double lmax, lmin, rmax, rmin, pmax, pmin;
+    extremum_minmax<P>(b, ul, alpha, 1.0, pa, p1, lmax, lmin);
+    extremum_minmax<P>(b, ur, 0.0, alpha, p0, pa, rmax, rmin);
+    extremum_minmax<P>(b, up, 0.0, 1.0, p0, p1, pmax, pmin);
+    double wmax = dmax2(lmax, rmax);
+    double wmin = dmin2(lmin, rmin);
     if ((mean_p > wmax) || (mean_p < wmin)) flags |= 4;
     double theta = 1.0;
     double dmx = pmax - mean_p;
