@@ -113,10 +113,13 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* block_left
 sk_status sk_ctx_destroy(sk_ctx* ctx);
 sk_status sk_ctx_set_stream(sk_ctx* ctx, void* cuda_stream);
 sk_status sk_ctx_set_eager_errors(sk_ctx* ctx, int on);
-/* Exact-reduction (parity) mode: charge density summed in the reference's
- * serial order and the Poisson solve replayed as dpbtrs in reference-BLAS order
+/* Exact (parity) mode: every sweep uses the reference's rounding sequence
+ * (no FMA contraction), the charge density is summed in the reference's serial
+ * order and the Poisson solve is replayed as dpbtrs in reference-BLAS order
  * (poisson.cpp:166-216), so whole trajectories are bitwise the reference's.
- * Off (default): parallel two-pass moment + block-cyclic-reduction solve. */
+ * Off (default, fast mode): DFMA-contracted sweeps (k <= 3), charge density
+ * fused into the first x sweep, block-cyclic-reduction solve; results agree
+ * with the reference to the 1e-12 relative tolerance. */
 sk_status sk_ctx_set_exact_reductions(sk_ctx* ctx, int on);
 /* Capacity of the deferred limiter-clamp list (troubled cells queued by the
  * sweeps, clamped by a fixup kernel); above it the fixup rescans the sweep.

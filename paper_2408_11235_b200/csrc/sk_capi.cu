@@ -110,6 +110,7 @@ struct sk_state {
     long step_host = 0;
     cudaGraphExec_t graph2 = nullptr;  // two loop bodies
     int graph_cur0 = -1, graph_cur1 = -1;
+    int graph_exact = -1;              // arithmetic mode the graph was captured in
     long long graph_launches = 0;      // kernels per graph replay
     int rank = 0, nranks = 1;          // v-shard of a multi-GPU run
     // optional per-phase CUDA-event timing (sk_state_set_phase_timing)
@@ -250,6 +251,7 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.inline_sldg = inline_sldg;
     a.periodic = periodic;
     a.check_finite = check_finite;
+    a.fma = !c->exact;
     a.threshold = threshold;
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
@@ -334,6 +336,7 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.inline_sldg = inline_sldg;
     a.periodic = periodic;
     a.check_finite = check_finite;
+    a.fma = !c->exact;
     a.threshold = threshold;
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
@@ -973,7 +976,11 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         a.nlines = cfg->v_cells * c->P;
         a.nspecies = 2;
         a.inline_sldg = cfg->limiter.inline_sldg;
-        const size_t need = (size_t)xsweep_rho_groups(a) * ne;
+        a.fma = 0;  // size for either arithmetic (sk_ctx_set_exact_reductions may flip it)
+        const int g0 = xsweep_rho_groups(a);
+        a.fma = 1;
+        const int g1 = xsweep_rho_groups(a);
+        const size_t need = (size_t)(g0 > g1 ? g0 : g1) * ne;
         if (need > c->rho_fpart_n) {
             if (c->rho_fpart) cudaFree(c->rho_fpart);
             CK(dalloc(&c->rho_fpart, need));
@@ -1034,7 +1041,11 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
         a.nlines = ncell * c->P;
         a.nspecies = 2;
         a.inline_sldg = cfg->limiter.inline_sldg;
-        const size_t need = (size_t)xsweep_rho_groups(a) * ne;
+        a.fma = 0;  // size for either arithmetic (sk_ctx_set_exact_reductions may flip it)
+        const int g0 = xsweep_rho_groups(a);
+        a.fma = 1;
+        const int g1 = xsweep_rho_groups(a);
+        const size_t need = (size_t)(g0 > g1 ? g0 : g1) * ne;
         if (need > c->rho_fpart_n) {
             if (c->rho_fpart) cudaFree(c->rho_fpart);
             CK(dalloc(&c->rho_fpart, need));
@@ -1224,7 +1235,8 @@ sk_status sk_run_steps(sk_state* s, int n) {
             if (sk_status rc = enq_run_body(s)) return rc;
         return after_launch(c);
     }
-    if (n >= 2 && (!s->graph2 || s->graph_cur0 != s->f[0]->cur || s->graph_cur1 != s->f[1]->cur)) {
+    if (n >= 2 && (!s->graph2 || s->graph_cur0 != s->f[0]->cur || s->graph_cur1 != s->f[1]->cur ||
+                   s->graph_exact != (int)c->exact)) {
         if (s->graph2) {
             cudaGraphExecDestroy(s->graph2);
             s->graph2 = nullptr;
@@ -1248,6 +1260,7 @@ sk_status sk_run_steps(sk_state* s, int n) {
         cudaGraphDestroy(g);
         s->graph_cur0 = c0;
         s->graph_cur1 = c1;
+        s->graph_exact = (int)c->exact;
     }
     int done = 0;
     for (; done + 2 <= n; done += 2) {

@@ -115,6 +115,9 @@ __device__ __forceinline__ void block_count_flags(DevStatus* st, const unsigned 
         atomicAdd(&st->stats[threadIdx.x / 3][threadIdx.x % 3], (unsigned long long)acc[threadIdx.x]);
 }
 
+template <int P>
+constexpr bool kHasFmaDev = P <= 4;  // fast-mode DFMA kernels exist for k <= 3
+
 // true when none of the P values is inf/NaN: one test on the OR of the
 // exponent fields' all-ones patterns instead of P separate isfinite()
 template <int P>
@@ -413,7 +416,7 @@ __device__ __forceinline__ void sts_cell(double* p, const double* u) {
     }
 }
 
-template <int P, bool INLINE, bool RHO>
+template <int P, bool INLINE, bool RHO, bool FMA>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
@@ -563,7 +566,12 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 #pragma unroll
             for (int j = 0; j < P; ++j) {
 #pragma unroll
-                for (int cc = 0; cc < C::CPT; ++cc) acc[cc] += am[j] * ul[cc][j] + bm[j] * ur[cc][j];
+                for (int cc = 0; cc < C::CPT; ++cc) {
+                    if constexpr (FMA)
+                        acc[cc] = fma(bm[j], ur[cc][j], fma(am[j], ul[cc][j], acc[cc]));
+                    else
+                        acc[cc] += am[j] * ul[cc][j] + bm[j] * ur[cc][j];
+                }
             }
 #pragma unroll
             for (int cc = 0; cc < C::CPT; ++cc) o[cc][m] = acc[cc];
@@ -577,15 +585,15 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             const int c = tid + cc * C::NT;
             if constexpr (INLINE) {
                 const double* ext = row + 2 + 2 * P * P;
-                tr[cc] = c < nt && inline_indicator_m<P>(cut, ext, ext + P, mean<P>(a.basis, ul[cc]),
-                                                         mean<P>(a.basis, ur[cc]), o[cc]);
+                tr[cc] = c < nt && inline_indicator_m<P, FMA>(cut, ext, ext + P, mean_f<P, FMA>(a.basis, ul[cc]),
+                                                              mean_f<P, FMA>(a.basis, ur[cc]), o[cc]);
                 entry[cc] = ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
                             (unsigned)(g.start[b] + c0 + c);
             }
             if (c < nt) {
                 if constexpr (RHO) {
 #pragma unroll
-                    for (int m = 0; m < P; ++m) racc[c * P + m] += wdv * o[cc][m];
+                    for (int m = 0; m < P; ++m) racc[c * P + m] = madd<FMA>(racc[c * P + m], wdv, o[cc][m]);
                 }
             }
         }
@@ -707,7 +715,7 @@ __device__ __forceinline__ void vissue(const double* gp, long long ld, bool vali
     for (int n = 0; n < P; ++n) cp_async8(slot + n * kVThreads, valid ? gp + n * ld : gp, valid);
 }
 
-template <int P, bool INLINE, bool PERIODIC>
+template <int P, bool INLINE, bool PERIODIC, bool FMA>
 __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant__ VSweepArgs a) {
     constexpr int R = vring<P>();
     static_assert(kVChunk % R == 0, "chunk must be a multiple of the ring depth");
@@ -766,7 +774,7 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
 #pragma unroll
         for (int n = 0; n < P; ++n) ul[n] = my[n * kVThreads];
         [[maybe_unused]] const ThrCut cut = make_thr_cut(a.threshold);
-        [[maybe_unused]] double mean_l = INLINE ? mean<P>(a.basis, ul) : 0.0;  // carried along the walk
+        [[maybe_unused]] double mean_l = INLINE ? mean_f<P, FMA>(a.basis, ul) : 0.0;  // carried along the walk
         const bool check = a.check_finite;
         if (R - 1 < ncells) vissue<P>(g_iss, ld, ok(s_iss), my + (R - 1) * P * kVThreads);
         cp_commit();
@@ -787,10 +795,10 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
                     ++s_iss;
                     g_iss = PERIODIC ? src_of(s_iss) : g_iss + cstride;
                     double o[P];
-                    project_cell<P>(A, B, ul, ur, o);
+                    project_cell_f<P, FMA>(A, B, ul, ur, o);
                     if constexpr (INLINE) {
-                        const double mean_r = mean<P>(a.basis, ur);
-                        const bool tr[1] = {inline_indicator_m<P>(cut, el, er, mean_l, mean_r, o)};
+                        const double mean_r = mean_f<P, FMA>(a.basis, ur);
+                        const bool tr[1] = {inline_indicator_m<P, FMA>(cut, el, er, mean_l, mean_r, o)};
                         const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
                                                              ((unsigned long long)(j0 + jj) << 32) |
                                                              (unsigned)xd};
@@ -832,6 +840,19 @@ __device__ __forceinline__ double rho_corr_value(unsigned long long hi, unsigned
     return (double)(long long)hi * 0x1p-30 + (double)(long long)lo * 0x1p-76;
 }
 
+// the sweep's troubled decision, recomputed by a fixup rescan with the same
+// arithmetic the sweep used
+template <int P>
+__device__ __forceinline__ bool rescan_indicator(const Basis& b, double thr, int fma, const double* el,
+                                                 const double* er, const double* ul, const double* ur,
+                                                 const double* o) {
+    const ThrCut cut = make_thr_cut(thr);
+    if constexpr (kHasFmaDev<P>)
+        if (fma)
+            return inline_indicator_m<P, true>(cut, el, er, mean_f<P, true>(b, ul), mean_f<P, true>(b, ur), o);
+    return inline_indicator_m<P, false>(cut, el, er, mean<P>(b, ul), mean<P>(b, ur), o);
+}
+
 template <int P>
 __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line, int cell, bool rescan,
                                           unsigned* ct, unsigned* cc, unsigned* co) {
@@ -866,7 +887,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
     double o[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) o[q] = up[q];
-    if (rescan && !inline_indicator<P>(a.basis, a.threshold, row + 2 + 2 * P * P,
+    if (rescan && !rescan_indicator<P>(a.basis, a.threshold, a.fma, row + 2 + 2 * P * P,
                                        row + 2 + 2 * P * P + P, uu[0], uu[1], o))
         return;
     double o0[P];
@@ -934,7 +955,7 @@ __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, in
             el[i] = t[(long long)(2 + 2 * P * P + i) * nx + xd];
             er[i] = t[(long long)(2 + 2 * P * P + P + i) * nx + xd];
         }
-        if (!inline_indicator<P>(a.basis, a.threshold, el, er, ul, ur, o)) return;
+        if (!rescan_indicator<P>(a.basis, a.threshold, a.fma, el, er, ul, ur, o)) return;
     }
     const int fl = inline_clamp<P>(a.basis, alpha, ul, ur, o);
 #pragma unroll
@@ -1576,18 +1597,23 @@ static int sm_count() {
     return n[dev & 31];
 }
 
-template <int P, bool INLINE, bool RHO>
+// fast-mode DFMA variants exist for k <= 3 (P <= 4); other degrees always
+// run the reference-order kernels
+template <int P>
+constexpr bool kHasFma = kHasFmaDev<P>;
+
+template <int P, bool INLINE, bool RHO, bool FMA>
 static cudaError_t configure_xsweep() {
     using Cf = XCfg<P>;
     static unsigned configured = 0;  // per-device bit
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured & (1u << (dev & 31)))) {
-        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO>,
+        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
         if (e != cudaSuccess) return e;
         // full shared-memory carveout so two pipelines share each SM
-        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO>,
+        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         configured |= 1u << (dev & 31);
@@ -1595,47 +1621,61 @@ static cudaError_t configure_xsweep() {
     return cudaSuccess;
 }
 
-template <int P, bool INLINE, bool RHO>
-static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
+// persistent grid of one x-sweep variant: resident CTAs, and for the fused
+// moment a multiple of the tiles per line (each CTA then always sees the same
+// tile column, so the per-group partial rows sum in a fixed order)
+template <int P, bool INLINE, bool RHO, bool FMA>
+static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out) {
     using Cf = XCfg<P>;
-    const size_t smem = Cf::SMEM;
-    if (cudaError_t e = configure_xsweep<P, INLINE, RHO>()) return e;
-    XSweepArgs b = a;
+    if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA>()) return e;
+    b = a;
     b.tile_start[0] = 0;
     for (int i = 0; i < a.grid.nblocks; ++i)
         b.tile_start[i + 1] = b.tile_start[i] + (a.grid.cells[i] + Cf::T - 1) / Cf::T;
-    const long long ntot = (long long)a.nspecies * a.nlines * b.tile_start[a.grid.nblocks];
-    const int nthreads = (Cf::NC + 1) * 32;
+    const int ntl = b.tile_start[a.grid.nblocks];
+    const long long ntot = (long long)a.nspecies * a.nlines * ntl;
     int blocks_per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO>, nthreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO, FMA>,
+                                                  (Cf::NC + 1) * 32, Cf::SMEM);
     long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
-    if (a.rho_fuse) {
-        const int ntl = b.tile_start[a.grid.nblocks];
+    if (RHO) {
         grid = grid >= ntl ? (grid / ntl) * ntl : ntl;
         const long long lines = (long long)a.nspecies * a.nlines;
         if (grid > lines * ntl) grid = lines * ntl;
     }
     if (grid > ntot) grid = ntot;
-    xsweep_kernel<P, INLINE, RHO><<<(int)grid, nthreads, smem, s>>>(b);
+    grid_out = (int)grid;
+    return cudaSuccess;
+}
+
+template <int P, bool INLINE, bool RHO, bool FMA>
+static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
+    XSweepArgs b;
+    int grid = 0;
+    if (cudaError_t e = xsweep_plan<P, INLINE, RHO, FMA>(a, b, grid)) return e;
+    xsweep_kernel<P, INLINE, RHO, FMA><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
     return cudaGetLastError();
+}
+
+template <int P, bool INLINE, bool RHO>
+static cudaError_t launch_xsweep_f(const XSweepArgs& a, cudaStream_t s) {
+    if constexpr (kHasFma<P>)
+        if (a.fma) return launch_xsweep_t<P, INLINE, RHO, true>(a, s);
+    return launch_xsweep_t<P, INLINE, RHO, false>(a, s);
 }
 
 template <int P, bool INLINE>
 static int rho_groups_t(const XSweepArgs& a) {
-    using Cf = XCfg<P>;
-    configure_xsweep<P, INLINE, true>();
-    int ntl = 0;
-    for (int i = 0; i < a.grid.nblocks; ++i) ntl += (a.grid.cells[i] + Cf::T - 1) / Cf::T;
-    const long long ntot = (long long)a.nspecies * a.nlines * ntl;
-    int blocks_per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, true>,
-                                                  (Cf::NC + 1) * 32, Cf::SMEM);
-    long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
-    grid = grid >= ntl ? (grid / ntl) * ntl : ntl;
-    const long long lines = (long long)a.nspecies * a.nlines;
-    if (grid > lines * ntl) grid = lines * ntl;
-    if (grid > ntot) grid = ntot;
-    return (int)(grid / ntl);
+    XSweepArgs b;
+    int grid = 0, ntl = 0;
+    cudaError_t e;
+    if constexpr (kHasFma<P>)
+        e = a.fma ? xsweep_plan<P, INLINE, true, true>(a, b, grid) : xsweep_plan<P, INLINE, true, false>(a, b, grid);
+    else
+        e = xsweep_plan<P, INLINE, true, false>(a, b, grid);
+    if (e != cudaSuccess) return 0;
+    ntl = b.tile_start[a.grid.nblocks];
+    return grid / ntl;
 }
 
 int xsweep_rho_groups(const XSweepArgs& a) {
@@ -1676,13 +1716,13 @@ cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream
 
 cudaError_t launch_xsweep(const XSweepArgs& a, int /*ntiles*/, cudaStream_t s) {
     if (a.inline_sldg && a.rho_fuse)
-        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, true, true>(a, s)))
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_f<PP, true, true>(a, s)))
     else if (a.inline_sldg)
-        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, true, false>(a, s)))
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_f<PP, true, false>(a, s)))
     else if (a.rho_fuse)
-        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, false, true>(a, s)))
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_f<PP, false, true>(a, s)))
     else
-        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_t<PP, false, false>(a, s)))
+        SK_DISPATCH_P(a.basis.p, return (launch_xsweep_f<PP, false, false>(a, s)))
     return cudaSuccess;
 }
 
@@ -1702,14 +1742,24 @@ cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int P, bool INLINE>
+static void launch_vsweep_f(const VSweepArgs& a, dim3 grid, cudaStream_t s) {
+    if constexpr (kHasFma<P>)
+        if (a.fma) {
+            vsweep_kernel<P, INLINE, false, true><<<grid, kVThreads, 0, s>>>(a);
+            return;
+        }
+    vsweep_kernel<P, INLINE, false, false><<<grid, kVThreads, 0, s>>>(a);
+}
+
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.n + kVChunk - 1) / kVChunk, a.nspecies);
     if (a.periodic)
-        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, true><<<grid, kVThreads, 0, s>>>(a)))
+        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, true, false><<<grid, kVThreads, 0, s>>>(a)))
     else if (a.inline_sldg)
-        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, false><<<grid, kVThreads, 0, s>>>(a)))
+        SK_DISPATCH_P(a.basis.p, (launch_vsweep_f<PP, true>(a, grid, s)))
     else
-        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, false, false><<<grid, kVThreads, 0, s>>>(a)))
+        SK_DISPATCH_P(a.basis.p, (launch_vsweep_f<PP, false>(a, grid, s)))
     return cudaGetLastError();
 }
 

@@ -46,6 +46,7 @@ struct XSweepArgs {
     int inline_sldg;
     int periodic;
     int check_finite;
+    int fma;  // fast-mode DFMA arithmetic (0: reference rounding sequence)
     double threshold;
     // deferred limiter clamp: troubled cells are queued here and clamped by
     // the fixup kernel so one slow cell never stalls a whole CTA
@@ -93,6 +94,7 @@ struct VSweepArgs {
     int inline_sldg;
     int periodic;
     int check_finite;
+    int fma;  // fast-mode DFMA arithmetic (0: reference rounding sequence)
     double threshold;
     unsigned long long* fix_list;
     unsigned int* fix_count;

@@ -311,6 +311,48 @@ SK_HD void shift_matrices(const Basis& b, double alpha, double* A, double* B) {
     }
 }
 
+// Fast-mode arithmetic: the same sums contracted into DFMA (acc += a*b as one
+// rounding). Used only when the context is not in exact mode; the north-star
+// tolerance (1e-12 relative) bounds its effect, the exact mode keeps the
+// reference's rounding sequence (-fmad=false everywhere else).
+template <bool FMA>
+SK_HD double madd(double acc, double a, double b) {
+    if constexpr (FMA)
+        return fma(a, b, acc);
+    else
+        return acc + a * b;
+}
+template <int P, bool FMA>
+SK_HD double mean_f(const Basis& b, const double* u) {
+    if constexpr (!FMA) {
+        return mean<P>(b, u);
+    } else {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) acc = fma(b.weights[j], u[j], acc);
+        return acc;
+    }
+}
+// one output node: reference acc += A*ul + B*ur (j ascending), or two DFMA
+template <int P, bool FMA>
+SK_HD double project_node(const double* am, const double* bm, const double* ul, const double* ur) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        if constexpr (FMA)
+            acc = fma(bm[j], ur[j], fma(am[j], ul[j], acc));
+        else
+            acc += am[j] * ul[j] + bm[j] * ur[j];
+    }
+    return acc;
+}
+template <int P, bool FMA>
+SK_HD void project_cell_f(const double* A, const double* B, const double* ul, const double* ur,
+                          double* o) {
+#pragma unroll
+    for (int m = 0; m < P; ++m) o[m] = project_node<P, FMA>(A + m * P, B + m * P, ul, ur);
+}
+
 // advection.cpp:95-101: acc += A*ul + B*ur, j ascending
 template <int P>
 SK_HD void project_cell(const double* A, const double* B, const double* ul, const double* ur,
@@ -375,15 +417,15 @@ SK_HD bool over_threshold(double num, double den, const ThrCut& t) {
 
 // inline_indicator with the source-cell means supplied by the caller (a sweep
 // that walks cells in order reuses the right mean as the next left one)
-template <int P>
+template <int P, bool FMA = false>
 SK_HD bool inline_indicator_m(const ThrCut& t, const double* ext_l, const double* ext_r,
                               double mean_l, double mean_r, const double* up) {
     double denom = dmax2(fabs(mean_l), fabs(mean_r));
     double el = 0.0, er = 0.0;
 #pragma unroll
     for (int n = 0; n < P; ++n) {
-        el += ext_l[n] * up[n];
-        er += ext_r[n] * up[n];
+        el = madd<FMA>(el, ext_l[n], up[n]);
+        er = madd<FMA>(er, ext_r[n], up[n]);
     }
     return over_threshold(fabs(el - mean_l) + fabs(er - mean_r), denom, t);
 }

@@ -322,7 +322,8 @@ class Context:
         _check(N.lib().sk_ctx_set_eager_errors(self.h, int(on)))
 
     def set_exact_reductions(self, on: bool):
-        """parity mode: reference-order charge density + sequential dpbtrs solve"""
+        """exact (parity) mode: reference rounding sequence in the sweeps (no FMA),
+        reference-order charge density, sequential dpbtrs solve"""
         _check(N.lib().sk_ctx_set_exact_reductions(self.h, int(on)))
 
     def synchronize(self):

@@ -2,14 +2,16 @@
 to the reference, tests/test_oracle_pin.py) and the reference's golden vectors.
 
 Bar:
-  * kernel level (same inputs, same E): BITWISE -- x/v sweeps with the inline
-    limiter and 3-block ghosts, post limiters, velocity cut-off, blob fill;
+  * kernel level (same inputs, same E), exact mode: BITWISE -- x/v sweeps with
+    the inline limiter and 3-block ghosts, post limiters, velocity cut-off,
+    blob fill; fast mode (DFMA-contracted sweeps): <= 1e-12 relative;
   * full steps: max|df|/max|f| <= 1e-12 per species after 1 and 10 steps,
     |dE| <= 1e-12 * max(1, max|E|), identical shrink steps and v_max,
     diagnostics (mass, L2, momentum, kinetic, electric energy) rel <= 1e-12.
     (The charge-density reduction order differs from the serial reference,
     so full steps are tolerance-level, App. A item 6.)
-  * full size (C3): sampled x and v lines of one GPU sweep, bitwise.
+  * full size (C3): sampled x and v lines of one GPU sweep, bitwise in exact
+    mode, <= 1e-12 in fast mode.
 """
 import os
 import subprocess
@@ -48,14 +50,20 @@ KERNEL_CFGS = [
 ]
 
 
-def _pair(sk, ora, kw):
+def _pair(sk, ora, kw, exact=True):
     cfg = cfg_of(sk, **kw)
-    return cfg, ora.state(**cfg.oracle_kwargs()), sk.SimulationState(cfg)
+    return cfg, ora.state(**cfg.oracle_kwargs()), sk.SimulationState(cfg, exact=exact)
 
 
+def _same(got, want, exact):
+    """exact mode: bitwise; fast mode: the north-star tolerance"""
+    return np.array_equal(got, want) if exact else rel(got, want) <= F_TOL
+
+
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
 @pytest.mark.parametrize("kw", KERNEL_CFGS, ids=lambda d: f"k{d['k']}m{d['m']}{d['limiter']}")
-def test_sweeps_bitwise(sk, ora, kw):
-    cfg, o, st = _pair(sk, ora, kw)
+def test_sweeps_bitwise(sk, ora, kw, exact):
+    cfg, o, st = _pair(sk, ora, kw, exact)
     for sp in (0, 1):
         assert np.array_equal(st.field(sp).download(), o.field(sp)), "blob fill"
     lim = sk.LimiterConfig.parse(cfg.limiter)
@@ -67,6 +75,7 @@ def test_sweeps_bitwise(sk, ora, kw):
     st.run_steps(3)
     for sp in (0, 1):
         assert st.field(sp).vmax() == o.vmax(sp)
+    st.ctx.set_exact_reductions(exact)
     E = o.E()
     for sp in (0, 1):
         f = st.field(sp)
@@ -75,7 +84,7 @@ def test_sweeps_bitwise(sk, ora, kw):
             sk.advect_x(f, tau, spar[sp], sk.SweepOptions(limiter=lim, max_ghost=-1))
             ref = o.field(sp)
             o.advect_x(sp, tau, limited=True, max_ghost=-1)
-            assert np.array_equal(f.download(), o.field(sp)), f"advect_x sp{sp} tau{tau}"
+            assert _same(f.download(), o.field(sp), exact), f"advect_x sp{sp} tau{tau}"
             o.set_field(sp, ref)
         x = np.linspace(-1.0, 1.0, E.size)
         for tau, Es in ((cfg.dt, E), (cfg.dt, 30.0 * np.sin(4.0 * x))):  # multi-cell v shifts
@@ -83,7 +92,7 @@ def test_sweeps_bitwise(sk, ora, kw):
             sk.advect_v(f, tau, Es, spar[sp], sk.SweepOptions(limiter=lim))
             ref = o.field(sp)
             o.advect_v(sp, tau, Es, limited=True)
-            assert np.array_equal(f.download(), o.field(sp)), f"advect_v sp{sp}"
+            assert _same(f.download(), o.field(sp), exact), f"advect_v sp{sp}"
             o.set_field(sp, ref)
 
 
@@ -354,13 +363,16 @@ def test_periodic_sweep_conserves_mass(sk):
         assert abs(f.mass() - m0) <= 1e-13 * abs(m0)
 
 
-def test_c3_full_size_sampled_lines_bitwise(sk, ora):
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
+def test_c3_full_size_sampled_lines_bitwise(sk, ora, exact):
     """C3 (2048x4096, k=3, mu=1836, sldg): one GPU x and v sweep at full size;
-    48 sampled lines recomputed by the oracle must match bit for bit."""
+    48 sampled lines recomputed by the oracle must match bit for bit (exact
+    mode) or to 1e-12 (fast mode)."""
     cfg = sk.named_config("C3")
     st = sk.SimulationState(cfg)
     st.run_steps(2)
     st.ctx.synchronize()
+    st.ctx.set_exact_reductions(exact)
     p = cfg.k + 1
     nx, nv = cfg.nx, cfg.v_cells
     rng = np.random.default_rng(7)
@@ -378,7 +390,7 @@ def test_c3_full_size_sampled_lines_bitwise(sk, ora):
             vnode = (vleft + vc * vdx) + vdx * nodes[vn]
             out = ora.advect_x_line(cfg.k, grid.left, grid.cells, grid.dx, vnode / spar.sqrt_mu,
                                     0.5 * cfg.dt, before[r], inline_sldg=True)
-            assert np.array_equal(out, after[r]), f"x line {r} sp{sp}"
+            assert _same(after[r], out, exact), f"x line {r} sp{sp}"
         # v sweep with a synthetic, strong field (multi-cell shifts)
         x = np.linspace(-1, 1, nx * p)
         E = 0.3 * np.sin(3 * x)
@@ -389,7 +401,7 @@ def test_c3_full_size_sampled_lines_bitwise(sk, ora):
         lines = after[:, cols].T.copy()  # [ncols, nv*p]
         ref = ora.advect_v_lines(cfg.k, lines, 0, nv, 0, E[cols], spar.charge_sign, spar.sqrt_mu,
                                  cfg.dt, vdx, limiter="sldg")
-        assert np.array_equal(ref, vout[:, cols].T), f"v lines sp{sp}"
+        assert _same(vout[:, cols].T, ref, exact), f"v lines sp{sp}"
 
 
 def test_cpp_mirror_runs_against_oracle():
