@@ -355,7 +355,7 @@ struct XCfg {
     static constexpr int HDR = 6;                   // tile header (8 ints + weight) from the producer
     static constexpr int STAGE = ((WIN + NF + HDR + 1) / 2) * 2;
     static constexpr int S = 5;                     // input stages (outputs go straight to HBM)
-    static constexpr int RACC = T * P;              // fused charge-density accumulators (RHO)
+    static constexpr int RACC = 0;                  // (fused-moment accumulators live in registers)
     static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + RACC) + 8 * 2 * S;
 };
 
@@ -504,8 +504,16 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     [[maybe_unused]] const ThrCut cut = make_thr_cut(a.threshold);
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
-    if constexpr (RHO)  // each thread owns its cells' x dofs: no sharing, no sync
-        for (int e = tid; e < C::RACC; e += C::NT) racc[e] = 0.0;
+    // fused moment: the grid is a multiple of the tiles per line, so this CTA
+    // always sees the same tile column and each thread the same cells -- the
+    // accumulators live in registers
+    [[maybe_unused]] double rreg[RHO ? C::CPT : 1][RHO ? P : 1];
+    if constexpr (RHO)
+#pragma unroll
+        for (int cc = 0; cc < C::CPT; ++cc)
+#pragma unroll
+            for (int m = 0; m < P; ++m) rreg[cc][m] = 0.0;
+    (void)racc;
     int rcol_nt = 0, rcol_base = 0;
     int it = 0;
     for (int t = blockIdx.x; t < ntot; t += G, ++it) {
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             if (c < nt) {
                 if constexpr (RHO) {
 #pragma unroll
-                    for (int m = 0; m < P; ++m) racc[c * P + m] = madd<FMA>(racc[c * P + m], wdv, o[cc][m]);
+                    for (int m = 0; m < P; ++m) rreg[cc][m] = madd<FMA>(rreg[cc][m], wdv, o[cc][m]);
                 }
             }
         }
@@ -640,7 +648,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             const int c = tid + cc * C::NT;
             if (c < rcol_nt) {
 #pragma unroll
-                for (int n = 0; n < P; ++n) prow[(long long)(rcol_base + c) * P + n] = racc[c * P + n];
+                for (int n = 0; n < P; ++n) prow[(long long)(rcol_base + c) * P + n] = rreg[cc][n];
             }
         }
     }
