@@ -861,9 +861,16 @@ __device__ __forceinline__ bool rescan_indicator(const Basis& b, double thr, int
     return inline_indicator_m<P, false>(cut, el, er, mean<P>(b, ul), mean<P>(b, ur), o);
 }
 
+// out-of-line ghost fetch for the fixup kernels (keeps their code small)
+template <int P>
+__device__ __noinline__ double x_fetch_outside_ool(const Basis& basis, const Grid& g, const double* line,
+                                                   int b, int s, int n) {
+    return x_fetch_outside<P>(basis, g, line, b, s, n);
+}
+
 template <int P>
 __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line, int cell, bool rescan,
-                                          unsigned* ct, unsigned* cc, unsigned* co) {
+                                       unsigned* ct, unsigned* cc, unsigned* co) {
     constexpr int NF = xnf<P>();
     const Grid& g = a.grid;
     int b = 0;
@@ -878,17 +885,14 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int s = local + istar + h;
-        for (int q = 0; q < P; ++q) {
-            double v;
-            if (a.periodic) {
-                const int ss = ((s % g.cells[b]) + g.cells[b]) % g.cells[b];
-                v = src[(long long)(g.start[b] + ss) * P + q];
-            } else if (s >= 0 && s < g.cells[b]) {
-                v = src[(long long)(g.start[b] + s) * P + q];
-            } else {
-                v = x_fetch_outside<P>(a.basis, g, src, b, s, q);
-            }
-            uu[h][q] = v;
+        if (a.periodic || (s >= 0 && s < g.cells[b])) {
+            const int ss = a.periodic ? ((s % g.cells[b]) + g.cells[b]) % g.cells[b] : s;
+            const double* cp = src + (long long)(g.start[b] + ss) * P;
+#pragma unroll
+            for (int q = 0; q < P; ++q) uu[h][q] = cp[q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) uu[h][q] = x_fetch_outside_ool<P>(a.basis, g, src, b, s, q);
         }
     }
     double* up = a.dst[sp] + lbase + (long long)cell * P;
@@ -926,26 +930,31 @@ __global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSwee
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
     const long long stride = (long long)gridDim.x * blockDim.x;
     const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (cnt <= a.fix_cap) {
-        for (long long i = i0; i < cnt; i += stride) {
+    // list mode, or (list overflowed) a rescan of every cell of the sweep; one
+    // loop so the clamp is inlined once (twice made the kernel fetch-bound)
+    const bool rescan = cnt > a.fix_cap;
+    const long long n = rescan ? (long long)a.nspecies * a.nlines * a.grid.ncells : (long long)cnt;
+    for (long long i = i0; i < n; i += stride) {
+        int sp, line, cell;
+        if (!rescan) {
             const unsigned long long e = a.fix_list[i];
-            xfix_cell<P>(a, (int)(e >> 63), (int)((e >> 32) & 0x7fffffffu), (int)(e & 0xffffffffu),
-                         false, ct, cc, co);
-        }
-    } else {  // list overflowed: rescan every cell of the sweep
-        const long long ncell = (long long)a.nspecies * a.nlines * a.grid.ncells;
-        for (long long i = i0; i < ncell; i += stride) {
-            const int cell = (int)(i % a.grid.ncells);
+            sp = (int)(e >> 63);
+            line = (int)((e >> 32) & 0x7fffffffu);
+            cell = (int)(e & 0xffffffffu);
+        } else {
+            cell = (int)(i % a.grid.ncells);
             const long long r = i / a.grid.ncells;
-            xfix_cell<P>(a, a.species0 + (int)(r / a.nlines), (int)(r % a.nlines), cell, true, ct, cc, co);
+            sp = a.species0 + (int)(r / a.nlines);
+            line = (int)(r % a.nlines);
         }
+        xfix_cell<P>(a, sp, line, cell, rescan, ct, cc, co);
     }
     block_count_flags(a.st, ct, cc, co);
 }
 
 template <int P>
 __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, int xd, bool rescan,
-                                          unsigned* ct, unsigned* cc, unsigned* co) {
+                                       unsigned* ct, unsigned* cc, unsigned* co) {
     const double* t = a.tab[sp];
     const int nx = a.nxd;
     const int istar = (int)t[xd];
@@ -979,19 +988,22 @@ __global__ void __launch_bounds__(128) vfix_kernel(const __grid_constant__ VSwee
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
     const long long stride = (long long)gridDim.x * blockDim.x;
     const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (cnt <= a.fix_cap) {
-        for (long long i = i0; i < cnt; i += stride) {
+    const bool rescan = cnt > a.fix_cap;  // see xfix_kernel
+    const long long n = rescan ? (long long)a.nspecies * a.n * a.nxd : (long long)cnt;
+    for (long long i = i0; i < n; i += stride) {
+        int sp, j, xd;
+        if (!rescan) {
             const unsigned long long e = a.fix_list[i];
-            vfix_cell<P>(a, (int)(e >> 63), (int)((e >> 32) & 0x7fffffffu), (int)(e & 0xffffffffu),
-                         false, ct, cc, co);
-        }
-    } else {  // list overflowed: rescan every cell
-        const long long ncell = (long long)a.nspecies * a.n * a.nxd;
-        for (long long i = i0; i < ncell; i += stride) {
-            const int xd = (int)(i % a.nxd);
+            sp = (int)(e >> 63);
+            j = (int)((e >> 32) & 0x7fffffffu);
+            xd = (int)(e & 0xffffffffu);
+        } else {
+            xd = (int)(i % a.nxd);
             const long long r = i / a.nxd;
-            vfix_cell<P>(a, a.species0 + (int)(r / a.n), (int)(r % a.n), xd, true, ct, cc, co);
+            sp = a.species0 + (int)(r / a.n);
+            j = (int)(r % a.n);
         }
+        vfix_cell<P>(a, sp, j, xd, rescan, ct, cc, co);
     }
     block_count_flags(a.st, ct, cc, co);
 }

@@ -5,14 +5,17 @@ def summary(rep, regex=None):
     cmd = ["ncu", "-i", rep, "--page", "raw", "--csv"]
     out = subprocess.run(cmd, capture_output=True, text=True).stdout.splitlines()
     r = csv.reader(out)
-    hdr = next(r); next(r)
+    hdr = next(r)
+    units = dict(zip(hdr, next(r)))
+    scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3,
+             "byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3}
     lines = []
     for vals in r:
         d = dict(zip(hdr, vals))
         name = d["Kernel Name"]
         if regex and regex not in name:
             continue
-        f = lambda k: float(d.get(k, "0").replace(",", "") or 0)
+        f = lambda k: float(d.get(k, "0").replace(",", "") or 0) * scale.get(units.get(k, ""), 1.0)
         st = {k: float(v.replace(",", "")) for k, v in d.items()
               if k.startswith("smsp__pcsamp_warps_issue_stalled") and not k.endswith("not_issued")
               and v.replace(",", "").replace(".", "").isdigit()}
