@@ -868,7 +868,7 @@ __device__ __noinline__ double x_fetch_outside_ool(const Basis& basis, const Gri
     return x_fetch_outside<P>(basis, g, line, b, s, n);
 }
 
-template <int P>
+template <int P, bool FMA>
 __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line, int cell, bool rescan,
                                        unsigned* ct, unsigned* cc, unsigned* co) {
     constexpr int NF = xnf<P>();
@@ -905,7 +905,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
     double o0[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) o0[q] = o[q];
-    const int fl = inline_clamp<P>(a.basis, alpha, uu[0], uu[1], o);
+    const int fl = inline_clamp_f<P, FMA>(a.basis, alpha, uu[0], uu[1], o);
 #pragma unroll
     for (int q = 0; q < P; ++q) up[q] = o[q];
     if (a.rho_fuse && (fl & 2)) {  // the fused moment summed the unclamped values
@@ -924,7 +924,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
     co[sp] += (fl >> 2) & 1;
 }
 
-template <int P>
+template <int P, bool FMA>
 __global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSweepArgs a) {
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
@@ -947,12 +947,12 @@ __global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSwee
             sp = a.species0 + (int)(r / a.nlines);
             line = (int)(r % a.nlines);
         }
-        xfix_cell<P>(a, sp, line, cell, rescan, ct, cc, co);
+        xfix_cell<P, FMA>(a, sp, line, cell, rescan, ct, cc, co);
     }
     block_count_flags(a.st, ct, cc, co);
 }
 
-template <int P>
+template <int P, bool FMA>
 __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, int xd, bool rescan,
                                        unsigned* ct, unsigned* cc, unsigned* co) {
     const double* t = a.tab[sp];
@@ -974,7 +974,7 @@ __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, in
         }
         if (!rescan_indicator<P>(a.basis, a.threshold, a.fma, el, er, ul, ur, o)) return;
     }
-    const int fl = inline_clamp<P>(a.basis, alpha, ul, ur, o);
+    const int fl = inline_clamp_f<P, FMA>(a.basis, alpha, ul, ur, o);
 #pragma unroll
     for (int m = 0; m < P; ++m) op[m * a.ld] = o[m];
     ct[sp] += fl & 1;
@@ -982,7 +982,7 @@ __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, in
     co[sp] += (fl >> 2) & 1;
 }
 
-template <int P>
+template <int P, bool FMA>
 __global__ void __launch_bounds__(128) vfix_kernel(const __grid_constant__ VSweepArgs a) {
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
@@ -1003,7 +1003,7 @@ __global__ void __launch_bounds__(128) vfix_kernel(const __grid_constant__ VSwee
             sp = a.species0 + (int)(r / a.n);
             j = (int)(r % a.n);
         }
-        vfix_cell<P>(a, sp, j, xd, rescan, ct, cc, co);
+        vfix_cell<P, FMA>(a, sp, j, xd, rescan, ct, cc, co);
     }
     block_count_flags(a.st, ct, cc, co);
 }
@@ -1746,13 +1746,32 @@ cudaError_t launch_xsweep(const XSweepArgs& a, int /*ntiles*/, cudaStream_t s) {
     return cudaSuccess;
 }
 
+template <int P>
+static void launch_xfix_t(const XSweepArgs& a, cudaStream_t s) {
+    if constexpr (kHasFma<P>)
+        if (a.fma) {
+            xfix_kernel<P, true><<<sm_count() * 8, 128, 0, s>>>(a);
+            return;
+        }
+    xfix_kernel<P, false><<<sm_count() * 8, 128, 0, s>>>(a);
+}
+template <int P>
+static void launch_vfix_t(const VSweepArgs& a, cudaStream_t s) {
+    if constexpr (kHasFma<P>)
+        if (a.fma) {
+            vfix_kernel<P, true><<<sm_count() * 8, 128, 0, s>>>(a);
+            return;
+        }
+    vfix_kernel<P, false><<<sm_count() * 8, 128, 0, s>>>(a);
+}
+
 cudaError_t launch_xfix(const XSweepArgs& a, cudaStream_t s) {
-    SK_DISPATCH_P(a.basis.p, (xfix_kernel<PP><<<sm_count() * 8, 128, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (launch_xfix_t<PP>(a, s)));
     return cudaGetLastError();
 }
 
 cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s) {
-    SK_DISPATCH_P(a.basis.p, (vfix_kernel<PP><<<sm_count() * 8, 128, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (launch_vfix_t<PP>(a, s)));
     return cudaGetLastError();
 }
 

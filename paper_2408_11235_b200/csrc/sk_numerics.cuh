@@ -459,6 +459,86 @@ SK_HD int inline_clamp(const Basis& b, double alpha, const double* ul, const dou
     return flags;
 }
 
+// Fast-mode clamp (k <= 3): the same candidate points (interval ends and the
+// interior roots of p'), but every value comes from Horner's rule on the
+// monomial coefficients the root search needs anyway -- no barycentric
+// divisions. Agrees with inline_clamp to rounding (tolerance mode only).
+template <int P>
+SK_HD void extremum_minmax_fast(const Basis& b, const double* u, double a, double bb, double& mx,
+                                double& mn) {
+    static_assert(P <= 4, "fast extremum search is for k <= 3");
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int d = 0; d < P; ++d) {
+        double acc = 0.0;
+#pragma unroll
+        for (int n = 0; n < P; ++n) acc = fma(b.mono[d * P + n], u[n], acc);
+        c[d] = acc;
+    }
+    auto horner = [&](double x) { return fma(fma(fma(c[3], x, c[2]), x, c[1]), x, c[0]); };
+    const double va = horner(a);
+    mx = va;
+    mn = va;
+    if (bb == a) return;
+    const double vb = horner(bb);
+    mx = fmax(mx, vb);
+    mn = fmin(mn, vb);
+    if constexpr (P >= 3) {
+        const double qa = 3.0 * c[3], qb = 2.0 * c[2], qc = c[1];
+        double x0 = 0.0, x1 = 0.0;
+        int nc = 0;
+        if (fabs(qa) > 0.0) {
+            const double disc = qb * qb - 4.0 * qa * qc;
+            if (disc >= 0.0) {
+                const double r = sqrt(disc), inv = 1.0 / (2.0 * qa);
+                x0 = (-qb + r) * inv;
+                x1 = (-qb - r) * inv;
+                nc = 2;
+            }
+        } else if (fabs(qb) > 0.0) {
+            x0 = -qc / qb;
+            nc = 1;
+        }
+        if (nc >= 1 && x0 > a && x0 < bb) {
+            const double v = horner(x0);
+            mx = fmax(mx, v);
+            mn = fmin(mn, v);
+        }
+        if (nc >= 2 && x1 > a && x1 < bb) {
+            const double v = horner(x1);
+            mx = fmax(mx, v);
+            mn = fmin(mn, v);
+        }
+    }
+}
+
+template <int P, bool FMA>
+SK_HD int inline_clamp_f(const Basis& b, double alpha, const double* ul, const double* ur, double* up) {
+    if constexpr (!FMA || P > 4) {
+        return inline_clamp<P>(b, alpha, ul, ur, up);
+    } else {
+        int flags = 1;
+        const double mean_p = mean_f<P, true>(b, up);
+        double lmax, lmin, rmax, rmin, pmax, pmin;
+        extremum_minmax_fast<P>(b, ul, alpha, 1.0, lmax, lmin);
+        extremum_minmax_fast<P>(b, ur, 0.0, alpha, rmax, rmin);
+        extremum_minmax_fast<P>(b, up, 0.0, 1.0, pmax, pmin);
+        const double wmax = dmax2(lmax, rmax), wmin = dmin2(lmin, rmin);
+        if ((mean_p > wmax) || (mean_p < wmin)) flags |= 4;
+        double theta = 1.0;
+        const double dmx = pmax - mean_p;
+        if (dmx != 0.0) theta = dmin2(theta, fabs((wmax - mean_p) / dmx));
+        const double dmn = pmin - mean_p;
+        if (dmn != 0.0) theta = dmin2(theta, fabs((wmin - mean_p) / dmn));
+        if (theta < 1.0) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) up[j] = fma(theta, up[j] - mean_p, mean_p);
+            flags |= 2;
+        }
+        return flags;
+    }
+}
+
 // Inline sLdG limiter, limiters.cpp:217-222 (indicator, then clamp).
 template <int P>
 SK_HD int inline_limit(const Basis& b, double alpha, double threshold, const double* ext_l,
