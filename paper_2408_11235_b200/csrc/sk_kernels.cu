@@ -1707,30 +1707,50 @@ int xsweep_rho_groups(const XSweepArgs& a) {
     return 0;
 }
 
-__global__ void rho_fused_reduce_kernel(const double* partial, const unsigned long long* corr,
-                                        int groups, int nxd, double* rho) {
-    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
-    if (xd >= nxd) return;
+// rho[x] = sum of the groups' partial rows + the clamp corrections. 32 x dofs
+// per CTA, 8 threads per x dof each summing a fixed residue class of rows,
+// combined in a fixed order: deterministic, and 64x more loads in flight than
+// one thread per x dof.
+constexpr int kRhoRedParts = 8;
+__global__ void __launch_bounds__(32 * kRhoRedParts)
+    rho_fused_reduce_kernel(const double* partial, const unsigned long long* corr, int groups, int nxd,
+                            double* rho) {
+    __shared__ double sp[kRhoRedParts][32];
+    __shared__ unsigned long long sh[kRhoRedParts][32], sl[kRhoRedParts][32];
+    const int l = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const int xd = blockIdx.x * 32 + l;
     double acc = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < groups; ++k) acc += __ldg(partial + (long long)k * nxd + xd);  // loads overlap
-    // clamp corrections (rho_corr_add): integer sums are exact, so neither the
-    // atomics' order nor the copy split changes rho
     unsigned long long ih = 0, il = 0;
-#pragma unroll 8
-    for (int k = 0; k < kRhoCorrCopies; ++k) {
-        ih += __ldg(corr + (long long)k * nxd + xd);
-        il += __ldg(corr + (long long)(kRhoCorrCopies + k) * nxd + xd);
+    if (xd < nxd) {
+#pragma unroll 4
+        for (int k = q; k < groups; k += kRhoRedParts) acc += __ldg(partial + (long long)k * nxd + xd);
+        // clamp corrections (rho_corr_add): integer sums are exact, so neither
+        // the atomics' order nor the copy split changes rho
+#pragma unroll 4
+        for (int k = q; k < kRhoCorrCopies; k += kRhoRedParts) {
+            ih += __ldg(corr + (long long)k * nxd + xd);
+            il += __ldg(corr + (long long)(kRhoCorrCopies + k) * nxd + xd);
+        }
     }
-    acc += rho_corr_value(ih, il);
-    rho[xd] = acc;
+    sp[q][l] = acc;
+    sh[q][l] = ih;
+    sl[q][l] = il;
+    __syncthreads();
+    if (q == 0 && xd < nxd) {
+        for (int j = 1; j < kRhoRedParts; ++j) {
+            acc += sp[j][l];
+            ih += sh[j][l];
+            il += sl[j][l];
+        }
+        rho[xd] = acc + rho_corr_value(ih, il);
+    }
 }
 
 cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s) {
     const int nxd = a.grid.ncells * a.basis.p;
     const int groups = xsweep_rho_groups(a);
-    rho_fused_reduce_kernel<<<(nxd + 127) / 128, 128, 0, s>>>(a.rho_partial, a.rho_corr, groups,
-                                                             nxd, rho);
+    rho_fused_reduce_kernel<<<(nxd + 31) / 32, 32 * kRhoRedParts, 0, s>>>(a.rho_partial, a.rho_corr, groups,
+                                                                        nxd, rho);
     return cudaGetLastError();
 }
 
