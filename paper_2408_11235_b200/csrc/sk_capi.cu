@@ -253,6 +253,11 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.check_finite = check_finite;
     a.fma = !c->exact;
     a.threshold = threshold;
+    {
+        const ThrCut cut = make_thr_cut(threshold);
+        a.thr_hi = cut.hi;
+        a.thr_lo = cut.lo;
+    }
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;
@@ -329,6 +334,9 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.nxd = c->grid.ncells * c->P;
     a.ld = a.nxd;
     a.n = fs[0]->nv;
+    // v tables (2P^2+2P+2 doubles per x dof and species) beyond ~24 MB would
+    // be evicted between the v chunks that reuse them: walk chunks first
+    a.chunk_major = (size_t)nspecies * a.nxd * (2 * c->P * c->P + 2 * c->P + 2) * 8 > (24u << 20);
     a.gl = fs[0]->gl();
     a.gr = fs[0]->gr();
     a.nspecies = nspecies;
@@ -338,6 +346,11 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.check_finite = check_finite;
     a.fma = !c->exact;
     a.threshold = threshold;
+    {
+        const ThrCut cut = make_thr_cut(threshold);
+        a.thr_hi = cut.hi;
+        a.thr_lo = cut.lo;
+    }
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;

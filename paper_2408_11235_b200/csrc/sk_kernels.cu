@@ -429,6 +429,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     const int ntot = a.nspecies * a.nlines * a.tile_start[g.nblocks];
     const int G = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int vb = blockIdx.x;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::S; ++i) {
@@ -441,14 +442,19 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 
     if (warp == C::NC) {
         // ---------------- producer warp ----------------
-        if (lane == 0) {
-            auto row_of = [&](const XTile& x) -> const double* {
-                return a.tab[x.sp] + ((long long)g.cls[x.b] * a.nlines + x.line) * C::NF;
-            };
-            XTile xn = decode_xtile(a, blockIdx.x, C::T);
-            int istar_next = blockIdx.x < ntot ? (int)__ldg(row_of(xn)) : 0;
+        // lane 0 streams windows with TMA; for even P (bulk copies then land
+        // exactly on cell boundaries) all 32 lanes first write the window cells
+        // outside the copyable range -- walls, 3-block ghosts, periodic wrap --
+        // so the consumers never wait on each other for edge tiles
+        constexpr bool PFILL = (P % 2) == 0;
+        auto row_of = [&](const XTile& x) -> const double* {
+            return a.tab[x.sp] + ((long long)g.cls[x.b] * a.nlines + x.line) * C::NF;
+        };
+        if (PFILL || lane == 0) {
+            XTile xn = decode_xtile(a, vb, C::T);
+            int istar_next = vb < ntot ? (int)__ldg(row_of(xn)) : 0;
             int it = 0;
-            for (int t = blockIdx.x; t < ntot; t += G, ++it) {
+            for (int t = vb; t < ntot; t += G, ++it) {
                 const int stg = it % C::S;
                 const XTile x = xn;
                 const int istar = istar_next;
@@ -462,6 +468,35 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 xvalid_range(a, x.b, vlo, vhi);
                 const int clo = max(s0, vlo), chi = min(s0 + x.nt + 1, vhi);
                 double* st = stages + stg * C::STAGE;
+                // element parity of window cell s0 in HBM decides the smem origin
+                const long long lbase = (long long)x.line * g.ncells * P;
+                const long long eg = lbase + ((long long)g.start[x.b] + s0) * P;
+                const int woff = (int)(eg & 1);
+                if constexpr (PFILL) {
+                    if (clo > s0 || chi < s0 + x.nt + 1) {
+                        const double* src = a.src[x.sp] + lbase;
+                        double* w = st + 2 + woff;
+                        const int cells_b = g.cells[x.b];
+                        const int nlo = (max(clo, s0) - s0) * P;
+                        const int nhi0 = (min(max(chi, s0), s0 + x.nt + 1) - s0) * P;
+                        const int nfill = nlo + ((x.nt + 1) * P - nhi0);
+                        for (int f = lane; f < nfill; f += 32) {
+                            const int e = f < nlo ? f : nhi0 + (f - nlo);
+                            const int wc = e / P, n = e - (e / P) * P;
+                            const int sc = s0 + wc;
+                            double v;
+                            if (a.periodic) {
+                                const int ss = ((sc % cells_b) + cells_b) % cells_b;
+                                v = src[(long long)(g.start[x.b] + ss) * P + n];
+                            } else {
+                                v = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n);
+                            }
+                            w[e] = v;
+                        }
+                    }
+                    __syncwarp();  // fills ordered before lane 0's arrive (release)
+                    if (lane != 0) continue;
+                }
                 // decoded tile for the consumers (released by the arrive below)
                 int* hdr = reinterpret_cast<int*>(st + C::WIN + C::NF);
                 hdr[0] = x.sp;
@@ -476,9 +511,6 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     const int vn = x.line - (x.line / P) * P;
                     reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * a.vg[x.sp]->dx;
                 }
-                // element parity of window cell s0 in HBM decides the smem origin
-                const long long eg = ((long long)x.line * g.ncells + g.start[x.b] + s0) * P;
-                const int woff = (int)(eg & 1);
                 unsigned bytes = C::NF * 8;
                 long long g0 = 0, g1 = 0;
                 if (chi > clo) {
@@ -501,7 +533,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 
     // ---------------- consumer warps ----------------
     const int tid = threadIdx.x;
-    [[maybe_unused]] const ThrCut cut = make_thr_cut(a.threshold);
+    [[maybe_unused]] const ThrCut cut{a.threshold, a.thr_hi, a.thr_lo};
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
     // fused moment: the grid is a multiple of the tiles per line, so this CTA
@@ -516,7 +548,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     (void)racc;
     int rcol_nt = 0, rcol_base = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < ntot; t += G, ++it) {
+    for (int t = vb; t < ntot; t += G, ++it) {
         const int stg = it % C::S;
         mbar_wait(&full[stg], (it / C::S) & 1);
         double* st = stages + stg * C::STAGE;
@@ -532,9 +564,9 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         const long long lbase = (long long)line * g.ncells * P;
         const long long eg = lbase + ((long long)g.start[b] + s0) * P;
         const double* win = st + 2 + (int)(eg & 1);  // window cell w, node n at win[w*P+n]
-        if (clo > s0 || chi < s0 + nt + 1) {
-            // walls (zero inflow), 3-block ghosts, periodic wrap: only the
-            // window cells outside [clo, chi) -- usually |i*|+1 of them
+        if (P % 2 != 0 && (clo > s0 || chi < s0 + nt + 1)) {
+            // (odd P) walls (zero inflow), 3-block ghosts, periodic wrap: only
+            // the window cells outside [clo, chi) -- usually |i*|+1 of them
             const double* src = a.src[sp] + lbase;
             double* w = const_cast<double*>(win);
             const int nlo = (max(clo, s0) - s0) * P;                 // [0, nlo)
@@ -642,7 +674,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         // this CTA always saw the same tile column (grid is a multiple of the
         // tiles per line): one partial row per (column, CTA group)
         const int ntl = a.tile_start[g.nblocks];
-        double* prow = a.rho_partial + (long long)(blockIdx.x / ntl) * g.ncells * P;
+        double* prow = a.rho_partial + (long long)(vb / ntl) * g.ncells * P;
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
             const int c = tid + cc * C::NT;
@@ -728,9 +760,14 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
     constexpr int R = vring<P>();
     static_assert(kVChunk % R == 0, "chunk must be a multiple of the ring depth");
     __shared__ double ring[R * P * kVThreads];
-    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
+    // chunk_major: v chunks are the fastest grid dimension, so the blocks that
+    // share an x range (and its table rows, ~1/3 of the bytes a chunk reads)
+    // run back to back -- chosen when the tables would not stay in L2
+    const int xb = a.chunk_major ? blockIdx.y : blockIdx.x;
+    const int jb = a.chunk_major ? blockIdx.x : blockIdx.y;
+    const int xd = xb * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
-    const int j0 = blockIdx.y * kVChunk;
+    const int j0 = jb * kVChunk;
     const int j1 = min(j0 + kVChunk, a.n);
     bool bad = false;
     double* my = ring + threadIdx.x;
@@ -781,7 +818,7 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
         cp_wait<R - 2>();
 #pragma unroll
         for (int n = 0; n < P; ++n) ul[n] = my[n * kVThreads];
-        [[maybe_unused]] const ThrCut cut = make_thr_cut(a.threshold);
+        [[maybe_unused]] const ThrCut cut{a.threshold, a.thr_hi, a.thr_lo};
         [[maybe_unused]] double mean_l = INLINE ? mean_f<P, FMA>(a.basis, ul) : 0.0;  // carried along the walk
         const bool check = a.check_finite;
         if (R - 1 < ncells) vissue<P>(g_iss, ld, ok(s_iss), my + (R - 1) * P * kVThreads);
@@ -1341,34 +1378,40 @@ __global__ void shrink_table_kernel(const __grid_constant__ ShrinkArgs a) {
 template <int P>
 __global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
     const int sp = blockIdx.z;
+    // bounded grid, (x block, v chunk) items by grid stride: on the (usual)
+    // steps without a shrink the whole launch is a few hundred early exits
     if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
-    const int xd = blockIdx.x * blockDim.x + threadIdx.x;
-    if (xd >= a.nxd) return;
-    const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
+    const int nxb = (a.nxd + blockDim.x - 1) / blockDim.x;
+    const long long nitems = (long long)nxb * ((a.nv + kVChunk - 1) / kVChunk);
     const double* f = a.f[sp];
     double* out = a.out[sp];
-    for (int j = j0; j < j1; ++j) {
-        double dst[P];
+    for (long long w = blockIdx.x; w < nitems; w += gridDim.x) {
+        const int xd = (int)(w % nxb) * blockDim.x + threadIdx.x;
+        if (xd >= a.nxd) continue;
+        const int j0 = (int)(w / nxb) * kVChunk, j1 = min(j0 + kVChunk, a.nv);
+        for (int j = j0; j < j1; ++j) {
+            double dst[P];
 #pragma unroll
-        for (int m = 0; m < P; ++m) dst[m] = 0.0;
-        const double* T = a.ttab[sp] + (long long)j * 4 * P * P;
-        const int* cellv = a.tcell[sp] + (long long)j * 4;
-        for (int pc = 0; pc < 4; ++pc) {
-            const int oc = cellv[pc];
-            if (oc < 0) break;
-            double src[P];
+            for (int m = 0; m < P; ++m) dst[m] = 0.0;
+            const double* T = a.ttab[sp] + (long long)j * 4 * P * P;
+            const int* cellv = a.tcell[sp] + (long long)j * 4;
+            for (int pc = 0; pc < 4; ++pc) {
+                const int oc = cellv[pc];
+                if (oc < 0) break;
+                double src[P];
 #pragma unroll
-            for (int n = 0; n < P; ++n) src[n] = f[((long long)oc * P + n) * a.ld + xd];
+                for (int n = 0; n < P; ++n) src[n] = f[((long long)oc * P + n) * a.ld + xd];
 #pragma unroll
-            for (int m = 0; m < P; ++m) {
-                double acc = 0.0;
+                for (int m = 0; m < P; ++m) {
+                    double acc = 0.0;
 #pragma unroll
-                for (int n = 0; n < P; ++n) acc += T[pc * P * P + m * P + n] * src[n];
-                dst[m] += acc;
+                    for (int n = 0; n < P; ++n) acc += T[pc * P * P + m * P + n] * src[n];
+                    dst[m] += acc;
+                }
             }
-        }
 #pragma unroll
-        for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = dst[m];
+            for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = dst[m];
+        }
     }
 }
 
@@ -1812,7 +1855,8 @@ static void launch_vsweep_f(const VSweepArgs& a, dim3 grid, cudaStream_t s) {
 }
 
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
-    dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.n + kVChunk - 1) / kVChunk, a.nspecies);
+    const int nxb = (a.nxd + kVThreads - 1) / kVThreads, nch = (a.n + kVChunk - 1) / kVChunk;
+    dim3 grid = a.chunk_major ? dim3(nch, nxb, a.nspecies) : dim3(nxb, nch, a.nspecies);
     if (a.periodic)
         SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, true, false><<<grid, kVThreads, 0, s>>>(a)))
     else if (a.inline_sldg)
@@ -1860,7 +1904,7 @@ cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s) {
         SK_DISPATCH_P(P, (shrink_check_kernel<PP><<<dim3((a.nxd + 255) / 256, 2), 256, 0, s>>>(a)));
     if (a.force < 0) return cudaGetLastError();
     SK_DISPATCH_P(P, (shrink_table_kernel<PP><<<dim3((a.nv + 127) / 128, 2), 128, 0, s>>>(a)));
-    SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3((a.nxd + 127) / 128, (a.nv + kVChunk - 1) / kVChunk, 2), 128, 0, s>>>(a)));
+    SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3(sm_count() * 16, 1, 2), 128, 0, s>>>(a)));
     const long long total = (long long)a.nv * P * a.nxd;
     shrink_commit_kernel<<<dim3(1184, 2), 256, 0, s>>>(a, total);
     shrink_finalize_kernel<<<1, 32, 0, s>>>(a);

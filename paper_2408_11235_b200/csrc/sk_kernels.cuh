@@ -48,6 +48,7 @@ struct XSweepArgs {
     int check_finite;
     int fma;  // fast-mode DFMA arithmetic (0: reference rounding sequence)
     double threshold;
+    double thr_hi, thr_lo;  // make_thr_cut(threshold), precomputed on the host
     // deferred limiter clamp: troubled cells are queued here and clamped by
     // the fixup kernel so one slow cell never stalls a whole CTA
     unsigned long long* fix_list;
@@ -94,8 +95,10 @@ struct VSweepArgs {
     int inline_sldg;
     int periodic;
     int check_finite;
+    int chunk_major;  // grid order: v chunks fastest (large tables, see vsweep_kernel)
     int fma;  // fast-mode DFMA arithmetic (0: reference rounding sequence)
     double threshold;
+    double thr_hi, thr_lo;  // make_thr_cut(threshold), precomputed on the host
     unsigned long long* fix_list;
     unsigned int* fix_count;
     unsigned int fix_cap;
