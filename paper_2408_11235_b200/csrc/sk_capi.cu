@@ -91,9 +91,26 @@ struct sk_field {
     double* vtab = nullptr;            // [vnf][nx*P]
     double* ttab = nullptr;            // shrink transfer [nv][4][P*P]
     int* tcell = nullptr;              // [nv][4]
+    // Device flag: set when a velocity cut-off left the projected field in the
+    // other buffer (shrink_finalize toggles it instead of copying back). Kernels
+    // resolve it themselves; host-side buffer access goes through live_ptr().
+    int* dflip = nullptr;
+    bool may_flip = false;             // a shrink projection was ever enqueued
     double* cur_ptr() { return buf[cur] + halo_off; }
     double* other_ptr() { return buf[cur ^ 1] + halo_off; }
     void swap() { cur ^= 1; }
+    // the buffer holding the field right now (synchronises the stream)
+    cudaError_t live_ptr(double** p) {
+        if (!may_flip) {
+            *p = cur_ptr();
+            return cudaSuccess;
+        }
+        int fl = 0;
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpy(&fl, dflip, sizeof fl, cudaMemcpyDeviceToHost);
+        *p = buf[cur ^ (fl & 1)] + halo_off;
+        return e;
+    }
     int gl() const { return cell0 > 0 ? halo : 0; }
     int gr() const { return cell0 + nv < nv_global ? halo : 0; }
 };
@@ -242,6 +259,7 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
         int sp = fs[i]->species;
         a.src[sp] = fs[i]->cur_ptr();
         a.dst[sp] = fs[i]->other_ptr();
+        a.flip[sp] = fs[i]->dflip;
         a.tab[sp] = fs[i]->xtab;
     }
     a.nlines = fs[0]->nv * c->P;
@@ -329,6 +347,7 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
         int sp = fs[i]->species;
         a.src[sp] = fs[i]->cur_ptr();
         a.dst[sp] = fs[i]->other_ptr();
+        a.flip[sp] = fs[i]->dflip;
         a.tab[sp] = fs[i]->vtab;
     }
     a.nxd = c->grid.ncells * c->P;
@@ -378,6 +397,7 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
         int sp = fs[i]->species;
         a.src[sp] = fs[i]->cur_ptr();
         a.dst[sp] = fs[i]->other_ptr();
+        a.flip[sp] = fs[i]->dflip;
     }
     a.cfg = post_cfg(lim);
     a.nxd = c->grid.ncells * c->P;
@@ -407,6 +427,10 @@ sk_status enq_rho(sk_field* fe, sk_field* fi, double* rho) {
     a.vg[1] = fi->vg;
     a.f[0] = fe->cur_ptr();
     a.f[1] = fi->cur_ptr();
+    a.alt[0] = fe->other_ptr();
+    a.alt[1] = fi->other_ptr();
+    a.flip[0] = fe->dflip;
+    a.flip[1] = fi->dflip;
     a.nxd = c->grid.ncells * c->P;
     a.ld = a.nxd;
     a.nrows = fe->nv * c->P;
@@ -442,6 +466,9 @@ sk_status enq_shrink(sk_field** fs, int nspecies, const sk_vadjust& pol, int for
         a.vg[sp] = fs[i]->vg;
         a.f[sp] = fs[i]->cur_ptr();
         a.out[sp] = fs[i]->other_ptr();
+        a.flip[sp] = fs[i]->dflip;
+        a.flip_w[sp] = fs[i]->dflip;
+        if (force >= 0) fs[i]->may_flip = true;
         a.ttab[sp] = fs[i]->ttab;
         a.tcell[sp] = fs[i]->tcell;
     }
@@ -456,7 +483,7 @@ sk_status enq_shrink(sk_field** fs, int nspecies, const sk_vadjust& pol, int for
     a.tol = pol.tol;
     a.cooldown = 10;
     CK(launch_shrink(a, c->stream));
-    c->launches += (force != 0) + (force != 1) + (force >= 0 ? 4 : 0);
+    c->launches += (force != 0) + (force != 1) + (force >= 0 ? 3 : 0);
     return SK_OK;
 }
 
@@ -483,6 +510,8 @@ sk_status moments(sk_field* f, double* out4) {
     a.grid = c->grid;
     a.vg = f->vg;
     a.f = f->cur_ptr();
+    a.alt = f->other_ptr();
+    a.flip = f->dflip;
     a.nxd = c->grid.ncells * c->P;
     a.ld = a.nxd;
     a.nrows = f->nv * c->P;
@@ -721,6 +750,8 @@ sk_status sk_field_create_shard(sk_ctx* c, int species, double v_left, double v_
     CK(cudaMemsetAsync(f->buf[0], 0, sizeof(double) * total, c->stream));
     CK(cudaMemsetAsync(f->buf[1], 0, sizeof(double) * total, c->stream));
     CK(dalloc(&f->vg, 1));
+    CK(dalloc(&f->dflip, 1));
+    CK(cudaMemsetAsync(f->dflip, 0, sizeof(int), c->stream));
     DevVGrid vg{v_left, dv, v_cells_global, cell0};
     CK(cudaMemcpy(f->vg, &vg, sizeof vg, cudaMemcpyHostToDevice));
     CK(dalloc(&f->xtab, (size_t)c->grid.nclass * ncell * P * xtab_nf(P)));
@@ -740,7 +771,8 @@ sk_status sk_field_create(sk_ctx* c, int species, double v_left, double v_right,
 sk_status sk_field_halo(sk_field* f, int side, int send, double** ptr, size_t* count) {
     if (f->halo == 0) return fail(SK_ERR_RUNTIME, "field has no v halo");
     const size_t hrows = f->halo_off;  // halo cells * P * row doubles
-    double* in = f->cur_ptr();
+    double* in = nullptr;
+    CK(f->live_ptr(&in));
     if (side == 0)
         *ptr = send ? in : in - hrows;
     else
@@ -756,6 +788,7 @@ sk_status sk_field_destroy(sk_field* f) {
     cudaFree(f->buf[0]);
     cudaFree(f->buf[1]);
     cudaFree(f->vg);
+    cudaFree(f->dflip);
     cudaFree(f->xtab);
     cudaFree(f->vtab);
     cudaFree(f->ttab);
@@ -765,31 +798,42 @@ sk_status sk_field_destroy(sk_field* f) {
 }
 
 size_t sk_field_size(const sk_field* f) { return f->n; }
-double* sk_field_data_dev(sk_field* f) { return f->cur_ptr(); }
+double* sk_field_data_dev(sk_field* f) {
+    double* p = nullptr;
+    return f->live_ptr(&p) == cudaSuccess ? p : nullptr;
+}
 
 sk_status sk_field_upload(sk_field* f, const double* host, size_t count) {
     if (count != f->n) return fail(SK_ERR_RUNTIME, "field upload: size mismatch");
-    CK(cudaMemcpyAsync(f->cur_ptr(), host, sizeof(double) * count, cudaMemcpyHostToDevice,
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    CK(cudaMemcpyAsync(live, host, sizeof(double) * count, cudaMemcpyHostToDevice,
                        f->ctx->stream));
     CK(cudaStreamSynchronize(f->ctx->stream));
     return SK_OK;
 }
 sk_status sk_field_download(sk_field* f, double* host, size_t count) {
     if (count != f->n) return fail(SK_ERR_RUNTIME, "field download: size mismatch");
-    CK(cudaMemcpyAsync(host, f->cur_ptr(), sizeof(double) * count, cudaMemcpyDeviceToHost,
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    CK(cudaMemcpyAsync(host, live, sizeof(double) * count, cudaMemcpyDeviceToHost,
                        f->ctx->stream));
     CK(cudaStreamSynchronize(f->ctx->stream));
     return SK_OK;
 }
 sk_status sk_field_upload_async(sk_field* f, const double* host, size_t count) {
     if (count != f->n) return fail(SK_ERR_RUNTIME, "field upload: size mismatch");
-    CK(cudaMemcpyAsync(f->cur_ptr(), host, sizeof(double) * count, cudaMemcpyHostToDevice,
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    CK(cudaMemcpyAsync(live, host, sizeof(double) * count, cudaMemcpyHostToDevice,
                        f->ctx->stream));
     return SK_OK;
 }
 sk_status sk_field_download_async(sk_field* f, double* host, size_t count) {
     if (count != f->n) return fail(SK_ERR_RUNTIME, "field download: size mismatch");
-    CK(cudaMemcpyAsync(host, f->cur_ptr(), sizeof(double) * count, cudaMemcpyDeviceToHost,
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    CK(cudaMemcpyAsync(host, live, sizeof(double) * count, cudaMemcpyDeviceToHost,
                        f->ctx->stream));
     return SK_OK;
 }
@@ -831,7 +875,9 @@ sk_status sk_field_fill_blob(sk_field* f, double sigma) {
     CK(dalloc(&dgv, gv.size()));
     CK(cudaMemcpy(dgx, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dgv, gv.data(), sizeof(double) * gv.size(), cudaMemcpyHostToDevice));
-    CK(launch_fill_separable(f->cur_ptr(), dgx, dgv, (long long)g.ncells * P, f->nv * P, c->stream));
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    CK(launch_fill_separable(live, dgx, dgv, (long long)g.ncells * P, f->nv * P, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     cudaFree(dgx);
     cudaFree(dgv);

@@ -430,6 +430,9 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     const int G = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int vb = blockIdx.x;
+    const unsigned fm = (field_flipped(a.flip[0]) ? 1u : 0u) | (field_flipped(a.flip[1]) ? 2u : 0u);
+    auto srcp = [&](int sp) -> const double* { return ((fm >> sp) & 1u) ? a.dst[sp] : a.src[sp]; };
+    auto dstp = [&](int sp) -> double* { return ((fm >> sp) & 1u) ? const_cast<double*>(a.src[sp]) : a.dst[sp]; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::S; ++i) {
@@ -474,7 +477,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 const int woff = (int)(eg & 1);
                 if constexpr (PFILL) {
                     if (clo > s0 || chi < s0 + x.nt + 1) {
-                        const double* src = a.src[x.sp] + lbase;
+                        const double* src = srcp(x.sp) + lbase;
                         double* w = st + 2 + woff;
                         const int cells_b = g.cells[x.b];
                         const int nlo = (max(clo, s0) - s0) * P;
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 tma_load_1d(st + C::WIN, row_of(x), C::NF * 8, &full[stg]);
                 if (chi > clo) {
                     double* dst = st + 2 + woff + (g0 - eg);
-                    tma_load_1d(dst, a.src[x.sp] + g0, (unsigned)(g1 - g0) * 8, &full[stg]);
+                    tma_load_1d(dst, srcp(x.sp) + g0, (unsigned)(g1 - g0) * 8, &full[stg]);
                 }
             }
         }
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         if (P % 2 != 0 && (clo > s0 || chi < s0 + nt + 1)) {
             // (odd P) walls (zero inflow), 3-block ghosts, periodic wrap: only
             // the window cells outside [clo, chi) -- usually |i*|+1 of them
-            const double* src = a.src[sp] + lbase;
+            const double* src = srcp(sp) + lbase;
             double* w = const_cast<double*>(win);
             const int nlo = (max(clo, s0) - s0) * P;                 // [0, nlo)
             const int nhi0 = (min(max(chi, s0), s0 + nt + 1) - s0) * P;  // [nhi0, (nt+1)P)
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         // the window stage is consumed: hand it back before the stores
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stg]);
-        double* dline = a.dst[sp] + lbase + (long long)(g.start[b] + c0) * P;
+        double* dline = dstp(sp) + lbase + (long long)(g.start[b] + c0) * P;
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
             const int c = tid + cc * C::NT;
@@ -776,7 +779,8 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
         const double* t = a.tab[sp];
         const int nx = a.nxd;
         const int istar = (int)t[xd];
-        const double* f = a.src[sp] + xd;
+        const bool fl = field_flipped(a.flip[sp]);
+        const double* f = (fl ? a.dst[sp] : a.src[sp]) + xd;
         const long long ld = a.ld;
         const long long cstride = (long long)P * ld;  // one v cell
         const int lo = -a.gl, hi = a.n + a.gr;
@@ -825,7 +829,7 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
         cp_commit();
         ++s_iss;
         g_iss = PERIODIC ? src_of(s_iss) : g_iss + cstride;
-        double* op = a.dst[sp] + xd + (long long)j0 * cstride;
+        double* op = (fl ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + xd + (long long)j0 * cstride;
         for (int jb = 0; jb < kVChunk; jb += R) {
 #pragma unroll
             for (int u = 0; u < R; ++u) {
@@ -917,7 +921,8 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
     const int istar = (int)row[0];
     const double alpha = row[1];
     const long long lbase = (long long)line * g.ncells * P;
-    const double* src = a.src[sp] + lbase;
+    const bool flipped = field_flipped(a.flip[sp]);
+    const double* src = (flipped ? a.dst[sp] : a.src[sp]) + lbase;
     double uu[2][P];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -932,7 +937,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
             for (int q = 0; q < P; ++q) uu[h][q] = x_fetch_outside_ool<P>(a.basis, g, src, b, s, q);
         }
     }
-    double* up = a.dst[sp] + lbase + (long long)cell * P;
+    double* up = (flipped ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + lbase + (long long)cell * P;
     double o[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) o[q] = up[q];
@@ -997,9 +1002,11 @@ __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, in
     const int istar = (int)t[xd];
     const double alpha = t[nx + xd];
     double ul[P], ur[P], o[P];
-    vload<P>(a.src[sp], a.ld, xd, j + istar, -a.gl, a.n + a.gr, a.periodic, a.n, ul);
-    vload<P>(a.src[sp], a.ld, xd, j + istar + 1, -a.gl, a.n + a.gr, a.periodic, a.n, ur);
-    double* op = a.dst[sp] + (long long)j * P * a.ld + xd;
+    const bool flipped = field_flipped(a.flip[sp]);
+    const double* src = flipped ? a.dst[sp] : a.src[sp];
+    vload<P>(src, a.ld, xd, j + istar, -a.gl, a.n + a.gr, a.periodic, a.n, ul);
+    vload<P>(src, a.ld, xd, j + istar + 1, -a.gl, a.n + a.gr, a.periodic, a.n, ur);
+    double* op = (flipped ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + (long long)j * P * a.ld + xd;
 #pragma unroll
     for (int m = 0; m < P; ++m) o[m] = op[m * a.ld];
     if (rescan) {
@@ -1056,7 +1063,7 @@ __global__ void rho_partial_kernel(const __grid_constant__ RhoArgs a) {
     const int chunk = blockIdx.y;
     const double dv = a.vg[sp]->dx;
     const int r0 = chunk * a.rows_per_chunk, r1 = min(r0 + a.rows_per_chunk, a.nrows);
-    const double* f = a.f[sp] + xd;
+    const double* f = (field_flipped(a.flip[sp]) ? a.alt[sp] : a.f[sp]) + xd;
     double acc = 0.0;
     for (int r = r0; r < r1; ++r) {
         const int vn = r - (r / P) * P;
@@ -1220,7 +1227,7 @@ __global__ void rho_exact_kernel(const __grid_constant__ RhoArgs a) {
         const int sp = s == 0 ? 1 : 0;
         const double sign = s == 0 ? 1.0 : -1.0;
         const double dv = a.vg[sp]->dx;
-        const double* f = a.f[sp] + xd;
+        const double* f = (field_flipped(a.flip[sp]) ? a.alt[sp] : a.f[sp]) + xd;
         for (int r = 0; r < a.nrows; ++r) {
             const int vn = r - (r / P) * P;
             const double w = sign * a.basis.weights[vn] * dv;
@@ -1301,7 +1308,7 @@ __global__ void shrink_check_kernel(const __grid_constant__ ShrinkArgs a) {
     const double dv = vg.dx;
     const double right = vg.left + vg.cells * vg.dx;
     const double probe = right * (1.0 - a.p - a.gamma);
-    const double* f = a.f[sp];
+    const double* f = field_flipped(a.flip[sp]) ? a.out[sp] : a.f[sp];
     bool fail = false;
     for (int s = 0; s < 2; ++s) {
         double vp = (s == 0 ? 1.0 : -1.0) * probe;
@@ -1383,8 +1390,9 @@ __global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
     if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
     const int nxb = (a.nxd + blockDim.x - 1) / blockDim.x;
     const long long nitems = (long long)nxb * ((a.nv + kVChunk - 1) / kVChunk);
-    const double* f = a.f[sp];
-    double* out = a.out[sp];
+    const bool fl = field_flipped(a.flip[sp]);
+    const double* f = fl ? a.out[sp] : a.f[sp];
+    double* out = fl ? a.f[sp] : a.out[sp];
     for (long long w = blockIdx.x; w < nitems; w += gridDim.x) {
         const int xd = (int)(w % nxb) * blockDim.x + threadIdx.x;
         if (xd >= a.nxd) continue;
@@ -1415,20 +1423,8 @@ __global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
     }
 }
 
-// copy the projection back and commit the new v grid (field.cpp:96-101)
-__global__ void shrink_commit_kernel(const __grid_constant__ ShrinkArgs a, long long total) {
-    const int sp = blockIdx.y;
-    if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    const double2* s2 = reinterpret_cast<const double2*>(a.out[sp]);
-    double2* d2 = reinterpret_cast<double2*>(a.f[sp]);
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total / 2; i += stride)
-        d2[i] = s2[i];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (total & 1) a.f[sp][total - 1] = a.out[sp][total - 1];
-    }
-}
-
+// commit the new v grid (field.cpp:96-101); the projection already sits in
+// the field's other buffer, so the buffers exchange roles instead of copying
 __global__ void shrink_finalize_kernel(const __grid_constant__ ShrinkArgs a) {
     const int sp = threadIdx.x;
     if (sp >= 2 || !((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
@@ -1440,6 +1436,7 @@ __global__ void shrink_finalize_kernel(const __grid_constant__ ShrinkArgs a) {
     a.st->vmax_before[sp] = vmax_before;
     a.st->last_shrink[sp] = a.st->step;
     a.st->shrink_count[sp] += 1;
+    *a.flip_w[sp] ^= 1;
 }
 
 __global__ void shrink_force_kernel(DevStatus* st, int mask) {
@@ -1455,6 +1452,7 @@ constexpr int kDiagThreads = 256;
 template <int P>
 __global__ void __launch_bounds__(kDiagThreads) diag_partial_kernel(const __grid_constant__ DiagArgs a) {
     const DevVGrid vg = a.vg[0];
+    const double* fb = field_flipped(a.flip) ? a.alt : a.f;
     const long long total = (long long)a.nrows * a.nxd;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1468,7 +1466,7 @@ __global__ void __launch_bounds__(kDiagThreads) diag_partial_kernel(const __grid
         const double wv = a.basis.weights[vn] * vg.dx;
         const double w = wv * a.basis.weights[xn] * a.grid.dx[b];
         const double v = (vg.left + (vc + vg.cell0) * vg.dx) + vg.dx * a.basis.nodes[vn];
-        const double f = a.f[(long long)r * a.ld + xd];
+        const double f = fb[(long long)r * a.ld + xd];
         s[0] += w * f;
         s[1] += w * f * f;
         s[2] += w * (v * f);
@@ -1546,7 +1544,8 @@ __global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant
     const int c0 = (tile - a.tile_start[b]) * T;
     const int nt = min(T, cells_b - c0);
     const long long lb = (long long)line * g.ncells * P;
-    const double* src = a.src[sp] + lb;
+    const bool fl = field_flipped(a.flip[sp]);
+    const double* src = (fl ? a.dst[sp] : a.src[sp]) + lb;
     const long long gbase = (long long)g.start[b] * P;
     for (int e = threadIdx.x; e < (nt + 2) * P; e += T) {
         const int wc = e / P, n = e - (e / P) * P;
@@ -1580,7 +1579,7 @@ __global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant
 #pragma unroll
             for (int n = 0; n < P; ++n) o[n] = u0[n];
         }
-        double* dst = a.dst[sp] + lb + gbase + (long long)(c0 + c) * P;
+        double* dst = (fl ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + lb + gbase + (long long)(c0 + c) * P;
 #pragma unroll
         for (int n = 0; n < P; ++n) dst[n] = o[n];
     }
@@ -1596,8 +1595,9 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
     const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
     unsigned flagged = 0;
     if (xd < a.nxd) {
-        const double* f = a.src[sp];
-        double* out = a.dst[sp];
+        const bool fl = field_flipped(a.flip[sp]);
+        const double* f = fl ? a.dst[sp] : a.src[sp];
+        double* out = fl ? const_cast<double*>(a.src[sp]) : a.dst[sp];
         double um[P], u0[P], up[P];
         vload<P>(f, a.ld, xd, j0 - 1, 0, a.nv, a.periodic, a.nv, um);
         vload<P>(f, a.ld, xd, j0, 0, a.nv, a.periodic, a.nv, u0);
@@ -1905,8 +1905,6 @@ cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s) {
     if (a.force < 0) return cudaGetLastError();
     SK_DISPATCH_P(P, (shrink_table_kernel<PP><<<dim3((a.nv + 127) / 128, 2), 128, 0, s>>>(a)));
     SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3(sm_count() * 16, 1, 2), 128, 0, s>>>(a)));
-    const long long total = (long long)a.nv * P * a.nxd;
-    shrink_commit_kernel<<<dim3(1184, 2), 256, 0, s>>>(a, total);
     shrink_finalize_kernel<<<1, 32, 0, s>>>(a);
     return cudaGetLastError();
 }

@@ -32,12 +32,18 @@ struct XTabArgs {
     long long step_index;  // <0: use st->step
 };
 
+// A field's two buffers exchange roles after a velocity cut-off event (the
+// projection lands in the other buffer; finalize toggles the field's flag
+// instead of copying it back). Every kernel resolves its buffers through it.
+__device__ __forceinline__ bool field_flipped(const int* flip) { return flip != nullptr && *flip != 0; }
+
 struct XSweepArgs {
     Basis basis;
     Grid grid;
     DevStatus* st;
     const double* src[2];
     double* dst[2];
+    const int* flip[2];   // per-field buffer flip (shrink events): swap src and dst
     const double* tab[2];
     int nlines;
     int nspecies;
@@ -85,6 +91,7 @@ struct VSweepArgs {
     DevStatus* st;
     const double* src[2];  // points at local cell 0 (halo rows before/after)
     double* dst[2];
+    const int* flip[2];
     const double* tab[2];
     long long ld;          // row stride (nx * P)
     int nxd;
@@ -108,6 +115,8 @@ struct RhoArgs {
     Basis basis;
     const DevVGrid* vg[2];
     const double* f[2];
+    const double* alt[2];  // the fields' other buffers (used when flipped)
+    const int* flip[2];
     double* partial;       // [2][nchunks][nxd]
     double* rho;
     long long ld;
@@ -134,6 +143,8 @@ struct ShrinkArgs {
     DevVGrid* vg[2];
     double* f[2];
     double* out[2];
+    const int* flip[2];    // f/out exchange roles when set; finalize toggles it
+    int* flip_w[2];
     double* ttab[2];       // [nv][4 pieces][P*P]
     int* tcell[2];         // [nv][4]
     long long ld;
@@ -151,6 +162,8 @@ struct DiagArgs {
     Grid grid;
     const DevVGrid* vg;
     const double* f;
+    const double* alt;
+    const int* flip;
     double* partial;       // [nblk][4]
     long long ld;
     int nxd;
@@ -163,6 +176,7 @@ struct PostArgs {
     DevStatus* st;
     const double* src[2];
     double* dst[2];
+    const int* flip[2];
     PostCfg cfg;
     long long ld;
     int nxd;
