@@ -20,9 +20,12 @@
 //   post_*          K3: minmod / mean-error indicators + simple / line WENO
 // All arithmetic is fp64 with -fmad=false so per-cell results are bitwise the
 // reference's.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "sk_kernels.cuh"
+
+#include <cstdlib>
 
 namespace sk {
 
@@ -1213,6 +1216,336 @@ __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ P
 }
 
 // ---------------------------------------------------------------------------
+// Poisson on a thread-block cluster: the same block-cyclic-reduction replay,
+// rows distributed over the cluster's CTAs (level vectors in shared memory,
+// neighbour rows through distributed shared memory, one cluster barrier per
+// level). CTA c owns the level-0 rows [c*B, (c+1)*B) with B a multiple of 2^K,
+// hence the level-l rows [cB/2^l, (c+1)B/2^l) for l <= K; the <= 2C rows left
+// at level K are finished by CTA 0 alone. Every row is computed with the
+// single-CTA kernel's expressions, so the result is bitwise the same.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+
+struct PClusterMap {
+    int N, C, B, K;
+    int splan;  // 1: this CTA's plan rows are prefetched into shared memory
+    __device__ __forceinline__ int lo(int c, int l) const {
+        const long long L = min((long long)c * B, (long long)N);
+        return (int)((L + (1LL << l) - 1) >> l);
+    }
+    __device__ __forceinline__ int nr(int c, int l) const { return lo(c + 1, l) - lo(c, l); }
+    __device__ __forceinline__ int owner(int r, int l) const { return min((int)(((long long)r << l) / B), C - 1); }
+    // offsets (doubles) of level l's b and x vectors in CTA c's shared memory
+    __device__ __forceinline__ int boff(int c, int l, int ps) const {
+        int o = 0;
+        for (int i = 0; i < l; ++i) o += nr(c, i);
+        return o * ps;
+    }
+    __device__ __forceinline__ int xoff(int c, int l, int ps) const { return boff(c, K + 1, ps) + boff(c, l, ps); }
+};
+
+// a plan matrix of one level seen as M(e, r) = base[e * stride + r - roff]
+struct PMat {
+    const double* base;
+    int stride, roff;
+    __device__ __forceinline__ double operator()(int e, int r) const { return base[(long long)e * stride + (r - roff)]; }
+};
+
+template <int PS>
+__global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_constant__ PoissonDev pd,
+                                                               const __grid_constant__ PClusterMap cm,
+                                                               const double* __restrict__ rho,
+                                                               double* __restrict__ E,
+                                                               double* __restrict__ phi) {
+    constexpr int pp = PS * PS;
+    extern __shared__ double psm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int c = (int)cl.block_rank();
+    const int k = PS - 2;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int K = cm.K;
+    // remote / local element (row r of level l, component m) of b or x
+    auto vec = [&](bool xv, int l, int r, int m) -> double* {
+        const int o = cm.owner(r, l);
+        double* base = cl.map_shared_rank(psm, o);
+        const int off = xv ? cm.xoff(o, l, PS) : cm.boff(o, l, PS);
+        return base + off + m * cm.nr(o, l) + (r - cm.lo(o, l));
+    };
+    // ---- load vector (poisson.cpp:135-149), own level-0 rows
+    {
+        const int l0 = cm.lo(c, 0), n0 = cm.nr(c, 0);
+        double* b0 = psm + cm.boff(c, 0, PS);
+        for (int i = tid; i < n0 * PS; i += nth) {
+            const int m = i / n0, q = i - (i / n0) * n0, cc = l0 + q;
+            double val = 0.0;
+#pragma unroll
+            for (int n = 0; n <= k; ++n) val += pd.interp[m * (k + 1) + n] * rho[cc * (k + 1) + n];
+            b0[i] = pd.ws[m] * pd.h[cc] * val;
+        }
+    }
+    // ---- plan rows of this CTA (levels 0..K-1) into shared memory: the sweeps
+    // evict the plan from L2 between solves, and a level that waits for its
+    // matrices holds up the whole cluster. Layout after the vectors: per level
+    // Alpha, Gamma [pp][nn] then Lo, Up, Dinv [pp][nodd].
+    double* plan_sm = psm + cm.xoff(c, K + 1, PS) + (c == 0 ? 2 * PS * 64 : 0);
+    auto plan_off = [&](int l) {  // doubles before level l's block
+        int o = 0;
+        for (int i = 0; i < l; ++i) o += pp * (2 * cm.nr(c, i + 1) + 3 * (cm.nr(c, i) / 2));
+        return o;
+    };
+    if (cm.splan) {
+        for (int l = 0; l < K; ++l) {
+            const int Nn = pd.level_n[l + 1], No = pd.level_n[l] / 2;
+            const int ln = cm.lo(c, l + 1), nn = cm.nr(c, l + 1), nodd = cm.nr(c, l) / 2;
+            double* dst = plan_sm + plan_off(l);
+            const double* srcs[5] = {pd.AlphaT + pd.keep_off[l] * pp, pd.GammaT + pd.keep_off[l] * pp,
+                                     pd.LoT + pd.odd_off[l] * pp, pd.UpT + pd.odd_off[l] * pp,
+                                     pd.DinvT + pd.odd_off[l] * pp};
+            for (int mtx = 0; mtx < 5; ++mtx) {
+                const int rows = mtx < 2 ? nn : nodd, stride = mtx < 2 ? Nn : No;
+                double* d = dst + (mtx < 2 ? mtx * pp * nn : 2 * pp * nn + (mtx - 2) * pp * nodd);
+                for (int i = tid; i < pp * rows; i += nth) {
+                    const int e = i / rows, r = i - (i / rows) * rows;
+                    d[i] = __ldg(srcs[mtx] + (long long)e * stride + ln + r);
+                }
+            }
+        }
+    }
+    auto mats = [&](int l, PMat& A, PMat& G, PMat& Lo, PMat& Up, PMat& Di) {
+        const int Nn = pd.level_n[l + 1], No = pd.level_n[l] / 2;
+        if (cm.splan) {
+            const int ln = cm.lo(c, l + 1), nn = cm.nr(c, l + 1), nodd = cm.nr(c, l) / 2;
+            const double* d = plan_sm + plan_off(l);
+            A = PMat{d, nn, ln};
+            G = PMat{d + pp * nn, nn, ln};
+            Lo = PMat{d + 2 * pp * nn, nodd, ln};
+            Up = PMat{d + 2 * pp * nn + pp * nodd, nodd, ln};
+            Di = PMat{d + 2 * pp * nn + 2 * pp * nodd, nodd, ln};
+        } else {
+            A = PMat{pd.AlphaT + pd.keep_off[l] * pp, Nn, 0};
+            G = PMat{pd.GammaT + pd.keep_off[l] * pp, Nn, 0};
+            Lo = PMat{pd.LoT + pd.odd_off[l] * pp, No, 0};
+            Up = PMat{pd.UpT + pd.odd_off[l] * pp, No, 0};
+            Di = PMat{pd.DinvT + pd.odd_off[l] * pp, No, 0};
+        }
+    };
+    cl.sync();
+    // ---- distributed reduction, levels 0 .. K-1
+    for (int l = 0; l < K; ++l) {
+        const int Nl = pd.level_n[l];
+        PMat Al, Gl, Lo_, Up_, Di_;
+        mats(l, Al, Gl, Lo_, Up_, Di_);
+        const int ln = cm.lo(c, l + 1), nn = cm.nr(c, l + 1);
+        const int lo_l = cm.lo(c, l), nr_l = cm.nr(c, l);
+        const double* bl = psm + cm.boff(c, l, PS);
+        double* bn = psm + cm.boff(c, l + 1, PS);
+        for (int i = tid; i < nn * PS; i += nth) {
+            const int m = i / nn, rr = i - (i / nn) * nn, r = ln + rr, q = 2 * r;
+            double v = bl[m * nr_l + (q - lo_l)];
+            if (q - 1 >= 0) {
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < PS; ++n) {
+                    const double bq = (q - 1 >= lo_l) ? bl[n * nr_l + (q - 1 - lo_l)] : *vec(false, l, q - 1, n);
+                    acc += Al(m * PS + n, r) * bq;
+                }
+                v += acc;
+            }
+            if (q + 1 < Nl) {
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < PS; ++n) {
+                    const double bq = (q + 1 < lo_l + nr_l) ? bl[n * nr_l + (q + 1 - lo_l)] : *vec(false, l, q + 1, n);
+                    acc += Gl(m * PS + n, r) * bq;
+                }
+                v += acc;
+            }
+            bn[m * nn + rr] = v;
+        }
+        cl.sync();
+    }
+    // ---- CTA 0: gather level K, finish the reduction and the top levels
+    double* top = psm + cm.xoff(c, K + 1, PS);  // CTA 0 only: [b levels K.. | x levels K..]
+    const int L = pd.nlevels;
+    if (c == 0) {
+        // top layout: b_l at tb[l] (l >= K), x_l at tx[l], SoA [m][N_l]
+        int tb[32], tx[32];
+        int o = 0;
+        for (int l = K; l < L; ++l) {
+            tb[l] = o;
+            o += pd.level_n[l] * PS;
+        }
+        for (int l = K; l < L; ++l) {
+            tx[l] = o;
+            o += pd.level_n[l] * PS;
+        }
+        const int NK = pd.level_n[K];
+        for (int i = tid; i < NK * PS; i += nth) {
+            const int m = i / NK, r = i - (i / NK) * NK;
+            top[tb[K] + i] = *vec(false, K, r, m);
+        }
+        __syncthreads();
+        for (int l = K; l + 1 < L; ++l) {
+            const int Nl = pd.level_n[l], Nn = pd.level_n[l + 1];
+            const double* bl = top + tb[l];
+            double* bn = top + tb[l + 1];
+            const double* Al = pd.AlphaT + pd.keep_off[l] * pp;
+            const double* Gl = pd.GammaT + pd.keep_off[l] * pp;
+            for (int i = tid; i < Nn * PS; i += nth) {
+                const int m = i / Nn, r = i - (i / Nn) * Nn, q = 2 * r;
+                double v = bl[m * Nl + q];
+                if (q - 1 >= 0) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int n = 0; n < PS; ++n) acc += Al[(long long)(m * PS + n) * Nn + r] * bl[n * Nl + q - 1];
+                    v += acc;
+                }
+                if (q + 1 < Nl) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int n = 0; n < PS; ++n) acc += Gl[(long long)(m * PS + n) * Nn + r] * bl[n * Nl + q + 1];
+                    v += acc;
+                }
+                bn[m * Nn + r] = v;
+            }
+            __syncthreads();
+        }
+        if (tid < PS) {
+            const double* bt = top + tb[L - 1];
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < PS; ++n) acc += pd.DinvTop[tid * PS + n] * bt[n];
+            top[tx[L - 1] + tid] = acc;
+        }
+        __syncthreads();
+        for (int l = L - 2; l >= K; --l) {
+            const int Nl = pd.level_n[l], Nn = pd.level_n[l + 1], No = Nl / 2;
+            double* bl = top + tb[l];
+            double* xl = top + tx[l];
+            const double* xn = top + tx[l + 1];
+            const double* Lo = pd.LoT + pd.odd_off[l] * pp;
+            const double* Up = pd.UpT + pd.odd_off[l] * pp;
+            const double* Di = pd.DinvT + pd.odd_off[l] * pp;
+            for (int i = tid; i < Nl * PS; i += nth) {
+                const int m = i / Nl, q = i - (i / Nl) * Nl;
+                if ((q & 1) == 0) {
+                    xl[m * Nl + q] = xn[m * Nn + q / 2];
+                } else {
+                    const int oo = q >> 1;
+                    double t = bl[m * Nl + q];
+                    double acc = 0.0;
+#pragma unroll
+                    for (int n = 0; n < PS; ++n) acc += Lo[(long long)(m * PS + n) * No + oo] * xn[n * Nn + oo];
+                    t -= acc;
+                    if (q + 1 < Nl) {
+                        acc = 0.0;
+#pragma unroll
+                        for (int n = 0; n < PS; ++n) acc += Up[(long long)(m * PS + n) * No + oo] * xn[n * Nn + oo + 1];
+                        t -= acc;
+                    }
+                    bl[m * Nl + q] = t;
+                }
+            }
+            __syncthreads();
+            for (int i = tid; i < No * PS; i += nth) {
+                const int m = i / No, oo = i - (i / No) * No, q = 2 * oo + 1;
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < PS; ++n) acc += Di[(long long)(m * PS + n) * No + oo] * bl[n * Nl + q];
+                xl[m * Nl + q] = acc;
+            }
+            __syncthreads();
+        }
+        // x_K into CTA 0's own distributed x slot for level K
+        {
+            const int nK = cm.nr(0, K);
+            double* xK = psm + cm.xoff(0, K, PS);
+            for (int i = tid; i < nK * PS; i += nth) {
+                const int m = i / nK, r = i - (i / nK) * nK;
+                xK[i] = top[tx[K] + m * NK + r];
+            }
+        }
+    }
+    cl.sync();
+    // every other CTA pulls its level-K x rows from CTA 0's top area
+    if (c != 0) {
+        const int NK = pd.level_n[K], lK = cm.lo(c, K), nK = cm.nr(c, K);
+        int o = 0;
+        for (int l = K; l < L; ++l) o += pd.level_n[l] * PS;  // x levels follow the b levels
+        const double* top0 = cl.map_shared_rank(psm, 0) + cm.xoff(0, K + 1, PS) + o;
+        double* xK = psm + cm.xoff(c, K, PS);
+        for (int i = tid; i < nK * PS; i += nth) {
+            const int m = i / nK, r = i - (i / nK) * nK;
+            xK[i] = top0[m * NK + lK + r];
+        }
+    }
+    cl.sync();
+    // ---- distributed back substitution, levels K-1 .. 0
+    for (int l = K - 1; l >= 0; --l) {
+        const int Nl = pd.level_n[l], No = Nl / 2;
+        const int lo_l = cm.lo(c, l), nr_l = cm.nr(c, l);
+        const int lo_n = cm.lo(c, l + 1), nr_n = cm.nr(c, l + 1);
+        double* bl = psm + cm.boff(c, l, PS);
+        double* xl = psm + cm.xoff(c, l, PS);
+        const double* xn = psm + cm.xoff(c, l + 1, PS);
+        PMat A_, G_, Lo, Up, Di;
+        mats(l, A_, G_, Lo, Up, Di);
+        for (int i = tid; i < nr_l * PS; i += nth) {
+            const int m = i / nr_l, qq = i - (i / nr_l) * nr_l, q = lo_l + qq;
+            if ((q & 1) == 0) {
+                xl[m * nr_l + qq] = xn[m * nr_n + (q / 2 - lo_n)];
+            } else {
+                const int oo = q >> 1;
+                double t = bl[m * nr_l + qq];
+                double acc = 0.0;
+#pragma unroll
+                for (int n = 0; n < PS; ++n) acc += Lo(m * PS + n, oo) * xn[n * nr_n + (oo - lo_n)];
+                t -= acc;
+                if (q + 1 < Nl) {
+                    acc = 0.0;
+#pragma unroll
+                    for (int n = 0; n < PS; ++n) {
+                        const double xv = (oo + 1 < lo_n + nr_n) ? xn[n * nr_n + (oo + 1 - lo_n)] : *vec(true, l + 1, oo + 1, n);
+                        acc += Up(m * PS + n, oo) * xv;
+                    }
+                    t -= acc;
+                }
+                bl[m * nr_l + qq] = t;
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < nr_l * PS; i += nth) {
+            const int m = i / nr_l, qq = i - (i / nr_l) * nr_l, q = lo_l + qq;
+            if ((q & 1) == 0) continue;
+            const int oo = q >> 1;
+            double acc = 0.0;
+#pragma unroll
+            for (int n = 0; n < PS; ++n) acc += Di(m * PS + n, oo) * bl[n * nr_l + qq];
+            xl[m * nr_l + qq] = acc;
+        }
+        cl.sync();
+    }
+    // ---- phi and E = -phi' (poisson.cpp:176-192), own cells
+    {
+        const int l0 = cm.lo(c, 0), n0 = cm.nr(c, 0);
+        const double* x0 = psm + cm.xoff(c, 0, PS);
+        if (phi)
+            for (int i = tid; i < n0 * PS; i += nth) {
+                const int q = i / PS, m = i - (i / PS) * PS;
+                phi[(long long)(l0 + q) * PS + m] = x0[m * n0 + q];
+            }
+        for (int i = tid; i < n0 * (k + 1); i += nth) {
+            const int q = i / (k + 1), m = i - (i / (k + 1)) * (k + 1), cc = l0 + q;
+            double dphi = 0.0;
+#pragma unroll
+            for (int n = 0; n < PS; ++n) dphi += pd.deriv[m * PS + n] * x0[n * n0 + q];
+            E[(long long)cc * (k + 1) + m] = -dphi / pd.h[cc];
+        }
+    }
+    cl.sync();  // no CTA may exit while others still read its shared memory
+}
+
+// ---------------------------------------------------------------------------
 // exact-reduction mode: the reference's serial orders, so that a whole
 // trajectory is bitwise the reference's (parity mode, not the fast path)
 // ---------------------------------------------------------------------------
@@ -1873,10 +2206,102 @@ cudaError_t launch_rho(const RhoArgs& a, int nspecies, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// cluster shape for the Poisson solve: largest cluster (16 non-portable, else
+// 8) the device can co-schedule with the needed shared memory; 0 = single CTA
+template <int PS>
+static int poisson_cluster_plan(const PoissonDev& pd, PClusterMap& cm, size_t& smem) {
+    const int N = pd.ncells;
+    // measured on B200: the cluster replay wins at nx = 16384 (0.31 vs 0.70 ms)
+    // but loses at nx = 2048 (0.15 vs 0.12 ms), where its per-level cluster
+    // barriers and CTA 0's serial top levels outweigh the spread-out work
+    if (N < 4096) return 0;
+    for (int C : {16, 8}) {
+        if (N < 4 * C) continue;
+        int K = 0;
+        const int per = (N + C - 1) / C;
+        while ((2 << K) <= per) ++K;  // 2^K <= ceil(N/C)
+        if (K >= pd.nlevels - 1) K = pd.nlevels - 2;
+        if (K < 1) continue;
+        const int B = ((per + (1 << K) - 1) >> K) << K;
+        // per-CTA rows over levels 0..K (b and x) + CTA 0's top area
+        long long rows = 0;
+        for (int l = 0; l <= K; ++l) rows += ((long long)B + (1LL << l) - 1) >> l;
+        long long top = 0;
+        for (int l = K; l < pd.nlevels; ++l) top += pd.level_n[l];
+        if (top > 64) continue;  // CTA 0's top area (see poisson_cluster_kernel)
+        const size_t vec_bytes = sizeof(double) * (size_t)PS * (size_t)(2 * rows + 2 * 64);
+        if (vec_bytes > 200 * 1024) continue;
+        // plan rows per CTA (Alpha, Gamma for reduced rows, Lo, Up, Dinv for odd rows)
+        long long plan = 0;
+        for (int l = 0; l < K; ++l) {
+            const long long nl = ((long long)B + (1LL << l) - 1) >> l;
+            plan += (long long)PS * PS * (2 * ((nl + 1) / 2) + 3 * (nl / 2));
+        }
+        const size_t plan_bytes = sizeof(double) * (size_t)plan;
+        const int splan = vec_bytes + plan_bytes <= 210 * 1024;
+        const size_t need = vec_bytes + (splan ? plan_bytes : 0);
+        auto kern = poisson_cluster_kernel<PS>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need) != cudaSuccess ||
+            (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+            cudaGetLastError();
+            continue;
+        }
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = C;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.gridDim = dim3(C);
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = need;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        cm = PClusterMap{N, C, B, K, splan};
+        smem = need;
+        return C;
+    }
+    return 0;
+}
+
+template <int PS>
+static cudaError_t launch_poisson_t(const PoissonDev& pd, const double* rho, double* E, double* phi,
+                                    cudaStream_t s) {
+    static int cached_n = -1, cached_c = 0;
+    static PClusterMap cached_cm{};
+    static size_t cached_smem = 0;
+    if (cached_n != pd.ncells || getenv("SK_POISSON_SINGLE")) {
+        cached_c = getenv("SK_POISSON_SINGLE") ? 0 : poisson_cluster_plan<PS>(pd, cached_cm, cached_smem);
+        cached_n = pd.ncells;
+    }
+    if (cached_c == 0) {
+        poisson_kernel<PS><<<1, 1024, 0, s>>>(pd, rho, E, phi);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cached_c;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cached_c);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = cached_smem;
+    cfg.stream = s;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, poisson_cluster_kernel<PS>, pd, cached_cm, rho, E, phi);
+}
+
 cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
                            cudaStream_t s) {
-    SK_DISPATCH_P(pd.ps - 1, (poisson_kernel<PP + 1><<<1, 1024, 0, s>>>(pd, rho, E, phi)));
-    return cudaGetLastError();
+    SK_DISPATCH_P(pd.ps - 1, return (launch_poisson_t<PP + 1>(pd, rho, E, phi, s)));
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s) {

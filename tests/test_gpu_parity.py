@@ -490,3 +490,25 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk):
         assert rel(got, ref.field(sp).download()) <= 1e-12, f"species {sp}"
     for ctx, h, *_ in shards:
         L.sk_state_destroy(h)
+
+
+@pytest.mark.parametrize("k,nf,nc,m", [(3, 1024, 2048, 1), (2, 1031, 2099, 3), (3, 4096, 8192, 1),
+                                       (2, 2048, 512, 8), (1, 2048, 4096, 1)])
+def test_poisson_cluster_equals_single_cta(sk, k, nf, nc, m):
+    """the cluster Poisson solve (rows over 8-16 CTAs, DSMEM neighbours) replays
+    the single-CTA block-cyclic reduction row for row: bitwise equal E, phi"""
+    grid = sk.Grid1D.three_block(-200.0, 200.0, nf, nc, m)
+    ctx = sk.Context(grid, k)
+    rng = np.random.default_rng(nf * 7 + nc)
+    rho = rng.standard_normal(ctx.nx * ctx.p) * 0.3
+    op = sk.PoissonOperator(ctx)
+    a = op.solve(rho)
+    Ea, pa = a.E.cpu().numpy().copy(), a.phi.cpu().numpy().copy()
+    os.environ["SK_POISSON_SINGLE"] = "1"
+    try:
+        b = op.solve(rho)
+    finally:
+        del os.environ["SK_POISSON_SINGLE"]
+    assert np.array_equal(Ea, b.E.cpu().numpy())
+    assert np.array_equal(pa, b.phi.cpu().numpy())
+    assert np.isfinite(Ea).all() and np.abs(Ea).max() > 0
