@@ -49,7 +49,11 @@ for vals in r:
     txt.append("  top stall reasons: " + ", ".join(f"{k[33:]}={100*v/s:.0f}%" for k, v in sorted(st.items(), key=lambda x: -x[1])[:6]))
     b = float(d["dram__bytes_read.sum"].replace(",", "")) + float(d["dram__bytes_write.sum"].replace(",", ""))
     unit = d.get("dram__bytes_read.sum", "")
-    key = "x_sweep" if "xsweep" in name else "v_sweep" if "vsweep" in name else name
+    # xsweep_kernel<P, INLINE, RHO, FMA>: the fused-moment variant is x sweep 1
+    targs = d["Kernel Name"].split("<", 1)[-1].split(">")[0].split(",")
+    rho = len(targs) > 2 and ("1" in targs[2] or "true" in targs[2])
+    key = (("x_sweep_1" if rho else "x_sweep_2") if "xsweep" in name
+           else "v_sweep" if "vsweep" in name else name)
     traffic.setdefault(key, b)
 open(os.path.join(P, f"{tag}_ncu_full.txt"), "w").write("\n".join(txt) + "\n")
 # units: ncu raw csv reports dram bytes in the unit row; convert GB -> bytes if needed
@@ -57,7 +61,7 @@ units_row = out[1]
 tr = {}
 for k, v in traffic.items():
     tr[k] = v * (1e9 if v < 1e4 else 1.0)
-json.dump({"C3": {"x_sweep_1": tr.get("x_sweep"), "x_sweep_2": tr.get("x_sweep"), "v_sweep": tr.get("v_sweep")}},
+json.dump({"C3": {"x_sweep_1": tr.get("x_sweep_1"), "x_sweep_2": tr.get("x_sweep_2"), "v_sweep": tr.get("v_sweep")}},
           open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 print(open(os.path.join(P, f"{tag}_ncu_full.txt")).read()[:3000])
 # 3) bench line
