@@ -1216,40 +1216,66 @@ __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ P
 }
 
 // ---------------------------------------------------------------------------
-// Poisson on a thread-block cluster: the same block-cyclic-reduction replay,
-// rows distributed over the cluster's CTAs (level vectors in shared memory,
-// neighbour rows through distributed shared memory, one cluster barrier per
-// level). CTA c owns the level-0 rows [c*B, (c+1)*B) with B a multiple of 2^K,
-// hence the level-l rows [cB/2^l, (c+1)B/2^l) for l <= K; the <= 2C rows left
-// at level K are finished by CTA 0 alone. Every row is computed with the
-// single-CTA kernel's expressions, so the result is bitwise the same.
+// Poisson on a thread-block cluster, communication-avoiding: the same block-
+// cyclic-reduction replay, every row computed with the single-CTA kernel's
+// expressions (bitwise the same result). CTA c owns the level-0 rows
+// [cB, (c+1)B) (B a multiple of 2^K). Instead of exchanging neighbour rows at
+// every level, each CTA recomputes the halo its own rows depend on: the
+// K reduction levels and the K back-substitution levels run CTA-locally with
+// __syncthreads; only the <= 2C rows of level K go through CTA 0 (two cluster
+// barriers around it). Level vectors live in shared memory.
 // ---------------------------------------------------------------------------
 namespace cg = cooperative_groups;
 
+constexpr int kPMaxLev = 32;
+
 struct PClusterMap {
     int N, C, B, K;
-    int splan;  // 1: this CTA's plan rows are prefetched into shared memory
-    __device__ __forceinline__ int lo(int c, int l) const {
-        const long long L = min((long long)c * B, (long long)N);
-        return (int)((L + (1LL << l) - 1) >> l);
-    }
-    __device__ __forceinline__ int nr(int c, int l) const { return lo(c + 1, l) - lo(c, l); }
-    __device__ __forceinline__ int owner(int r, int l) const { return min((int)(((long long)r << l) / B), C - 1); }
-    // offsets (doubles) of level l's b and x vectors in CTA c's shared memory
-    __device__ __forceinline__ int boff(int c, int l, int ps) const {
-        int o = 0;
-        for (int i = 0; i < l; ++i) o += nr(c, i);
-        return o * ps;
-    }
-    __device__ __forceinline__ int xoff(int c, int l, int ps) const { return boff(c, K + 1, ps) + boff(c, l, ps); }
 };
 
-// a plan matrix of one level seen as M(e, r) = base[e * stride + r - roff]
-struct PMat {
-    const double* base;
-    int stride, roff;
-    __device__ __forceinline__ double operator()(int e, int r) const { return base[(long long)e * stride + (r - roff)]; }
+// row ranges of CTA c: b_l on [ra, rb) (reduction + back-substitution needs),
+// x_l on [xa, xb) (back substitution), own level-l rows [lo, hi)
+struct PRanges {
+    int ra[kPMaxLev], rb[kPMaxLev], xa[kPMaxLev], xb[kPMaxLev];
 };
+__host__ __device__ inline int pc_lo(const PClusterMap& m, int c, int l) {
+    const long long L = (long long)c * m.B < m.N ? (long long)c * m.B : m.N;
+    return (int)((L + (1LL << l) - 1) >> l);
+}
+__host__ __device__ inline void pc_ranges(const PClusterMap& m, const int* level_n, int c, PRanges& R) {
+    const int K = m.K;
+    R.xa[0] = pc_lo(m, c, 0);
+    R.xb[0] = pc_lo(m, c + 1, 0);
+    for (int l = 0; l < K; ++l) {
+        R.xa[l + 1] = R.xa[l] >> 1;
+        const int e = (R.xb[l] >> 1) + 1;
+        R.xb[l + 1] = e < level_n[l + 1] ? e : level_n[l + 1];
+        if (R.xb[l] <= R.xa[l]) R.xb[l + 1] = R.xa[l + 1];  // nothing to solve
+    }
+    R.ra[K] = pc_lo(m, c, K);
+    R.rb[K] = pc_lo(m, c + 1, K);
+    for (int l = K - 1; l >= 0; --l) {
+        int a = 2 * R.ra[l + 1] - 1, b = 2 * R.rb[l + 1];
+        if (R.rb[l + 1] <= R.ra[l + 1]) {  // no reduction rows above: back-sub needs only
+            a = R.xa[l];
+            b = R.xb[l];
+        } else {
+            if (R.xb[l] > R.xa[l]) {
+                a = a < R.xa[l] ? a : R.xa[l];
+                b = b > R.xb[l] ? b : R.xb[l];
+            }
+        }
+        R.ra[l] = a > 0 ? a : 0;
+        R.rb[l] = b < level_n[l] ? b : level_n[l];
+        if (R.rb[l] < R.ra[l]) R.rb[l] = R.ra[l];
+    }
+}
+// doubles of shared memory: b levels 0..K, x levels 0..K, then (CTA 0) the top
+__host__ __device__ inline int pc_vec_doubles(const PClusterMap& m, const PRanges& R, int ps) {
+    int o = 0;
+    for (int l = 0; l <= m.K; ++l) o += (R.rb[l] - R.ra[l]) + (R.xb[l] - R.xa[l]);
+    return o * ps;
+}
 
 template <int PS>
 __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_constant__ PoissonDev pd,
@@ -1263,113 +1289,69 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
     const int c = (int)cl.block_rank();
     const int k = PS - 2;
     const int tid = threadIdx.x, nth = blockDim.x;
-    const int K = cm.K;
-    // remote / local element (row r of level l, component m) of b or x
-    auto vec = [&](bool xv, int l, int r, int m) -> double* {
-        const int o = cm.owner(r, l);
-        double* base = cl.map_shared_rank(psm, o);
-        const int off = xv ? cm.xoff(o, l, PS) : cm.boff(o, l, PS);
-        return base + off + m * cm.nr(o, l) + (r - cm.lo(o, l));
-    };
-    // ---- load vector (poisson.cpp:135-149), own level-0 rows
+    const int K = cm.K, L = pd.nlevels;
+    __shared__ PRanges R;
+    __shared__ int bo[kPMaxLev], xo[kPMaxLev];
+    if (tid == 0) {
+        pc_ranges(cm, pd.level_n, c, R);
+        int o = 0;
+        for (int l = 0; l <= K; ++l) {
+            bo[l] = o;
+            o += (R.rb[l] - R.ra[l]) * PS;
+        }
+        for (int l = 0; l <= K; ++l) {
+            xo[l] = o;
+            o += (R.xb[l] - R.xa[l]) * PS;
+        }
+    }
+    __syncthreads();
+    // ---- load vector (poisson.cpp:135-149) on [ra0, rb0): own rows + halo
     {
-        const int l0 = cm.lo(c, 0), n0 = cm.nr(c, 0);
-        double* b0 = psm + cm.boff(c, 0, PS);
+        const int a0 = R.ra[0], n0 = R.rb[0] - a0;
+        double* b0 = psm + bo[0];
         for (int i = tid; i < n0 * PS; i += nth) {
-            const int m = i / n0, q = i - (i / n0) * n0, cc = l0 + q;
+            const int m = i / n0, q = i - (i / n0) * n0, cc = a0 + q;
             double val = 0.0;
 #pragma unroll
             for (int n = 0; n <= k; ++n) val += pd.interp[m * (k + 1) + n] * rho[cc * (k + 1) + n];
             b0[i] = pd.ws[m] * pd.h[cc] * val;
         }
     }
-    // ---- plan rows of this CTA (levels 0..K-1) into shared memory: the sweeps
-    // evict the plan from L2 between solves, and a level that waits for its
-    // matrices holds up the whole cluster. Layout after the vectors: per level
-    // Alpha, Gamma [pp][nn] then Lo, Up, Dinv [pp][nodd].
-    double* plan_sm = psm + cm.xoff(c, K + 1, PS) + (c == 0 ? 2 * PS * 64 : 0);
-    auto plan_off = [&](int l) {  // doubles before level l's block
-        int o = 0;
-        for (int i = 0; i < l; ++i) o += pp * (2 * cm.nr(c, i + 1) + 3 * (cm.nr(c, i) / 2));
-        return o;
-    };
-    if (cm.splan) {
-        for (int l = 0; l < K; ++l) {
-            const int Nn = pd.level_n[l + 1], No = pd.level_n[l] / 2;
-            const int ln = cm.lo(c, l + 1), nn = cm.nr(c, l + 1), nodd = cm.nr(c, l) / 2;
-            double* dst = plan_sm + plan_off(l);
-            const double* srcs[5] = {pd.AlphaT + pd.keep_off[l] * pp, pd.GammaT + pd.keep_off[l] * pp,
-                                     pd.LoT + pd.odd_off[l] * pp, pd.UpT + pd.odd_off[l] * pp,
-                                     pd.DinvT + pd.odd_off[l] * pp};
-            for (int mtx = 0; mtx < 5; ++mtx) {
-                const int rows = mtx < 2 ? nn : nodd, stride = mtx < 2 ? Nn : No;
-                double* d = dst + (mtx < 2 ? mtx * pp * nn : 2 * pp * nn + (mtx - 2) * pp * nodd);
-                for (int i = tid; i < pp * rows; i += nth) {
-                    const int e = i / rows, r = i - (i / rows) * rows;
-                    d[i] = __ldg(srcs[mtx] + (long long)e * stride + ln + r);
-                }
-            }
-        }
-    }
-    auto mats = [&](int l, PMat& A, PMat& G, PMat& Lo, PMat& Up, PMat& Di) {
-        const int Nn = pd.level_n[l + 1], No = pd.level_n[l] / 2;
-        if (cm.splan) {
-            const int ln = cm.lo(c, l + 1), nn = cm.nr(c, l + 1), nodd = cm.nr(c, l) / 2;
-            const double* d = plan_sm + plan_off(l);
-            A = PMat{d, nn, ln};
-            G = PMat{d + pp * nn, nn, ln};
-            Lo = PMat{d + 2 * pp * nn, nodd, ln};
-            Up = PMat{d + 2 * pp * nn + pp * nodd, nodd, ln};
-            Di = PMat{d + 2 * pp * nn + 2 * pp * nodd, nodd, ln};
-        } else {
-            A = PMat{pd.AlphaT + pd.keep_off[l] * pp, Nn, 0};
-            G = PMat{pd.GammaT + pd.keep_off[l] * pp, Nn, 0};
-            Lo = PMat{pd.LoT + pd.odd_off[l] * pp, No, 0};
-            Up = PMat{pd.UpT + pd.odd_off[l] * pp, No, 0};
-            Di = PMat{pd.DinvT + pd.odd_off[l] * pp, No, 0};
-        }
-    };
-    cl.sync();
-    // ---- distributed reduction, levels 0 .. K-1
+    __syncthreads();
+    // ---- reduction, levels 0 .. K-1, CTA-local
     for (int l = 0; l < K; ++l) {
-        const int Nl = pd.level_n[l];
-        PMat Al, Gl, Lo_, Up_, Di_;
-        mats(l, Al, Gl, Lo_, Up_, Di_);
-        const int ln = cm.lo(c, l + 1), nn = cm.nr(c, l + 1);
-        const int lo_l = cm.lo(c, l), nr_l = cm.nr(c, l);
-        const double* bl = psm + cm.boff(c, l, PS);
-        double* bn = psm + cm.boff(c, l + 1, PS);
+        const int Nl = pd.level_n[l], Nn = pd.level_n[l + 1];
+        const double* Al = pd.AlphaT + pd.keep_off[l] * pp;
+        const double* Gl = pd.GammaT + pd.keep_off[l] * pp;
+        const int al = R.ra[l], nl = R.rb[l] - al;
+        const int an = R.ra[l + 1], nn = R.rb[l + 1] - an;
+        const double* bl = psm + bo[l];
+        double* bn = psm + bo[l + 1];
         for (int i = tid; i < nn * PS; i += nth) {
-            const int m = i / nn, rr = i - (i / nn) * nn, r = ln + rr, q = 2 * r;
-            double v = bl[m * nr_l + (q - lo_l)];
+            const int m = i / nn, rr = i - (i / nn) * nn, r = an + rr, q = 2 * r;
+            double v = bl[m * nl + (q - al)];
             if (q - 1 >= 0) {
                 double acc = 0.0;
 #pragma unroll
-                for (int n = 0; n < PS; ++n) {
-                    const double bq = (q - 1 >= lo_l) ? bl[n * nr_l + (q - 1 - lo_l)] : *vec(false, l, q - 1, n);
-                    acc += Al(m * PS + n, r) * bq;
-                }
+                for (int n = 0; n < PS; ++n) acc += Al[(long long)(m * PS + n) * Nn + r] * bl[n * nl + (q - 1 - al)];
                 v += acc;
             }
             if (q + 1 < Nl) {
                 double acc = 0.0;
 #pragma unroll
-                for (int n = 0; n < PS; ++n) {
-                    const double bq = (q + 1 < lo_l + nr_l) ? bl[n * nr_l + (q + 1 - lo_l)] : *vec(false, l, q + 1, n);
-                    acc += Gl(m * PS + n, r) * bq;
-                }
+                for (int n = 0; n < PS; ++n) acc += Gl[(long long)(m * PS + n) * Nn + r] * bl[n * nl + (q + 1 - al)];
                 v += acc;
             }
             bn[m * nn + rr] = v;
         }
-        cl.sync();
+        __syncthreads();
     }
-    // ---- CTA 0: gather level K, finish the reduction and the top levels
-    double* top = psm + cm.xoff(c, K + 1, PS);  // CTA 0 only: [b levels K.. | x levels K..]
-    const int L = pd.nlevels;
+    cl.sync();  // every CTA's own level-K rows are in place
+    double* top = psm + pc_vec_doubles(cm, R, PS);  // CTA 0: [b levels K.. | x levels K..]
+    int tofs = 0;                                   // doubles of the top b levels (x levels follow)
+    for (int l = K; l < L; ++l) tofs += pd.level_n[l] * PS;
     if (c == 0) {
-        // top layout: b_l at tb[l] (l >= K), x_l at tx[l], SoA [m][N_l]
-        int tb[32], tx[32];
+        int tb[kPMaxLev], tx[kPMaxLev];
         int o = 0;
         for (int l = K; l < L; ++l) {
             tb[l] = o;
@@ -1380,9 +1362,16 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
             o += pd.level_n[l] * PS;
         }
         const int NK = pd.level_n[K];
+        // gather level K from the owners (DSMEM)
         for (int i = tid; i < NK * PS; i += nth) {
             const int m = i / NK, r = i - (i / NK) * NK;
-            top[tb[K] + i] = *vec(false, K, r, m);
+            const int ow = min((int)(((long long)r << K) / cm.B), cm.C - 1);
+            PRanges Ro;
+            pc_ranges(cm, pd.level_n, ow, Ro);
+            int off = 0;
+            for (int l = 0; l < K; ++l) off += (Ro.rb[l] - Ro.ra[l]) * PS;
+            const double* src = cl.map_shared_rank(psm, ow);
+            top[tb[K] + i] = src[off + m * (Ro.rb[K] - Ro.ra[K]) + (r - Ro.ra[K])];
         }
         __syncthreads();
         for (int l = K; l + 1 < L; ++l) {
@@ -1456,79 +1445,69 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
             }
             __syncthreads();
         }
-        // x_K into CTA 0's own distributed x slot for level K
-        {
-            const int nK = cm.nr(0, K);
-            double* xK = psm + cm.xoff(0, K, PS);
-            for (int i = tid; i < nK * PS; i += nth) {
-                const int m = i / nK, r = i - (i / nK) * nK;
-                xK[i] = top[tx[K] + m * NK + r];
-            }
+    }
+    cl.sync();  // x_K complete in CTA 0
+    {
+        const int NK = pd.level_n[K], xa = R.xa[K], nx = R.xb[K] - xa;
+        // CTA 0's top area sits after CTA 0's own vectors
+        PRanges R0;
+        pc_ranges(cm, pd.level_n, 0, R0);
+        const double* xK0 = cl.map_shared_rank(psm, 0) + pc_vec_doubles(cm, R0, PS) + tofs;
+        double* xK = psm + xo[K];
+        for (int i = tid; i < nx * PS; i += nth) {
+            const int m = i / nx, r = i - (i / nx) * nx;
+            xK[i] = xK0[m * NK + xa + r];
         }
     }
-    cl.sync();
-    // every other CTA pulls its level-K x rows from CTA 0's top area
-    if (c != 0) {
-        const int NK = pd.level_n[K], lK = cm.lo(c, K), nK = cm.nr(c, K);
-        int o = 0;
-        for (int l = K; l < L; ++l) o += pd.level_n[l] * PS;  // x levels follow the b levels
-        const double* top0 = cl.map_shared_rank(psm, 0) + cm.xoff(0, K + 1, PS) + o;
-        double* xK = psm + cm.xoff(c, K, PS);
-        for (int i = tid; i < nK * PS; i += nth) {
-            const int m = i / nK, r = i - (i / nK) * nK;
-            xK[i] = top0[m * NK + lK + r];
-        }
-    }
-    cl.sync();
-    // ---- distributed back substitution, levels K-1 .. 0
+    cl.sync();  // CTA 0's top area is no longer read
+    // ---- back substitution, levels K-1 .. 0, CTA-local on [xa_l, xb_l)
     for (int l = K - 1; l >= 0; --l) {
         const int Nl = pd.level_n[l], No = Nl / 2;
-        const int lo_l = cm.lo(c, l), nr_l = cm.nr(c, l);
-        const int lo_n = cm.lo(c, l + 1), nr_n = cm.nr(c, l + 1);
-        double* bl = psm + cm.boff(c, l, PS);
-        double* xl = psm + cm.xoff(c, l, PS);
-        const double* xn = psm + cm.xoff(c, l + 1, PS);
-        PMat A_, G_, Lo, Up, Di;
-        mats(l, A_, G_, Lo, Up, Di);
-        for (int i = tid; i < nr_l * PS; i += nth) {
-            const int m = i / nr_l, qq = i - (i / nr_l) * nr_l, q = lo_l + qq;
+        const int xa = R.xa[l], nx = R.xb[l] - xa, ax = R.xa[l + 1], nxn = R.xb[l + 1] - ax;
+        const int al = R.ra[l], nl = R.rb[l] - al;
+        double* bl = psm + bo[l];
+        double* xl = psm + xo[l];
+        const double* xn = psm + xo[l + 1];
+        const double* Lo = pd.LoT + pd.odd_off[l] * pp;
+        const double* Up = pd.UpT + pd.odd_off[l] * pp;
+        const double* Di = pd.DinvT + pd.odd_off[l] * pp;
+        for (int i = tid; i < nx * PS; i += nth) {
+            const int m = i / nx, qq = i - (i / nx) * nx, q = xa + qq;
             if ((q & 1) == 0) {
-                xl[m * nr_l + qq] = xn[m * nr_n + (q / 2 - lo_n)];
+                xl[m * nx + qq] = xn[m * nxn + (q / 2 - ax)];
             } else {
                 const int oo = q >> 1;
-                double t = bl[m * nr_l + qq];
+                double t = bl[m * nl + (q - al)];
                 double acc = 0.0;
 #pragma unroll
-                for (int n = 0; n < PS; ++n) acc += Lo(m * PS + n, oo) * xn[n * nr_n + (oo - lo_n)];
+                for (int n = 0; n < PS; ++n) acc += Lo[(long long)(m * PS + n) * No + oo] * xn[n * nxn + (oo - ax)];
                 t -= acc;
                 if (q + 1 < Nl) {
                     acc = 0.0;
 #pragma unroll
-                    for (int n = 0; n < PS; ++n) {
-                        const double xv = (oo + 1 < lo_n + nr_n) ? xn[n * nr_n + (oo + 1 - lo_n)] : *vec(true, l + 1, oo + 1, n);
-                        acc += Up(m * PS + n, oo) * xv;
-                    }
+                    for (int n = 0; n < PS; ++n)
+                        acc += Up[(long long)(m * PS + n) * No + oo] * xn[n * nxn + (oo + 1 - ax)];
                     t -= acc;
                 }
-                bl[m * nr_l + qq] = t;
+                bl[m * nl + (q - al)] = t;
             }
         }
         __syncthreads();
-        for (int i = tid; i < nr_l * PS; i += nth) {
-            const int m = i / nr_l, qq = i - (i / nr_l) * nr_l, q = lo_l + qq;
+        for (int i = tid; i < nx * PS; i += nth) {
+            const int m = i / nx, qq = i - (i / nx) * nx, q = xa + qq;
             if ((q & 1) == 0) continue;
             const int oo = q >> 1;
             double acc = 0.0;
 #pragma unroll
-            for (int n = 0; n < PS; ++n) acc += Di(m * PS + n, oo) * bl[n * nr_l + qq];
-            xl[m * nr_l + qq] = acc;
+            for (int n = 0; n < PS; ++n) acc += Di[(long long)(m * PS + n) * No + oo] * bl[n * nl + (q - al)];
+            xl[m * nx + qq] = acc;
         }
-        cl.sync();
+        __syncthreads();
     }
     // ---- phi and E = -phi' (poisson.cpp:176-192), own cells
     {
-        const int l0 = cm.lo(c, 0), n0 = cm.nr(c, 0);
-        const double* x0 = psm + cm.xoff(c, 0, PS);
+        const int l0 = R.xa[0], n0 = R.xb[0] - l0;
+        const double* x0 = psm + xo[0];
         if (phi)
             for (int i = tid; i < n0 * PS; i += nth) {
                 const int q = i / PS, m = i - (i / PS) * PS;
@@ -1542,7 +1521,6 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
             E[(long long)cc * (k + 1) + m] = -dphi / pd.h[cc];
         }
     }
-    cl.sync();  // no CTA may exit while others still read its shared memory
 }
 
 // ---------------------------------------------------------------------------
@@ -2211,35 +2189,41 @@ cudaError_t launch_rho(const RhoArgs& a, int nspecies, cudaStream_t s) {
 template <int PS>
 static int poisson_cluster_plan(const PoissonDev& pd, PClusterMap& cm, size_t& smem) {
     const int N = pd.ncells;
-    // measured on B200: the cluster replay wins at nx = 16384 (0.31 vs 0.70 ms)
-    // but loses at nx = 2048 (0.15 vs 0.12 ms), where its per-level cluster
-    // barriers and CTA 0's serial top levels outweigh the spread-out work
-    if (N < 4096) return 0;
+    if (getenv("SK_POISSON_CLUSTER_MIN")) {
+        if (N < atoi(getenv("SK_POISSON_CLUSTER_MIN"))) return 0;
+    } else if (N < 1024) {
+        return 0;
+    }
     for (int C : {16, 8}) {
         if (N < 4 * C) continue;
-        int K = 0;
+        int Kmax = 0;
         const int per = (N + C - 1) / C;
-        while ((2 << K) <= per) ++K;  // 2^K <= ceil(N/C)
-        if (K >= pd.nlevels - 1) K = pd.nlevels - 2;
-        if (K < 1) continue;
-        const int B = ((per + (1 << K) - 1) >> K) << K;
-        // per-CTA rows over levels 0..K (b and x) + CTA 0's top area
-        long long rows = 0;
-        for (int l = 0; l <= K; ++l) rows += ((long long)B + (1LL << l) - 1) >> l;
-        long long top = 0;
-        for (int l = K; l < pd.nlevels; ++l) top += pd.level_n[l];
-        if (top > 64) continue;  // CTA 0's top area (see poisson_cluster_kernel)
-        const size_t vec_bytes = sizeof(double) * (size_t)PS * (size_t)(2 * rows + 2 * 64);
-        if (vec_bytes > 200 * 1024) continue;
-        // plan rows per CTA (Alpha, Gamma for reduced rows, Lo, Up, Dinv for odd rows)
-        long long plan = 0;
-        for (int l = 0; l < K; ++l) {
-            const long long nl = ((long long)B + (1LL << l) - 1) >> l;
-            plan += (long long)PS * PS * (2 * ((nl + 1) / 2) + 3 * (nl / 2));
+        while ((2 << Kmax) <= per) ++Kmax;  // 2^K <= ceil(N/C)
+        if (Kmax >= pd.nlevels - 1) Kmax = pd.nlevels - 2;
+        // fewer CTA-local levels shrink the recomputed halos (2^K rows per side)
+        // at the price of more rows for CTA 0's top levels: largest K that fits
+        PClusterMap m{};
+        size_t need = 0;
+        for (int K = Kmax; K >= 1; --K) {
+            if (K >= kPMaxLev - 1) continue;
+            const int B = ((per + (1 << K) - 1) >> K) << K;
+            const PClusterMap t{N, C, B, K};
+            long long top = 0;
+            for (int l = K; l < pd.nlevels; ++l) top += pd.level_n[l];
+            int vmax = 0;
+            for (int c = 0; c < C; ++c) {
+                PRanges R;
+                pc_ranges(t, pd.level_n, c, R);
+                const int v = pc_vec_doubles(t, R, PS) + (c == 0 ? (int)(2 * top * PS) : 0);
+                vmax = v > vmax ? v : vmax;
+            }
+            if (sizeof(double) * (size_t)vmax <= 220 * 1024) {
+                m = t;
+                need = sizeof(double) * (size_t)vmax;
+                break;
+            }
         }
-        const size_t plan_bytes = sizeof(double) * (size_t)plan;
-        const int splan = vec_bytes + plan_bytes <= 210 * 1024;
-        const size_t need = vec_bytes + (splan ? plan_bytes : 0);
+        if (need == 0) continue;
         auto kern = poisson_cluster_kernel<PS>;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need) != cudaSuccess ||
             (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
@@ -2262,7 +2246,7 @@ static int poisson_cluster_plan(const PoissonDev& pd, PClusterMap& cm, size_t& s
             cudaGetLastError();
             continue;
         }
-        cm = PClusterMap{N, C, B, K, splan};
+        cm = m;
         smem = need;
         return C;
     }
@@ -2275,7 +2259,7 @@ static cudaError_t launch_poisson_t(const PoissonDev& pd, const double* rho, dou
     static int cached_n = -1, cached_c = 0;
     static PClusterMap cached_cm{};
     static size_t cached_smem = 0;
-    if (cached_n != pd.ncells || getenv("SK_POISSON_SINGLE")) {
+    if (cached_n != pd.ncells || getenv("SK_POISSON_SINGLE") || getenv("SK_POISSON_CLUSTER_MIN")) {
         cached_c = getenv("SK_POISSON_SINGLE") ? 0 : poisson_cluster_plan<PS>(pd, cached_cm, cached_smem);
         cached_n = pd.ncells;
     }

@@ -492,8 +492,8 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk):
         L.sk_state_destroy(h)
 
 
-@pytest.mark.parametrize("k,nf,nc,m", [(3, 1024, 2048, 1), (2, 1031, 2099, 3), (3, 4096, 8192, 1),
-                                       (2, 2048, 512, 8), (1, 2048, 4096, 1)])
+@pytest.mark.parametrize("k,nf,nc,m", [(3, 512, 1024, 1), (2, 1031, 2099, 3), (3, 4096, 8192, 1),
+                                       (2, 1024, 256, 8), (1, 2048, 4096, 1), (3, 300, 421, 2)])
 def test_poisson_cluster_equals_single_cta(sk, k, nf, nc, m):
     """the cluster Poisson solve (rows over 8-16 CTAs, DSMEM neighbours) replays
     the single-CTA block-cyclic reduction row for row: bitwise equal E, phi"""
