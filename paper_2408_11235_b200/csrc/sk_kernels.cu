@@ -970,7 +970,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
 }
 
 template <int P, bool FMA>
-__global__ void __launch_bounds__(128) xfix_kernel(const __grid_constant__ XSweepArgs a) {
+__global__ void __launch_bounds__(128, 8) xfix_kernel(const __grid_constant__ XSweepArgs a) {
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1030,7 +1030,7 @@ __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, in
 }
 
 template <int P, bool FMA>
-__global__ void __launch_bounds__(128) vfix_kernel(const __grid_constant__ VSweepArgs a) {
+__global__ void __launch_bounds__(128, 8) vfix_kernel(const __grid_constant__ VSweepArgs a) {
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1708,6 +1708,11 @@ __global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
         const int xd = (int)(w % nxb) * blockDim.x + threadIdx.x;
         if (xd >= a.nxd) continue;
         const int j0 = (int)(w / nxb) * kVChunk, j1 = min(j0 + kVChunk, a.nv);
+        // old cells come in increasing order and consecutive new cells share
+        // their boundary old cell: keep the last one in registers (halves the
+        // DRAM reads of a shrink)
+        int last = -1;
+        double lastv[P];
         for (int j = j0; j < j1; ++j) {
             double dst[P];
 #pragma unroll
@@ -1717,9 +1722,14 @@ __global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
             for (int pc = 0; pc < 4; ++pc) {
                 const int oc = cellv[pc];
                 if (oc < 0) break;
+                if (oc != last) {
+#pragma unroll
+                    for (int n = 0; n < P; ++n) lastv[n] = f[((long long)oc * P + n) * a.ld + xd];
+                    last = oc;
+                }
                 double src[P];
 #pragma unroll
-                for (int n = 0; n < P; ++n) src[n] = f[((long long)oc * P + n) * a.ld + xd];
+                for (int n = 0; n < P; ++n) src[n] = lastv[n];
 #pragma unroll
                 for (int m = 0; m < P; ++m) {
                     double acc = 0.0;
