@@ -150,6 +150,9 @@ sk_status sk_field_download_async(sk_field* f, double* host_pinned, size_t count
 sk_status sk_field_create_shard(sk_ctx* ctx, int species, double v_left, double v_right,
                                 int v_cells_global, int cell0, int ncell, int halo, sk_field** out);
 sk_status sk_field_halo(sk_field* f, int side, int send, double** ptr_dev, size_t* count);
+/* the same for an explicit width of `cells` halo cells (<= the allocated halo);
+ * a sharded velocity shrink exchanges sk_state_shrink_halo cells */
+sk_status sk_field_halo_n(sk_field* f, int side, int send, int cells, double** ptr_dev, size_t* count);
 /* v grid: left, dx, cells (synchronises: the cut-off updates it on device) */
 sk_status sk_field_v_grid(sk_field* f, double* left, double* dx, int* cells);
 /* run.cpp:41-46 blob f = (2 pi)^-1/2 exp(-x^2/(2 sigma^2)) exp(-v^2/2) */
@@ -187,11 +190,18 @@ sk_status sk_state_download_E(sk_state* s, double* host, size_t count);
 /* v-sharded state: rank `rank` of `nranks` holds v_cells/nranks cells of each
  * species plus `halo` cells; the step runs as phase 2 (x half sweep + local
  * rho) -> caller all-reduces rho (sk_state_rho_dev) and exchanges the halos
- * -> phase 3 (Poisson, v sweep, x half sweep). Phases 0/1: local initial rho
- * and the Poisson solve of the all-reduced rho (initial field). */
+ * -> phase 3 (Poisson, v sweep, x half sweep, step end; with the velocity
+ * cut-off also the local shrink check: the ranks holding the probe cells
+ * clear sk_state_shrink_flags_dev) -> caller all-reduces the two int flags
+ * (MIN) and, for a species whose flag is set, exchanges
+ * sk_state_shrink_halo cells with sk_field_halo_n -> phase 4 (shrink).
+ * Phases 0/1: local initial rho and the Poisson solve of the all-reduced rho
+ * (initial field). */
 sk_status sk_state_create_shard(sk_ctx* ctx, const sk_run_config* cfg, int rank, int nranks,
                                 int halo, sk_state** out);
 double* sk_state_rho_dev(sk_state* s);
+int* sk_state_shrink_flags_dev(sk_state* s); /* int[2], device: 1 = shrink this step */
+int sk_state_shrink_halo(sk_state* s);        /* halo cells a sharded shrink reads */
 sk_status sk_state_phase(sk_state* s, int phase);
 /* one strang_step (no shrink); max_ghost < 0: run()'s rule */
 sk_status sk_strang_step(sk_state* s);

@@ -72,8 +72,11 @@ SIGNATURES = {
     "sk_field_v_grid": (_i, [_vp, _dp, _dp, _ip]),
     "sk_field_create_shard": (_i, [_vp, _i, _d, _d, _i, _i, _i, _i, C.POINTER(_vp)]),
     "sk_field_halo": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_sz)]),
+    "sk_field_halo_n": (_i, [_vp, _i, _i, _i, C.POINTER(_vp), C.POINTER(_sz)]),
     "sk_state_create_shard": (_i, [_vp, C.POINTER(sk_run_config), _i, _i, _i, C.POINTER(_vp)]),
     "sk_state_rho_dev": (_vp, [_vp]),
+    "sk_state_shrink_flags_dev": (_vp, [_vp]),
+    "sk_state_shrink_halo": (_i, [_vp]),
     "sk_state_phase": (_i, [_vp, _i]),
     "sk_field_fill_blob": (_i, [_vp, _d]),
     "sk_advect_x": (_i, [_vp, _d, _d, _i, C.POINTER(sk_limiter), _i, C.c_long]),

@@ -82,6 +82,7 @@ struct sk_field {
     int nv_global = 0;
     int cell0 = 0;                     // first global v cell (v-shard)
     int halo = 0;                      // halo cells stored below and above
+    int xhalo = 0;                     // of which the v sweep reads / exchanges each step
     size_t n = 0;                      // interior doubles
     size_t halo_off = 0;               // doubles from buffer start to the interior
     double* buf[2] = {nullptr, nullptr};
@@ -111,8 +112,8 @@ struct sk_field {
         *p = buf[cur ^ (fl & 1)] + halo_off;
         return e;
     }
-    int gl() const { return cell0 > 0 ? halo : 0; }
-    int gr() const { return cell0 + nv < nv_global ? halo : 0; }
+    int gl() const { return cell0 > 0 ? xhalo : 0; }
+    int gr() const { return cell0 + nv < nv_global ? xhalo : 0; }
 };
 
 struct sk_state {
@@ -130,6 +131,7 @@ struct sk_state {
     int graph_exact = -1;              // arithmetic mode the graph was captured in
     long long graph_launches = 0;      // kernels per graph replay
     int rank = 0, nranks = 1;          // v-shard of a multi-GPU run
+    int shrink_halo = 0;               // halo cells a sharded shrink reads
     // optional per-phase CUDA-event timing (sk_state_set_phase_timing)
     bool timing = false;
     std::vector<std::pair<int, cudaEvent_t>> marks;
@@ -178,6 +180,11 @@ sk_status collect_errors(sk_ctx* c) {
         case 5:
             msg = "step " + std::to_string(step) + ": insufficient v halo: v sweep shifts " +
                   std::to_string(h.err_need) + " cells, shard halo is " + std::to_string(h.err_have);
+            break;
+        case 6:
+            msg = "step " + std::to_string(step) + ": velocity shrink reads old cell " +
+                  std::to_string(h.err_need) + " outside the shard and its " + std::to_string(h.err_have) +
+                  "-cell halo";
             break;
         default:
             msg = "velocity shrink: transfer table overflow";
@@ -475,6 +482,9 @@ sk_status enq_shrink(sk_field** fs, int nspecies, const sk_vadjust& pol, int for
     a.nxd = c->grid.ncells * c->P;
     a.ld = a.nxd;
     a.nv = fs[0]->nv;
+    a.nv_global = fs[0]->nv_global;
+    a.cell0 = fs[0]->cell0;
+    a.halo = fs[0]->halo;
     a.species_mask = mask;
     a.v_adjust = v_adjust;
     a.force = force;
@@ -483,7 +493,7 @@ sk_status enq_shrink(sk_field** fs, int nspecies, const sk_vadjust& pol, int for
     a.tol = pol.tol;
     a.cooldown = 10;
     CK(launch_shrink(a, c->stream));
-    c->launches += (force != 0) + (force != 1) + (force >= 0 ? 3 : 0);
+    c->launches += (force == 1 || force == -1) + (force != 1 && force != 2) + (force >= 0 ? 3 : 0);
     return SK_OK;
 }
 
@@ -740,6 +750,7 @@ sk_status sk_field_create_shard(sk_ctx* c, int species, double v_left, double v_
     f->nv_global = v_cells_global;
     f->cell0 = cell0;
     f->halo = halo;
+    f->xhalo = halo;
     const int P = c->P;
     const size_t row = (size_t)c->grid.ncells * P;  // one v row (x line)
     f->n = (size_t)ncell * P * row;
@@ -768,17 +779,23 @@ sk_status sk_field_create(sk_ctx* c, int species, double v_left, double v_right,
     return sk_field_create_shard(c, species, v_left, v_right, v_cells, 0, v_cells, 0, out);
 }
 
-sk_status sk_field_halo(sk_field* f, int side, int send, double** ptr, size_t* count) {
+sk_status sk_field_halo_n(sk_field* f, int side, int send, int cells, double** ptr, size_t* count) {
     if (f->halo == 0) return fail(SK_ERR_RUNTIME, "field has no v halo");
-    const size_t hrows = f->halo_off;  // halo cells * P * row doubles
+    if (cells < 1 || cells > f->halo || cells > f->nv)
+        return fail(SK_ERR_RUNTIME, "v halo: width must be in 1..min(allocated halo, shard cells)");
+    const size_t rows = f->halo_off / f->halo * cells;  // cells * P * row doubles
     double* in = nullptr;
     CK(f->live_ptr(&in));
     if (side == 0)
-        *ptr = send ? in : in - hrows;
+        *ptr = send ? in : in - rows;
     else
-        *ptr = send ? in + (f->n - hrows) : in + f->n;
-    *count = hrows;
+        *ptr = send ? in + (f->n - rows) : in + f->n;
+    *count = rows;
     return SK_OK;
+}
+
+sk_status sk_field_halo(sk_field* f, int side, int send, double** ptr, size_t* count) {
+    return sk_field_halo_n(f, side, send, f->xhalo > 0 ? f->xhalo : 1, ptr, count);
 }
 
 sk_status sk_field_destroy(sk_field* f) {
@@ -1063,8 +1080,6 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
     *out = nullptr;
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SK_ERR_RUNTIME, "v shard: bad rank");
     if (cfg->v_cells % nranks) return fail(SK_ERR_RUNTIME, "v shard: v_cells must divide by the rank count");
-    if (nranks > 1 && cfg->v_adjust)
-        return fail(SK_ERR_RUNTIME, "v shard: the velocity cut-off is not supported across ranks yet");
     if (nranks > 1 && cfg->limiter.indicator)
         return fail(SK_ERR_RUNTIME, "v shard: post limiters are not supported across ranks yet");
     if (cfg->k != c->k) return fail(SK_ERR_RUNTIME, "state: degree differs from the context");
@@ -1073,6 +1088,17 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
     if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
     const int ncell = cfg->v_cells / nranks, cell0 = rank * ncell;
     if (nranks > 1 && halo > ncell) return fail(SK_ERR_RUNTIME, "v shard: halo wider than a shard");
+    // a velocity shrink maps new cell j to old cells up to p*nv/2 cells closer
+    // to v = 0 (adaptivity.cpp:52-90): shards keep a halo that wide, filled
+    // only on shrink steps
+    int hs = 0;
+    if (nranks > 1 && cfg->v_adjust) {
+        if (sk_status rc = validate_policy(&cfg->policy)) return rc;
+        hs = (int)std::ceil(cfg->policy.p * cfg->v_cells * 0.5) + 3;
+        if (hs > ncell)
+            return fail(SK_ERR_RUNTIME, "v shard: shards too small for the velocity cut-off (need " +
+                                            std::to_string(hs) + " cells per shard)");
+    }
     auto* s = new sk_state;
     s->ctx = c;
     s->cfg = *cfg;
@@ -1081,12 +1107,17 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
     s->sqrt_mu[0] = 1.0;
     s->sqrt_mu[1] = std::sqrt(cfg->mu);
     const int h = nranks > 1 ? halo : 0;
+    const int halloc = h > hs ? h : hs;
     sk_status rc;
-    if ((rc = sk_field_create_shard(c, 0, -cfg->vmax_e, cfg->vmax_e, cfg->v_cells, cell0, ncell, h, &s->f[0])) ||
-        (rc = sk_field_create_shard(c, 1, -cfg->vmax_i, cfg->vmax_i, cfg->v_cells, cell0, ncell, h, &s->f[1]))) {
+    if ((rc = sk_field_create_shard(c, 0, -cfg->vmax_e, cfg->vmax_e, cfg->v_cells, cell0, ncell, halloc,
+                                    &s->f[0])) ||
+        (rc = sk_field_create_shard(c, 1, -cfg->vmax_i, cfg->vmax_i, cfg->v_cells, cell0, ncell, halloc,
+                                    &s->f[1]))) {
         sk_state_destroy(s);
         return rc;
     }
+    s->f[0]->xhalo = s->f[1]->xhalo = h;
+    s->shrink_halo = hs;
     double sigma = cfg->sigma < 0 ? 0.1 * cfg->L : cfg->sigma;
     if ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma))) {
         sk_state_destroy(s);
@@ -1248,6 +1279,8 @@ sk_status enq_run_body(sk_state* s) {
 }  // namespace
 
 double* sk_state_rho_dev(sk_state* s) { return s->rho; }
+int* sk_state_shrink_flags_dev(sk_state* s) { return s->ctx->st->shrink_flag; }
+int sk_state_shrink_halo(sk_state* s) { return s->shrink_halo; }
 
 sk_status sk_state_phase(sk_state* s, int phase) {
     sk_ctx* c = s->ctx;
@@ -1259,9 +1292,19 @@ sk_status sk_state_phase(sk_state* s, int phase) {
         case 2: rc = enq_phase_a(s); break;
         case 3:
             if ((rc = enq_phase_b(s))) break;
-            CK(launch_step_end(c->st, 0, 10, 0, c->stream));
+            CK(launch_step_end(c->st, s->cfg.v_adjust, 10, 3, c->stream));
             c->launches += 1;
             s->step_host += 1;
+            if (s->cfg.v_adjust) {  // local part of the cut-off decision
+                sk_field* fs[2] = {s->f[0], s->f[1]};
+                rc = enq_shrink(fs, 2, s->cfg.policy, -2, 1);
+            }
+            break;
+        case 4:  // shrink with the (all-reduced) decision in sk_state_shrink_flags_dev
+            if (s->cfg.v_adjust) {
+                sk_field* fs[2] = {s->f[0], s->f[1]};
+                rc = enq_shrink(fs, 2, s->cfg.policy, 2, 1);
+            }
             break;
         default: return fail(SK_ERR_RUNTIME, "unknown step phase");
     }

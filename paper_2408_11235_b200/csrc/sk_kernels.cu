@@ -1625,11 +1625,13 @@ __global__ void shrink_check_kernel(const __grid_constant__ ShrinkArgs a) {
         double vp = (s == 0 ? 1.0 : -1.0) * probe;
         int vc = (int)floor((vp - vg.left) / dv);
         vc = min(max(vc, 0), vg.cells - 1);
+        const int vl = vc - a.cell0;  // a v shard evaluates only the probe cells it holds
+        if (vl < 0 || vl >= a.nv) continue;
         double xi = (vp - (vg.left + vc * vg.dx)) / dv;
         double val = 0.0;
 #pragma unroll
         for (int vn = 0; vn < P; ++vn)
-            val += lagrange<P>(a.basis, vn, xi) * f[((long long)vc * P + vn) * a.ld + xd];
+            val += lagrange<P>(a.basis, vn, xi) * f[((long long)vl * P + vn) * a.ld + xd];
         if (fabs(val) >= a.tol) fail = true;
     }
     if (fail) a.st->shrink_flag[sp] = 0;
@@ -1640,13 +1642,13 @@ template <int P>
 __global__ void shrink_table_kernel(const __grid_constant__ ShrinkArgs a) {
     const int sp = blockIdx.y;
     if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= a.nv) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;  // global new cell
+    if (j >= a.nv_global) return;
     const DevVGrid ov = *a.vg[sp];
     const double vmax_before = ov.left + ov.cells * ov.dx;
     const double new_vmax = vmax_before * (1.0 - a.p);
     const double nleft = -new_vmax;
-    const double ndx = (new_vmax - (-new_vmax)) / a.nv;  // Grid1D::uniform (grid.cpp:31-34)
+    const double ndx = (new_vmax - (-new_vmax)) / a.nv_global;  // Grid1D::uniform (grid.cpp:31-34)
     const double old_dx = ov.dx;
     const double aa = nleft + j * ndx;
     const double h = ndx;
@@ -1717,11 +1719,17 @@ __global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
             double dst[P];
 #pragma unroll
             for (int m = 0; m < P; ++m) dst[m] = 0.0;
-            const double* T = a.ttab[sp] + (long long)j * 4 * P * P;
-            const int* cellv = a.tcell[sp] + (long long)j * 4;
+            const long long jg = (long long)a.cell0 + j;  // global new cell
+            const double* T = a.ttab[sp] + jg * 4 * P * P;
+            const int* cellv = a.tcell[sp] + jg * 4;
             for (int pc = 0; pc < 4; ++pc) {
-                const int oc = cellv[pc];
+                int oc = cellv[pc];
                 if (oc < 0) break;
+                oc -= a.cell0;  // local old cell; a shard reads up to `halo` beyond its range
+                if (oc < -a.halo || oc >= a.nv + a.halo) {
+                    raise_error(a.st, 1, 6, oc, a.halo, a.st->step);
+                    break;
+                }
                 if (oc != last) {
 #pragma unroll
                     for (int n = 0; n < P; ++n) lastv[n] = f[((long long)oc * P + n) * a.ld + xd];
@@ -1753,7 +1761,7 @@ __global__ void shrink_finalize_kernel(const __grid_constant__ ShrinkArgs a) {
     const double vmax_before = ov.left + ov.cells * ov.dx;
     const double new_vmax = vmax_before * (1.0 - a.p);
     a.vg[sp]->left = -new_vmax;
-    a.vg[sp]->dx = (new_vmax - (-new_vmax)) / a.nv;
+    a.vg[sp]->dx = (new_vmax - (-new_vmax)) / a.nv_global;
     a.st->vmax_before[sp] = vmax_before;
     a.st->last_shrink[sp] = a.st->step;
     a.st->shrink_count[sp] += 1;
@@ -2317,12 +2325,12 @@ cudaError_t launch_step_end(DevStatus* st, int v_adjust, long long cooldown, int
 
 cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s) {
     const int P = a.basis.p;
-    // force: 0 = run() cadence (flags from step_end), -1 = check only, 1 = shrink unchecked
-    if (a.force) shrink_force_kernel<<<1, 1, 0, s>>>(a.st, a.species_mask);
-    if (a.force != 1)
+    // force: see ShrinkArgs
+    if (a.force == 1 || a.force == -1) shrink_force_kernel<<<1, 1, 0, s>>>(a.st, a.species_mask);
+    if (a.force != 1 && a.force != 2)
         SK_DISPATCH_P(P, (shrink_check_kernel<PP><<<dim3((a.nxd + 255) / 256, 2), 256, 0, s>>>(a)));
     if (a.force < 0) return cudaGetLastError();
-    SK_DISPATCH_P(P, (shrink_table_kernel<PP><<<dim3((a.nv + 127) / 128, 2), 128, 0, s>>>(a)));
+    SK_DISPATCH_P(P, (shrink_table_kernel<PP><<<dim3((a.nv_global + 127) / 128, 2), 128, 0, s>>>(a)));
     SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3(sm_count() * 16, 1, 2), 128, 0, s>>>(a)));
     shrink_finalize_kernel<<<1, 32, 0, s>>>(a);
     return cudaGetLastError();

@@ -149,10 +149,16 @@ struct ShrinkArgs {
     int* tcell[2];         // [nv][4]
     long long ld;
     int nxd;
-    int nv;
+    int nv;                // v cells held by this field (a v shard: nv < nv_global)
+    int nv_global;
+    int cell0;             // first global v cell held
+    int halo;              // allocated halo cells below/above (old cells a shard may read)
     int species_mask;      // which species to consider
     int v_adjust;
-    int force;             // 1: bypass check/cooldown (standalone shrink)
+    // 0: run() cadence (check + shrink), 1: shrink unchecked (standalone),
+    // -1: forced check only (standalone), -2: cadence check only (v shards,
+    // before the decision is all-reduced), 2: shrink only (decision taken)
+    int force;
     double p, gamma, tol;
     long long cooldown;
 };

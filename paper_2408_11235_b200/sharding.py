@@ -8,12 +8,16 @@ of each species for all x, plus `halo` cells below and above. Then
     followed by an all-reduce(sum) of nx*(k+1) doubles;
   * the Poisson solve is replicated (every rank gets the same E);
   * the v sweep reads `halo` cells from the neighbouring ranks, exchanged
-    point-to-point right after the first x sweep.
+    point-to-point right after the first x sweep;
+  * the velocity cut-off (adaptivity.cpp:16-130, run.cpp:98-114): the ranks
+    holding the probe cells decide locally, an all-reduce(MIN) of two ints
+    makes the decision global, and on a shrink step each rank exchanges the
+    ceil(p*nv/2)+3 cells the projection reads across its shard edges.
 
 Plumbing is torch.distributed: NCCL over NVLink/NVSwitch for device buffers,
 gloo for the CPU tests (tests/test_sharding.py drive exactly these functions
-with the C oracle as the per-rank compute). The velocity cut-off and the
-literature post limiters are not sharded yet (the C ABI refuses them).
+with the C oracle as the per-rank compute). The literature post limiters are
+not sharded yet (the C ABI refuses them).
 """
 from __future__ import annotations
 
@@ -103,15 +107,22 @@ def allreduce_rho(rho, group=None):
 class _DevView:
     """__cuda_array_interface__ over a raw device pointer (no ownership)."""
 
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+    def __init__(self, ptr: int, n: int, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
                                          "version": 3, "strides": None, "stream": None}
 
 
-def _dev_tensor(ptr: int, n: int, device: int):
+def _dev_tensor(ptr: int, n: int, device: int, typestr: str = "<f8"):
     import torch
 
-    return torch.as_tensor(_DevView(ptr, n), device=f"cuda:{device}")
+    return torch.as_tensor(_DevView(ptr, n, typestr), device=f"cuda:{device}")
+
+
+def allreduce_shrink_flags(flags, group=None):
+    """cut-off decision: shrink only if no rank's probe cells failed (MIN)"""
+    import torch.distributed as dist
+
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=group)
 
 
 class ShardedState:
@@ -136,6 +147,12 @@ class ShardedState:
                   for sp in (0, 1)]
         n_rho = self.ctx.nx * self.ctx.p
         self.rho = _dev_tensor(L.sk_state_rho_dev(h), n_rho, device)
+        self.flags = _dev_tensor(L.sk_state_shrink_flags_dev(h), 2, device, "<i4")
+        self.shrink_halo = int(L.sk_state_shrink_halo(h))
+        # host mirror of the device cooldown gate (run.cpp:98-101, step_end_kernel):
+        # steps on which no species may shrink need no decision round trip
+        self._step = 0
+        self._last_shrink = [-10, -10]
         # initial field: local moment (created) -> all-reduce -> Poisson
         self._reduce_rho()
         self._phase(1)
@@ -152,29 +169,55 @@ class ShardedState:
         allreduce_rho(self.rho, self.group)
         self.ctx.enter()
 
-    def _exchange(self):
+    def _exchange(self, cells=None, species=(0, 1)):
         if self.plan.nranks == 1:
             return
         from .solver import _check
 
         self.ctx.leave()
-        for f in self.f:
+        for sp in species:
+            f = self.f[sp]
             views = []
             for side in (0, 1):
                 for send in (1, 0):
                     ptr, cnt = C.c_void_p(), C.c_size_t()
-                    _check(N.lib().sk_field_halo(f.h, side, send, C.byref(ptr), C.byref(cnt)))
+                    if cells is None:
+                        _check(N.lib().sk_field_halo(f.h, side, send, C.byref(ptr), C.byref(cnt)))
+                    else:
+                        _check(N.lib().sk_field_halo_n(f.h, side, send, cells, C.byref(ptr), C.byref(cnt)))
                     views.append(_dev_tensor(ptr.value, cnt.value, self.device))
             exchange_halos(views[0], views[1], views[2], views[3], self.plan, self.group)
         self.ctx.enter()
 
+    def _cutoff(self):
+        """run.cpp:98-114 across ranks: global decision, halo fill, shrink"""
+        self._step += 1
+        if not self.cfg.v_adjust:
+            return
+        if all(self._step - last < 10 for last in self._last_shrink):
+            return
+        if self.plan.nranks > 1:
+            self.ctx.leave()
+            allreduce_shrink_flags(self.flags, self.group)
+            self.ctx.enter()
+        fl = self.flags.cpu().tolist()  # the host decides whether halos must move
+        if not any(fl):
+            return
+        for sp in (0, 1):
+            if fl[sp]:
+                self._last_shrink[sp] = self._step
+        self._exchange(self.shrink_halo, [sp for sp in (0, 1) if fl[sp]])
+        self._phase(4)
+
     def step(self):
-        """one strang_step: x half sweep (+ local rho) | all-reduce rho, halo
-        exchange | Poisson, v sweep, x half sweep"""
+        """one run() loop body: x half sweep (+ local rho) | all-reduce rho,
+        halo exchange | Poisson, v sweep, x half sweep, step end, local cut-off
+        check | all-reduce decision, shrink halos | shrink"""
         self._phase(2)
         self._reduce_rho()
         self._exchange()
         self._phase(3)
+        self._cutoff()
 
     def close(self):
         if getattr(self, "h", None):
@@ -193,9 +236,6 @@ def bench_sharded(args, cfg, metric, unit, config):
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    import dataclasses
-
-    cfg = dataclasses.replace(cfg, v_adjust=False)  # cut-off is not sharded yet
     dv = 2 * cfg.vmax_e / cfg.v_cells
     halo = max(4, min(cfg.v_cells // world, halo_cells_needed(0.5, cfg.dt, dv)))
     st = ShardedState(cfg, rank, world, halo=halo, device=local)
@@ -219,7 +259,7 @@ def bench_sharded(args, cfg, metric, unit, config):
         value = cfg.dof_total * args.steps / (ms / 1e3)
         cfgd = dict(config)
         cfgd["parallelism"] = f"v-shard x{world} (halo {halo} cells, NCCL all-reduce + P2P)"
-        cfgd["v_cutoff"] = "off (not sharded yet)"
+        cfgd["v_cutoff"] = "on (sharded: all-reduced decision, halo on shrink steps)" if cfg.v_adjust else "off"
         line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

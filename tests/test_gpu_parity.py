@@ -418,10 +418,12 @@ def test_cpp_mirror_runs_against_oracle():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-def test_two_v_shards_on_one_gpu_match_unsharded(sk):
+@pytest.mark.parametrize("v_adjust", [False, True], ids=["no_cutoff", "cutoff"])
+def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust):
     """The CUDA v-shard path (global cell offsets in the x tables, halo reads in
-    the v sweep, local fused charge density) driven like two ranks, with the
-    all-reduce and the halo exchange done by device copies in one process."""
+    the v sweep, local fused charge density, sharded velocity cut-off) driven
+    like two ranks, with the all-reduces and the halo exchanges done by device
+    copies in one process; 12 run() loop bodies cover two shrink events."""
     import ctypes as C
 
     import torch
@@ -430,7 +432,7 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk):
     from paper_2408_11235_b200.sharding import VShardPlan, _dev_tensor
     from paper_2408_11235_b200.solver import Context, Grid1D, _check
 
-    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter="sldg", v_adjust=False)
+    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter="sldg", v_adjust=v_adjust)
     ref = sk.SimulationState(cfg)
     L = N.lib()
     grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
@@ -443,29 +445,38 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk):
         ccfg = cfg.to_c()
         _check(L.sk_state_create_shard(ctx.h, C.byref(ccfg), r, world, halo, C.byref(h)))
         rho = _dev_tensor(L.sk_state_rho_dev(h), ctx.nx * ctx.p, 0)
-        shards.append((ctx, h, rho, VShardPlan(cfg.v_cells, world, r, halo)))
+        flags = _dev_tensor(L.sk_state_shrink_flags_dev(h), 2, 0, "<i4")
+        shards.append((ctx, h, rho, VShardPlan(cfg.v_cells, world, r, halo), flags))
+    hs = L.sk_state_shrink_halo(shards[0][1])
+    assert (hs > 0) == v_adjust
 
-    def reduce_rho():
+    def sync():
         for ctx, *_ in shards:
             ctx.synchronize()
+        torch.cuda.synchronize()
+
+    def reduce_rho():
+        sync()
         tot = sum(s[2].clone() for s in shards)
         for s in shards:
             s[2].copy_(tot)
         torch.cuda.synchronize()
 
-    def exchange():
-        for ctx, *_ in shards:
-            ctx.synchronize()
+    def exchange(cells=None, species=(0, 1)):
+        sync()
         views = {}
-        for r, (ctx, h, _, _) in enumerate(shards):
-            for sp in (0, 1):
+        for r, (ctx, h, *_) in enumerate(shards):
+            for sp in species:
                 f = L.sk_state_field(h, sp)
                 for side in (0, 1):
                     for send in (1, 0):
                         ptr, cnt = C.c_void_p(), C.c_size_t()
-                        _check(L.sk_field_halo(f, side, send, C.byref(ptr), C.byref(cnt)))
+                        if cells is None:
+                            _check(L.sk_field_halo(f, side, send, C.byref(ptr), C.byref(cnt)))
+                        else:
+                            _check(L.sk_field_halo_n(f, side, send, cells, C.byref(ptr), C.byref(cnt)))
                         views[(r, sp, side, send)] = _dev_tensor(ptr.value, cnt.value, 0)
-        for sp in (0, 1):  # rank0 upper halo <- rank1 lower interior, and back
+        for sp in species:  # rank0 upper halo <- rank1 lower interior, and back
             views[(0, sp, 1, 0)].copy_(views[(1, sp, 0, 1)])
             views[(1, sp, 0, 0)].copy_(views[(0, sp, 1, 1)])
         torch.cuda.synchronize()
@@ -473,19 +484,37 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk):
     reduce_rho()
     for ctx, h, *_ in shards:
         _check(L.sk_state_phase(h, 1))
-    for _ in range(4):
-        ref.strang_step()
+    shrinks = 0
+    for _ in range(12):
+        if v_adjust:
+            ref.run_step()
+        else:
+            ref.strang_step()
         for ctx, h, *_ in shards:
             _check(L.sk_state_phase(h, 2))
         reduce_rho()
         exchange()
         for ctx, h, *_ in shards:
             _check(L.sk_state_phase(h, 3))
+        if v_adjust:
+            sync()
+            fl = torch.minimum(shards[0][4], shards[1][4])
+            for s in shards:
+                s[4].copy_(fl)
+            fl = fl.cpu().tolist()
+            if any(fl):
+                shrinks += 1
+                exchange(hs, [sp for sp in (0, 1) if fl[sp]])
+                for ctx, h, *_ in shards:
+                    _check(L.sk_state_phase(h, 4))
+    if v_adjust:
+        assert shrinks >= 2
     for sp in (0, 1):
         parts = []
-        for ctx, h, _, plan in shards:
+        for ctx, h, _, plan, _ in shards:
             f = sk.NodalField(ctx, sp, None, _handle=L.sk_state_field(h, sp))
             parts.append(f.download())
+            assert f.vmax() == ref.field(sp).vmax()
         got = np.concatenate(parts)
         assert rel(got, ref.field(sp).download()) <= 1e-12, f"species {sp}"
     for ctx, h, *_ in shards:

@@ -127,3 +127,70 @@ def test_shard_plan():
         VShardPlan(100, 8, 0, 4)
     # C5 electrons at |E| = 0.2: shift 0.2*0.1/(24/16384) = 13.65 cells -> 15
     assert halo_cells_needed(0.2, 0.1, 24 / 16384) == 15
+
+
+def _cutoff_worker(rank, world, port, cfg, outdir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import math
+
+    import torch
+    import torch.distributed as dist
+
+    from oracle import Oracle
+    from paper_2408_11235_b200.sharding import VShardPlan, allreduce_shrink_flags, exchange_halos
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    ora = Oracle()
+    st = ora.state(**cfg)
+    st.step()
+    k, nv, nx = cfg["k"], cfg["nv"], st.nx
+    p = k + 1
+    hs = math.ceil(0.05 * nv * 0.5) + 3  # sk_state_shrink_halo for the default policy
+    plan = VShardPlan(nv, world, rank, hs)
+    full = st.field(0).reshape(nv * p, nx * p)
+    rows, h = plan.ncell * p, hs * p
+    buf = torch.zeros((plan.ncell + 2 * hs) * p, nx * p, dtype=torch.float64)
+    buf[h: h + rows] = torch.from_numpy(full[plan.cell0 * p: plan.cell0 * p + rows])
+    exchange_halos(buf[h: 2 * h].contiguous().view(-1), buf[0:h].view(-1),
+                   buf[rows: rows + h].contiguous().view(-1), buf[rows + h: rows + 2 * h].view(-1), plan)
+    # the decision: only the ranks holding the probe cells evaluate; MIN makes it global
+    ok_global = ora.state(**cfg)
+    ok_global.step()
+    want = int(ok_global.check_shrink(0))
+    vmax = st.vmax(0)
+    probe = vmax * (1 - 0.05 - 0.05)
+    cells = [min(max(int((v + vmax) / (2 * vmax / nv)), 0), nv - 1) for v in (probe, -probe)]
+    holds = any(plan.cell0 <= c < plan.cell0 + plan.ncell for c in cells)
+    flags = torch.tensor([want if holds else 1, 1], dtype=torch.int32)
+    allreduce_shrink_flags(flags)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), buf=buf.numpy(), flags=flags.numpy(),
+             want=want, cell0=plan.cell0, ncell=plan.ncell, hs=hs)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_cutoff_decision_and_shrink_halos(ora):
+    """the sharded velocity cut-off's host protocol: MIN-all-reduced decision
+    equals the serial check, and the shrink-width halos hold the neighbours'
+    old cells (what shrink_project reads across the shard edges)"""
+    cfg = dict(k=2, nf=8, nc=16, m=1, nv=64, limiter="none", v_adjust=1, dt=0.1, mu=400.0)
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_cutoff_worker, args=(world, _free_port(), cfg, d), nprocs=world, join=True)
+        parts = [dict(np.load(os.path.join(d, f"rank{r}.npz"))) for r in range(world)]
+    st = ora.state(**cfg)
+    st.step()
+    p = cfg["k"] + 1
+    full = st.field(0).reshape(cfg["nv"] * p, -1)
+    for part in parts:
+        assert int(part["flags"][0]) == int(part["want"])
+        c0, n, hs = int(part["cell0"]), int(part["ncell"]), int(part["hs"])
+        buf = part["buf"]
+        lo = max(c0 - hs, 0)
+        hi = min(c0 + n + hs, cfg["nv"])
+        # every old cell in [c0-hs, c0+n+hs) that exists globally is present
+        assert np.array_equal(buf[(lo - c0 + hs) * p:(hi - c0 + hs) * p], full[lo * p:hi * p])
