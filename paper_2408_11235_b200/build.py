@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(LIB_DIR, src + ".o")
         cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
                "-ccbin", "/usr/bin/g++", "-Xcompiler", "-fPIC,-ffp-contract=off",
-               "-c", os.path.join(CSRC, src), "-o", obj]
+               "-c", os.path.join(CSRC, src), "-o", obj] + os.environ.get("SK_NVCC_EXTRA", "").split()
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         objs.append((cmd, obj))
