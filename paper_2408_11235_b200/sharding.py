@@ -228,9 +228,16 @@ class ShardedState:
 
 def bench_sharded(args, cfg, metric, unit, config):
     """bench.py under torchrun: N ranks, one GPU each, NCCL; device time is
-    the max over ranks of the CUDA-event time around K steps."""
+    the max over ranks of the CUDA-event time around K steps. The line carries
+    the same keys as the single-GPU one: roofline (whole step, 48 B/DoF
+    against N x the measured HBM peak), e2e through the sharded API with host
+    buffers, clocks of this rank's GPU, and the kernels launched."""
+    import time
+
     import torch
     import torch.distributed as dist
+
+    import bench
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -245,6 +252,9 @@ def bench_sharded(args, cfg, metric, unit, config):
     st.ctx.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
+    launches0 = int(N.lib().sk_ctx_launch_count(st.ctx.h))
+    clocks = bench.ClockSampler(local)
+    clocks.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(st.ctx.stream)
     for _ in range(args.steps):
@@ -252,11 +262,38 @@ def bench_sharded(args, cfg, metric, unit, config):
     t1.record(st.ctx.stream)
     torch.cuda.synchronize()
     st.ctx.synchronize()
+    clk = clocks.stop()
+    launches = int(N.lib().sk_ctx_launch_count(st.ctx.h)) - launches0
     ms = torch.tensor([t0.elapsed_time(t1)], device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    # e2e: every step moves this rank's shard host -> device and back
+    e2e = None
+    if not getattr(args, "no_e2e", False):
+        n = st.f[0].size
+        host = [torch.empty(n, dtype=torch.float64, pin_memory=True).numpy() for _ in (0, 1)]
+        for sp in (0, 1):
+            host[sp][:] = st.f[sp].download()
+        k2 = max(1, getattr(args, "e2e_steps", 3))
+        dist.barrier()
+        w0 = time.perf_counter()
+        dp = C.POINTER(C.c_double)
+        for _ in range(k2):
+            for sp in (0, 1):  # pinned buffers: DMA at PCIe speed
+                N.lib().sk_field_upload_async(st.f[sp].h, host[sp].ctypes.data_as(dp), n)
+            st.step()
+            for sp in (0, 1):
+                N.lib().sk_field_download_async(st.f[sp].h, host[sp].ctypes.data_as(dp), n)
+            st.ctx.synchronize()
+        wall = torch.tensor([time.perf_counter() - w0], device=f"cuda:{local}")
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfg.dof_total * k2 / float(wall.item()), "unit": unit,
+               "h2d_bytes_per_step": 2 * 8 * n * world, "d2h_bytes_per_step": 2 * 8 * n * world,
+               "steps": k2, "api": "ShardedState (sk_state_create_shard / sk_state_phase, sk_field_upload_async)"}
     if rank == 0:
         value = cfg.dof_total * args.steps / (ms / 1e3)
+        peak, peak_kind = bench.peaks()
+        step_gbs = 3 * bench.BYTES_PER_DOF_SWEEP * cfg.dof_total * args.steps / (ms / 1e3) / 1e9
         cfgd = dict(config)
         cfgd["parallelism"] = f"v-shard x{world} (halo {halo} cells, NCCL all-reduce + P2P)"
         cfgd["v_cutoff"] = "on (sharded: all-reduced decision, halo on shrink steps)" if cfg.v_adjust else "off"
@@ -264,7 +301,13 @@ def bench_sharded(args, cfg, metric, unit, config):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (blob initial condition, run.cpp:41-46)",
-                "config": cfgd}
+                "config": cfgd,
+                "roofline": {"bound": "hbm", "kernel": "whole step (48 B/DoF)", "achieved": step_gbs,
+                             "peak": peak * world, "peak_kind": peak_kind, "unit": "GB/s",
+                             "frac": step_gbs / (peak * world), "traffic": None},
+                "gpu_launches": launches, "clocks": clk}
+        if e2e:
+            line["e2e"] = e2e
         print(json.dumps(line), flush=True)
     st.close()
     dist.destroy_process_group()
