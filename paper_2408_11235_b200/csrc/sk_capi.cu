@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -1332,7 +1333,7 @@ sk_status sk_run_steps(sk_state* s, int n) {
     CK(cudaSetDevice(c->device));
     // Two loop bodies leave both ping-pong buffers where they started, so a
     // captured pair replays with fixed pointers.
-    if (s->timing) {  // per-phase events: plain enqueue, no graph
+    if (s->timing || getenv("SK_NO_GRAPH")) {  // per-phase events: plain enqueue, no graph
         for (int i = 0; i < n; ++i)
             if (sk_status rc = enq_run_body(s)) return rc;
         return after_launch(c);

@@ -196,11 +196,13 @@ class ShardedState:
             return
         if all(self._step - last < 10 for last in self._last_shrink):
             return
+        # torch's stream (all-reduce, the read below) must follow the check
+        # kernels on the library stream, and phase 4 must follow the all-reduce
+        self.ctx.leave()
         if self.plan.nranks > 1:
-            self.ctx.leave()
             allreduce_shrink_flags(self.flags, self.group)
-            self.ctx.enter()
         fl = self.flags.cpu().tolist()  # the host decides whether halos must move
+        self.ctx.enter()
         if not any(fl):
             return
         for sp in (0, 1):

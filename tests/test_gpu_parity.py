@@ -541,3 +541,34 @@ def test_poisson_cluster_equals_single_cta(sk, k, nf, nc, m):
     assert np.array_equal(Ea, b.E.cpu().numpy())
     assert np.array_equal(pa, b.phi.cpu().numpy())
     assert np.isfinite(Ea).all() and np.abs(Ea).max() > 0
+
+
+def test_sharded_state_one_rank_matches_run_steps(sk):
+    """ShardedState (the torchrun path of bench.py --gpus N) on one NCCL rank
+    against SimulationState.run_steps: same run() loop bodies, including the
+    host-side cut-off protocol (stream ordering of the decision read)"""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2408_11235_b200.sharding import ShardedState
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=1, nv=64, mu=1836.0, limiter="sldg", v_adjust=True)
+    ref = sk.SimulationState(cfg)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        st = ShardedState(cfg, 0, 1, halo=4)
+        for _ in range(23):
+            st.step()
+        ref.run_steps(23)
+        assert ref.shrinks(0)[0] >= 2
+        for sp in (0, 1):
+            assert st.f[sp].vmax() == ref.field(sp).vmax()
+            assert rel(st.f[sp].download(), ref.field(sp).download()) <= 1e-12
+        st.close()
+    finally:
+        dist.destroy_process_group()
