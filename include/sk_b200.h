@@ -195,6 +195,10 @@ sk_status sk_state_download_E(sk_state* s, double* host, size_t count);
  * clear sk_state_shrink_flags_dev) -> caller all-reduces the two int flags
  * (MIN) and, for a species whose flag is set, exchanges
  * sk_state_shrink_halo cells with sk_field_halo_n -> phase 4 (shrink).
+ * With a post limiter (apply_post_limiter), phase 3 stops after
+ * the v sweep: the caller exchanges one-cell halos (sk_field_halo_n, cells 1)
+ * and phase 5 runs post V, the second x half sweep, post X, the step end and
+ * the local cut-off check.
  * Phases 0/1: local initial rho and the Poisson solve of the all-reduced rho
  * (initial field). */
 sk_status sk_state_create_shard(sk_ctx* ctx, const sk_run_config* cfg, int rank, int nranks,

@@ -415,6 +415,8 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     a.nspecies = nspecies;
     a.species0 = nspecies == 2 ? 0 : fs[0]->species;
     a.periodic = periodic;
+    a.gl = fs[0]->gl() > 0 ? 1 : 0;
+    a.gr = fs[0]->gr() > 0 ? 1 : 0;
     std::memcpy(a.tile_start, c->ptiles, sizeof a.tile_start);
     if (dir == SK_DIR_X) {
         CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
@@ -1081,8 +1083,8 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
     *out = nullptr;
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SK_ERR_RUNTIME, "v shard: bad rank");
     if (cfg->v_cells % nranks) return fail(SK_ERR_RUNTIME, "v shard: v_cells must divide by the rank count");
-    if (nranks > 1 && cfg->limiter.indicator)
-        return fail(SK_ERR_RUNTIME, "v shard: post limiters are not supported across ranks yet");
+    if (nranks > 1 && cfg->limiter.indicator && halo < 1)
+        return fail(SK_ERR_RUNTIME, "v shard: post limiters need a v halo of at least one cell");
     if (cfg->k != c->k) return fail(SK_ERR_RUNTIME, "state: degree differs from the context");
     if (!(cfg->dt > 0)) return fail(SK_ERR_RUNTIME, "dt: must be positive");
     if (!(cfg->mu > 0)) return fail(SK_ERR_RUNTIME, "SpeciesParams::ion: mass ratio must be positive");
@@ -1231,7 +1233,8 @@ sk_status enq_phase_a(sk_state* s) {
 }
 
 // phase B: Poisson, v sweep, second x half sweep (rho already global)
-sk_status enq_phase_b(sk_state* s) {
+// phase B, first part: Poisson, v tables, v sweep
+sk_status enq_phase_b1(sk_state* s) {
     sk_ctx* c = s->ctx;
     const sk_limiter* lim = &s->cfg.limiter;
     const int inl = lim->inline_sldg;
@@ -1239,7 +1242,6 @@ sk_status enq_phase_b(sk_state* s) {
     const double dt = s->cfg.dt;
     sk_field* fs[2] = {s->f[0], s->f[1]};
     sk_status rc;
-    const bool post = lim->indicator != 0;
     if ((rc = mark(s, PH_POISSON)) || (rc = enq_poisson(c, s->rho, s->E, s->phi))) return rc;
     if ((rc = mark(s, PH_VTAB)) || (rc = enq_vtab(fs, 2, s->E, dt, s->charge, s->sqrt_mu, inl, thr)))
         return rc;
@@ -1247,6 +1249,18 @@ sk_status enq_phase_b(sk_state* s) {
         FixTimer ft(s, PH_V_FIX);
         if ((rc = mark(s, PH_V)) || (rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;
     }
+    return SK_OK;
+}
+
+// phase B, second part: post limiter V (a v shard exchanges a one-cell halo
+// before it), second x half sweep, post limiter X
+sk_status enq_phase_b2(sk_state* s) {
+    const sk_limiter* lim = &s->cfg.limiter;
+    const int inl = lim->inline_sldg;
+    const double thr = lim->threshold;
+    sk_field* fs[2] = {s->f[0], s->f[1]};
+    sk_status rc;
+    const bool post = lim->indicator != 0;
     if (post && ((rc = mark(s, PH_POST_V)) || (rc = enq_post(fs, 2, SK_DIR_V, lim, 0)))) return rc;
     {
         FixTimer ft(s, PH_X2_FIX);
@@ -1254,6 +1268,11 @@ sk_status enq_phase_b(sk_state* s) {
     }
     if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     return SK_OK;
+}
+
+sk_status enq_phase_b(sk_state* s) {
+    if (sk_status rc = enq_phase_b1(s)) return rc;
+    return enq_phase_b2(s);
 }
 
 // stepper.cpp:44-103 (blob: no source term), all on the context stream.
@@ -1283,6 +1302,19 @@ double* sk_state_rho_dev(sk_state* s) { return s->rho; }
 int* sk_state_shrink_flags_dev(sk_state* s) { return s->ctx->st->shrink_flag; }
 int sk_state_shrink_halo(sk_state* s) { return s->shrink_halo; }
 
+// step end + the local part of the cut-off decision (v-sharded phases)
+static sk_status enq_shard_step_end(sk_state* s) {
+    sk_ctx* c = s->ctx;
+    CK(launch_step_end(c->st, s->cfg.v_adjust, 10, 3, c->stream));
+    c->launches += 1;
+    s->step_host += 1;
+    if (s->cfg.v_adjust) {
+        sk_field* fs[2] = {s->f[0], s->f[1]};
+        return enq_shrink(fs, 2, s->cfg.policy, -2, 1);
+    }
+    return SK_OK;
+}
+
 sk_status sk_state_phase(sk_state* s, int phase) {
     sk_ctx* c = s->ctx;
     CK(cudaSetDevice(c->device));
@@ -1292,14 +1324,16 @@ sk_status sk_state_phase(sk_state* s, int phase) {
         case 1: rc = enq_poisson(c, s->rho, s->E, s->phi); break;
         case 2: rc = enq_phase_a(s); break;
         case 3:
-            if ((rc = enq_phase_b(s))) break;
-            CK(launch_step_end(c->st, s->cfg.v_adjust, 10, 3, c->stream));
-            c->launches += 1;
-            s->step_host += 1;
-            if (s->cfg.v_adjust) {  // local part of the cut-off decision
-                sk_field* fs[2] = {s->f[0], s->f[1]};
-                rc = enq_shrink(fs, 2, s->cfg.policy, -2, 1);
+            // a post-limited shard stops after the v sweep: the caller swaps
+            // one-cell v halos and continues with phase 5
+            if (s->nranks > 1 && s->cfg.limiter.indicator) {
+                rc = enq_phase_b1(s);
+                break;
             }
+            if (!(rc = enq_phase_b(s))) rc = enq_shard_step_end(s);
+            break;
+        case 5:  // post-limited shards: post V, x half sweep, post X, step end, check
+            if (!(rc = enq_phase_b2(s))) rc = enq_shard_step_end(s);
             break;
         case 4:  // shrink with the (all-reduced) decision in sk_state_shrink_flags_dev
             if (s->cfg.v_adjust) {

@@ -1928,10 +1928,12 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
         const double* f = fl ? a.dst[sp] : a.src[sp];
         double* out = fl ? const_cast<double*>(a.src[sp]) : a.dst[sp];
         double um[P], u0[P], up[P];
-        vload<P>(f, a.ld, xd, j0 - 1, 0, a.nv, a.periodic, a.nv, um);
-        vload<P>(f, a.ld, xd, j0, 0, a.nv, a.periodic, a.nv, u0);
+        // a v shard reads one halo cell from each neighbour (zero at the walls)
+        const int lo = -a.gl, hi = a.nv + a.gr;
+        vload<P>(f, a.ld, xd, j0 - 1, lo, hi, a.periodic, a.nv, um);
+        vload<P>(f, a.ld, xd, j0, lo, hi, a.periodic, a.nv, u0);
         for (int j = j0; j < j1; ++j) {
-            vload<P>(f, a.ld, xd, j + 1, 0, a.nv, a.periodic, a.nv, up);
+            vload<P>(f, a.ld, xd, j + 1, lo, hi, a.periodic, a.nv, up);
             double o[P];
             if (post_flag<P>(a.cfg, a.basis, um, u0, up)) {
                 ++flagged;

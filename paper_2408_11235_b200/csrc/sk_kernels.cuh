@@ -183,6 +183,7 @@ struct PostArgs {
     const double* src[2];
     double* dst[2];
     const int* flip[2];
+    int gl, gr;            // readable v halo cells below/above (v shards; 0 at walls)
     PostCfg cfg;
     long long ld;
     int nxd;

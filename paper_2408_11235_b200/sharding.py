@@ -16,8 +16,8 @@ of each species for all x, plus `halo` cells below and above. Then
 
 Plumbing is torch.distributed: NCCL over NVLink/NVSwitch for device buffers,
 gloo for the CPU tests (tests/test_sharding.py drive exactly these functions
-with the C oracle as the per-rank compute). The literature post limiters are
-not sharded yet (the C ABI refuses them).
+with the C oracle as the per-rank compute). The literature post limiters
+exchange one more one-cell halo between the v sweep and post limiter V.
 """
 from __future__ import annotations
 
@@ -153,6 +153,9 @@ class ShardedState:
         # steps on which no species may shrink need no decision round trip
         self._step = 0
         self._last_shrink = [-10, -10]
+        from .solver import LimiterConfig
+
+        self._post = LimiterConfig.parse(cfg.limiter).to_c().indicator != 0
         # initial field: local moment (created) -> all-reduce -> Poisson
         self._reduce_rho()
         self._phase(1)
@@ -219,6 +222,9 @@ class ShardedState:
         self._reduce_rho()
         self._exchange()
         self._phase(3)
+        if self._post and self.plan.nranks > 1:
+            self._exchange(1)  # post limiter V reads one cell across each shard edge
+            self._phase(5)
         self._cutoff()
 
     def close(self):

@@ -418,8 +418,9 @@ def test_cpp_mirror_runs_against_oracle():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("v_adjust", [False, True], ids=["no_cutoff", "cutoff"])
-def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust):
+@pytest.mark.parametrize("v_adjust,limiter", [(False, "sldg"), (True, "sldg"), (True, "minmod+line")],
+                         ids=["no_cutoff", "cutoff", "cutoff_post"])
+def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust, limiter):
     """The CUDA v-shard path (global cell offsets in the x tables, halo reads in
     the v sweep, local fused charge density, sharded velocity cut-off) driven
     like two ranks, with the all-reduces and the halo exchanges done by device
@@ -432,8 +433,9 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust):
     from paper_2408_11235_b200.sharding import VShardPlan, _dev_tensor
     from paper_2408_11235_b200.solver import Context, Grid1D, _check
 
-    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter="sldg", v_adjust=v_adjust)
+    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter=limiter, v_adjust=v_adjust)
     ref = sk.SimulationState(cfg)
+    post = limiter != "sldg"
     L = N.lib()
     grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
                               cfg.refinement_ratio)
@@ -496,6 +498,10 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust):
         exchange()
         for ctx, h, *_ in shards:
             _check(L.sk_state_phase(h, 3))
+        if post:  # post limiter V reads one cell across the shard edge
+            exchange(1)
+            for ctx, h, *_ in shards:
+                _check(L.sk_state_phase(h, 5))
         if v_adjust:
             sync()
             fl = torch.minimum(shards[0][4], shards[1][4])
