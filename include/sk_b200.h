@@ -98,6 +98,11 @@ typedef struct {
     int v_adjust;
     sk_vadjust policy;
     double penalty_scale;
+    /* scenario (config.hpp:11,18): 0 blob (run.cpp:41-46 initial data), 1
+     * injection (zero initial data, neutral source blob(x,v)/t0 for t <= t0
+     * applied as source_half_step before and after the sweeps, stepper.cpp:29-42) */
+    int scenario;
+    double t0;
 } sk_run_config;
 
 /* ---- errors ---- */

@@ -64,6 +64,8 @@ class Oracle(_Lib):
         L = self.lib
         L.sko_last_error.restype = C.c_char_p
         L.sko_state_new.restype = C.c_void_p
+        L.sko_state_set_injection.argtypes = [C.c_void_p, C.c_double]
+        L.sko_state_set_injection.restype = C.c_int
         L.sko_state_new.argtypes = [C.c_double, C.c_double, C.c_int, C.c_double, C.c_double,
                                     C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.c_char_p, C.c_double, C.c_int, C.c_double, C.c_double,
@@ -247,7 +249,7 @@ class Oracle(_Lib):
 def _cfg_args(cfg):
     c = dict(L=200.0, dt=0.1, k=3, mu=400.0, sigma=-1.0, vmax_e=12.0, vmax_i=12.0, nf=50, nc=50,
              m=1, nv=40, limiter="none", limiter_threshold=0.5, v_adjust=1, adapt_p=0.05,
-             adapt_gamma=0.05, adapt_tol=1e-14, penalty_scale=10.0)
+             adapt_gamma=0.05, adapt_tol=1e-14, penalty_scale=10.0, scenario="blob", t0=2000.0)
     unknown = set(cfg) - set(c) - {"threads"}
     if unknown:
         raise KeyError(f"unknown oracle config keys {unknown}")
@@ -293,6 +295,9 @@ class OracleState(_StateBase):
                                         c["adapt_tol"], c["penalty_scale"])
         if not self.h:
             raise RuntimeError(owner.last_error())
+        if c["scenario"] == "injection":
+            if self.lib.sko_state_set_injection(self.h, c["t0"]):
+                raise RuntimeError(owner.last_error())
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -389,6 +394,8 @@ class Ref(_Lib):
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
         L.ref_state_create.restype = C.c_void_p
+        L.ref_state_set_injection.argtypes = [C.c_void_p, C.c_double]
+        L.ref_state_set_injection.restype = C.c_int
         L.ref_state_create.argtypes = [C.c_double, C.c_double, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                                        C.c_int, C.c_char_p, C.c_double, C.c_int, C.c_double,
@@ -522,6 +529,9 @@ class RefState(_StateBase):
                                            c["penalty_scale"], int(threads))
         if not self.h:
             raise RuntimeError(owner.last_error())
+        if c["scenario"] == "injection":
+            if self.lib.ref_state_set_injection(self.h, c["t0"]):
+                raise RuntimeError(owner.last_error())
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -138,6 +138,19 @@ void* ref_state_create(double L, double dt, int k, double mu, double sigma, doub
 
 void ref_state_free(void* hp) { delete static_cast<RefHandle*>(hp); }
 
+// scenario "injection" (config.hpp:11,18; run.cpp:47-53): rebuild the state
+int ref_state_set_injection(void* hp, double t0) {
+    auto* h = static_cast<RefHandle*>(hp);
+    return guarded([&] {
+        h->cfg.scenario = "injection";
+        h->cfg.t0 = t0;
+        h->cfg.validate();
+        h->state = build_initial_state(h->cfg);
+        h->last_shrink_e = h->last_shrink_i = -10;
+        h->shrinks_e = h->shrinks_i = 0;
+    });
+}
+
 // run.cpp:124-131 loop body, including the shrink cadence of run.cpp:98-114.
 int ref_state_step(void* hp) {
     auto* h = static_cast<RefHandle*>(hp);

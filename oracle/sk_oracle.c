@@ -1411,6 +1411,7 @@ int sko_state_init(sko_state* S, double L, double dt, int k, double mu, double s
     if ((rc = field_init(&S->fi, 1, &xg, vmax_i, nv, k))) return rc;
     fill_blob(&S->fe, sigma);
     fill_blob(&S->fi, sigma);
+    S->sigma = sigma;
     S->sqrt_mu_e = 1.0;
     S->charge_e = -1.0;
     if (!(mu > 0)) return fail(SKO_ERR_RUNTIME, "SpeciesParams::ion: mass ratio must be positive");
@@ -1437,6 +1438,44 @@ int sko_state_init(sko_state* S, double L, double dt, int k, double mu, double s
     return SKO_OK;
 }
 
+/* run.cpp:47-51 source.eval: H(t0 - t) blob(x, v) / t0, H(0) = 1 */
+static double source_eval(double t, double x, double v, double t0, double sigma) {
+    if (t > t0) return 0.0;
+    return gaussian_blob(x, v, sigma) / t0;
+}
+
+/* stepper.cpp:29-42; SourceTerm::active (stepper.hpp:19-21): t <= t_end */
+void sko_source_half_step(sko_field* f, double t, double half_dt, double t0, double sigma) {
+    if (!(t <= t0)) return;
+    const int p = f->k + 1;
+    for (int vc = 0; vc < f->v.ncells; ++vc)
+        for (int vn = 0; vn < p; ++vn) {
+            double v = sko_v_node(f, vc, vn);
+            for (int xc = 0; xc < f->x.ncells; ++xc)
+                for (int xn = 0; xn < p; ++xn) {
+                    double x = sko_x_node(f, xc, xn);
+                    f->data[fidx(f, xc, xn, vc, vn)] +=
+                        0.5 * half_dt * (source_eval(t, x, v, t0, sigma) + source_eval(t + half_dt, x, v, t0, sigma));
+                }
+        }
+}
+
+long sko_state_field_size(sko_state* S, int species);
+
+int sko_state_set_injection(sko_state* S, double t0) {
+    if (!(t0 > 0)) return fail(SKO_ERR_RUNTIME, "injection: t0 must be positive");
+    S->injection = 1;
+    S->t0 = t0;
+    memset(S->fe.data, 0, sizeof(double) * (size_t)sko_state_field_size(S, 0));
+    memset(S->fi.data, 0, sizeof(double) * (size_t)sko_state_field_size(S, 1));
+    size_t nE = (size_t)S->fe.x.ncells * (S->fe.k + 1);
+    double* rho = (double*)calloc(nE, sizeof(double));
+    sko_charge_density(&S->fe, &S->fi, rho);
+    sko_poisson_solve(&S->poisson, rho, S->phi, S->E);
+    free(rho);
+    return SKO_OK;
+}
+
 void sko_state_free(sko_state* S) {
     free(S->fe.data);
     free(S->fi.data);
@@ -1445,13 +1484,17 @@ void sko_state_free(sko_state* S) {
     sko_poisson_free(&S->poisson);
 }
 
-/* stepper.cpp:44-103 strang_step (blob: no source) */
+/* stepper.cpp:44-103 strang_step */
 int sko_strang_step(sko_state* S, int max_ghost) {
     const double dt = S->dt;
     if (dt == 0.0) return fail(SKO_ERR_RUNTIME, "strang_step: dt must be nonzero");
     const double half = 0.5 * dt;
     const sko_limiter* lim = &S->limiter;
     int rc;
+    if (S->injection) {
+        sko_source_half_step(&S->fe, S->time, half, S->t0, S->sigma);
+        sko_source_half_step(&S->fi, S->time, half, S->t0, S->sigma);
+    }
 #define POST(dir)                                                                  \
     if (lim->indicator != SKO_IND_NONE) {                                          \
         if ((rc = sko_post_limiter(&S->fe, dir, lim, S->bc, &S->stats))) return rc; \
@@ -1480,6 +1523,10 @@ int sko_strang_step(sko_state* S, int max_ghost) {
         return rc;
     POST(0);
 #undef POST
+    if (S->injection) {
+        sko_source_half_step(&S->fe, S->time + half, half, S->t0, S->sigma);
+        sko_source_half_step(&S->fi, S->time + half, half, S->t0, S->sigma);
+    }
     S->time += dt;
     S->step += 1;
     if (!sko_all_finite(&S->fe) || !sko_all_finite(&S->fi)) {

@@ -202,6 +202,8 @@ typedef struct {
     long last_shrink_e, last_shrink_i;
     int shrinks_e, shrinks_i;
     sko_stats stats;
+    int injection;        /* scenario "injection": neutral source (run.cpp:47-53) */
+    double t0, sigma;     /* source window and width */
 } sko_state;
 /* blob initial state (run.cpp:26-58). Allocates field/E storage. */
 int sko_state_init(sko_state* S, double L, double dt, int k, double mu, double sigma, double vmax_e,
@@ -209,6 +211,12 @@ int sko_state_init(sko_state* S, double L, double dt, int k, double mu, double s
                    double limiter_threshold, int v_adjust, double adapt_p, double adapt_gamma,
                    double adapt_tol, double penalty_scale);
 void sko_state_free(sko_state* S);
+/* switch to the injection scenario (run.cpp:47-53): zero initial fields, the
+ * source S = blob(x, v)/t0 for t <= t0, applied as source_half_step
+ * (stepper.cpp:29-42) before and after the sweeps */
+int sko_state_set_injection(sko_state* S, double t0);
+/* stepper.cpp:29-42 Heun half step of df/dt = S */
+void sko_source_half_step(sko_field* f, double t, double half_dt, double t0, double sigma);
 int sko_strang_step(sko_state* S, int max_ghost);
 /* one run() loop body: ghost width, strang_step, shrink checks (run.cpp:124-131) */
 int sko_run_step(sko_state* S);

@@ -41,7 +41,8 @@ class sk_run_config(C.Structure):
                 ("vmax_e", C.c_double), ("vmax_i", C.c_double), ("k", C.c_int),
                 ("fine_block_cells", C.c_int), ("coarse_block_cells", C.c_int),
                 ("refinement_ratio", C.c_int), ("v_cells", C.c_int), ("limiter", sk_limiter),
-                ("v_adjust", C.c_int), ("policy", sk_vadjust), ("penalty_scale", C.c_double)]
+                ("v_adjust", C.c_int), ("policy", sk_vadjust), ("penalty_scale", C.c_double),
+                ("scenario", C.c_int), ("t0", C.c_double)]
 
 
 _vp, _dp, _ip, _lp = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_long)

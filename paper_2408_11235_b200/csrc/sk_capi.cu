@@ -133,6 +133,8 @@ struct sk_state {
     long long graph_launches = 0;      // kernels per graph replay
     int rank = 0, nranks = 1;          // v-shard of a multi-GPU run
     int shrink_halo = 0;               // halo cells a sharded shrink reads
+    double* src_gx = nullptr;          // injection source tables (SourceArgs)
+    double* src_gv[2] = {nullptr, nullptr};
     // optional per-phase CUDA-event timing (sk_state_set_phase_timing)
     bool timing = false;
     std::vector<std::pair<int, cudaEvent_t>> marks;
@@ -181,6 +183,10 @@ sk_status collect_errors(sk_ctx* c) {
         case 5:
             msg = "step " + std::to_string(step) + ": insufficient v halo: v sweep shifts " +
                   std::to_string(h.err_need) + " cells, shard halo is " + std::to_string(h.err_have);
+            break;
+        case 7:
+            msg = "injection source: more than " + std::to_string(h.err_have) +
+                  " velocity shrinks (host exp tables exhausted)";
             break;
         case 6:
             msg = "step " + std::to_string(step) + ": velocity shrink reads old cell " +
@@ -1021,10 +1027,17 @@ sk_status sk_electric_energy(sk_ctx* c, const double* E, double* out) {
 }
 
 // ---------------------------------------------------------------------------
+namespace {
+sk_status build_source_tables(sk_state* s);  // below (injection scenario)
+}  // namespace
+
 sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
     *out = nullptr;
     if (cfg->k != c->k) return fail(SK_ERR_RUNTIME, "state: degree differs from the context");
     if (!(cfg->dt > 0)) return fail(SK_ERR_RUNTIME, "dt: must be positive");
+    if (cfg->scenario != 0 && cfg->scenario != 1)
+        return fail(SK_ERR_RUNTIME, "scenario: must be blob (0) or injection (1)");
+    if (cfg->scenario == 1 && !(cfg->t0 > 0)) return fail(SK_ERR_RUNTIME, "t0: must be positive");
     if (!(cfg->mu > 0)) return fail(SK_ERR_RUNTIME, "SpeciesParams::ion: mass ratio must be positive");
     if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
     if (cfg->v_adjust)
@@ -1043,7 +1056,9 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         return rc;
     }
     double sigma = cfg->sigma < 0 ? 0.1 * cfg->L : cfg->sigma;  // config.cpp resolve()
-    if ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma))) {
+    // run.cpp:41-53: blob initial data, or (injection) zero data + source tables
+    if (cfg->scenario == 1 ? (rc = build_source_tables(s))
+                           : ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma)))) {
         sk_state_destroy(s);
         return rc;
     }
@@ -1087,6 +1102,9 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
         return fail(SK_ERR_RUNTIME, "v shard: post limiters need a v halo of at least one cell");
     if (cfg->k != c->k) return fail(SK_ERR_RUNTIME, "state: degree differs from the context");
     if (!(cfg->dt > 0)) return fail(SK_ERR_RUNTIME, "dt: must be positive");
+    if (cfg->scenario != 0 && cfg->scenario != 1)
+        return fail(SK_ERR_RUNTIME, "scenario: must be blob (0) or injection (1)");
+    if (cfg->scenario == 1 && !(cfg->t0 > 0)) return fail(SK_ERR_RUNTIME, "t0: must be positive");
     if (!(cfg->mu > 0)) return fail(SK_ERR_RUNTIME, "SpeciesParams::ion: mass ratio must be positive");
     if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
     const int ncell = cfg->v_cells / nranks, cell0 = rank * ncell;
@@ -1122,7 +1140,8 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
     s->f[0]->xhalo = s->f[1]->xhalo = h;
     s->shrink_halo = hs;
     double sigma = cfg->sigma < 0 ? 0.1 * cfg->L : cfg->sigma;
-    if ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma))) {
+    if (cfg->scenario == 1 ? (rc = build_source_tables(s))
+                           : ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma)))) {
         sk_state_destroy(s);
         return rc;
     }
@@ -1164,6 +1183,9 @@ sk_status sk_state_destroy(sk_state* s) {
     cudaStreamSynchronize(s->ctx->stream);
     for (auto& m : s->marks) cudaEventDestroy(m.second);
     for (auto e : s->pool) cudaEventDestroy(e);
+    cudaFree(s->src_gx);
+    cudaFree(s->src_gv[0]);
+    cudaFree(s->src_gv[1]);
     sk_field_destroy(s->f[0]);
     sk_field_destroy(s->f[1]);
     cudaFree(s->E);
@@ -1205,6 +1227,70 @@ struct FixTimer {
 };
 
 
+// injection source tables: x factor per x node, v factor per v node of each
+// v-grid level the cut-off can reach (the host replays shrink_finalize's
+// arithmetic), all with libm exp exactly as run.cpp:19-22 evaluates them
+sk_status build_source_tables(sk_state* s) {
+    sk_ctx* c = s->ctx;
+    const int P = c->P;
+    const Grid& g = c->grid;
+    double sigma = s->cfg.sigma < 0 ? 0.1 * s->cfg.L : s->cfg.sigma;
+    std::vector<double> gx((size_t)g.ncells * P);
+    const double cst = 1.0 / std::sqrt(2.0 * M_PI);
+    for (int xc = 0; xc < g.ncells; ++xc)
+        for (int xn = 0; xn < P; ++xn) {
+            double x = grid_cell_left(g, xc) + grid_cell_width(g, xc) * c->basis.nodes[xn];
+            gx[(size_t)xc * P + xn] = cst * std::exp(-x * x / (2.0 * sigma * sigma));
+        }
+    CK(dalloc(&s->src_gx, gx.size()));
+    CK(cudaMemcpy(s->src_gx, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
+    for (int sp = 0; sp < 2; ++sp) {
+        sk_field* f = s->f[sp];
+        const int nv = f->nv_global, nrows = f->nv * P;
+        const double vmax = sp == 0 ? s->cfg.vmax_e : s->cfg.vmax_i;
+        double left = -vmax, dx = (vmax - left) / nv;  // Grid1D::uniform (grid.cpp:31-34)
+        std::vector<double> gv((size_t)kSourceLevels * nrows);
+        for (int lev = 0; lev < kSourceLevels; ++lev) {
+            for (int vc = 0; vc < f->nv; ++vc)
+                for (int vn = 0; vn < P; ++vn) {
+                    double v = (left + (vc + f->cell0) * dx) + dx * c->basis.nodes[vn];
+                    gv[(size_t)lev * nrows + (size_t)vc * P + vn] = std::exp(-v * v / 2.0);
+                }
+            // shrink_finalize_kernel (adaptivity.cpp:103-104)
+            const double vmax_before = left + nv * dx;
+            const double new_vmax = vmax_before * (1.0 - s->cfg.policy.p);
+            left = -new_vmax;
+            dx = (new_vmax - (-new_vmax)) / nv;
+        }
+        CK(dalloc(&s->src_gv[sp], gv.size()));
+        CK(cudaMemcpy(s->src_gv[sp], gv.data(), sizeof(double) * gv.size(), cudaMemcpyHostToDevice));
+    }
+    return SK_OK;
+}
+
+sk_status enq_source(sk_state* s, int second) {
+    if (s->cfg.scenario != 1) return SK_OK;
+    sk_ctx* c = s->ctx;
+    SourceArgs a{};
+    for (int sp = 0; sp < 2; ++sp) {
+        a.f[sp] = s->f[sp]->cur_ptr();
+        a.alt[sp] = s->f[sp]->other_ptr();
+        a.flip[sp] = s->f[sp]->dflip;
+        a.gv[sp] = s->src_gv[sp];
+    }
+    a.gx = s->src_gx;
+    a.nrows = s->f[0]->nv * c->P;
+    a.nxd = c->grid.ncells * c->P;
+    a.ld = a.nxd;
+    a.st = c->st;
+    a.half = 0.5 * s->cfg.dt;
+    a.t0 = s->cfg.t0;
+    a.second = second;
+    CK(launch_source(a, c->stream));
+    c->launches += 1;
+    return SK_OK;
+}
+
 // phase A: x tables + first x half sweep (+ fused local charge density)
 sk_status enq_phase_a(sk_state* s) {
     sk_ctx* c = s->ctx;
@@ -1215,6 +1301,8 @@ sk_status enq_phase_a(sk_state* s) {
     sk_field* fs[2] = {s->f[0], s->f[1]};
     sk_status rc;
     const bool post = lim->indicator != 0;
+    // stepper.cpp:68-72 (injection): source half step at state.time
+    if ((rc = enq_source(s, 0))) return rc;
     // x tables serve both x half-sweeps (same tau, same v grid within a step)
     if ((rc = mark(s, PH_XTAB)) || (rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1)))
         return rc;
@@ -1267,7 +1355,8 @@ sk_status enq_phase_b2(sk_state* s) {
         if ((rc = mark(s, PH_X2)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
     }
     if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
-    return SK_OK;
+    // stepper.cpp:93-97 (injection): source half step at state.time + half
+    return enq_source(s, 1);
 }
 
 sk_status enq_phase_b(sk_state* s) {
@@ -1285,7 +1374,7 @@ sk_status enq_run_body(sk_state* s) {
     sk_ctx* c = s->ctx;
     if (sk_status rc = enq_strang(s)) return rc;
     if (sk_status rc = mark(s, PH_SHRINK)) return rc;
-    CK(launch_step_end(c->st, s->cfg.v_adjust, 10, 3, c->stream));
+    CK(launch_step_end(c->st, s->cfg.dt, s->cfg.v_adjust, 10, 3, c->stream));
     c->launches += 1;
     if (s->cfg.v_adjust) {
         sk_field* fs[2] = {s->f[0], s->f[1]};
@@ -1305,7 +1394,7 @@ int sk_state_shrink_halo(sk_state* s) { return s->shrink_halo; }
 // step end + the local part of the cut-off decision (v-sharded phases)
 static sk_status enq_shard_step_end(sk_state* s) {
     sk_ctx* c = s->ctx;
-    CK(launch_step_end(c->st, s->cfg.v_adjust, 10, 3, c->stream));
+    CK(launch_step_end(c->st, s->cfg.dt, s->cfg.v_adjust, 10, 3, c->stream));
     c->launches += 1;
     s->step_host += 1;
     if (s->cfg.v_adjust) {
@@ -1351,7 +1440,7 @@ sk_status sk_strang_step(sk_state* s) {
     sk_ctx* c = s->ctx;
     CK(cudaSetDevice(c->device));
     if (sk_status rc = enq_strang(s)) return rc;
-    CK(launch_step_end(c->st, 0, 10, 0, c->stream));
+    CK(launch_step_end(c->st, s->cfg.dt, 0, 10, 0, c->stream));
     s->step_host += 1;
     return after_launch(c);
 }

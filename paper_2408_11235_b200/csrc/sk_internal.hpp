@@ -53,6 +53,7 @@ struct DevStatus {
     double vmax_before[2];        // of the last shrink
     int nonfinite;
     int pad;
+    double time;                  // state.time (stepper.cpp:98), advanced at each step end
 };
 
 // Host-side reference-cell constants (bitwise equal to basis.cpp).

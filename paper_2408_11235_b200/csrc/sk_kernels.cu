@@ -1597,7 +1597,8 @@ __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constan
 // step end: step counter, nonfinite -> SimulationError (stepper.cpp:99-102),
 // shrink cooldown gate (run.cpp:98-101)
 // ---------------------------------------------------------------------------
-__global__ void step_end_kernel(DevStatus* st, int v_adjust, long long cooldown, int mask) {
+__global__ void step_end_kernel(DevStatus* st, double dt, int v_adjust, long long cooldown, int mask) {
+    st->time += dt;  // stepper.cpp:98
     st->step += 1;
     if (st->nonfinite) raise_error(st, 2, 3, 0, 0, st->step);
     for (int sp = 0; sp < 2; ++sp)
@@ -2319,9 +2320,44 @@ cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double
     return cudaGetLastError();
 }
 
-cudaError_t launch_step_end(DevStatus* st, int v_adjust, long long cooldown, int mask,
+cudaError_t launch_step_end(DevStatus* st, double dt, int v_adjust, long long cooldown, int mask,
                             cudaStream_t s) {
-    step_end_kernel<<<1, 1, 0, s>>>(st, v_adjust, cooldown, mask);
+    step_end_kernel<<<1, 1, 0, s>>>(st, dt, v_adjust, cooldown, mask);
+    return cudaGetLastError();
+}
+
+// stepper.cpp:29-42 source_half_step with run.cpp:47-53's source: per node
+// f += (0.5 half) (S(t) + S(t + half)), S = H(t0 - t) blob(x, v) / t0. The
+// exponentials come from host tables (libm, as the reference computes them),
+// indexed by the species' v-grid level (its shrink count), so the increment
+// is bitwise the reference's.
+__global__ void source_kernel(const __grid_constant__ SourceArgs a) {
+    const int sp = blockIdx.y;
+    const double t = a.second ? a.st->time + a.half : a.st->time;
+    if (!(t <= a.t0)) return;  // SourceTerm::active (stepper.hpp:19-21)
+    const int lev = a.st->shrink_count[sp];
+    if (lev >= kSourceLevels) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) raise_error(a.st, 1, 7, lev, kSourceLevels, a.st->step);
+        return;
+    }
+    const double t2 = t + a.half;
+    double* f = field_flipped(a.flip[sp]) ? a.alt[sp] : a.f[sp];
+    const double* gv = a.gv[sp] + (long long)lev * a.nrows;
+    const double w = 0.5 * a.half;
+    const long long total = (long long)a.nrows * a.ld;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const long long r = i / a.ld;
+        const int xd = (int)(i - r * a.ld);
+        const double blob = a.gx[xd] * gv[r];  // run.cpp:19-22
+        const double s1 = t > a.t0 ? 0.0 : blob / a.t0;
+        const double s2 = t2 > a.t0 ? 0.0 : blob / a.t0;
+        f[i] = f[i] + w * (s1 + s2);
+    }
+}
+
+cudaError_t launch_source(const SourceArgs& a, cudaStream_t s) {
+    source_kernel<<<dim3(sm_count() * 8, 2), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -212,7 +212,23 @@ cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, d
 cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s);
 cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double* E, double* phi,
                                  cudaStream_t s);
-cudaError_t launch_step_end(DevStatus* st, int v_adjust, long long cooldown, int species_mask,
+// injection source half step (stepper.cpp:29-42), both species
+constexpr int kSourceLevels = 48;  // v-grid levels (velocity shrinks) with host-built exp tables
+struct SourceArgs {
+    double* f[2];
+    double* alt[2];
+    const int* flip[2];
+    const double* gx;     // [nxd]: (2 pi)^-1/2 exp(-x^2 / (2 sigma^2)) at the x nodes
+    const double* gv[2];  // [kSourceLevels][nrows]: exp(-v^2/2) at the v nodes of each v-grid level
+    int nrows, nxd;
+    long long ld;
+    DevStatus* st;
+    double half, t0;
+    int second;           // 0: source at state.time, 1: at state.time + half
+};
+cudaError_t launch_source(const SourceArgs& a, cudaStream_t s);
+
+cudaError_t launch_step_end(DevStatus* st, double dt, int v_adjust, long long cooldown, int species_mask,
                             cudaStream_t s);
 cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s);
 cudaError_t launch_diag(const DiagArgs& a, double* out4, double* partial, cudaStream_t s);

@@ -158,6 +158,7 @@ class RunConfig:
     """config.hpp:11-41 (defaults) -- the keys that shape the step."""
 
     scenario: str = "blob"
+    t0: float = 2000.0  # injection source window (config.hpp:18)
     L: float = 200.0
     dt: float = 0.1
     k: int = 3
@@ -195,12 +196,11 @@ class RunConfig:
                     limiter=self.limiter, limiter_threshold=self.limiter_threshold,
                     v_adjust=int(self.v_adjust), adapt_p=self.adapt_p,
                     adapt_gamma=self.adapt_gamma, adapt_tol=self.adapt_tol,
-                    penalty_scale=self.penalty_scale)
+                    penalty_scale=self.penalty_scale, scenario=self.scenario, t0=self.t0)
 
     def to_c(self) -> N.sk_run_config:
-        if self.scenario != "blob":
-            raise RuntimeError("scenario: only 'blob' is on the B200 path (injection source "
-                               "term is SURVEY.md §8f N2)")
+        if self.scenario not in ("blob", "injection"):
+            raise RuntimeError("RunConfig: scenario must be blob or injection")
         lim = LimiterConfig.parse(self.limiter)
         lim.threshold = self.limiter_threshold
         c = N.sk_run_config()
@@ -212,6 +212,8 @@ class RunConfig:
         c.v_adjust = int(self.v_adjust)
         c.policy = N.sk_vadjust(self.adapt_p, self.adapt_gamma, self.adapt_tol)
         c.penalty_scale = self.penalty_scale
+        c.scenario = 1 if self.scenario == "injection" else 0
+        c.t0 = self.t0
         return c
 
 

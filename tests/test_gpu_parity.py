@@ -578,3 +578,31 @@ def test_sharded_state_one_rank_matches_run_steps(sk):
         st.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
+@pytest.mark.parametrize("kw", [
+    dict(k=2, nf=8, nc=16, m=2, nv=32, limiter="sldg", scenario="injection", t0=0.35),
+    dict(k=3, nf=16, nc=32, m=1, nv=48, mu=1836.0, limiter="sldg", scenario="injection", t0=1.05),
+    dict(k=3, nf=6, nc=12, m=1, nv=24, mu=1836.0, limiter="minmod+line", scenario="injection", t0=0.8)],
+    ids=["k2_m2", "k3_mu1836", "k3_post"])
+def test_injection_scenario(sk, ora, kw, exact):
+    """§8f N2: the injection source half steps on the device (host exp tables
+    per v-grid level) -- bitwise trajectories in exact mode, 1e-12 in fast
+    mode -- across the source window's end and velocity shrinks"""
+    cfg = cfg_of(sk, **kw)
+    o = ora.state(**cfg.oracle_kwargs())
+    st = sk.SimulationState(cfg, exact=exact)
+    for sp in (0, 1):
+        assert not st.field(sp).download().any()
+    for s in range(14):
+        o.step()
+        st.run_step()
+        for sp in (0, 1):
+            got, want = st.field(sp).download(), o.field(sp)
+            if exact:
+                assert np.array_equal(got, want), f"step {s + 1} species {sp}"
+            else:
+                assert rel(got, want) <= F_TOL, f"step {s + 1} species {sp}"
+            assert st.field(sp).vmax() == o.vmax(sp)
+    assert st.shrinks(0)[0] >= 2
