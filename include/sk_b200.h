@@ -185,6 +185,27 @@ sk_status sk_field_moments(sk_field* f, double* out4);
 /* electric_energy (diagnostics.cpp:71-83) of E_dev; synchronises */
 sk_status sk_electric_energy(sk_ctx* ctx, const double* E_dev, double* out);
 
+/* FluxSample (diagnostics.hpp:24-32) */
+typedef struct {
+    double t;
+    double je_plus, je_minus, ji_plus, ji_minus, je_naive, ji_naive;
+    double mass_e, mass_i, e_energy, vmax_e, vmax_i;
+} sk_flux_sample;
+
+/* Summary (diagnostics.hpp:34-40) */
+typedef struct {
+    double mass_e, mass_i, charge, l2_e, l2_i, e_energy, vmax_e, vmax_i;
+} sk_summary;
+
+/* RunResult subset (run.hpp:20-33) */
+typedef struct {
+    int exit_code;          /* 0 ok, 1 SimulationError (message in sk_last_error) */
+    long steps_done;
+    long shrinks_e, shrinks_i;
+    double wall_seconds;
+    sk_stats stats;
+} sk_run_result;
+
 /* ---- state + step: build_initial_state (run.cpp:26-58), strang_step
  *      (stepper.cpp:44-103), run() loop body (run.cpp:124-131) ---- */
 sk_status sk_state_create(sk_ctx* ctx, const sk_run_config* cfg, sk_state** out);
@@ -212,6 +233,29 @@ double* sk_state_rho_dev(sk_state* s);
 int* sk_state_shrink_flags_dev(sk_state* s); /* int[2], device: 1 = shrink this step */
 int sk_state_shrink_halo(sk_state* s);        /* halo cells a sharded shrink reads */
 sk_status sk_state_phase(sk_state* s, int phase);
+/* ---- diagnostics and output (diagnostics.cpp, run.cpp:60-169).
+ * Single-GPU states; all synchronise. */
+/* state.time (stepper.cpp:98) */
+sk_status sk_state_time(sk_state* s, double* t);
+/* wall_flux (diagnostics.cpp:24-69): side 0 left, 1 right; bitwise the
+ * reference's (boundary cells downloaded, the reference's loop on the host) */
+sk_status sk_state_wall_flux(sk_state* s, int species, int side, double* outflow, double* naive);
+/* sample_fluxes (diagnostics.cpp:98-116); masses from the device reduction */
+sk_status sk_state_sample_fluxes(sk_state* s, sk_flux_sample* out);
+/* summarize (diagnostics.cpp:85-96) */
+sk_status sk_state_summarize(sk_state* s, sk_summary* out);
+/* OutputWriter::write_snapshot (diagnostics.cpp:161-194): dir/snapshot_<step>.bin
+ * (SOLKSNP1 layout) + .meta, byte-compatible with the reference's files */
+sk_status sk_state_write_snapshot(sk_state* s, const char* dir);
+/* OutputWriter::write_profiles (diagnostics.cpp:196-220): dir/profiles_<step>.csv */
+sk_status sk_state_write_profiles(sk_state* s, const char* dir);
+/* run() (run.cpp:60-169): nsteps run() loop bodies with a flux.csv row every
+ * `cadence` steps (and at step 0), snapshots / profiles at their cadences (0:
+ * off), run.log, into out_dir (NULL: no files). The steps between samples run
+ * as CUDA-graph replays. */
+sk_status sk_run(sk_ctx* ctx, const sk_run_config* cfg, long nsteps, int cadence, int snapshot_cadence,
+                 int profile_cadence, const char* out_dir, sk_run_result* out);
+
 /* one strang_step (no shrink); max_ghost < 0: run()'s rule */
 sk_status sk_strang_step(sk_state* s);
 /* one run() loop body: strang_step + shrink checks with the 10-step cooldown */

@@ -396,6 +396,14 @@ class Ref(_Lib):
         L.ref_state_create.restype = C.c_void_p
         L.ref_state_set_injection.argtypes = [C.c_void_p, C.c_double]
         L.ref_state_set_injection.restype = C.c_int
+        L.ref_state_wall_flux.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        L.ref_state_wall_flux.restype = C.c_int
+        L.ref_state_time.argtypes = [C.c_void_p]
+        L.ref_state_time.restype = C.c_double
+        L.ref_state_write_snapshot.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_state_write_snapshot.restype = C.c_int
+        L.ref_run_files.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_char_p]
+        L.ref_run_files.restype = C.c_int
         L.ref_state_create.argtypes = [C.c_double, C.c_double, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                                        C.c_int, C.c_char_p, C.c_double, C.c_int, C.c_double,
@@ -537,6 +545,25 @@ class RefState(_StateBase):
         if getattr(self, "h", None):
             self.lib.ref_state_free(self.h)
             self.h = None
+
+    def wall_flux(self, species, side):
+        out = (C.c_double * 2)()
+        if self.lib.ref_state_wall_flux(self.h, species, side, out):
+            raise RuntimeError(self.owner.last_error())
+        return out[0], out[1]
+
+    def time(self):
+        return self.lib.ref_state_time(self.h)
+
+    def write_snapshot(self, directory):
+        if self.lib.ref_state_write_snapshot(self.h, str(directory).encode()):
+            raise RuntimeError(self.owner.last_error())
+
+    def run_files(self, t_final, cadence, snapshot_cadence, profile_cadence, directory):
+        """the reference's run() with files for this configuration (fresh state)"""
+        if self.lib.ref_run_files(self.h, t_final, cadence, snapshot_cadence, profile_cadence,
+                                  str(directory).encode()):
+            raise RuntimeError(self.owner.last_error())
 
     def _check(self, rc):
         if rc:

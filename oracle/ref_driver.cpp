@@ -138,6 +138,39 @@ void* ref_state_create(double L, double dt, int k, double mu, double sigma, doub
 
 void ref_state_free(void* hp) { delete static_cast<RefHandle*>(hp); }
 
+// diagnostics of the live state (diagnostics.cpp)
+int ref_state_wall_flux(void* hp, int species, int side, double* out2) {
+    auto* h = static_cast<RefHandle*>(hp);
+    return guarded([&] {
+        WallFlux w = wall_flux(field_of(h, species), side == 1 ? WallSide::Right : WallSide::Left);
+        out2[0] = w.outflow;
+        out2[1] = w.naive;
+    });
+}
+double ref_state_time(void* hp) { return static_cast<RefHandle*>(hp)->state.time; }
+int ref_state_write_snapshot(void* hp, const char* dir) {
+    auto* h = static_cast<RefHandle*>(hp);
+    return guarded([&] {
+        OutputWriter w(dir);
+        w.write_snapshot(h->state.step, h->state.time, h->state.f_e, h->state.f_i);
+    });
+}
+// run() with files (run.cpp:60-169) for this handle's configuration
+int ref_run_files(void* hp, double t_final, int cadence, int snapshot_cadence, int profile_cadence,
+                  const char* dir) {
+    auto* h = static_cast<RefHandle*>(hp);
+    return guarded([&] {
+        RunConfig c = h->cfg;
+        c.t_final = t_final;
+        c.cadence = cadence;
+        c.snapshot_cadence = snapshot_cadence;
+        c.profile_cadence = profile_cadence;
+        c.out_dir = dir;
+        RunResult r = run(c, true);
+        if (r.exit_code) throw std::runtime_error(r.error);
+    });
+}
+
 // scenario "injection" (config.hpp:11,18; run.cpp:47-53): rebuild the state
 int ref_state_set_injection(void* hp, double t0) {
     auto* h = static_cast<RefHandle*>(hp);

@@ -27,6 +27,11 @@ class sk_stats(C.Structure):
                                             "post_troubled")]
 
 
+class sk_run_result(C.Structure):
+    _fields_ = [("exit_code", C.c_int), ("steps_done", C.c_long), ("shrinks_e", C.c_long),
+                ("shrinks_i", C.c_long), ("wall_seconds", C.c_double), ("stats", sk_stats)]
+
+
 class sk_vadjust(C.Structure):
     _fields_ = [("p", C.c_double), ("gamma", C.c_double), ("tol", C.c_double)]
 
@@ -34,6 +39,16 @@ class sk_vadjust(C.Structure):
 class sk_shrink_result(C.Structure):
     _fields_ = [("vmax_before", C.c_double), ("vmax_after", C.c_double),
                 ("mass_before", C.c_double), ("mass_after", C.c_double)]
+
+
+class sk_flux_sample(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("t", "je_plus", "je_minus", "ji_plus", "ji_minus", "je_naive",
+                                          "ji_naive", "mass_e", "mass_i", "e_energy", "vmax_e", "vmax_i")]
+
+
+class sk_summary(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("mass_e", "mass_i", "charge", "l2_e", "l2_i", "e_energy",
+                                          "vmax_e", "vmax_i")]
 
 
 class sk_run_config(C.Structure):
@@ -100,6 +115,13 @@ SIGNATURES = {
     "sk_state_step_index": (_i, [_vp, _lp]),
     "sk_state_shrinks": (_i, [_vp, _i, _ip, _lp]),
     "sk_run_step_host": (_i, [_vp, _dp, _dp, _sz]),
+    "sk_state_time": (_i, [_vp, _dp]),
+    "sk_state_wall_flux": (_i, [_vp, _i, _i, _dp, _dp]),
+    "sk_state_sample_fluxes": (_i, [_vp, C.POINTER(sk_flux_sample)]),
+    "sk_state_summarize": (_i, [_vp, C.POINTER(sk_summary)]),
+    "sk_state_write_snapshot": (_i, [_vp, C.c_char_p]),
+    "sk_state_write_profiles": (_i, [_vp, C.c_char_p]),
+    "sk_run": (_i, [_vp, C.POINTER(sk_run_config), C.c_long, _i, _i, _i, C.c_char_p, C.POINTER(sk_run_result)]),
     "sk_state_set_phase_timing": (_i, [_vp, _i]),
     "sk_state_phase_times": (_i, [_vp, _dp, _lp, _i]),
     "sk_ctx_launch_count": (C.c_longlong, [_vp]),

@@ -11,7 +11,10 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <chrono>
+#include <cstdint>
 #include <string>
+#include <sys/stat.h>
 #include <vector>
 
 #include "../../include/sk_b200.h"
@@ -1549,6 +1552,364 @@ sk_status sk_run_step_host(sk_state* s, double* fe, double* fi, size_t count) {
     if (sk_status rc = sk_field_download_async(s->f[0], fe, count)) return rc;
     if (sk_status rc = sk_field_download_async(s->f[1], fi, count)) return rc;
     return collect_errors(c);
+}
+
+
+// ---------------------------------------------------------------------------
+// diagnostics + output (diagnostics.cpp, run.cpp:60-169), SURVEY.md §8f N3
+// ---------------------------------------------------------------------------
+namespace {
+
+std::string g17(double v) {
+    char buf[32];
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return buf;
+}
+
+// basis.cpp:123-134 evaluate (second barycentric form), runtime degree
+double host_evaluate(const Basis& b, const double* u, double xi) {
+    double num = 0.0, den = 0.0;
+    for (int n = 0; n < b.p; ++n) {
+        if (xi == b.nodes[n]) return u[n];
+        double t = b.bary[n] / (xi - b.nodes[n]);
+        num += t * u[n];
+        den += t;
+    }
+    return num / den;
+}
+
+// the P x-node columns of boundary cell xc for every v row, from the live buffer
+sk_status download_wall_cells(sk_field* f, int xc, std::vector<double>& out) {
+    sk_ctx* c = f->ctx;
+    const int P = c->P;
+    const size_t ld = (size_t)c->grid.ncells * P, rows = (size_t)f->nv * P;
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    out.resize(rows * P);
+    CK(cudaMemcpy2DAsync(out.data(), sizeof(double) * P, live + (size_t)xc * P, sizeof(double) * ld,
+                         sizeof(double) * P, rows, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
+
+// diagnostics.cpp:24-69, operation for operation
+sk_status wall_flux(sk_field* f, int side, double* outflow, double* naive) {
+    sk_ctx* c = f->ctx;
+    const Basis& basis = c->basis;
+    const int p = c->P, nv = f->nv;
+    const int xc = side == 1 ? c->grid.ncells - 1 : 0;
+    const double edge = side == 1 ? 1.0 : 0.0;
+    std::vector<double> wc;
+    if (sk_status rc = download_wall_cells(f, xc, wc)) return rc;
+    std::vector<double> tx(p);
+    for (int n = 0; n < p; ++n) tx[n] = host_lagrange(basis, n, edge);
+    std::vector<double> fw((size_t)nv * p, 0.0);
+    for (int vc = 0; vc < nv; ++vc)
+        for (int vn = 0; vn < p; ++vn) {
+            double acc = 0.0;
+            for (int xn = 0; xn < p; ++xn) acc += tx[xn] * wc[((size_t)vc * p + vn) * p + xn];
+            fw[(size_t)vc * p + vn] = acc;
+        }
+    double left, dv;
+    int cells;
+    if (sk_status rc = sk_field_v_grid(f, &left, &dv, &cells)) return rc;
+    double o = 0.0, nv_ = 0.0;
+    for (int vc = 0; vc < nv; ++vc) {
+        double a = left + vc * dv, b = a + dv;
+        const double* cell = fw.data() + (size_t)vc * p;
+        for (int q = 0; q < p; ++q) {
+            double vq = a + dv * basis.nodes[q];
+            nv_ += basis.weights[q] * dv * vq * cell[q];
+        }
+        double lo = a, hi = b;
+        if (side == 1)
+            lo = std::max(a, 0.0);
+        else
+            hi = std::min(b, 0.0);
+        if (hi <= lo) continue;
+        double len = hi - lo;
+        for (int q = 0; q < p; ++q) {
+            double vq = lo + len * basis.nodes[q];
+            double fv = host_evaluate(basis, cell, (vq - a) / dv);
+            o += basis.weights[q] * len * std::abs(vq) * fv;
+        }
+    }
+    *outflow = o;
+    *naive = nv_;
+    return SK_OK;
+}
+
+double field_vmax(sk_field* f) {
+    double left = 0, dx = 0;
+    int cells = 0;
+    sk_field_v_grid(f, &left, &dx, &cells);
+    return left + cells * dx;  // Grid1D::right (grid.cpp:48-51)
+}
+
+sk_status write_file(const std::string& path, const std::string& text) {
+    std::FILE* fp = std::fopen(path.c_str(), "w");
+    if (!fp) return fail(SK_ERR_RUNTIME, "cannot open '" + path + "' for writing");
+    bool ok = std::fwrite(text.data(), 1, text.size(), fp) == text.size();
+    ok = (std::fclose(fp) == 0) && ok;
+    return ok ? SK_OK : fail(SK_ERR_RUNTIME, "write failed on '" + path + "'");
+}
+
+const char* species_name(int sp) { return sp == 0 ? "electron" : "ion"; }
+
+}  // namespace
+
+sk_status sk_state_time(sk_state* s, double* t) {
+    if (sk_status rc = collect_errors(s->ctx)) return rc;
+    *t = s->ctx->st_host->time;
+    return SK_OK;
+}
+
+sk_status sk_state_wall_flux(sk_state* s, int species, int side, double* outflow, double* naive) {
+    if (s->nranks > 1) return fail(SK_ERR_RUNTIME, "wall_flux: single-GPU states only");
+    CK(cudaSetDevice(s->ctx->device));
+    return wall_flux(s->f[species & 1], side, outflow, naive);
+}
+
+sk_status sk_state_sample_fluxes(sk_state* s, sk_flux_sample* o) {
+    if (s->nranks > 1) return fail(SK_ERR_RUNTIME, "sample_fluxes: single-GPU states only");
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    std::memset(o, 0, sizeof *o);
+    if (sk_status rc = sk_state_time(s, &o->t)) return rc;
+    double dummy, m4[4];
+    sk_status rc;
+    if ((rc = wall_flux(s->f[0], 1, &o->je_plus, &o->je_naive)) ||
+        (rc = wall_flux(s->f[0], 0, &o->je_minus, &dummy)) ||
+        (rc = wall_flux(s->f[1], 1, &o->ji_plus, &o->ji_naive)) ||
+        (rc = wall_flux(s->f[1], 0, &o->ji_minus, &dummy)))
+        return rc;
+    if ((rc = moments(s->f[0], m4))) return rc;
+    o->mass_e = m4[0];
+    if ((rc = moments(s->f[1], m4))) return rc;
+    o->mass_i = m4[0];
+    if ((rc = sk_electric_energy(c, s->E, &o->e_energy))) return rc;
+    o->vmax_e = field_vmax(s->f[0]);
+    o->vmax_i = field_vmax(s->f[1]);
+    return SK_OK;
+}
+
+sk_status sk_state_summarize(sk_state* s, sk_summary* o) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    double m4[4];
+    sk_status rc;
+    if ((rc = moments(s->f[0], m4))) return rc;
+    o->mass_e = m4[0];
+    o->l2_e = m4[1];
+    if ((rc = moments(s->f[1], m4))) return rc;
+    o->mass_i = m4[0];
+    o->l2_i = m4[1];
+    o->charge = o->mass_i - o->mass_e;
+    if ((rc = sk_electric_energy(c, s->E, &o->e_energy))) return rc;
+    o->vmax_e = field_vmax(s->f[0]);
+    o->vmax_i = field_vmax(s->f[1]);
+    return SK_OK;
+}
+
+sk_status sk_state_write_snapshot(sk_state* s, const char* dir) {
+    if (s->nranks > 1) return fail(SK_ERR_RUNTIME, "write_snapshot: single-GPU states only");
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    long step = 0;
+    double time = 0;
+    if (sk_status rc = sk_state_step_index(s, &step)) return rc;
+    if (sk_status rc = sk_state_time(s, &time)) return rc;
+    const std::string base = std::string(dir) + "/snapshot_" + std::to_string(step);
+    std::FILE* fp = std::fopen((base + ".bin").c_str(), "wb");
+    if (!fp) return fail(SK_ERR_RUNTIME, "cannot open '" + base + ".bin' for writing");
+    const char magic[8] = {'S', 'O', 'L', 'K', 'S', 'N', 'P', '1'};
+    std::fwrite(magic, 1, 8, fp);
+    int64_t step64 = step;
+    std::fwrite(&step64, sizeof(int64_t), 1, fp);
+    std::fwrite(&time, sizeof(double), 1, fp);
+    int32_t nspecies = 2;
+    std::fwrite(&nspecies, sizeof(int32_t), 1, fp);
+    const Grid& g = c->grid;
+    const int p = c->P, nx = g.ncells;
+    std::string meta = "snapshot " + std::to_string(step) + " at t=" + g17(time) + "\n";
+    meta += "layout: magic[8]='SOLKSNP1', int64 step, double time, int32 nspecies\n";
+    meta += "per species: int32 k, int32 nx_cells, int32 nv_cells,\n";
+    meta += "  double x_edges[nx_cells+1], double v_edges[nv_cells+1],\n";
+    meta += "  double values[nx_cells*(k+1)*nv_cells*(k+1)] row-major in\n";
+    meta += "  (x_cell, x_node, v_cell, v_node); nodes are Gauss-Legendre on each cell\n";
+    meta += "species order: electron, ion\n";
+    bool ok = true;
+    for (int sp = 0; sp < 2; ++sp) {  // diagnostics.cpp:140-159 write_species_block
+        sk_field* f = s->f[sp];
+        const int nv = f->nv;
+        int32_t header[3] = {c->k, nx, nv};
+        std::fwrite(header, sizeof(int32_t), 3, fp);
+        std::vector<double> xe, ve;
+        for (int i = 0; i < nx; ++i) xe.push_back(grid_cell_left(g, i));
+        xe.push_back(grid_right(g));
+        double vl, vdx;
+        int vcells;
+        if (sk_status rc = sk_field_v_grid(f, &vl, &vdx, &vcells)) {
+            std::fclose(fp);
+            return rc;
+        }
+        for (int i = 0; i < nv; ++i) ve.push_back(vl + i * vdx);
+        ve.push_back(vl + nv * vdx);
+        std::fwrite(xe.data(), sizeof(double), xe.size(), fp);
+        std::fwrite(ve.data(), sizeof(double), ve.size(), fp);
+        std::vector<double> h(f->n), t(f->n);
+        if (sk_status rc = sk_field_download(f, h.data(), f->n)) {
+            std::fclose(fp);
+            return rc;
+        }
+        // device layout ((vc*p+vn)*nx+xc)*p+xn -> (xc, xn, vc, vn)
+        const size_t ld = (size_t)nx * p, rows = (size_t)nv * p;
+        for (size_t r = 0; r < rows; ++r)
+            for (size_t xd = 0; xd < ld; ++xd) t[xd * rows + r] = h[r * ld + xd];
+        ok = std::fwrite(t.data(), sizeof(double), t.size(), fp) == t.size() && ok;
+        meta += std::string(species_name(sp)) + ": k=" + std::to_string(c->k) + " nx=" + std::to_string(nx) +
+                " nv=" + std::to_string(nv) + " x=[" + g17(g.left[0]) + "," + g17(grid_right(g)) + "]" +
+                " v=[" + g17(vl) + "," + g17(vl + nv * vdx) + "]\n";
+    }
+    ok = (std::fclose(fp) == 0) && ok;
+    if (!ok) return fail(SK_ERR_RUNTIME, "write failed on '" + base + ".bin'");
+    return write_file(std::string(dir) + "/snapshot_" + std::to_string(step) + ".meta", meta);
+}
+
+sk_status sk_state_write_profiles(sk_state* s, const char* dir) {
+    if (s->nranks > 1) return fail(SK_ERR_RUNTIME, "write_profiles: single-GPU states only");
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    long step = 0;
+    if (sk_status rc = sk_state_step_index(s, &step)) return rc;
+    const Grid& g = c->grid;
+    const int p = c->P, nx = g.ncells;
+    const size_t ne = (size_t)nx * p;
+    double* drho = nullptr;
+    CK(dalloc(&drho, ne));
+    sk_status rc = enq_rho(s->f[0], s->f[1], drho);  // charge_density(f_e, f_i)
+    std::vector<double> rho(ne), E(ne), phi((size_t)nx * (p + 1));
+    if (!rc) {
+        CK(cudaMemcpyAsync(rho.data(), drho, sizeof(double) * ne, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(E.data(), s->E, sizeof(double) * ne, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(phi.data(), s->phi, sizeof(double) * phi.size(), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    cudaFree(drho);
+    if (rc) return rc;
+    const Basis bs = make_basis(c->k + 1);
+    std::string out = "x,rho,phi,E\n";
+    for (int cc = 0; cc < nx; ++cc) {
+        double xl = grid_cell_left(g, cc), h = grid_cell_width(g, cc);
+        for (int n = 0; n < p; ++n) {
+            double xi = c->basis.nodes[n];
+            double ph = host_evaluate(bs, phi.data() + (size_t)cc * (p + 1), xi);
+            out += g17(xl + h * xi) + "," + g17(rho[(size_t)cc * p + n]) + "," + g17(ph) + "," +
+                   g17(E[(size_t)cc * p + n]) + "\n";
+        }
+    }
+    return write_file(std::string(dir) + "/profiles_" + std::to_string(step) + ".csv", out);
+}
+
+sk_status sk_run(sk_ctx* c, const sk_run_config* cfg, long nsteps, int cadence, int snapshot_cadence,
+                 int profile_cadence, const char* out_dir, sk_run_result* res) {
+    auto t_start = std::chrono::steady_clock::now();
+    std::memset(res, 0, sizeof *res);
+    if (cadence < 1) return fail(SK_ERR_RUNTIME, "run: cadence must be >= 1");
+    const bool files = out_dir != nullptr;
+    std::string dir = files ? out_dir : "";
+    if (files) mkdir(dir.c_str(), 0755);
+    sk_state* s = nullptr;
+    if (sk_status rc = sk_state_create(c, cfg, &s)) return rc;
+    sk_ctx_set_eager_errors(c, 0);
+    sk_stats_reset(c);
+    std::string flux, log;
+    auto sample = [&]() -> sk_status {
+        sk_flux_sample fs;
+        if (sk_status rc = sk_state_sample_fluxes(s, &fs)) return rc;
+        if (files) {
+            if (flux.empty())
+                flux = "t,je_plus,je_minus,ji_plus,ji_minus,je_naive,ji_naive,mass_e,mass_i,E_energy,vmax_e,vmax_i\n";
+            flux += g17(fs.t) + "," + g17(fs.je_plus) + "," + g17(fs.je_minus) + "," + g17(fs.ji_plus) + "," +
+                    g17(fs.ji_minus) + "," + g17(fs.je_naive) + "," + g17(fs.ji_naive) + "," + g17(fs.mass_e) +
+                    "," + g17(fs.mass_i) + "," + g17(fs.e_energy) + "," + g17(fs.vmax_e) + "," +
+                    g17(fs.vmax_i) + "\n";
+            return write_file(dir + "/flux.csv", flux);
+        }
+        return SK_OK;
+    };
+    auto outputs = [&](long step) -> sk_status {
+        if (!files) return SK_OK;
+        if (snapshot_cadence > 0 && step % snapshot_cadence == 0)
+            if (sk_status rc = sk_state_write_snapshot(s, dir.c_str())) return rc;
+        if (profile_cadence > 0 && step % profile_cadence == 0)
+            if (sk_status rc = sk_state_write_profiles(s, dir.c_str())) return rc;
+        return SK_OK;
+    };
+    sk_status rc = sample();
+    if (!rc) rc = outputs(0);
+    int seen[2] = {0, 0};
+    long step = 0;
+    while (!rc && step < nsteps) {
+        // run the steps up to the next output event as graph replays
+        long next = nsteps;
+        auto upto = [&](long cad) {
+            if (cad > 0) next = std::min(next, (step / cad + 1) * cad);
+        };
+        upto(cadence);
+        upto(snapshot_cadence);
+        upto(profile_cadence);
+        sk_status r = sk_run_steps(s, (int)(next - step));
+        if (r == SK_OK) r = collect_errors(c);
+        if (r == SK_ERR_SIMULATION) {
+            res->exit_code = 1;
+            log += std::string("ABORT: ") + sk_last_error() + "\n";
+            long at = 0;
+            sk_state_step_index(s, &at);
+            res->steps_done = at;
+            if (files) {
+                sk_state_write_snapshot(s, dir.c_str());
+                sk_state_write_profiles(s, dir.c_str());
+            }
+            break;
+        }
+        if ((rc = r)) break;
+        step = next;
+        res->steps_done = step;
+        for (int sp = 0; sp < 2; ++sp) {  // run.cpp:103-112 shrink log lines
+            int cnt = 0;
+            long last = 0;
+            sk_state_shrinks(s, sp, &cnt, &last);
+            if (cnt > seen[sp] && files) {
+                log += "step " + std::to_string(last) + ": " + species_name(sp) + " v domain shrink " +
+                       g17(c->st_host->vmax_before[sp]) + " -> " + g17(field_vmax(s->f[sp])) + "\n";
+            }
+            seen[sp] = cnt;
+        }
+        if (step % cadence == 0) {
+            if ((rc = sample())) break;
+            if (files && (cfg->limiter.inline_sldg || cfg->limiter.indicator)) {
+                sk_stats st;
+                sk_stats_get(c, &st);
+                log += "step " + std::to_string(step) + ": inline_troubled=" + std::to_string(st.inline_troubled) +
+                       " inline_clamped=" + std::to_string(st.inline_clamped) +
+                       " inline_mean_outside=" + std::to_string(st.inline_mean_outside) +
+                       " post_troubled=" + std::to_string(st.post_troubled) + "/" +
+                       std::to_string(st.post_checked) + "\n";
+            }
+        }
+        if ((rc = outputs(step))) break;
+    }
+    res->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    res->shrinks_e = seen[0];
+    res->shrinks_i = seen[1];
+    sk_stats_get(c, &res->stats);
+    if (files) {
+        log += "wall=" + g17(res->wall_seconds) + " s\n";
+        write_file(dir + "/run.log", log);
+    }
+    sk_state_destroy(s);
+    return rc;
 }
 
 }  // extern "C"

@@ -615,6 +615,39 @@ class SimulationState:
         _check(N.lib().sk_state_shrinks(self.h, species, C.byref(cnt), C.byref(last)))
         return cnt.value, last.value
 
+    # ---- diagnostics + output (diagnostics.cpp) ----
+    def time(self) -> float:
+        """state.time (stepper.cpp:98)"""
+        t = C.c_double()
+        _check(N.lib().sk_state_time(self.h, C.byref(t)))
+        return t.value
+
+    def wall_flux(self, species: int, side: int) -> tuple:
+        """wall_flux (diagnostics.cpp:24-69): (outflow, naive); side 0 left, 1 right"""
+        o, n = C.c_double(), C.c_double()
+        _check(N.lib().sk_state_wall_flux(self.h, species, side, C.byref(o), C.byref(n)))
+        return o.value, n.value
+
+    def sample_fluxes(self) -> dict:
+        """sample_fluxes (diagnostics.cpp:98-116)"""
+        out = N.sk_flux_sample()
+        _check(N.lib().sk_state_sample_fluxes(self.h, C.byref(out)))
+        return {k: getattr(out, k) for k, _ in out._fields_}
+
+    def summarize(self) -> dict:
+        """summarize (diagnostics.cpp:85-96)"""
+        out = N.sk_summary()
+        _check(N.lib().sk_state_summarize(self.h, C.byref(out)))
+        return {k: getattr(out, k) for k, _ in out._fields_}
+
+    def write_snapshot(self, directory: str):
+        """OutputWriter::write_snapshot: <dir>/snapshot_<step>.bin (SOLKSNP1) + .meta"""
+        _check(N.lib().sk_state_write_snapshot(self.h, str(directory).encode()))
+
+    def write_profiles(self, directory: str):
+        """OutputWriter::write_profiles: <dir>/profiles_<step>.csv"""
+        _check(N.lib().sk_state_write_profiles(self.h, str(directory).encode()))
+
     def stats(self) -> dict:
         s = self.ctx.stats()
         p = self.ctx.p
@@ -638,3 +671,30 @@ def strang_step(state: SimulationState):
 
 def run_step(state: SimulationState):
     state.run_step()
+
+
+def run(cfg: RunConfig, nsteps: int | None = None, cadence: int = 10, snapshot_cadence: int = 0,
+        profile_cadence: int = 0, out_dir: str | None = "out", device: int = 0,
+        exact: bool = False) -> dict:
+    """run() (run.cpp:60-169): nsteps (default t_final/dt, config.cpp:220) run()
+    loop bodies with flux.csv rows every `cadence` steps, snapshots / profiles
+    at their cadences, run.log -- into out_dir (None: no files)."""
+    if nsteps is None:
+        nsteps = int(math.floor(cfg.t_final / cfg.dt + 0.5))  # std::lround
+    grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
+                              cfg.refinement_ratio)
+    ctx = Context(grid, cfg.k, cfg.penalty_scale, device)
+    if exact:
+        ctx.set_exact_reductions(True)
+    try:
+        res = N.sk_run_result()
+        ccfg = cfg.to_c()
+        rc = N.lib().sk_run(ctx.h, C.byref(ccfg), int(nsteps), int(cadence), int(snapshot_cadence),
+                            int(profile_cadence), None if out_dir is None else str(out_dir).encode(),
+                            C.byref(res))
+        _check(rc)
+        return dict(exit_code=res.exit_code, steps_done=res.steps_done, shrinks_e=res.shrinks_e,
+                    shrinks_i=res.shrinks_i, wall_seconds=res.wall_seconds,
+                    error=N.lib().sk_last_error().decode() if res.exit_code else "")
+    finally:
+        ctx.close()

@@ -606,3 +606,45 @@ def test_injection_scenario(sk, ora, kw, exact):
                 assert rel(got, want) <= F_TOL, f"step {s + 1} species {sp}"
             assert st.field(sp).vmax() == o.vmax(sp)
     assert st.shrinks(0)[0] >= 2
+
+
+def test_diagnostics_and_outputs_match_reference(sk, ref, tmp_path):
+    """§8f N3: wall fluxes, state time, SOLKSNP1 snapshots and a whole run()
+    with files against the reference's own diagnostics.cpp / run.cpp (exact
+    mode: f, E and the fluxes bitwise; the masses come from a parallel device
+    reduction and agree to 1e-12)"""
+    kw = dict(k=3, nf=16, nc=32, m=1, nv=48, mu=1836.0, limiter="sldg")
+    cfg = cfg_of(sk, **kw)
+    st = sk.SimulationState(cfg, exact=True)
+    r = ref.state(**cfg.oracle_kwargs())
+    for _ in range(12):
+        st.run_step()
+        r.step()
+    assert st.time() == r.time()
+    for sp in (0, 1):
+        for side in (0, 1):
+            assert st.wall_flux(sp, side) == r.wall_flux(sp, side), (sp, side)
+    a, b = tmp_path / "gpu", tmp_path / "ref"
+    a.mkdir()
+    b.mkdir()
+    st.write_snapshot(a)
+    r.write_snapshot(b)
+    for ext in (".bin", ".meta"):
+        assert (a / f"snapshot_12{ext}").read_bytes() == (b / f"snapshot_12{ext}").read_bytes()
+    fs = st.sample_fluxes()
+    assert fs["je_plus"] == r.wall_flux(0, 1)[0] and fs["t"] == r.time()
+    # whole run() with files: flux.csv rows, snapshots, profiles
+    ra, rb = tmp_path / "run_gpu", tmp_path / "run_ref"
+    out = sk.run(cfg, nsteps=25, cadence=5, snapshot_cadence=10, profile_cadence=10,
+                 out_dir=str(ra), exact=True)
+    assert out["exit_code"] == 0 and out["steps_done"] == 25
+    ref.state(**cfg.oracle_kwargs()).run_files(25 * cfg.dt, 5, 10, 10, rb)
+    ga = np.loadtxt(ra / "flux.csv", delimiter=",", skiprows=1)
+    gb = np.loadtxt(rb / "flux.csv", delimiter=",", skiprows=1)
+    assert ga.shape == gb.shape == (6, 12)
+    cols = [0, 1, 2, 3, 4, 5, 6, 9, 10, 11]  # t, fluxes, E energy, vmax: bitwise
+    assert np.array_equal(ga[:, cols], gb[:, cols])
+    assert np.abs(ga[:, 7:9] - gb[:, 7:9]).max() <= 1e-12 * np.abs(gb[:, 7:9]).max()
+    for step in (0, 10, 20):
+        assert (ra / f"snapshot_{step}.bin").read_bytes() == (rb / f"snapshot_{step}.bin").read_bytes()
+        assert (ra / f"profiles_{step}.csv").read_text() == (rb / f"profiles_{step}.csv").read_text()
