@@ -240,4 +240,41 @@ class SimulationState {
 inline void strang_step(SimulationState& s) { check(sk_strang_step(s.get())); }
 inline void run_step(SimulationState& s) { check(sk_run_step(s.get())); }
 
+// diagnostics.cpp: WallFlux (diagnostics.hpp:17-21), sample_fluxes, summarize
+enum class WallSide { Left = 0, Right = 1 };
+struct WallFlux {
+    double outflow = 0.0, naive = 0.0;
+};
+inline WallFlux wall_flux(SimulationState& s, Species sp, WallSide side) {
+    WallFlux w;
+    check(sk_state_wall_flux(s.get(), static_cast<int>(sp), static_cast<int>(side), &w.outflow, &w.naive));
+    return w;
+}
+inline sk_flux_sample sample_fluxes(SimulationState& s) {
+    sk_flux_sample out;
+    check(sk_state_sample_fluxes(s.get(), &out));
+    return out;
+}
+inline sk_summary summarize(SimulationState& s) {
+    sk_summary out;
+    check(sk_state_summarize(s.get(), &out));
+    return out;
+}
+// OutputWriter::write_snapshot / write_profiles (diagnostics.cpp:161-220)
+inline void write_snapshot(SimulationState& s, const std::string& dir) {
+    check(sk_state_write_snapshot(s.get(), dir.c_str()));
+}
+inline void write_profiles(SimulationState& s, const std::string& dir) {
+    check(sk_state_write_profiles(s.get(), dir.c_str()));
+}
+// run() (run.cpp:60-169); out_dir empty: no files. SimulationError ends the
+// run with exit_code 1 (the reference's contract), other failures throw.
+inline sk_run_result run(const Context& ctx, const sk_run_config& cfg, long nsteps, int cadence = 10,
+                         int snapshot_cadence = 0, int profile_cadence = 0, const std::string& out_dir = "out") {
+    sk_run_result r;
+    check(sk_run(ctx.get(), &cfg, nsteps, cadence, snapshot_cadence, profile_cadence,
+                 out_dir.empty() ? nullptr : out_dir.c_str(), &r));
+    return r;
+}
+
 }  // namespace solkin_b200
