@@ -77,6 +77,7 @@ struct sk_ctx {
     unsigned long long* fix_list = nullptr;  // deferred limiter clamps
     unsigned int* fix_count = nullptr;
     unsigned int fix_cap = 0;
+    unsigned int fix_alloc = 0;
 };
 
 struct sk_field {
@@ -427,13 +428,16 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     a.gl = fs[0]->gl() > 0 ? 1 : 0;
     a.gr = fs[0]->gr() > 0 ? 1 : 0;
     std::memcpy(a.tile_start, c->ptiles, sizeof a.tile_start);
-    if (dir == SK_DIR_X) {
+    post_cfg_points(c->basis, a.cfg);
+    a.fix_list = c->fix_list;
+    a.fix_count = c->fix_count;
+    a.fix_cap = c->fix_cap;
+    CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
+    if (dir == SK_DIR_X)
         CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
-        c->launches += 1;
-    } else {
+    else
         CK(launch_post_v(a, c->stream));
-        c->launches += 2;
-    }
+    c->launches += 3;
     for (int i = 0; i < nspecies; ++i) fs[i]->swap();
     return SK_OK;
 }
@@ -656,7 +660,7 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
     CK(dalloc(&c->diag_partial, 592 * 4));
     CK(dalloc(&c->diag_out, 4));
     CK(cudaMallocHost((void**)&c->pinned, sizeof(double) * 64));
-    c->fix_cap = 1u << 22;  // 4 Mi queued cells (32 MiB); overflow clamps inline
+    c->fix_cap = c->fix_alloc = 1u << 22;  // 4 Mi queued cells (32 MiB); overflow: the fixup rescans
     CK(dalloc(&c->fix_list, c->fix_cap));
     CK(dalloc(&c->fix_count, 1));
     CK(cudaMemset(c->fix_count, 0, sizeof(unsigned int)));
@@ -699,10 +703,25 @@ sk_status sk_ctx_set_stream(sk_ctx* c, void* s) {
 }
 
 sk_status sk_ctx_set_fix_capacity(sk_ctx* c, unsigned int cap) {
-    if (cap > (1u << 22)) return fail(SK_ERR_RUNTIME, "fix capacity above the allocation");
+    if (cap > c->fix_alloc) return fail(SK_ERR_RUNTIME, "fix capacity above the allocation");
     c->fix_cap = cap;
     return SK_OK;
 }
+
+namespace {
+// the deferred-limiter list must hold a pass's flagged cells: the sweeps flag
+// ~0.5 % of the cells, the literature post limiters ~5-10 % (outside capture)
+sk_status ensure_fix_capacity(sk_ctx* c, size_t cells) {
+    const size_t want = std::min<size_t>(cells, 0xffffffffu);
+    if (want <= c->fix_alloc) return SK_OK;
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->fix_list);
+    c->fix_list = nullptr;
+    CK(dalloc(&c->fix_list, want));
+    c->fix_alloc = c->fix_cap = (unsigned)want;
+    return SK_OK;
+}
+}  // namespace
 
 sk_status sk_ctx_set_exact_reductions(sk_ctx* c, int on) {
     c->exact = on != 0;
@@ -1045,6 +1064,10 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
     if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
     if (cfg->v_adjust)
         if (sk_status rc = validate_policy(&cfg->policy)) return rc;
+    {  // cells per pass, both species: room for the flagged ones
+        const size_t cells = 2 * (size_t)cfg->v_cells * c->P * c->grid.ncells;
+        if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 64)) return rc;
+    }
     auto* s = new sk_state;
     s->ctx = c;
     s->cfg = *cfg;
@@ -1112,6 +1135,10 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
     if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
     const int ncell = cfg->v_cells / nranks, cell0 = rank * ncell;
     if (nranks > 1 && halo > ncell) return fail(SK_ERR_RUNTIME, "v shard: halo wider than a shard");
+    {
+        const size_t cells = 2 * (size_t)ncell * c->P * c->grid.ncells;
+        if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 64)) return rc;
+    }
     // a velocity shrink maps new cell j to old cells up to p*nv/2 cells closer
     // to v = 0 (adaptivity.cpp:52-90): shards keep a halo that wide, filled
     // only on shrink steps

@@ -20,6 +20,7 @@
 //   post_*          K3: minmod / mean-error indicators + simple / line WENO
 // All arithmetic is fp64 with -fmad=false so per-cell results are bitwise the
 // reference's.
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -1846,8 +1847,8 @@ __global__ void copy_kernel(double* dst, const double* src, long long n) {
 template <int P>
 __device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, const double* um,
                                           const double* u0, const double* up) {
-    return cfg.indicator == 1 ? indicator_minmod<P>(b, um, u0, up)
-                              : indicator_meanerr<P>(b, um, u0, up, cfg.threshold);
+    return cfg.indicator == 1 ? indicator_minmod_pre<P>(b, um, u0, up)
+                              : indicator_meanerr_pre<P>(b, cfg, um, u0, up);
 }
 
 template <int P>
@@ -1859,63 +1860,154 @@ __device__ __forceinline__ void post_modify(const PostCfg& cfg, const Basis& b, 
         modify_line_weno<P>(b, um, u0, up, cfg, out);
 }
 
+// Post limiters as two passes, like the sweeps' limiter: a streaming pass
+// flags cells (cheap indicator), copies u0 and queues the flagged ones; the
+// modifier kernel recomputes the (rare, expensive, divergent) WENO
+// modification of queued cells from the untouched pre-pass data. Results are
+// exactly the single-pass ones.
+
+// the three cells of x stencil (line, block-local cell c) from the pre-pass data
+template <int P>
+__device__ __forceinline__ void post_x_stencil(const PostArgs& a, const double* src, int b, int c,
+                                               double* um, double* u0, double* up) {
+    const Grid& g = a.grid;
+    const int cells_b = g.cells[b];
+    const long long gbase = (long long)g.start[b] * P;
+    double* u[3] = {um, u0, up};
+    for (int h = 0; h < 3; ++h) {
+        const int s = c - 1 + h;
+        if (s >= 0 && s < cells_b) {
+#pragma unroll
+            for (int n = 0; n < P; ++n) u[h][n] = src[gbase + (long long)s * P + n];
+        } else if (a.periodic) {
+            const int ss = ((s % cells_b) + cells_b) % cells_b;
+#pragma unroll
+            for (int n = 0; n < P; ++n) u[h][n] = src[gbase + (long long)ss * P + n];
+        } else {
+#pragma unroll
+            for (int n = 0; n < P; ++n) u[h][n] = x_fetch_outside_ool<P>(a.basis, g, src, b, s, n);
+        }
+    }
+}
+
+// streaming pass X: persistent CTAs walk (species, line, tile) tiles of
+// kPostCPT*256 cells (kPostCPT cells per thread); the window of the next tile
+// is fetched with cp.async into the other half of a double buffer while the
+// current tile's indicators run
+template <int P>
+__host__ __device__ constexpr int post_cpt() { return P <= 4 ? 4 : 2; }
+template <int P>
+__host__ __device__ constexpr int post_tile() { return post_cpt<P>() * kXThreads; }
+template <int P>
+__host__ __device__ constexpr size_t post_x_smem() {
+    return sizeof(double) * 2 * P * xs_stride<P, post_tile<P>()>();
+}
+
 template <int P>
 __global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant__ PostArgs a) {
-    constexpr int T = kXThreads;
+    constexpr int T = post_tile<P>(), CPT = post_cpt<P>();
     constexpr int W = xs_stride<P, T>();
-    __shared__ double win[P * W];
-    const int line = blockIdx.x;
-    const int sp = a.species0 + blockIdx.z;
-    const int tile = blockIdx.y;
+    extern __shared__ __align__(16) double pxs[];  // [2][node][window cell]
     const Grid& g = a.grid;
-    int b = 0;
-    while (tile >= a.tile_start[b + 1]) ++b;
-    const int cells_b = g.cells[b];
-    const int c0 = (tile - a.tile_start[b]) * T;
-    const int nt = min(T, cells_b - c0);
-    const long long lb = (long long)line * g.ncells * P;
-    const bool fl = field_flipped(a.flip[sp]);
-    const double* src = (fl ? a.dst[sp] : a.src[sp]) + lb;
-    const long long gbase = (long long)g.start[b] * P;
-    for (int e = threadIdx.x; e < (nt + 2) * P; e += T) {
-        const int wc = e / P, n = e - (e / P) * P;
-        const int s = c0 - 1 + wc;
-        double v;
-        if (s >= 0 && s < cells_b) {
-            v = src[gbase + (long long)s * P + n];
-        } else if (a.periodic) {
-            int ss = ((s % cells_b) + cells_b) % cells_b;
-            v = src[gbase + (long long)ss * P + n];
-        } else {
-            v = x_fetch_outside<P>(a.basis, g, src, b, s, n);
+    const int ntl = a.tile_start[g.nblocks];
+    const long long ntot = (long long)a.nspecies * a.nrows * ntl;
+    const int tid = threadIdx.x;
+    struct Tile {
+        int sp, line, b, c0, nt;
+    };
+    auto decode = [&](long long t) {
+        Tile x;
+        const int tl = (int)(t % ntl);
+        const long long r = t / ntl;
+        x.line = (int)(r % a.nrows);
+        x.sp = a.species0 + (int)(r / a.nrows);
+        int b = 0;
+        while (tl >= a.tile_start[b + 1]) ++b;
+        x.b = b;
+        x.c0 = (tl - a.tile_start[b]) * T;
+        x.nt = min(T, g.cells[b] - x.c0);
+        return x;
+    };
+    auto srcof = [&](const Tile& x) -> const double* {
+        const bool fl = field_flipped(a.flip[x.sp]);
+        return (fl ? a.dst[x.sp] : a.src[x.sp]) + (long long)x.line * g.ncells * P;
+    };
+    // issue the window of tile x into buffer bi: cells c0-1 .. c0+nt (block-local)
+    auto issue = [&](const Tile& x, int bi) {
+        const double* src = srcof(x);
+        const int cells_b = g.cells[x.b];
+        const long long gbase = (long long)g.start[x.b] * P;
+        double* wb = pxs + bi * P * W;
+        for (int e = tid; e < (x.nt + 2) * P; e += kXThreads) {
+            const int wc = e / P, n = e - (e / P) * P;
+            int sc = x.c0 - 1 + wc;
+            bool ok = sc >= 0 && sc < cells_b;
+            if (!ok && a.periodic) {
+                sc = ((sc % cells_b) + cells_b) % cells_b;
+                ok = true;
+            }
+            cp_async8(&wb[n * W + wc], ok ? src + gbase + (long long)sc * P + n : src, ok);
         }
-        win[n * W + wc] = v;
+    };
+    long long t = blockIdx.x;
+    Tile cur{};
+    if (t < ntot) {
+        cur = decode(t);
+        issue(cur, 0);
     }
-    __syncthreads();
-    const int c = threadIdx.x;
-    unsigned flagged = 0;
-    if (c < nt) {
-        double um[P], u0[P], up[P], o[P];
-#pragma unroll
-        for (int n = 0; n < P; ++n) {
-            um[n] = win[n * W + c];
-            u0[n] = win[n * W + c + 1];
-            up[n] = win[n * W + c + 2];
+    cp_commit();
+    for (int it = 0; t < ntot; t += gridDim.x, ++it) {
+        const int bi = it & 1;
+        double* wb = pxs + bi * P * W;
+        const long long tn = t + gridDim.x;
+        Tile nxt{};
+        if (tn < ntot) {
+            nxt = decode(tn);
+            issue(nxt, bi ^ 1);
         }
-        if (post_flag<P>(a.cfg, a.basis, um, u0, up)) {
-            flagged = 1;
-            post_modify<P>(a.cfg, a.basis, um, u0, up, o);
-        } else {
-#pragma unroll
-            for (int n = 0; n < P; ++n) o[n] = u0[n];
+        cp_commit();
+        cp_wait<1>();
+        // window cells outside the block (walls, 3-block ghosts): computed here
+        if (!a.periodic && (cur.c0 == 0 || cur.c0 + cur.nt == g.cells[cur.b])) {
+            const double* src = srcof(cur);
+            for (int e = tid; e < (cur.nt + 2) * P; e += kXThreads) {
+                const int wc = e / P, n = e - (e / P) * P;
+                const int sc = cur.c0 - 1 + wc;
+                if (sc < 0 || sc >= g.cells[cur.b])
+                    wb[n * W + wc] = x_fetch_outside_ool<P>(a.basis, g, src, cur.b, sc, n);
+            }
         }
-        double* dst = (fl ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + lb + gbase + (long long)(c0 + c) * P;
+        __syncthreads();
+        bool tr[CPT];
+        unsigned long long entry[CPT];
+        const bool fl = field_flipped(a.flip[cur.sp]);
+        double* dline = (fl ? const_cast<double*>(a.src[cur.sp]) : a.dst[cur.sp]) +
+                        (long long)cur.line * g.ncells * P + ((long long)g.start[cur.b] + cur.c0) * P;
 #pragma unroll
-        for (int n = 0; n < P; ++n) dst[n] = o[n];
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int c = tid + cc * kXThreads;
+            tr[cc] = false;
+            entry[cc] = ((unsigned long long)(cur.sp & 1) << 63) | ((unsigned long long)cur.line << 32) |
+                        (unsigned)(g.start[cur.b] + cur.c0 + c);
+            if (c < cur.nt) {
+                double um[P], u0[P], up[P];
+#pragma unroll
+                for (int n = 0; n < P; ++n) {
+                    um[n] = wb[n * W + c];
+                    u0[n] = wb[n * W + c + 1];
+                    up[n] = wb[n * W + c + 2];
+                }
+                tr[cc] = post_flag<P>(a.cfg, a.basis, um, u0, up);
+                double* dst = dline + (long long)c * P;
+#pragma unroll
+                for (int n = 0; n < P; ++n) dst[n] = u0[n];  // flagged cells: rewritten by post_fix_kernel
+            }
+        }
+        defer_push_n<CPT>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+        __syncthreads();  // buffer bi is refilled two tiles from now
+        cur = nxt;
     }
-    unsigned tot = __reduce_add_sync(0xffffffffu, flagged);
-    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&a.st->stats[sp][3], (unsigned long long)tot);
-    if (threadIdx.x == 0) atomicAdd(&a.st->post_checked[sp], (unsigned long long)nt);
+    cp_wait<0>();
 }
 
 template <int P>
@@ -1923,7 +2015,7 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
     const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
-    unsigned flagged = 0;
+    const unsigned members = __ballot_sync(0xffffffffu, xd < a.nxd);
     if (xd < a.nxd) {
         const bool fl = field_flipped(a.flip[sp]);
         const double* f = fl ? a.dst[sp] : a.src[sp];
@@ -1935,16 +2027,12 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
         vload<P>(f, a.ld, xd, j0, lo, hi, a.periodic, a.nv, u0);
         for (int j = j0; j < j1; ++j) {
             vload<P>(f, a.ld, xd, j + 1, lo, hi, a.periodic, a.nv, up);
-            double o[P];
-            if (post_flag<P>(a.cfg, a.basis, um, u0, up)) {
-                ++flagged;
-                post_modify<P>(a.cfg, a.basis, um, u0, up, o);
-            } else {
+            const bool tr[1] = {post_flag<P>(a.cfg, a.basis, um, u0, up)};
+            const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
+                                                 ((unsigned long long)j << 32) | (unsigned)xd};
+            defer_push_n<1>(a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
 #pragma unroll
-                for (int n = 0; n < P; ++n) o[n] = u0[n];
-            }
-#pragma unroll
-            for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = o[m];
+            for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = u0[m];
 #pragma unroll
             for (int n = 0; n < P; ++n) {
                 um[n] = u0[n];
@@ -1952,8 +2040,68 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
             }
         }
     }
-    unsigned tot = __reduce_add_sync(0xffffffffu, flagged);
-    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&a.st->stats[sp][3], (unsigned long long)tot);
+}
+
+// modifier of queued (or, after a list overflow, all re-flagged) cells
+template <int P, int DIR>
+__global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ PostArgs a) {
+    const unsigned cnt = *a.fix_count;
+    const bool rescan = cnt > a.fix_cap;
+    const Grid& g = a.grid;
+    const long long per_sp = DIR == 0 ? (long long)a.nrows * g.ncells : (long long)a.nv * a.nxd;
+    const long long n = rescan ? (long long)a.nspecies * per_sp : (long long)cnt;
+    unsigned flagged[2] = {0, 0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int sp, row, col;  // x: row = line, col = cell; v: row = v cell, col = x dof
+        if (!rescan) {
+            const unsigned long long e = a.fix_list[i];
+            sp = (int)(e >> 63);
+            row = (int)((e >> 32) & 0x7fffffffu);
+            col = (int)(e & 0xffffffffu);
+        } else {
+            sp = a.species0 + (int)(i / per_sp);
+            const long long r = i - (i / per_sp) * per_sp;
+            const long long ncol = DIR == 0 ? g.ncells : a.nxd;
+            row = (int)(r / ncol);
+            col = (int)(r - (r / ncol) * ncol);
+        }
+        const bool fl = field_flipped(a.flip[sp]);
+        const double* f = fl ? a.dst[sp] : a.src[sp];
+        double* out = fl ? const_cast<double*>(a.src[sp]) : a.dst[sp];
+        double um[P], u0[P], up[P], o[P];
+        if constexpr (DIR == 0) {
+            int b = 0;
+            while (col >= g.start[b + 1]) ++b;
+            const long long lb = (long long)row * g.ncells * P;
+            post_x_stencil<P>(a, f + lb, b, col - g.start[b], um, u0, up);
+            if (rescan && !post_flag<P>(a.cfg, a.basis, um, u0, up)) continue;
+            post_modify<P>(a.cfg, a.basis, um, u0, up, o);
+#pragma unroll
+            for (int m = 0; m < P; ++m) out[lb + (long long)col * P + m] = o[m];
+        } else {
+            const int lo = -a.gl, hi = a.nv + a.gr;
+            vload<P>(f, a.ld, col, row - 1, lo, hi, a.periodic, a.nv, um);
+            vload<P>(f, a.ld, col, row, lo, hi, a.periodic, a.nv, u0);
+            vload<P>(f, a.ld, col, row + 1, lo, hi, a.periodic, a.nv, up);
+            if (rescan && !post_flag<P>(a.cfg, a.basis, um, u0, up)) continue;
+            post_modify<P>(a.cfg, a.basis, um, u0, up, o);
+#pragma unroll
+            for (int m = 0; m < P; ++m) out[((long long)row * P + m) * a.ld + col] = o[m];
+        }
+        flagged[sp & 1] += 1;
+    }
+    // limiter counters (post_troubled): block reduction, one atomic per block
+    __shared__ unsigned acc[2];
+    if (threadIdx.x < 2) acc[threadIdx.x] = 0;
+    __syncthreads();
+    for (int sp = 0; sp < 2; ++sp) {
+        const unsigned v = __reduce_add_sync(0xffffffffu, flagged[sp]);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&acc[sp], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 && acc[threadIdx.x])
+        atomicAdd(&a.st->stats[threadIdx.x][3], (unsigned long long)acc[threadIdx.x]);
 }
 
 __global__ void post_v_count_kernel(DevStatus* st, int mask, unsigned long long per_species) {
@@ -2388,15 +2536,39 @@ cudaError_t launch_fill_separable(double* f, const double* gx, const double* gv,
     return cudaGetLastError();
 }
 
+template <int P>
+static void launch_post_x_t(const PostArgs& a, cudaStream_t s) {
+    constexpr size_t smem = post_x_smem<P>();
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(post_x_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    PostArgs b = a;  // tiles of post_tile<P>() cells
+    b.tile_start[0] = 0;
+    for (int i = 0; i < a.grid.nblocks; ++i)
+        b.tile_start[i + 1] = b.tile_start[i] + (a.grid.cells[i] + post_tile<P>() - 1) / post_tile<P>();
+    const long long ntot = (long long)a.nspecies * a.nrows * b.tile_start[a.grid.nblocks];
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, post_x_kernel<P>, kXThreads, smem);
+    const long long grid = std::min<long long>((long long)sm_count() * std::max(per_sm, 1), ntot);
+    post_x_kernel<P><<<(int)std::max<long long>(grid, 1), kXThreads, smem, s>>>(b);
+}
+
 cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s) {
-    dim3 grid(a.nrows, ntiles, a.nspecies);
-    SK_DISPATCH_P(a.basis.p, (post_x_kernel<PP><<<grid, kXThreads, 0, s>>>(a)));
+    (void)ntiles;
+    SK_DISPATCH_P(a.basis.p, (launch_post_x_t<PP>(a, s)));
+    SK_DISPATCH_P(a.basis.p, (post_fix_kernel<PP, 0><<<sm_count() * 8, 128, 0, s>>>(a)));
+    int mask = 0;
+    for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
+    post_v_count_kernel<<<1, 1, 0, s>>>(a.st, mask, (unsigned long long)a.nrows * a.grid.ncells);
     return cudaGetLastError();
 }
 
 cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
     SK_DISPATCH_P(a.basis.p, (post_v_kernel<PP><<<grid, kVThreads, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (post_fix_kernel<PP, 1><<<sm_count() * 8, 128, 0, s>>>(a)));
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
     post_v_count_kernel<<<1, 1, 0, s>>>(a.st, mask, (unsigned long long)a.nv * a.nxd);

@@ -193,6 +193,10 @@ struct PostArgs {
     int species0;
     int periodic;
     int tile_start[kMaxBlocks + 1];
+    // flagged cells are queued for the modifier kernel (overflow: it rescans)
+    unsigned long long* fix_list;
+    unsigned int* fix_count;
+    unsigned int fix_cap;
 };
 
 // launchers (P = k+1 dispatch inside)

@@ -620,7 +620,83 @@ struct PostCfg {
     double gamma_simple[3];
     double gamma_line[3];
     double epsilon;
+    // evaluate() at the quadrature points of integrate(u, 1, 2) (ip) and of
+    // integrate(u, -1, 0) (im), basis.cpp:142-150: barycentric terms and
+    // their ordered sums, computed once on the host with evaluate()'s
+    // operations (the points never coincide with a node)
+    double ipt[SK_MAXP][SK_MAXP], ipden[SK_MAXP];
+    double imt[SK_MAXP][SK_MAXP], imden[SK_MAXP];
 };
+
+// host: fill PostCfg's evaluation points for a basis
+inline void post_cfg_points(const Basis& b, PostCfg& c) {
+    for (int side = 0; side < 2; ++side) {
+        const double a = side == 0 ? 1.0 : -1.0, len = (side == 0 ? 2.0 : 0.0) - a;
+        for (int q = 0; q < b.p; ++q) {
+            const double xi = a + len * b.nodes[q];
+            double den = 0.0;
+            for (int n = 0; n < b.p; ++n) {
+                const double t = b.bary[n] / (xi - b.nodes[n]);
+                (side == 0 ? c.ipt : c.imt)[q][n] = t;
+                den += t;
+            }
+            (side == 0 ? c.ipden : c.imden)[q] = den;
+        }
+    }
+}
+
+// integrate(u, 1, 2) / integrate(u, -1, 0) with the precomputed points:
+// bitwise integrate<P>(b, u, a, a + 1)
+template <int P>
+SK_HD double integrate_pre(const Basis& b, const double (*t)[SK_MAXP], const double* den, const double* u) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        double num = 0.0;
+#pragma unroll
+        for (int n = 0; n < P; ++n) num += t[q][n] * u[n];
+        acc += b.weights[q] * (num / den[q]);
+    }
+    return acc * 1.0;
+}
+
+// indicator_minmod / indicator_meanerr with the division-heavy evaluations
+// replaced by precomputed points (same operations, same results)
+template <int P>
+SK_HD bool indicator_minmod_pre(const Basis& b, const double* um, const double* u0, const double* up) {
+    double mean_m = mean<P>(b, um);
+    double mean_0 = mean<P>(b, u0);
+    double mean_p = mean<P>(b, up);
+    double u0_plus = eval_at<P>(basis_evalpt<P>(b, 1), u0) - mean_0;
+    double u0_minus = mean_0 - eval_at<P>(basis_evalpt<P>(b, 0), u0);
+    double d_plus = mean_p - mean_0;
+    double d_minus = mean_0 - mean_m;
+    double scale = fabs(mean_m);
+    double v;
+    v = fabs(mean_0); if (scale < v) scale = v;
+    v = fabs(mean_p); if (scale < v) scale = v;
+    v = fabs(u0_plus); if (scale < v) scale = v;
+    v = fabs(u0_minus); if (scale < v) scale = v;
+    v = fabs(d_plus); if (scale < v) scale = v;
+    v = fabs(d_minus); if (scale < v) scale = v;
+    double guard = 1e-13 * scale;
+    return fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard ||
+           fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard;
+}
+
+template <int P>
+SK_HD bool indicator_meanerr_pre(const Basis& b, const PostCfg& c, const double* um, const double* u0,
+                                 const double* up) {
+    double mean_m = mean<P>(b, um);
+    double mean_0 = mean<P>(b, u0);
+    double mean_p = mean<P>(b, up);
+    double denom = dmax2(fabs(mean_m), dmax2(fabs(mean_0), fabs(mean_p)));
+    if (denom <= 0.0) return false;
+    double ext_m = integrate_pre<P>(b, c.ipt, c.ipden, um);
+    double ext_p = integrate_pre<P>(b, c.imt, c.imden, up);
+    double ind = (fabs(ext_m - mean_0) + fabs(ext_p - mean_0)) / denom;
+    return ind > c.threshold;
+}
 
 template <int P>
 SK_HD void modify_simple_weno(const Basis& b, const double* um, const double* u0, const double* up,
