@@ -652,3 +652,23 @@ def test_diagnostics_and_outputs_match_reference(sk, ref, tmp_path):
     for step in (0, 10, 20):
         assert (ra / f"snapshot_{step}.bin").read_bytes() == (rb / f"snapshot_{step}.bin").read_bytes()
         assert (ra / f"profiles_{step}.csv").read_text() == (rb / f"profiles_{step}.csv").read_text()
+
+
+@pytest.mark.parametrize("mode", ["minmod+simple", "minmod+line", "meanerr+simple", "meanerr+line"])
+def test_post_limiters_conserve_mass(sk, mode):
+    """C4 conservation check: the WENO modifiers are mean-preserving (the
+    reference's design, limiters.cpp:102-165), so a post-limiter pass leaves
+    each species' mass unchanged to rounding, on the C3 mesh after a few
+    steps (steep, limited data)"""
+    import dataclasses
+
+    cfg = dataclasses.replace(sk.named_config("C3"), limiter="sldg")
+    st = sk.SimulationState(cfg)
+    st.run_steps(6)
+    lim = sk.LimiterConfig.parse(mode)
+    for sp in (0, 1):
+        f = st.field(sp)
+        for direction in (0, 1):
+            before = f.mass()
+            sk.apply_post_limiter(f, direction, lim)
+            assert abs(f.mass() - before) <= 1e-13 * abs(before), (sp, direction)
