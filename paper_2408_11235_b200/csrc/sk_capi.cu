@@ -429,6 +429,7 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     a.gr = fs[0]->gr() > 0 ? 1 : 0;
     std::memcpy(a.tile_start, c->ptiles, sizeof a.tile_start);
     post_cfg_points(c->basis, a.cfg);
+    a.fma = !c->exact;
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;

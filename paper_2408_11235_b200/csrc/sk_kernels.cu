@@ -1844,11 +1844,15 @@ __global__ void copy_kernel(double* dst, const double* src, long long n) {
 // K3: literature post-limiters (limiters.cpp:254-345). Flags from pre-pass data
 // (out of place). X: tiles with a 1-cell halo (block ghosts via fill_ghost j=1).
 // ---------------------------------------------------------------------------
-template <int P>
+template <int P, bool FAST = false>
 __device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, const double* um,
                                           const double* u0, const double* up) {
-    return cfg.indicator == 1 ? indicator_minmod_pre<P>(b, um, u0, up)
-                              : indicator_meanerr_pre<P>(b, cfg, um, u0, up);
+    if constexpr (FAST)
+        return cfg.indicator == 1 ? indicator_minmod_fast<P>(b, cfg, um, u0, up)
+                                  : indicator_meanerr_fast<P>(b, cfg, um, u0, up);
+    else
+        return cfg.indicator == 1 ? indicator_minmod_pre<P>(b, um, u0, up)
+                                  : indicator_meanerr_pre<P>(b, cfg, um, u0, up);
 }
 
 template <int P>
@@ -1903,7 +1907,7 @@ __host__ __device__ constexpr size_t post_x_smem() {
     return sizeof(double) * 2 * P * xs_stride<P, post_tile<P>()>();
 }
 
-template <int P>
+template <int P, bool FAST>
 __global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant__ PostArgs a) {
     constexpr int T = post_tile<P>(), CPT = post_cpt<P>();
     constexpr int W = xs_stride<P, T>();
@@ -1997,7 +2001,7 @@ __global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant
                     u0[n] = wb[n * W + c + 1];
                     up[n] = wb[n * W + c + 2];
                 }
-                tr[cc] = post_flag<P>(a.cfg, a.basis, um, u0, up);
+                tr[cc] = post_flag<P, FAST>(a.cfg, a.basis, um, u0, up);
                 double* dst = dline + (long long)c * P;
 #pragma unroll
                 for (int n = 0; n < P; ++n) dst[n] = u0[n];  // flagged cells: rewritten by post_fix_kernel
@@ -2010,7 +2014,7 @@ __global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant
     cp_wait<0>();
 }
 
-template <int P>
+template <int P, bool FAST>
 __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant__ PostArgs a) {
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
@@ -2027,7 +2031,7 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
         vload<P>(f, a.ld, xd, j0, lo, hi, a.periodic, a.nv, u0);
         for (int j = j0; j < j1; ++j) {
             vload<P>(f, a.ld, xd, j + 1, lo, hi, a.periodic, a.nv, up);
-            const bool tr[1] = {post_flag<P>(a.cfg, a.basis, um, u0, up)};
+            const bool tr[1] = {post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)};
             const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
                                                  ((unsigned long long)j << 32) | (unsigned)xd};
             defer_push_n<1>(a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
@@ -2043,7 +2047,7 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
 }
 
 // modifier of queued (or, after a list overflow, all re-flagged) cells
-template <int P, int DIR>
+template <int P, int DIR, bool FAST>
 __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ PostArgs a) {
     const unsigned cnt = *a.fix_count;
     const bool rescan = cnt > a.fix_cap;
@@ -2075,7 +2079,7 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
             while (col >= g.start[b + 1]) ++b;
             const long long lb = (long long)row * g.ncells * P;
             post_x_stencil<P>(a, f + lb, b, col - g.start[b], um, u0, up);
-            if (rescan && !post_flag<P>(a.cfg, a.basis, um, u0, up)) continue;
+            if (rescan && !post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)) continue;
             post_modify<P>(a.cfg, a.basis, um, u0, up, o);
 #pragma unroll
             for (int m = 0; m < P; ++m) out[lb + (long long)col * P + m] = o[m];
@@ -2084,7 +2088,7 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
             vload<P>(f, a.ld, col, row - 1, lo, hi, a.periodic, a.nv, um);
             vload<P>(f, a.ld, col, row, lo, hi, a.periodic, a.nv, u0);
             vload<P>(f, a.ld, col, row + 1, lo, hi, a.periodic, a.nv, up);
-            if (rescan && !post_flag<P>(a.cfg, a.basis, um, u0, up)) continue;
+            if (rescan && !post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)) continue;
             post_modify<P>(a.cfg, a.basis, um, u0, up, o);
 #pragma unroll
             for (int m = 0; m < P; ++m) out[((long long)row * P + m) * a.ld + col] = o[m];
@@ -2536,12 +2540,12 @@ cudaError_t launch_fill_separable(double* f, const double* gx, const double* gv,
     return cudaGetLastError();
 }
 
-template <int P>
+template <int P, bool FAST>
 static void launch_post_x_t(const PostArgs& a, cudaStream_t s) {
     constexpr size_t smem = post_x_smem<P>();
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(post_x_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(post_x_kernel<P, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     PostArgs b = a;  // tiles of post_tile<P>() cells
@@ -2550,15 +2554,26 @@ static void launch_post_x_t(const PostArgs& a, cudaStream_t s) {
         b.tile_start[i + 1] = b.tile_start[i] + (a.grid.cells[i] + post_tile<P>() - 1) / post_tile<P>();
     const long long ntot = (long long)a.nspecies * a.nrows * b.tile_start[a.grid.nblocks];
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, post_x_kernel<P>, kXThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, post_x_kernel<P, FAST>, kXThreads, smem);
     const long long grid = std::min<long long>((long long)sm_count() * std::max(per_sm, 1), ntot);
-    post_x_kernel<P><<<(int)std::max<long long>(grid, 1), kXThreads, smem, s>>>(b);
+    post_x_kernel<P, FAST><<<(int)std::max<long long>(grid, 1), kXThreads, smem, s>>>(b);
+    post_fix_kernel<P, 0, FAST><<<sm_count() * 8, 128, 0, s>>>(a);
+}
+
+template <int P, bool FAST>
+static void launch_post_v_t(const PostArgs& a, cudaStream_t s) {
+    dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
+    post_v_kernel<P, FAST><<<grid, kVThreads, 0, s>>>(a);
+    post_fix_kernel<P, 1, FAST><<<sm_count() * 8, 128, 0, s>>>(a);
 }
 
 cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s) {
     (void)ntiles;
-    SK_DISPATCH_P(a.basis.p, (launch_post_x_t<PP>(a, s)));
-    SK_DISPATCH_P(a.basis.p, (post_fix_kernel<PP, 0><<<sm_count() * 8, 128, 0, s>>>(a)));
+    if (a.fma) {
+        SK_DISPATCH_P(a.basis.p, (launch_post_x_t<PP, true>(a, s)));
+    } else {
+        SK_DISPATCH_P(a.basis.p, (launch_post_x_t<PP, false>(a, s)));
+    }
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
     post_v_count_kernel<<<1, 1, 0, s>>>(a.st, mask, (unsigned long long)a.nrows * a.grid.ncells);
@@ -2566,9 +2581,11 @@ cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s) {
 }
 
 cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s) {
-    dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
-    SK_DISPATCH_P(a.basis.p, (post_v_kernel<PP><<<grid, kVThreads, 0, s>>>(a)));
-    SK_DISPATCH_P(a.basis.p, (post_fix_kernel<PP, 1><<<sm_count() * 8, 128, 0, s>>>(a)));
+    if (a.fma) {
+        SK_DISPATCH_P(a.basis.p, (launch_post_v_t<PP, true>(a, s)));
+    } else {
+        SK_DISPATCH_P(a.basis.p, (launch_post_v_t<PP, false>(a, s)));
+    }
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
     post_v_count_kernel<<<1, 1, 0, s>>>(a.st, mask, (unsigned long long)a.nv * a.nxd);

@@ -193,6 +193,7 @@ struct PostArgs {
     int species0;
     int periodic;
     int tile_start[kMaxBlocks + 1];
+    int fma;               // fast-mode indicators (0: the reference's operation order)
     // flagged cells are queued for the modifier kernel (overflow: it rescans)
     unsigned long long* fix_list;
     unsigned int* fix_count;

@@ -626,6 +626,8 @@ struct PostCfg {
     // operations (the points never coincide with a node)
     double ipt[SK_MAXP][SK_MAXP], ipden[SK_MAXP];
     double imt[SK_MAXP][SK_MAXP], imden[SK_MAXP];
+    // fast mode: reciprocals of the denominators (and of evaluate()'s at 0, 1)
+    double iprc[SK_MAXP], imrc[SK_MAXP], ev0rc, ev1rc;
 };
 
 // host: fill PostCfg's evaluation points for a basis
@@ -641,8 +643,11 @@ inline void post_cfg_points(const Basis& b, PostCfg& c) {
                 den += t;
             }
             (side == 0 ? c.ipden : c.imden)[q] = den;
+            (side == 0 ? c.iprc : c.imrc)[q] = 1.0 / den;
         }
     }
+    c.ev0rc = 1.0 / b.ev0den;
+    c.ev1rc = 1.0 / b.ev1den;
 }
 
 // integrate(u, 1, 2) / integrate(u, -1, 0) with the precomputed points:
@@ -696,6 +701,56 @@ SK_HD bool indicator_meanerr_pre(const Basis& b, const PostCfg& c, const double*
     double ext_p = integrate_pre<P>(b, c.imt, c.imden, up);
     double ind = (fabs(ext_m - mean_0) + fabs(ext_p - mean_0)) / denom;
     return ind > c.threshold;
+}
+
+// fast-mode indicators (tolerance mode): DFMA sums and multiplication by the
+// precomputed reciprocals instead of the exact-order divisions
+template <int P>
+SK_HD double eval_end_fast(const Basis& b, const double* u, int one, double rc) {
+    double num = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) num = fma(one ? b.ev1[n] : b.ev0[n], u[n], num);
+    return num * rc;
+}
+template <int P>
+SK_HD bool indicator_minmod_fast(const Basis& b, const PostCfg& c, const double* um, const double* u0,
+                                 const double* up) {
+    const double mean_m = mean_f<P, true>(b, um);
+    const double mean_0 = mean_f<P, true>(b, u0);
+    const double mean_p = mean_f<P, true>(b, up);
+    const double u0_plus = eval_end_fast<P>(b, u0, 1, c.ev1rc) - mean_0;
+    const double u0_minus = mean_0 - eval_end_fast<P>(b, u0, 0, c.ev0rc);
+    const double d_plus = mean_p - mean_0;
+    const double d_minus = mean_0 - mean_m;
+    double scale = fmax(fmax(fmax(fabs(mean_m), fabs(mean_0)), fmax(fabs(mean_p), fabs(u0_plus))),
+                        fmax(fmax(fabs(u0_minus), fabs(d_plus)), fabs(d_minus)));
+    const double guard = 1e-13 * scale;
+    return fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard ||
+           fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard;
+}
+template <int P>
+SK_HD double integrate_fast(const Basis& b, const double (*t)[SK_MAXP], const double* rc, const double* u) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        double num = 0.0;
+#pragma unroll
+        for (int n = 0; n < P; ++n) num = fma(t[q][n], u[n], num);
+        acc = fma(b.weights[q], num * rc[q], acc);
+    }
+    return acc;
+}
+template <int P>
+SK_HD bool indicator_meanerr_fast(const Basis& b, const PostCfg& c, const double* um, const double* u0,
+                                  const double* up) {
+    const double mean_m = mean_f<P, true>(b, um);
+    const double mean_0 = mean_f<P, true>(b, u0);
+    const double mean_p = mean_f<P, true>(b, up);
+    const double denom = fmax(fabs(mean_m), fmax(fabs(mean_0), fabs(mean_p)));
+    if (!(denom > 0.0)) return false;
+    const double ext_m = integrate_fast<P>(b, c.ipt, c.iprc, um);
+    const double ext_p = integrate_fast<P>(b, c.imt, c.imrc, up);
+    return fabs(ext_m - mean_0) + fabs(ext_p - mean_0) > c.threshold * denom;
 }
 
 template <int P>
