@@ -449,11 +449,13 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 
     if (warp == C::NC) {
         // ---------------- producer warp ----------------
-        // lane 0 streams windows with TMA; for even P (bulk copies then land
-        // exactly on cell boundaries) all 32 lanes first write the window cells
-        // outside the copyable range -- walls, 3-block ghosts, periodic wrap --
-        // so the consumers never wait on each other for edge tiles
-        constexpr bool PFILL = (P % 2) == 0;
+        // lane 0 streams windows with TMA (bulk copies cover only the 16-byte
+        // aligned interior of the valid cells; lane 0 moves the <= 2 leftover
+        // doubles itself), so no copy lands outside the valid cells and all 32
+        // lanes can write the window cells outside that range -- walls, 3-block
+        // ghosts, periodic wrap -- before the stage is armed: the consumers
+        // never wait on each other for edge tiles
+        constexpr bool PFILL = true;
         auto row_of = [&](const XTile& x) -> const double* {
             return a.tab[x.sp] + ((long long)g.cls[x.b] * a.nlines + x.line) * C::NF;
         };
@@ -519,19 +521,26 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * a.vg[x.sp]->dx;
                 }
                 unsigned bytes = C::NF * 8;
-                long long g0 = 0, g1 = 0;
+                long long ga = 0, gb = 0;
                 if (chi > clo) {
-                    g0 = eg + (long long)(clo - s0) * P;
-                    g1 = eg + (long long)(chi - s0) * P;
-                    g0 &= ~1LL;
-                    g1 = (g1 + 1) & ~1LL;
-                    bytes += (unsigned)(g1 - g0) * 8;
+                    // element g of the line sits at st + 2 + woff + (g - eg): same
+                    // parity in HBM and shared memory
+                    const long long g0 = eg + (long long)(clo - s0) * P;
+                    const long long g1 = eg + (long long)(chi - s0) * P;
+                    ga = (g0 + 1) & ~1LL;
+                    gb = g1 & ~1LL;
+                    if (gb < ga) gb = ga;
+                    double* wbase = st + 2 + woff - eg;
+                    const double* gsrc = srcp(x.sp);
+                    for (long long g = g0; g < ga && g < g1; ++g) wbase[g] = gsrc[g];
+                    for (long long g = gb > g0 ? gb : g0; g < g1; ++g) wbase[g] = gsrc[g];
+                    bytes += (unsigned)(gb - ga) * 8;
                 }
                 mbar_expect_tx(&full[stg], bytes);
                 tma_load_1d(st + C::WIN, row_of(x), C::NF * 8, &full[stg]);
-                if (chi > clo) {
-                    double* dst = st + 2 + woff + (g0 - eg);
-                    tma_load_1d(dst, srcp(x.sp) + g0, (unsigned)(g1 - g0) * 8, &full[stg]);
+                if (gb > ga) {
+                    double* dst = st + 2 + woff + (ga - eg);
+                    tma_load_1d(dst, srcp(x.sp) + ga, (unsigned)(gb - ga) * 8, &full[stg]);
                 }
             }
         }
@@ -571,29 +580,6 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         const long long lbase = (long long)line * g.ncells * P;
         const long long eg = lbase + ((long long)g.start[b] + s0) * P;
         const double* win = st + 2 + (int)(eg & 1);  // window cell w, node n at win[w*P+n]
-        if (P % 2 != 0 && (clo > s0 || chi < s0 + nt + 1)) {
-            // (odd P) walls (zero inflow), 3-block ghosts, periodic wrap: only
-            // the window cells outside [clo, chi) -- usually |i*|+1 of them
-            const double* src = srcp(sp) + lbase;
-            double* w = const_cast<double*>(win);
-            const int nlo = (max(clo, s0) - s0) * P;                 // [0, nlo)
-            const int nhi0 = (min(max(chi, s0), s0 + nt + 1) - s0) * P;  // [nhi0, (nt+1)P)
-            const int nfill = nlo + ((nt + 1) * P - nhi0);
-            for (int f = tid; f < nfill; f += C::NT) {
-                const int e = f < nlo ? f : nhi0 + (f - nlo);
-                const int wc = e / P, n = e - (e / P) * P;
-                const int s = s0 + wc;
-                double v;
-                if (a.periodic) {
-                    const int ss = ((s % cells_b) + cells_b) % cells_b;
-                    v = src[(long long)(g.start[b] + ss) * P + n];
-                } else {
-                    v = x_fetch_outside<P>(a.basis, g, src, b, s, n);
-                }
-                w[e] = v;
-            }
-            consumer_sync(C::NT);
-        }
         double ul[C::CPT][P], ur[C::CPT][P], o[C::CPT][P];
 #pragma unroll
         for (int cc = 0; cc < C::CPT; ++cc) {
