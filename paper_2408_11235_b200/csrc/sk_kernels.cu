@@ -307,6 +307,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         "r"(parity), "n"(1000000)
         : "memory");
 }
+// the barrier's current phase also waits for this thread's prior cp.async
+// copies (pending count +1 now, -1 when they land)
+__device__ __forceinline__ void mbar_cp_async_arrive(unsigned long long* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, unsigned bytes,
                                             unsigned long long* bar) {
     asm volatile(
@@ -532,8 +537,10 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     if (gb < ga) gb = ga;
                     double* wbase = st + 2 + woff - eg;
                     const double* gsrc = srcp(x.sp);
-                    for (long long g = g0; g < ga && g < g1; ++g) wbase[g] = gsrc[g];
-                    for (long long g = gb > g0 ? gb : g0; g < g1; ++g) wbase[g] = gsrc[g];
+                    bool any = false;  // leftovers: async, completion tracked by the stage barrier
+                    for (long long g = g0; g < ga && g < g1; ++g, any = true) cp_async8(wbase + g, gsrc + g, true);
+                    for (long long g = gb > g0 ? gb : g0; g < g1; ++g, any = true) cp_async8(wbase + g, gsrc + g, true);
+                    if (any) mbar_cp_async_arrive(&full[stg]);
                     bytes += (unsigned)(gb - ga) * 8;
                 }
                 mbar_expect_tx(&full[stg], bytes);
