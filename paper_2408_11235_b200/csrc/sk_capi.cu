@@ -78,6 +78,9 @@ struct sk_ctx {
     unsigned int* fix_count = nullptr;
     unsigned int fix_cap = 0;
     unsigned int fix_alloc = 0;
+    double* xghost = nullptr;          // 3-block ghost cells (xghost_kernel)
+    size_t xghost_n = 0;
+    int xghost_cap = 16;               // ghost cells per (species, line, block)
 };
 
 struct sk_field {
@@ -266,6 +269,27 @@ sk_status enq_xtab(sk_field** fs, int nspecies, double tau, const double* sqrt_m
     return SK_OK;
 }
 
+size_t xghost_doubles(const sk_ctx* c, int nlines) {
+    return (size_t)2 * nlines * c->grid.nblocks * c->xghost_cap * c->P;
+}
+
+// sized outside graph capture (sk_state_create, or the first eager sweep)
+sk_status ensure_xghost(sk_ctx* c, int nlines) {
+    if (!xghost_grid(c->grid)) return SK_OK;
+    const size_t want = xghost_doubles(c, nlines);
+    if (want <= c->xghost_n) return SK_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return SK_OK;
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->xghost);
+    c->xghost = nullptr;
+    c->xghost_n = 0;
+    CK(dalloc(&c->xghost, want));
+    c->xghost_n = want;
+    return SK_OK;
+}
+
 sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
                      int check_finite, double* rho_out = nullptr) {
     sk_ctx* c = fs[0]->ctx;
@@ -310,6 +334,18 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
         a.rho_partial = c->rho_fpart;
         a.rho_corr = c->rho_corr;
         CK(cudaMemsetAsync(c->rho_corr, 0, sizeof(unsigned long long) * nxd * 2 * kRhoCorrCopies, c->stream));
+    }
+    if (!periodic && xghost_grid(c->grid)) {
+        // ghost cells across the dx jumps: precomputed so the sweep only copies
+        // them (without a buffer -- first use inside a capture -- the sweep
+        // evaluates them itself)
+        if (sk_status rc = ensure_xghost(c, a.nlines)) return rc;
+        if (c->xghost_n >= xghost_doubles(c, a.nlines)) {
+            a.ghost = c->xghost;
+            a.ghost_cap = c->xghost_cap;
+            CK(launch_xghost(a, c->stream));
+            c->launches += 1;
+        }
     }
     if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
@@ -683,6 +719,7 @@ sk_status sk_ctx_destroy(sk_ctx* c) {
     cudaFree(c->fix_count);
     cudaFree(c->rho_fpart);
     cudaFree(c->rho_corr);
+    cudaFree(c->xghost);
     cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -721,6 +758,19 @@ sk_status ensure_fix_capacity(sk_ctx* c, size_t cells) {
     CK(dalloc(&c->fix_list, want));
     c->fix_alloc = c->fix_cap = (unsigned)want;
     return SK_OK;
+}
+
+// ghost capacity from the run's largest x shift (half step, fastest species,
+// finest block) -- cells beyond it would be evaluated inside the sweep
+sk_status ensure_xghost_cfg(sk_ctx* c, const sk_run_config* cfg, int nlines) {
+    if (!xghost_grid(c->grid)) return SK_OK;
+    double dxmin = c->grid.dx[0];
+    for (int b = 1; b < c->grid.nblocks; ++b) dxmin = std::min(dxmin, c->grid.dx[b]);
+    const double vmax = std::max(std::fabs(cfg->vmax_e), std::fabs(cfg->vmax_i) / std::sqrt(cfg->mu));
+    const double shift = vmax * 0.5 * cfg->dt / dxmin;
+    const int cap = shift < 250.0 ? (int)std::ceil(shift) + 2 : 252;
+    if (cap > c->xghost_cap) c->xghost_cap = cap;
+    return ensure_xghost(c, nlines);
 }
 }  // namespace
 
@@ -1069,6 +1119,7 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         const size_t cells = 2 * (size_t)cfg->v_cells * c->P * c->grid.ncells;
         if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 64)) return rc;
     }
+    if (sk_status rc = ensure_xghost_cfg(c, cfg, cfg->v_cells * c->P)) return rc;
     auto* s = new sk_state;
     s->ctx = c;
     s->cfg = *cfg;
@@ -1140,6 +1191,7 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
         const size_t cells = 2 * (size_t)ncell * c->P * c->grid.ncells;
         if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 64)) return rc;
     }
+    if (sk_status rc = ensure_xghost_cfg(c, cfg, ncell * c->P)) return rc;
     // a velocity shrink maps new cell j to old cells up to p*nv/2 cells closer
     // to v = 0 (adaptivity.cpp:52-90): shards keep a halo that wide, filled
     // only on shrink steps

@@ -21,6 +21,7 @@
 // All arithmetic is fp64 with -fmad=false so per-cell results are bitwise the
 // reference's.
 #include <algorithm>
+#include <type_traits>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -226,7 +227,7 @@ __global__ void xtab_kernel(const __grid_constant__ XTabArgs a) {
 
 // ghost cell value for block-local cell s outside [0, cells_b) (fill_ghost,
 // adaptivity.cpp:169-207): copy / coarse_to_fine piece / fine_to_coarse.
-template <int P>
+template <int P, int MC = 0>
 __device__ double x_fetch_outside(const Basis& basis, const Grid& g, const double* line, int b,
                                   int s, int n) {
     const bool left = s < 0;
@@ -248,19 +249,19 @@ __device__ double x_fetch_outside(const Basis& basis, const Grid& g, const doubl
         return line[(long long)src * P + n];
     }
     if (g.dx[nb] > g.dx[b]) {
-        int m = (int)llround(g.dx[nb] / g.dx[b]);
+        const int m = MC > 0 ? MC : (int)llround(g.dx[nb] / g.dx[b]);
         int coarse = left ? iface - 1 - (j - 1) / m : iface + (j - 1) / m;
         if (coarse < nb_begin || coarse >= nb_end) return 0.0;
         int piece = left ? m - 1 - (j - 1) % m : (j - 1) % m;
         double u[P];
 #pragma unroll
         for (int q = 0; q < P; ++q) u[q] = line[(long long)coarse * P + q];
-        return coarse_to_fine_node<P>(basis, u, m, piece, n);
+        return coarse_to_fine_node<P, MC>(basis, u, m, piece, n);
     }
-    int m = (int)llround(g.dx[b] / g.dx[nb]);
+    const int m = MC > 0 ? MC : (int)llround(g.dx[b] / g.dx[nb]);
     int lo = left ? iface - j * m : iface + (j - 1) * m;
     if (lo < nb_begin || lo + m > nb_end) return 0.0;
-    return fine_to_coarse_node<P>(basis, line + (long long)lo * P, m, n);
+    return fine_to_coarse_node<P, MC>(basis, line + (long long)lo * P, m, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -339,6 +340,52 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+
+// does block b's side (0 left, 1 right) border a block of another dx? Those
+// ghost cells are projections (fill_ghost) and come from the xghost buffer
+__device__ __forceinline__ bool xghost_side(const Grid& g, int b, int side) {
+    const int nb = side == 0 ? b - 1 : b + 1;
+    return nb >= 0 && nb < g.nblocks && g.dx[nb] != g.dx[b];
+}
+
+// K1a: 3-block ghost pre-pass, one warp per (species, line, block). A line's
+// windows in block b span cells [istar, cells_b + istar + 1), so they reach
+// -istar cells past the left edge (istar < 0) or istar + 1 past the right one.
+// Those across a dx jump are evaluated here with x_fetch_outside's arithmetic
+// (adaptivity.cpp:169-207), off the sweep producer's critical path: its fill
+// is then an asynchronous copy, not a chain of dependent loads.
+template <int P>
+__global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ XSweepArgs a) {
+    const Grid& g = a.grid;
+    const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    const int nb = g.nblocks;
+    if (w >= a.nspecies * a.nlines * nb) return;
+    const int b = w % nb;
+    const int line = (w / nb) % a.nlines;
+    const int sp = a.species0 + w / (nb * a.nlines);
+    const int istar = (int)__ldg(a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * xnf<P>());
+    const int side = istar < 0 ? 0 : 1;
+    if (!xghost_side(g, b, side)) return;
+    const int need = min(side == 0 ? -istar : istar + 1, a.ghost_cap);
+    const double* src = (field_flipped(a.flip[sp]) ? a.dst[sp] : a.src[sp]) + (long long)line * g.ncells * P;
+    double* out = a.ghost + ((long long)(sp * a.nlines + line) * nb + b) * a.ghost_cap * P;
+    const int nbr = side == 0 ? b - 1 : b + 1;
+    const int m = (int)llround(g.dx[nbr] > g.dx[b] ? g.dx[nbr] / g.dx[b] : g.dx[b] / g.dx[nbr]);
+    auto fill = [&](auto mc) {
+        constexpr int MC = decltype(mc)::value;
+        for (int e = lane; e < need * P; e += 32) {
+            const int j = e / P + 1, n = e - (e / P) * P;
+            out[e] = x_fetch_outside<P, MC>(a.basis, g, src, b, side == 0 ? -j : g.cells[b] - 1 + j, n);
+        }
+    };
+    switch (m) {  // the usual refinement ratios unrolled; others at run time
+        case 2: fill(std::integral_constant<int, 2>{}); break;
+        case 4: fill(std::integral_constant<int, 4>{}); break;
+        case 8: fill(std::integral_constant<int, 8>{}); break;
+        case 16: fill(std::integral_constant<int, 16>{}); break;
+        default: fill(std::integral_constant<int, 0>{}); break;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -464,18 +511,31 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         auto row_of = [&](const XTile& x) -> const double* {
             return a.tab[x.sp] + ((long long)g.cls[x.b] * a.nlines + x.line) * C::NF;
         };
-        if (PFILL || lane == 0) {
-            XTile xn = decode_xtile(a, vb, C::T);
-            int istar_next = vb < ntot ? (int)__ldg(row_of(xn)) : 0;
+        // (sign * w_vn) * dv of a v row: dv per species, loaded once
+        [[maybe_unused]] double dvs[2] = {0.0, 0.0};
+        if (RHO && lane == 0)
+            for (int i = 0; i < 2; ++i)
+                if (a.vg[i]) dvs[i] = a.vg[i]->dx;
+        static_assert(PFILL, "the istar batches need all producer lanes");
+        {
+            // table shifts of this CTA's tiles in batches of 32, one per lane,
+            // loaded a batch ahead: short tiles (3-block meshes) would otherwise
+            // wait out one load latency each
+            auto batch_istar = [&](int it0) -> int {
+                const long long t = vb + (long long)(it0 + lane) * G;
+                return t < ntot ? (int)__ldg(row_of(decode_xtile(a, (int)t, C::T))) : 0;
+            };
+            int ist_cur = batch_istar(0);
+            int ist_nxt = batch_istar(32);
             int it = 0;
             for (int t = vb; t < ntot; t += G, ++it) {
                 const int stg = it % C::S;
-                const XTile x = xn;
-                const int istar = istar_next;
-                if (t + G < ntot) {  // hide the table latency behind this tile
-                    xn = decode_xtile(a, t + G, C::T);
-                    istar_next = (int)__ldg(row_of(xn));
+                if ((it & 31) == 0 && it > 0) {
+                    ist_cur = ist_nxt;
+                    ist_nxt = batch_istar(it + 32);
                 }
+                const XTile x = decode_xtile(a, t, C::T);
+                const int istar = __shfl_sync(0xffffffffu, ist_cur, it & 31);
                 mbar_wait(&empty[stg], ((it / C::S) & 1) ^ 1);
                 const int s0 = x.c0 + istar;
                 int vlo, vhi;
@@ -494,19 +554,30 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                         const int nlo = (max(clo, s0) - s0) * P;
                         const int nhi0 = (min(max(chi, s0), s0 + x.nt + 1) - s0) * P;
                         const int nfill = nlo + ((x.nt + 1) * P - nhi0);
+                        const double* gh = a.ghost ? a.ghost + ((long long)(x.sp * a.nlines + x.line) * g.nblocks + x.b) *
+                                                                   a.ghost_cap * P
+                                                   : nullptr;
+                        bool anyc = false;  // async fills: tracked by the stage barrier
                         for (int f = lane; f < nfill; f += 32) {
                             const int e = f < nlo ? f : nhi0 + (f - nlo);
                             const int wc = e / P, n = e - (e / P) * P;
                             const int sc = s0 + wc;
-                            double v;
                             if (a.periodic) {
                                 const int ss = ((sc % cells_b) + cells_b) % cells_b;
-                                v = src[(long long)(g.start[x.b] + ss) * P + n];
-                            } else {
-                                v = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n);
+                                cp_async8(w + e, src + (long long)(g.start[x.b] + ss) * P + n, true);
+                                anyc = true;
+                                continue;
                             }
-                            w[e] = v;
+                            const int side = sc < 0 ? 0 : 1;
+                            const int j = side == 0 ? -sc : sc - cells_b + 1;
+                            if (gh && j <= a.ghost_cap && xghost_side(g, x.b, side)) {
+                                cp_async8(w + e, gh + (j - 1) * P + n, true);
+                                anyc = true;
+                            } else {
+                                w[e] = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n);
+                            }
                         }
+                        if (anyc) mbar_cp_async_arrive(&full[stg]);
                     }
                     __syncwarp();  // fills ordered before lane 0's arrive (release)
                     if (lane != 0) continue;
@@ -523,7 +594,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 hdr[7] = chi;
                 if (RHO) {  // (sign * w_vn) * dv of this v row (poisson.cpp:207)
                     const int vn = x.line - (x.line / P) * P;
-                    reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * a.vg[x.sp]->dx;
+                    reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * dvs[x.sp];
                 }
                 unsigned bytes = C::NF * 8;
                 long long ga = 0, gb = 0;
@@ -2195,6 +2266,19 @@ static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     if (cudaError_t e = xsweep_plan<P, INLINE, RHO, FMA>(a, b, grid)) return e;
     xsweep_kernel<P, INLINE, RHO, FMA><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
     return cudaGetLastError();
+}
+
+template <int P>
+static cudaError_t launch_xghost_t(const XSweepArgs& a, cudaStream_t s) {
+    const long long warps = (long long)a.nspecies * a.nlines * a.grid.nblocks;
+    const int grid = (int)((warps * 32 + 255) / 256);
+    if (grid > 0) xghost_kernel<P><<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xghost(const XSweepArgs& a, cudaStream_t s) {
+    SK_DISPATCH_P(a.basis.p, return launch_xghost_t<PP>(a, s))
+    return cudaErrorInvalidValue;
 }
 
 template <int P, bool INLINE, bool RHO>

@@ -67,6 +67,11 @@ struct XSweepArgs {
     unsigned long long* rho_corr;
     const DevVGrid* vg[2];
     double charge_w[2];   // +1 ions, -1 electrons (poisson.cpp:202-214)
+    // 3-block ghost cells across a dx jump, precomputed by xghost_kernel:
+    // [(sp * nlines + line) * nblocks + b][j - 1][P], j = 1..ghost_cap cells
+    // outward on the side the line's shift reaches (null: computed in-kernel)
+    double* ghost;
+    int ghost_cap;
 };
 
 struct VTabArgs {
@@ -203,6 +208,14 @@ struct PostArgs {
 // launchers (P = k+1 dispatch inside)
 cudaError_t launch_xtab(const XTabArgs& a, cudaStream_t s);
 cudaError_t launch_xsweep(const XSweepArgs& a, int ntiles, cudaStream_t s);
+// 3-block ghost pre-pass (a.ghost, a.ghost_cap set); needed only when adjacent
+// blocks differ in dx and the boundary is not periodic
+cudaError_t launch_xghost(const XSweepArgs& a, cudaStream_t s);
+inline bool xghost_grid(const Grid& g) {
+    for (int b = 0; b + 1 < g.nblocks; ++b)
+        if (g.dx[b] != g.dx[b + 1]) return true;
+    return false;
+}
 cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s);
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_xfix(const XSweepArgs& a, cudaStream_t s);

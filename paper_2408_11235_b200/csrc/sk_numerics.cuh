@@ -814,16 +814,21 @@ SK_HD void modify_line_weno(const Basis& b, const double* um, const double* u0, 
 }
 
 // ---------------- sheath-mesh transfer (adaptivity.cpp:132-156) ----------------
+// (MC > 0: the refinement ratio m == MC known at compile time, so the loops
+// unroll and every load issues up front -- same operations, same order)
 // coarse_to_fine, one piece, one node: evaluate(coarse, (piece + x_q)/m)
-template <int P>
+template <int P, int MC = 0>
 SK_HD double coarse_to_fine_node(const Basis& b, const double* coarse, int m, int piece, int q) {
+    if constexpr (MC > 0) m = MC;
     return evaluate<P>(b, coarse, (piece + b.nodes[q]) / m);
 }
 
 // fine_to_coarse, output node mm, from m consecutive fine cells (stride P)
-template <int P>
+template <int P, int MC = 0>
 SK_HD double fine_to_coarse_node(const Basis& b, const double* fine, int m, int mm) {
+    if constexpr (MC > 0) m = MC;
     double acc = 0.0;
+#pragma unroll (MC > 0 ? MC : 1)
     for (int j = 0; j < m; ++j) {
         const double* cell = fine + j * P;
 #pragma unroll
