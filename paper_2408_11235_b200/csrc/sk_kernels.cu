@@ -349,41 +349,67 @@ __device__ __forceinline__ bool xghost_side(const Grid& g, int b, int side) {
     return nb >= 0 && nb < g.nblocks && g.dx[nb] != g.dx[b];
 }
 
-// K1a: 3-block ghost pre-pass, one warp per (species, line, block). A line's
-// windows in block b span cells [istar, cells_b + istar + 1), so they reach
-// -istar cells past the left edge (istar < 0) or istar + 1 past the right one.
-// Those across a dx jump are evaluated here with x_fetch_outside's arithmetic
-// (adaptivity.cpp:169-207), off the sweep producer's critical path: its fill
-// is then an asynchronous copy, not a chain of dependent loads.
+// K1a: 3-block ghost pre-pass, one warp per (species, line). A line's windows
+// in block b span cells [istar_b, cells_b + istar_b + 1), so they reach
+// -istar_b cells past the left edge (istar_b < 0) or istar_b + 1 past the
+// right one. Those across a dx jump are evaluated here with x_fetch_outside's
+// arithmetic (adaptivity.cpp:169-207), off the sweep producer's critical path:
+// its fill is then an asynchronous copy, not a chain of dependent loads. The
+// lanes load the blocks' shifts together and share the line's ghost values.
 template <int P>
 __global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ XSweepArgs a) {
     const Grid& g = a.grid;
     const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     const int nb = g.nblocks;
-    if (w >= a.nspecies * a.nlines * nb) return;
-    const int b = w % nb;
-    const int line = (w / nb) % a.nlines;
-    const int sp = a.species0 + w / (nb * a.nlines);
-    const int istar = (int)__ldg(a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * xnf<P>());
-    const int side = istar < 0 ? 0 : 1;
-    if (!xghost_side(g, b, side)) return;
-    const int need = min(side == 0 ? -istar : istar + 1, a.ghost_cap);
+    if (w >= a.nspecies * a.nlines) return;
+    const int line = w % a.nlines;
+    const int sp = a.species0 + w / a.nlines;
+    int ist = 0, cnt = 0, ratio = 0;
+    if (lane < nb) {
+        ist = (int)__ldg(a.tab[sp] + ((long long)g.cls[lane] * a.nlines + line) * xnf<P>());
+        const int side = ist < 0 ? 0 : 1;
+        if (xghost_side(g, lane, side)) {
+            cnt = min(side == 0 ? -ist : ist + 1, a.ghost_cap) * P;
+            const double d0 = g.dx[lane], d1 = g.dx[side == 0 ? lane - 1 : lane + 1];
+            ratio = (int)llround(d1 > d0 ? d1 / d0 : d0 / d1);
+        }
+    }
+    int pre[kMaxBlocks + 1], sgn[kMaxBlocks];
+    pre[0] = 0;
+#pragma unroll
+    for (int b = 0; b < kMaxBlocks; ++b) {
+        pre[b + 1] = pre[b] + __shfl_sync(0xffffffffu, cnt, b);
+        sgn[b] = __shfl_sync(0xffffffffu, ist, b) < 0 ? 0 : 1;
+    }
+    const int total = pre[kMaxBlocks];
+    if (total == 0) return;
+    // one refinement ratio for all jumps (the 3-block mesh): unrolled loops
+    const int rmax = __reduce_max_sync(0xffffffffu, ratio);
+    const int rmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)(ratio > 0 ? ratio : 0x7fffffff));
+    const int m = rmax == rmin ? rmax : 0;
     const double* src = (field_flipped(a.flip[sp]) ? a.dst[sp] : a.src[sp]) + (long long)line * g.ncells * P;
-    double* out = a.ghost + ((long long)(sp * a.nlines + line) * nb + b) * a.ghost_cap * P;
-    const int nbr = side == 0 ? b - 1 : b + 1;
-    const int m = (int)llround(g.dx[nbr] > g.dx[b] ? g.dx[nbr] / g.dx[b] : g.dx[b] / g.dx[nbr]);
+    double* out = a.ghost + (long long)(sp * a.nlines + line) * nb * a.ghost_cap * P;
     auto fill = [&](auto mc) {
         constexpr int MC = decltype(mc)::value;
-        for (int e = lane; e < need * P; e += 32) {
-            const int j = e / P + 1, n = e - (e / P) * P;
-            out[e] = x_fetch_outside<P, MC>(a.basis, g, src, b, side == 0 ? -j : g.cells[b] - 1 + j, n);
+        for (int e = lane; e < total; e += 32) {
+            int b = 0, base = 0, sg = 0;  // last block starting at or before e (register selects)
+#pragma unroll
+            for (int k = 0; k < kMaxBlocks; ++k)
+                if (e >= pre[k]) {
+                    b = k;
+                    base = pre[k];
+                    sg = sgn[k];
+                }
+            const int l = e - base;
+            const int j = l / P + 1, n = l - (l / P) * P;
+            out[(long long)b * a.ghost_cap * P + l] =
+                x_fetch_outside<P, MC>(a.basis, g, src, b, sg == 0 ? -j : g.cells[b] - 1 + j, n);
         }
     };
     switch (m) {  // the usual refinement ratios unrolled; others at run time
         case 2: fill(std::integral_constant<int, 2>{}); break;
         case 4: fill(std::integral_constant<int, 4>{}); break;
         case 8: fill(std::integral_constant<int, 8>{}); break;
-        case 16: fill(std::integral_constant<int, 16>{}); break;
         default: fill(std::integral_constant<int, 0>{}); break;
     }
 }
@@ -658,87 +684,104 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         const long long lbase = (long long)line * g.ncells * P;
         const long long eg = lbase + ((long long)g.start[b] + s0) * P;
         const double* win = st + 2 + (int)(eg & 1);  // window cell w, node n at win[w*P+n]
-        double ul[C::CPT][P], ur[C::CPT][P], o[C::CPT][P];
+        // cells per thread this warp has in this tile (warp-uniform): short
+        // tiles (3-block meshes) skip the idle slots instead of recomputing
+        const int ncc = min(C::CPT, nt > warp * 32 + C::NT ? 2 : (nt > warp * 32 ? 1 : 0));
+        auto cells = [&](auto ncc_c) {
+            constexpr int NCC = decltype(ncc_c)::value;
+            double ul[NCC][P], ur[NCC][P], o[NCC][P];
 #pragma unroll
-        for (int cc = 0; cc < C::CPT; ++cc) {
-            const int c = min(tid + cc * C::NT, nt - 1);
-            lds_cell<P>(win + c * P, ul[cc]);
-            lds_cell<P>(win + (c + 1) * P, ur[cc]);
-        }
-        // advection.cpp:95-101, both cells share each broadcast matrix load
+            for (int cc = 0; cc < NCC; ++cc) {
+                const int c = min(tid + cc * C::NT, nt - 1);
+                lds_cell<P>(win + c * P, ul[cc]);
+                lds_cell<P>(win + (c + 1) * P, ur[cc]);
+            }
+            // advection.cpp:95-101, both cells share each broadcast matrix load
 #pragma unroll
-        for (int m = 0; m < P; ++m) {
-            double acc[C::CPT];
+            for (int m = 0; m < P; ++m) {
+                double acc[NCC];
 #pragma unroll
-            for (int cc = 0; cc < C::CPT; ++cc) acc[cc] = 0.0;
-            double am[P], bm[P];
-            lds_cell<P>(row + 2 + m * P, am);
-            lds_cell<P>(row + 2 + P * P + m * P, bm);
+                for (int cc = 0; cc < NCC; ++cc) acc[cc] = 0.0;
+                double am[P], bm[P];
+                lds_cell<P>(row + 2 + m * P, am);
+                lds_cell<P>(row + 2 + P * P + m * P, bm);
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
+                for (int j = 0; j < P; ++j) {
 #pragma unroll
-                for (int cc = 0; cc < C::CPT; ++cc) {
-                    if constexpr (FMA)
-                        acc[cc] = fma(bm[j], ur[cc][j], fma(am[j], ul[cc][j], acc[cc]));
-                    else
-                        acc[cc] += am[j] * ul[cc][j] + bm[j] * ur[cc][j];
+                    for (int cc = 0; cc < NCC; ++cc) {
+                        if constexpr (FMA)
+                            acc[cc] = fma(bm[j], ur[cc][j], fma(am[j], ul[cc][j], acc[cc]));
+                        else
+                            acc[cc] += am[j] * ul[cc][j] + bm[j] * ur[cc][j];
+                    }
+                }
+#pragma unroll
+                for (int cc = 0; cc < NCC; ++cc) o[cc][m] = acc[cc];
+            }
+            double wdv = 0.0;
+            if constexpr (RHO) wdv = reinterpret_cast<const double*>(hdr)[4];
+            [[maybe_unused]] bool tr[NCC];
+            [[maybe_unused]] unsigned long long entry[NCC];
+#pragma unroll
+            for (int cc = 0; cc < NCC; ++cc) {
+                const int c = tid + cc * C::NT;
+                if constexpr (INLINE) {
+                    const double* ext = row + 2 + 2 * P * P;
+                    tr[cc] = c < nt && inline_indicator_m<P, FMA>(cut, ext, ext + P, mean_f<P, FMA>(a.basis, ul[cc]),
+                                                                  mean_f<P, FMA>(a.basis, ur[cc]), o[cc]);
+                    entry[cc] = ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
+                                (unsigned)(g.start[b] + c0 + c);
+                }
+                if (c < nt) {
+                    if constexpr (RHO) {
+#pragma unroll
+                        for (int m = 0; m < P; ++m) rreg[cc][m] = madd<FMA>(rreg[cc][m], wdv, o[cc][m]);
+                    }
                 }
             }
+            if (a.check_finite) {  // stepper.cpp:99-102, only on the step's last sweep
 #pragma unroll
-            for (int cc = 0; cc < C::CPT; ++cc) o[cc][m] = acc[cc];
-        }
-        double wdv = 0.0;
-        if constexpr (RHO) wdv = reinterpret_cast<const double*>(hdr)[4];
-        [[maybe_unused]] bool tr[C::CPT];
-        [[maybe_unused]] unsigned long long entry[C::CPT];
-#pragma unroll
-        for (int cc = 0; cc < C::CPT; ++cc) {
-            const int c = tid + cc * C::NT;
-            if constexpr (INLINE) {
-                const double* ext = row + 2 + 2 * P * P;
-                tr[cc] = c < nt && inline_indicator_m<P, FMA>(cut, ext, ext + P, mean_f<P, FMA>(a.basis, ul[cc]),
-                                                              mean_f<P, FMA>(a.basis, ur[cc]), o[cc]);
-                entry[cc] = ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
-                            (unsigned)(g.start[b] + c0 + c);
+                for (int cc = 0; cc < NCC; ++cc)
+                    if (tid + cc * C::NT < nt) bad |= !all_finite<P>(o[cc]);
             }
-            if (c < nt) {
-                if constexpr (RHO) {
+            // the window stage is consumed (all that follows is in registers):
+            // hand it back before the queue atomics and the stores
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+            // troubled cells are queued for the fixup kernel (on overflow it rescans)
+            if constexpr (INLINE) defer_push_n<NCC>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+            double* dline = dstp(sp) + lbase + (long long)(g.start[b] + c0) * P;
 #pragma unroll
-                    for (int m = 0; m < P; ++m) rreg[cc][m] = madd<FMA>(rreg[cc][m], wdv, o[cc][m]);
-                }
-            }
-        }
-        // troubled cells are queued for the fixup kernel (on overflow it rescans)
-        if constexpr (INLINE) defer_push_n<C::CPT>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
-        if (a.check_finite) {  // stepper.cpp:99-102, only on the step's last sweep
+            for (int cc = 0; cc < NCC; ++cc) {
+                const int c = tid + cc * C::NT;
+                if (c < nt) {
+                    // straight to HBM: the warp's lanes cover 32 contiguous cells
+                    double* dp = dline + (long long)c * P;
+                    if constexpr (P % 2 == 0) {
+                        if ((((unsigned long long)dp) & 15) == 0) {
 #pragma unroll
-            for (int cc = 0; cc < C::CPT; ++cc)
-                if (tid + cc * C::NT < nt) bad |= !all_finite<P>(o[cc]);
-        }
-        // the window stage is consumed: hand it back before the stores
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stg]);
-        double* dline = dstp(sp) + lbase + (long long)(g.start[b] + c0) * P;
+                            for (int i = 0; i < P / 2; ++i)
+                                reinterpret_cast<double2*>(dp)[i] = make_double2(o[cc][2 * i], o[cc][2 * i + 1]);
+                        } else {
 #pragma unroll
-        for (int cc = 0; cc < C::CPT; ++cc) {
-            const int c = tid + cc * C::NT;
-            if (c < nt) {
-                // straight to HBM: the warp's lanes cover 32 contiguous cells
-                double* dp = dline + (long long)c * P;
-                if constexpr (P % 2 == 0) {
-                    if ((((unsigned long long)dp) & 15) == 0) {
-#pragma unroll
-                        for (int i = 0; i < P / 2; ++i)
-                            reinterpret_cast<double2*>(dp)[i] = make_double2(o[cc][2 * i], o[cc][2 * i + 1]);
+                            for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
+                        }
                     } else {
 #pragma unroll
                         for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
                     }
-                } else {
-#pragma unroll
-                    for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
                 }
             }
+        };
+        // (the fused-moment variant keeps one body: its register accumulators
+        // leave no room for a second)
+        if ((C::CPT == 2 && ncc == 2) || (RHO && ncc >= 1)) {
+            cells(std::integral_constant<int, C::CPT>{});
+        } else if (!RHO && ncc >= 1) {
+            cells(std::integral_constant<int, 1>{});
+        } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
         }
     }
     if (RHO && rcol_nt > 0) {
@@ -2270,7 +2313,7 @@ static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
 
 template <int P>
 static cudaError_t launch_xghost_t(const XSweepArgs& a, cudaStream_t s) {
-    const long long warps = (long long)a.nspecies * a.nlines * a.grid.nblocks;
+    const long long warps = (long long)a.nspecies * a.nlines;
     const int grid = (int)((warps * 32 + 255) / 256);
     if (grid > 0) xghost_kernel<P><<<grid, 256, 0, s>>>(a);
     return cudaGetLastError();
