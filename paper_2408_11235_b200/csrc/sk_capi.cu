@@ -269,8 +269,15 @@ sk_status enq_xtab(sk_field** fs, int nspecies, double tau, const double* sqrt_m
     return SK_OK;
 }
 
+// ghost cells per (species, line, block); SK_XGHOST_CAP overrides it (tests
+// force the in-kernel evaluation of the cells beyond a small capacity)
+int xghost_cap(const sk_ctx* c) {
+    const char* e = getenv("SK_XGHOST_CAP");
+    return e && atoi(e) > 0 ? atoi(e) : c->xghost_cap;
+}
+
 size_t xghost_doubles(const sk_ctx* c, int nlines) {
-    return (size_t)2 * nlines * c->grid.nblocks * c->xghost_cap * c->P;
+    return (size_t)2 * nlines * c->grid.nblocks * xghost_cap(c) * c->P;
 }
 
 // sized outside graph capture (sk_state_create, or the first eager sweep)
@@ -342,7 +349,7 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
         if (sk_status rc = ensure_xghost(c, a.nlines)) return rc;
         if (c->xghost_n >= xghost_doubles(c, a.nlines)) {
             a.ghost = c->xghost;
-            a.ghost_cap = c->xghost_cap;
+            a.ghost_cap = xghost_cap(c);
             CK(launch_xghost(a, c->stream));
             c->launches += 1;
         }

@@ -96,6 +96,27 @@ def test_sweeps_bitwise(sk, ora, kw, exact):
             o.set_field(sp, ref)
 
 
+@pytest.mark.parametrize("cap", [1, 3])
+@pytest.mark.parametrize("kw", [c for c in KERNEL_CFGS if c["m"] > 1][:3], ids=lambda d: f"k{d['k']}m{d['m']}")
+def test_x_ghosts_beyond_buffer_bitwise(sk, ora, kw, cap, monkeypatch):
+    """3-block ghosts: the pre-pass buffers ghost_cap cells per (line, block),
+    the sweep evaluates the ones further out itself. A tiny capacity and a
+    multi-cell shift run both paths in one sweep; exact mode stays bitwise."""
+    cfg, o, st = _pair(sk, ora, kw, True)
+    spar = [sk.SpeciesParams.electron(), sk.SpeciesParams.ion(cfg.mu)]
+    lim = sk.LimiterConfig.parse(cfg.limiter)
+    monkeypatch.setenv("SK_XGHOST_CAP", str(cap))
+    for sp in (0, 1):
+        f = st.field(sp)
+        for tau in (1.1, -2.3):
+            f.upload(o.field(sp))
+            sk.advect_x(f, tau, spar[sp], sk.SweepOptions(limiter=lim, max_ghost=-1))
+            ref = o.field(sp)
+            o.advect_x(sp, tau, limited=True, max_ghost=-1)
+            assert np.array_equal(f.download(), o.field(sp)), f"advect_x sp{sp} tau{tau} cap{cap}"
+            o.set_field(sp, ref)
+
+
 @pytest.mark.parametrize("mode", ["minmod+simple", "minmod+line", "meanerr+simple", "meanerr+line"])
 @pytest.mark.parametrize("m", [1, 4])
 def test_post_limiters_bitwise(sk, ora, mode, m):
