@@ -78,6 +78,8 @@ struct sk_ctx {
     unsigned int* fix_count = nullptr;
     unsigned int fix_cap = 0;
     unsigned int fix_alloc = 0;
+    double* fix_vals = nullptr;        // post-limiter modifications [fix_alloc][P]
+    size_t fix_vals_n = 0;
     double* xghost = nullptr;          // 3-block ghost cells (xghost_kernel)
     size_t xghost_n = 0;
     int xghost_cap = 16;               // ghost cells per (species, line, block)
@@ -274,6 +276,23 @@ sk_status enq_xtab(sk_field** fs, int nspecies, double tau, const double* sqrt_m
 int xghost_cap(const sk_ctx* c) {
     const char* e = getenv("SK_XGHOST_CAP");
     return e && atoi(e) > 0 ? atoi(e) : c->xghost_cap;
+}
+
+// post-limiter modification buffer, one row of P doubles per queue entry
+// (sized outside graph capture; a capture only checks it)
+sk_status ensure_fix_vals(sk_ctx* c) {
+    const size_t want = (size_t)c->fix_alloc * c->P;
+    if (want <= c->fix_vals_n) return SK_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return SK_OK;
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->fix_vals);
+    c->fix_vals = nullptr;
+    c->fix_vals_n = 0;
+    CK(dalloc(&c->fix_vals, want));
+    c->fix_vals_n = want;
+    return SK_OK;
 }
 
 size_t xghost_doubles(const sk_ctx* c, int nlines) {
@@ -473,16 +492,20 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     std::memcpy(a.tile_start, c->ptiles, sizeof a.tile_start);
     post_cfg_points(c->basis, a.cfg);
     a.fma = !c->exact;
+    if (sk_status rc = ensure_fix_vals(c)) return rc;
+    if (c->fix_vals_n < (size_t)c->fix_cap * c->P)
+        return fail(SK_ERR_RUNTIME, "internal: post-limiter buffers not sized");  // (first use in a capture)
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;
+    a.fix_vals = c->fix_vals;
     CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     if (dir == SK_DIR_X)
         CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
     else
         CK(launch_post_v(a, c->stream));
-    c->launches += 3;
-    for (int i = 0; i < nspecies; ++i) fs[i]->swap();
+    c->launches += 5;  // flag pass, overflow copy, fix, scatter, counter
+    // in place: the field stays in its buffer
     return SK_OK;
 }
 
@@ -727,6 +750,7 @@ sk_status sk_ctx_destroy(sk_ctx* c) {
     cudaFree(c->rho_fpart);
     cudaFree(c->rho_corr);
     cudaFree(c->xghost);
+    cudaFree(c->fix_vals);
     cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -1127,6 +1151,8 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 64)) return rc;
     }
     if (sk_status rc = ensure_xghost_cfg(c, cfg, cfg->v_cells * c->P)) return rc;
+    if (cfg->limiter.indicator)
+        if (sk_status rc = ensure_fix_vals(c)) return rc;
     auto* s = new sk_state;
     s->ctx = c;
     s->cfg = *cfg;
@@ -1199,6 +1225,8 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
         if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 64)) return rc;
     }
     if (sk_status rc = ensure_xghost_cfg(c, cfg, ncell * c->P)) return rc;
+    if (cfg->limiter.indicator)
+        if (sk_status rc = ensure_fix_vals(c)) return rc;
     // a velocity shrink maps new cell j to old cells up to p*nv/2 cells closer
     // to v = 0 (adaptivity.cpp:52-90): shards keep a halo that wide, filled
     // only on shrink steps

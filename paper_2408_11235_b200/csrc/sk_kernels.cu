@@ -414,6 +414,18 @@ __global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ 
     }
 }
 
+// literature post-limiter indicator of one cell from its x or v stencil
+template <int P, bool FAST = false>
+__device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, const double* um,
+                                          const double* u0, const double* up) {
+    if constexpr (FAST)
+        return cfg.indicator == 1 ? indicator_minmod_fast<P>(b, cfg, um, u0, up)
+                                  : indicator_meanerr_fast<P>(b, cfg, um, u0, up);
+    else
+        return cfg.indicator == 1 ? indicator_minmod_pre<P>(b, um, u0, up)
+                                  : indicator_meanerr_pre<P>(b, cfg, um, u0, up);
+}
+
 // ---------------------------------------------------------------------------
 // K1: x sweep -- warp-specialised TMA pipeline over tiles
 //   tile = (species, x row, block, T cells); its source window is T+1 cells
@@ -498,10 +510,17 @@ __device__ __forceinline__ void sts_cell(double* p, const double* u) {
     }
 }
 
-template <int P, bool INLINE, bool RHO, bool FMA>
+// MODE 0: the x sweep. MODE 1: the post-limiter flag pass in x (limiters.cpp:
+// 254-345) on the same pipeline -- window = the tile's cells and one neighbour
+// on each side (tiles of T-1 cells), no table row, the literature indicator
+// per cell, flagged cells queued; in place (nothing stored).
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
+    static_assert(MODE == 0 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
+    constexpr int TT = MODE == 1 ? C::T - 1 : C::T;  // cells per tile
+    constexpr int WX = MODE == 1 ? 2 : 1;            // window cells beyond the tile
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;                                   // S x STAGE
     double* racc = smem + C::S * C::STAGE;                   // [T][P] this CTA's column (RHO)
@@ -549,7 +568,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             // wait out one load latency each
             auto batch_istar = [&](int it0) -> int {
                 const long long t = vb + (long long)(it0 + lane) * G;
-                return t < ntot ? (int)__ldg(row_of(decode_xtile(a, (int)t, C::T))) : 0;
+                if constexpr (MODE == 1) return -1;  // window starts one cell left
+                return t < ntot ? (int)__ldg(row_of(decode_xtile(a, (int)t, TT))) : 0;
             };
             int ist_cur = batch_istar(0);
             int ist_nxt = batch_istar(32);
@@ -560,26 +580,26 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     ist_cur = ist_nxt;
                     ist_nxt = batch_istar(it + 32);
                 }
-                const XTile x = decode_xtile(a, t, C::T);
+                const XTile x = decode_xtile(a, t, TT);
                 const int istar = __shfl_sync(0xffffffffu, ist_cur, it & 31);
                 mbar_wait(&empty[stg], ((it / C::S) & 1) ^ 1);
                 const int s0 = x.c0 + istar;
                 int vlo, vhi;
                 xvalid_range(a, x.b, vlo, vhi);
-                const int clo = max(s0, vlo), chi = min(s0 + x.nt + 1, vhi);
+                const int clo = max(s0, vlo), chi = min(s0 + x.nt + WX, vhi);
                 double* st = stages + stg * C::STAGE;
                 // element parity of window cell s0 in HBM decides the smem origin
                 const long long lbase = (long long)x.line * g.ncells * P;
                 const long long eg = lbase + ((long long)g.start[x.b] + s0) * P;
                 const int woff = (int)(eg & 1);
                 if constexpr (PFILL) {
-                    if (clo > s0 || chi < s0 + x.nt + 1) {
+                    if (clo > s0 || chi < s0 + x.nt + WX) {
                         const double* src = srcp(x.sp) + lbase;
                         double* w = st + 2 + woff;
                         const int cells_b = g.cells[x.b];
                         const int nlo = (max(clo, s0) - s0) * P;
-                        const int nhi0 = (min(max(chi, s0), s0 + x.nt + 1) - s0) * P;
-                        const int nfill = nlo + ((x.nt + 1) * P - nhi0);
+                        const int nhi0 = (min(max(chi, s0), s0 + x.nt + WX) - s0) * P;
+                        const int nfill = nlo + ((x.nt + WX) * P - nhi0);
                         const double* gh = a.ghost ? a.ghost + ((long long)(x.sp * a.nlines + x.line) * g.nblocks + x.b) *
                                                                    a.ghost_cap * P
                                                    : nullptr;
@@ -622,7 +642,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     const int vn = x.line - (x.line / P) * P;
                     reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * dvs[x.sp];
                 }
-                unsigned bytes = C::NF * 8;
+                unsigned bytes = MODE == 1 ? 0u : C::NF * 8;
                 long long ga = 0, gb = 0;
                 if (chi > clo) {
                     // element g of the line sits at st + 2 + woff + (g - eg): same
@@ -641,7 +661,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     bytes += (unsigned)(gb - ga) * 8;
                 }
                 mbar_expect_tx(&full[stg], bytes);
-                tma_load_1d(st + C::WIN, row_of(x), C::NF * 8, &full[stg]);
+                if constexpr (MODE == 0) tma_load_1d(st + C::WIN, row_of(x), C::NF * 8, &full[stg]);
                 if (gb > ga) {
                     double* dst = st + 2 + woff + (ga - eg);
                     tma_load_1d(dst, srcp(x.sp) + ga, (unsigned)(gb - ga) * 8, &full[stg]);
@@ -687,6 +707,40 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         // cells per thread this warp has in this tile (warp-uniform): short
         // tiles (3-block meshes) skip the idle slots instead of recomputing
         const int ncc = min(C::CPT, nt > warp * 32 + C::NT ? 2 : (nt > warp * 32 ? 1 : 0));
+        if constexpr (MODE == 1) {
+            // post-limiter flags: cell c's stencil is window cells c, c+1, c+2
+            auto flags = [&](auto ncc_c) {
+                constexpr int NCC = decltype(ncc_c)::value;
+                bool tr[NCC];
+                unsigned long long entry[NCC];
+#pragma unroll
+                for (int cc = 0; cc < NCC; ++cc) {
+                    const int c = tid + cc * C::NT;
+                    tr[cc] = false;
+                    entry[cc] = ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
+                                (unsigned)(g.start[b] + c0 + c);
+                    if (c < nt) {
+                        double um[P], u0[P], up[P];
+                        lds_cell<P>(win + c * P, um);
+                        lds_cell<P>(win + (c + 1) * P, u0);
+                        lds_cell<P>(win + (c + 2) * P, up);
+                        tr[cc] = post_flag<P, FMA>(a.post, a.basis, um, u0, up);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stg]);
+                defer_push_n<NCC>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+            };
+            if (C::CPT == 2 && ncc == 2) {
+                flags(std::integral_constant<int, C::CPT>{});
+            } else if (ncc >= 1) {
+                flags(std::integral_constant<int, 1>{});
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stg]);
+            }
+            continue;
+        }
         auto cells = [&](auto ncc_c) {
             constexpr int NCC = decltype(ncc_c)::value;
             double ul[NCC][P], ur[NCC][P], o[NCC][P];
@@ -1951,17 +2005,6 @@ __global__ void copy_kernel(double* dst, const double* src, long long n) {
 // K3: literature post-limiters (limiters.cpp:254-345). Flags from pre-pass data
 // (out of place). X: tiles with a 1-cell halo (block ghosts via fill_ghost j=1).
 // ---------------------------------------------------------------------------
-template <int P, bool FAST = false>
-__device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, const double* um,
-                                          const double* u0, const double* up) {
-    if constexpr (FAST)
-        return cfg.indicator == 1 ? indicator_minmod_fast<P>(b, cfg, um, u0, up)
-                                  : indicator_meanerr_fast<P>(b, cfg, um, u0, up);
-    else
-        return cfg.indicator == 1 ? indicator_minmod_pre<P>(b, um, u0, up)
-                                  : indicator_meanerr_pre<P>(b, cfg, um, u0, up);
-}
-
 template <int P>
 __device__ __forceinline__ void post_modify(const PostCfg& cfg, const Basis& b, const double* um,
                                             const double* u0, const double* up, double* out) {
@@ -1971,11 +2014,14 @@ __device__ __forceinline__ void post_modify(const PostCfg& cfg, const Basis& b, 
         modify_line_weno<P>(b, um, u0, up, cfg, out);
 }
 
-// Post limiters as two passes, like the sweeps' limiter: a streaming pass
-// flags cells (cheap indicator), copies u0 and queues the flagged ones; the
-// modifier kernel recomputes the (rare, expensive, divergent) WENO
-// modification of queued cells from the untouched pre-pass data. Results are
-// exactly the single-pass ones.
+// Post limiters in place, like the sweeps' limiter: a flag pass reads the
+// field once (x: xsweep_kernel MODE 1 on the TMA pipeline; v: post_v_kernel)
+// and queues the flagged cells; post_fix_kernel computes their (rare,
+// expensive, divergent) WENO modifications from the untouched field into a
+// side buffer, and post_scatter_kernel writes them -- so every modification
+// sees pre-pass data, exactly the reference's single out-of-place pass. If the
+// queue overflowed, post_copy_kernel first copies the field to the other
+// buffer and the fix kernel rescans every cell from that copy.
 
 // the three cells of x stencil (line, block-local cell c) from the pre-pass data
 template <int P>
@@ -2001,126 +2047,15 @@ __device__ __forceinline__ void post_x_stencil(const PostArgs& a, const double* 
     }
 }
 
-// streaming pass X: persistent CTAs walk (species, line, tile) tiles of
-// kPostCPT*256 cells (kPostCPT cells per thread); the window of the next tile
-// is fetched with cp.async into the other half of a double buffer while the
-// current tile's indicators run
-template <int P>
-__host__ __device__ constexpr int post_cpt() { return P <= 4 ? 4 : 2; }
-template <int P>
-__host__ __device__ constexpr int post_tile() { return post_cpt<P>() * kXThreads; }
-template <int P>
-__host__ __device__ constexpr size_t post_x_smem() {
-    return sizeof(double) * 2 * P * xs_stride<P, post_tile<P>()>();
+// the field (live buffer) and the other buffer of species sp
+__device__ __forceinline__ double* post_live(const PostArgs& a, int sp) {
+    return const_cast<double*>(field_flipped(a.flip[sp]) ? a.dst[sp] : a.src[sp]);
+}
+__device__ __forceinline__ double* post_other(const PostArgs& a, int sp) {
+    return const_cast<double*>(field_flipped(a.flip[sp]) ? a.src[sp] : a.dst[sp]);
 }
 
-template <int P, bool FAST>
-__global__ void __launch_bounds__(kXThreads) post_x_kernel(const __grid_constant__ PostArgs a) {
-    constexpr int T = post_tile<P>(), CPT = post_cpt<P>();
-    constexpr int W = xs_stride<P, T>();
-    extern __shared__ __align__(16) double pxs[];  // [2][node][window cell]
-    const Grid& g = a.grid;
-    const int ntl = a.tile_start[g.nblocks];
-    const long long ntot = (long long)a.nspecies * a.nrows * ntl;
-    const int tid = threadIdx.x;
-    struct Tile {
-        int sp, line, b, c0, nt;
-    };
-    auto decode = [&](long long t) {
-        Tile x;
-        const int tl = (int)(t % ntl);
-        const long long r = t / ntl;
-        x.line = (int)(r % a.nrows);
-        x.sp = a.species0 + (int)(r / a.nrows);
-        int b = 0;
-        while (tl >= a.tile_start[b + 1]) ++b;
-        x.b = b;
-        x.c0 = (tl - a.tile_start[b]) * T;
-        x.nt = min(T, g.cells[b] - x.c0);
-        return x;
-    };
-    auto srcof = [&](const Tile& x) -> const double* {
-        const bool fl = field_flipped(a.flip[x.sp]);
-        return (fl ? a.dst[x.sp] : a.src[x.sp]) + (long long)x.line * g.ncells * P;
-    };
-    // issue the window of tile x into buffer bi: cells c0-1 .. c0+nt (block-local)
-    auto issue = [&](const Tile& x, int bi) {
-        const double* src = srcof(x);
-        const int cells_b = g.cells[x.b];
-        const long long gbase = (long long)g.start[x.b] * P;
-        double* wb = pxs + bi * P * W;
-        for (int e = tid; e < (x.nt + 2) * P; e += kXThreads) {
-            const int wc = e / P, n = e - (e / P) * P;
-            int sc = x.c0 - 1 + wc;
-            bool ok = sc >= 0 && sc < cells_b;
-            if (!ok && a.periodic) {
-                sc = ((sc % cells_b) + cells_b) % cells_b;
-                ok = true;
-            }
-            cp_async8(&wb[n * W + wc], ok ? src + gbase + (long long)sc * P + n : src, ok);
-        }
-    };
-    long long t = blockIdx.x;
-    Tile cur{};
-    if (t < ntot) {
-        cur = decode(t);
-        issue(cur, 0);
-    }
-    cp_commit();
-    for (int it = 0; t < ntot; t += gridDim.x, ++it) {
-        const int bi = it & 1;
-        double* wb = pxs + bi * P * W;
-        const long long tn = t + gridDim.x;
-        Tile nxt{};
-        if (tn < ntot) {
-            nxt = decode(tn);
-            issue(nxt, bi ^ 1);
-        }
-        cp_commit();
-        cp_wait<1>();
-        // window cells outside the block (walls, 3-block ghosts): computed here
-        if (!a.periodic && (cur.c0 == 0 || cur.c0 + cur.nt == g.cells[cur.b])) {
-            const double* src = srcof(cur);
-            for (int e = tid; e < (cur.nt + 2) * P; e += kXThreads) {
-                const int wc = e / P, n = e - (e / P) * P;
-                const int sc = cur.c0 - 1 + wc;
-                if (sc < 0 || sc >= g.cells[cur.b])
-                    wb[n * W + wc] = x_fetch_outside_ool<P>(a.basis, g, src, cur.b, sc, n);
-            }
-        }
-        __syncthreads();
-        bool tr[CPT];
-        unsigned long long entry[CPT];
-        const bool fl = field_flipped(a.flip[cur.sp]);
-        double* dline = (fl ? const_cast<double*>(a.src[cur.sp]) : a.dst[cur.sp]) +
-                        (long long)cur.line * g.ncells * P + ((long long)g.start[cur.b] + cur.c0) * P;
-#pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) {
-            const int c = tid + cc * kXThreads;
-            tr[cc] = false;
-            entry[cc] = ((unsigned long long)(cur.sp & 1) << 63) | ((unsigned long long)cur.line << 32) |
-                        (unsigned)(g.start[cur.b] + cur.c0 + c);
-            if (c < cur.nt) {
-                double um[P], u0[P], up[P];
-#pragma unroll
-                for (int n = 0; n < P; ++n) {
-                    um[n] = wb[n * W + c];
-                    u0[n] = wb[n * W + c + 1];
-                    up[n] = wb[n * W + c + 2];
-                }
-                tr[cc] = post_flag<P, FAST>(a.cfg, a.basis, um, u0, up);
-                double* dst = dline + (long long)c * P;
-#pragma unroll
-                for (int n = 0; n < P; ++n) dst[n] = u0[n];  // flagged cells: rewritten by post_fix_kernel
-            }
-        }
-        defer_push_n<CPT>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
-        __syncthreads();  // buffer bi is refilled two tiles from now
-        cur = nxt;
-    }
-    cp_wait<0>();
-}
-
+// v flag pass: one thread per x dof walks kVChunk v cells (in place)
 template <int P, bool FAST>
 __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant__ PostArgs a) {
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2128,9 +2063,7 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
     const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
     const unsigned members = __ballot_sync(0xffffffffu, xd < a.nxd);
     if (xd < a.nxd) {
-        const bool fl = field_flipped(a.flip[sp]);
-        const double* f = fl ? a.dst[sp] : a.src[sp];
-        double* out = fl ? const_cast<double*>(a.src[sp]) : a.dst[sp];
+        const double* f = post_live(a, sp);
         double um[P], u0[P], up[P];
         // a v shard reads one halo cell from each neighbour (zero at the walls)
         const int lo = -a.gl, hi = a.nv + a.gr;
@@ -2143,8 +2076,6 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
                                                  ((unsigned long long)j << 32) | (unsigned)xd};
             defer_push_n<1>(a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
 #pragma unroll
-            for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = u0[m];
-#pragma unroll
             for (int n = 0; n < P; ++n) {
                 um[n] = u0[n];
                 u0[n] = up[n];
@@ -2153,7 +2084,22 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
     }
 }
 
-// modifier of queued (or, after a list overflow, all re-flagged) cells
+// overflow only: the field (with its readable v halo rows) into the other buffer
+__global__ void post_copy_kernel(const __grid_constant__ PostArgs a, int P) {
+    if (*a.fix_count <= a.fix_cap) return;
+    const long long r0 = -(long long)a.gl * P, r1 = (long long)(a.nv + a.gr) * P;
+    const long long n = (r1 - r0) * a.ld;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (int k = 0; k < a.nspecies; ++k) {
+        const int sp = a.species0 + k;
+        const double* src = post_live(a, sp) + r0 * a.ld;
+        double* dst = post_other(a, sp) + r0 * a.ld;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+    }
+}
+
+// modifier of queued cells into fix_vals (or, after an overflow, of every
+// re-flagged cell from the copy straight into the field)
 template <int P, int DIR, bool FAST>
 __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ PostArgs a) {
     const unsigned cnt = *a.fix_count;
@@ -2177,28 +2123,34 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
             row = (int)(r / ncol);
             col = (int)(r - (r / ncol) * ncol);
         }
-        const bool fl = field_flipped(a.flip[sp]);
-        const double* f = fl ? a.dst[sp] : a.src[sp];
-        double* out = fl ? const_cast<double*>(a.src[sp]) : a.dst[sp];
+        const double* f = rescan ? post_other(a, sp) : post_live(a, sp);
         double um[P], u0[P], up[P], o[P];
+        long long at;  // first dof of the cell, stride ds between its nodes
+        long long ds;
         if constexpr (DIR == 0) {
             int b = 0;
             while (col >= g.start[b + 1]) ++b;
             const long long lb = (long long)row * g.ncells * P;
             post_x_stencil<P>(a, f + lb, b, col - g.start[b], um, u0, up);
-            if (rescan && !post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)) continue;
-            post_modify<P>(a.cfg, a.basis, um, u0, up, o);
-#pragma unroll
-            for (int m = 0; m < P; ++m) out[lb + (long long)col * P + m] = o[m];
+            at = lb + (long long)col * P;
+            ds = 1;
         } else {
             const int lo = -a.gl, hi = a.nv + a.gr;
             vload<P>(f, a.ld, col, row - 1, lo, hi, a.periodic, a.nv, um);
             vload<P>(f, a.ld, col, row, lo, hi, a.periodic, a.nv, u0);
             vload<P>(f, a.ld, col, row + 1, lo, hi, a.periodic, a.nv, up);
-            if (rescan && !post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)) continue;
-            post_modify<P>(a.cfg, a.basis, um, u0, up, o);
+            at = (long long)row * P * a.ld + col;
+            ds = a.ld;
+        }
+        if (rescan && !post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)) continue;
+        post_modify<P>(a.cfg, a.basis, um, u0, up, o);
+        if (rescan) {
+            double* out = post_live(a, sp);
 #pragma unroll
-            for (int m = 0; m < P; ++m) out[((long long)row * P + m) * a.ld + col] = o[m];
+            for (int m = 0; m < P; ++m) out[at + m * ds] = o[m];
+        } else {
+#pragma unroll
+            for (int m = 0; m < P; ++m) a.fix_vals[i * P + m] = o[m];
         }
         flagged[sp & 1] += 1;
     }
@@ -2213,6 +2165,26 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
     __syncthreads();
     if (threadIdx.x < 2 && acc[threadIdx.x])
         atomicAdd(&a.st->stats[threadIdx.x][3], (unsigned long long)acc[threadIdx.x]);
+}
+
+// the queued modifications into the field (list mode only)
+template <int P, int DIR>
+__global__ void __launch_bounds__(128) post_scatter_kernel(const __grid_constant__ PostArgs a) {
+    const unsigned cnt = *a.fix_count;
+    if (cnt > a.fix_cap) return;
+    const Grid& g = a.grid;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
+        const unsigned long long e = a.fix_list[i];
+        const int sp = (int)(e >> 63);
+        const int row = (int)((e >> 32) & 0x7fffffffu);
+        const int col = (int)(e & 0xffffffffu);
+        double* out = post_live(a, sp);
+        const long long at = DIR == 0 ? ((long long)row * g.ncells + col) * P : (long long)row * P * a.ld + col;
+        const long long ds = DIR == 0 ? 1 : a.ld;
+#pragma unroll
+        for (int m = 0; m < P; ++m) out[at + m * ds] = a.fix_vals[i * P + m];
+    }
 }
 
 __global__ void post_v_count_kernel(DevStatus* st, int mask, unsigned long long per_species) {
@@ -2256,18 +2228,18 @@ static int sm_count() {
 template <int P>
 constexpr bool kHasFma = kHasFmaDev<P>;
 
-template <int P, bool INLINE, bool RHO, bool FMA>
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 static cudaError_t configure_xsweep() {
     using Cf = XCfg<P>;
     static unsigned configured = 0;  // per-device bit
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured & (1u << (dev & 31)))) {
-        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA>,
+        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
         if (e != cudaSuccess) return e;
         // full shared-memory carveout so two pipelines share each SM
-        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA>,
+        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         configured |= 1u << (dev & 31);
@@ -2278,18 +2250,19 @@ static cudaError_t configure_xsweep() {
 // persistent grid of one x-sweep variant: resident CTAs, and for the fused
 // moment a multiple of the tiles per line (each CTA then always sees the same
 // tile column, so the per-group partial rows sum in a fixed order)
-template <int P, bool INLINE, bool RHO, bool FMA>
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out) {
     using Cf = XCfg<P>;
-    if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA>()) return e;
+    constexpr int TT = MODE == 1 ? Cf::T - 1 : Cf::T;
+    if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA, MODE>()) return e;
     b = a;
     b.tile_start[0] = 0;
     for (int i = 0; i < a.grid.nblocks; ++i)
-        b.tile_start[i + 1] = b.tile_start[i] + (a.grid.cells[i] + Cf::T - 1) / Cf::T;
+        b.tile_start[i + 1] = b.tile_start[i] + (a.grid.cells[i] + TT - 1) / TT;
     const int ntl = b.tile_start[a.grid.nblocks];
     const long long ntot = (long long)a.nspecies * a.nlines * ntl;
     int blocks_per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO, FMA>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
                                                   (Cf::NC + 1) * 32, Cf::SMEM);
     long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
     if (RHO) {
@@ -2660,39 +2633,57 @@ cudaError_t launch_fill_separable(double* f, const double* gx, const double* gv,
     return cudaGetLastError();
 }
 
-template <int P, bool FAST>
-static void launch_post_x_t(const PostArgs& a, cudaStream_t s) {
-    constexpr size_t smem = post_x_smem<P>();
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(post_x_kernel<P, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
-    PostArgs b = a;  // tiles of post_tile<P>() cells
-    b.tile_start[0] = 0;
-    for (int i = 0; i < a.grid.nblocks; ++i)
-        b.tile_start[i + 1] = b.tile_start[i] + (a.grid.cells[i] + post_tile<P>() - 1) / post_tile<P>();
-    const long long ntot = (long long)a.nspecies * a.nrows * b.tile_start[a.grid.nblocks];
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, post_x_kernel<P, FAST>, kXThreads, smem);
-    const long long grid = std::min<long long>((long long)sm_count() * std::max(per_sm, 1), ntot);
-    post_x_kernel<P, FAST><<<(int)std::max<long long>(grid, 1), kXThreads, smem, s>>>(b);
-    post_fix_kernel<P, 0, FAST><<<sm_count() * 8, 128, 0, s>>>(a);
+// after a flag pass: overflow copy (device-gated), modifications, scatter
+template <int P, int DIR, bool FAST>
+static void launch_post_tail(const PostArgs& a, cudaStream_t s) {
+    post_copy_kernel<<<sm_count() * 4, 256, 0, s>>>(a, P);
+    post_fix_kernel<P, DIR, FAST><<<sm_count() * 8, 128, 0, s>>>(a);
+    post_scatter_kernel<P, DIR><<<sm_count() * 4, 128, 0, s>>>(a);
 }
 
 template <int P, bool FAST>
-static void launch_post_v_t(const PostArgs& a, cudaStream_t s) {
+static cudaError_t launch_post_x_t(const PostArgs& a, cudaStream_t s) {
+    // the x flag pass runs on the x-sweep pipeline (xsweep_kernel MODE 1)
+    XSweepArgs x{};
+    x.basis = a.basis;
+    x.grid = a.grid;
+    x.st = a.st;
+    for (int sp = 0; sp < 2; ++sp) {
+        x.src[sp] = a.src[sp];
+        x.dst[sp] = a.dst[sp];
+        x.flip[sp] = a.flip[sp];
+    }
+    x.nlines = a.nrows;
+    x.nspecies = a.nspecies;
+    x.species0 = a.species0;
+    x.periodic = a.periodic;
+    x.fma = a.fma;
+    x.fix_list = a.fix_list;
+    x.fix_count = a.fix_count;
+    x.fix_cap = a.fix_cap;
+    x.post = a.cfg;
+    XSweepArgs b;
+    int grid = 0;
+    if (cudaError_t e = xsweep_plan<P, false, false, FAST, 1>(x, b, grid)) return e;
+    if (grid > 0) xsweep_kernel<P, false, false, FAST, 1><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
+    launch_post_tail<P, 0, FAST>(a, s);
+    return cudaGetLastError();
+}
+
+template <int P, bool FAST>
+static cudaError_t launch_post_v_t(const PostArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
     post_v_kernel<P, FAST><<<grid, kVThreads, 0, s>>>(a);
-    post_fix_kernel<P, 1, FAST><<<sm_count() * 8, 128, 0, s>>>(a);
+    launch_post_tail<P, 1, FAST>(a, s);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s) {
     (void)ntiles;
     if (a.fma) {
-        SK_DISPATCH_P(a.basis.p, (launch_post_x_t<PP, true>(a, s)));
+        SK_DISPATCH_P(a.basis.p, if (cudaError_t e = launch_post_x_t<PP, true>(a, s)) return e)
     } else {
-        SK_DISPATCH_P(a.basis.p, (launch_post_x_t<PP, false>(a, s)));
+        SK_DISPATCH_P(a.basis.p, if (cudaError_t e = launch_post_x_t<PP, false>(a, s)) return e)
     }
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
@@ -2702,9 +2693,9 @@ cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s) {
 
 cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s) {
     if (a.fma) {
-        SK_DISPATCH_P(a.basis.p, (launch_post_v_t<PP, true>(a, s)));
+        SK_DISPATCH_P(a.basis.p, if (cudaError_t e = launch_post_v_t<PP, true>(a, s)) return e)
     } else {
-        SK_DISPATCH_P(a.basis.p, (launch_post_v_t<PP, false>(a, s)));
+        SK_DISPATCH_P(a.basis.p, if (cudaError_t e = launch_post_v_t<PP, false>(a, s)) return e)
     }
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);

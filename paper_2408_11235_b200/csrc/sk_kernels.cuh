@@ -72,6 +72,9 @@ struct XSweepArgs {
     // outward on the side the line's shift reaches (null: computed in-kernel)
     double* ghost;
     int ghost_cap;
+    // post-limiter flag pass (xsweep_kernel MODE 1): the literature indicator
+    // of every cell from its window, in place; flagged cells are queued
+    PostCfg post;
 };
 
 struct VTabArgs {
@@ -203,6 +206,7 @@ struct PostArgs {
     unsigned long long* fix_list;
     unsigned int* fix_count;
     unsigned int fix_cap;
+    double* fix_vals;      // [fix_cap][P] modified values, scattered after all are computed
 };
 
 // launchers (P = k+1 dispatch inside)
