@@ -388,6 +388,31 @@ def test_periodic_sweep_conserves_mass(sk):
         assert abs(f.mass() - m0) <= 1e-13 * abs(m0)
 
 
+@pytest.mark.parametrize("mode", ["minmod+line", "meanerr+simple"])
+def test_periodic_post_limiter_translation_invariant(sk, mode):
+    """Periodic post limiting (the reference oracle has walls only): rolling
+    the input by r cells in x (or v) must roll the output bit for bit. 1200 x
+    cells make three flag-pass tiles, so the wrap windows and the tile edges
+    are both exercised; a rough field makes many cells flagged."""
+    k, nx, nv = 3, 1200, 40
+    P = k + 1
+    ctx = sk.Context(sk.Grid1D.uniform(-1.0, 1.0, nx), k)
+    f = sk.NodalField(ctx, 0, sk.Grid1D.uniform(-4.0, 4.0, nv))
+    rng = np.random.default_rng(7)
+    base = np.abs(rng.standard_normal(f.size)) * (rng.random(f.size) < 0.2) + 0.1
+    lim = sk.LimiterConfig.parse(mode)
+    for d, r in ((0, 517), (1, 13)):
+        shape = (nv * P, nx, P) if d == 0 else (nv, P, nx * P)
+        rolled = np.roll(base.reshape(shape), r, axis=0 if d else 1).ravel()
+        outs = []
+        for u in (base, rolled):
+            f.upload(u)
+            sk.apply_post_limiter(f, d, lim, bc=1)
+            outs.append(f.download())
+        assert not np.array_equal(outs[0], base), "nothing flagged"
+        assert np.array_equal(np.roll(outs[0].reshape(shape), r, axis=0 if d else 1).ravel(), outs[1]), f"dir {d}"
+
+
 @pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
 def test_c3_full_size_sampled_lines_bitwise(sk, ora, exact):
     """C3 (2048x4096, k=3, mu=1836, sldg): one GPU x and v sweep at full size;
