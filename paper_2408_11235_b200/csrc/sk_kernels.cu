@@ -426,6 +426,20 @@ __device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, co
                                   : indicator_meanerr_pre<P>(b, cfg, um, u0, up);
 }
 
+// the same with the indicator fixed at compile time (flag passes: straight-line
+// code, so a thread's cells interleave)
+template <int P, bool FAST, int IND>
+__device__ __forceinline__ bool post_flag_t(const PostCfg& cfg, const Basis& b, const double* um,
+                                            const double* u0, const double* up) {
+    if constexpr (FAST) {
+        if constexpr (IND == 1) return indicator_minmod_fast<P>(b, cfg, um, u0, up);
+        else return indicator_meanerr_fast<P>(b, cfg, um, u0, up);
+    } else {
+        if constexpr (IND == 1) return indicator_minmod_pre<P>(b, um, u0, up);
+        else return indicator_meanerr_pre<P>(b, cfg, um, u0, up);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K1: x sweep -- warp-specialised TMA pipeline over tiles
 //   tile = (species, x row, block, T cells); its source window is T+1 cells
@@ -510,17 +524,18 @@ __device__ __forceinline__ void sts_cell(double* p, const double* u) {
     }
 }
 
-// MODE 0: the x sweep. MODE 1: the post-limiter flag pass in x (limiters.cpp:
-// 254-345) on the same pipeline -- window = the tile's cells and one neighbour
-// on each side (tiles of T-1 cells), no table row, the literature indicator
-// per cell, flagged cells queued; in place (nothing stored).
+// MODE 0: the x sweep. MODE 1 / 2: the post-limiter flag pass in x with the
+// minmod / mean-error indicator (limiters.cpp:254-345) on the same pipeline --
+// window = the tile's cells and one neighbour on each side (tiles of T-1
+// cells), no table row, the indicator per cell, flagged cells queued; in place
+// (nothing stored).
 template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
     static_assert(MODE == 0 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
-    constexpr int TT = MODE == 1 ? C::T - 1 : C::T;  // cells per tile
-    constexpr int WX = MODE == 1 ? 2 : 1;            // window cells beyond the tile
+    constexpr int TT = MODE >= 1 ? C::T - 1 : C::T;  // cells per tile
+    constexpr int WX = MODE >= 1 ? 2 : 1;            // window cells beyond the tile
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;                                   // S x STAGE
     double* racc = smem + C::S * C::STAGE;                   // [T][P] this CTA's column (RHO)
@@ -568,7 +583,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             // wait out one load latency each
             auto batch_istar = [&](int it0) -> int {
                 const long long t = vb + (long long)(it0 + lane) * G;
-                if constexpr (MODE == 1) return -1;  // window starts one cell left
+                if constexpr (MODE >= 1) return -1;  // window starts one cell left
                 return t < ntot ? (int)__ldg(row_of(decode_xtile(a, (int)t, TT))) : 0;
             };
             int ist_cur = batch_istar(0);
@@ -642,7 +657,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     const int vn = x.line - (x.line / P) * P;
                     reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * dvs[x.sp];
                 }
-                unsigned bytes = MODE == 1 ? 0u : C::NF * 8;
+                unsigned bytes = MODE >= 1 ? 0u : C::NF * 8;
                 long long ga = 0, gb = 0;
                 if (chi > clo) {
                     // element g of the line sits at st + 2 + woff + (g - eg): same
@@ -707,7 +722,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         // cells per thread this warp has in this tile (warp-uniform): short
         // tiles (3-block meshes) skip the idle slots instead of recomputing
         const int ncc = min(C::CPT, nt > warp * 32 + C::NT ? 2 : (nt > warp * 32 ? 1 : 0));
-        if constexpr (MODE == 1) {
+        if constexpr (MODE >= 1) {
             // post-limiter flags: cell c's stencil is window cells c, c+1, c+2
             auto flags = [&](auto ncc_c) {
                 constexpr int NCC = decltype(ncc_c)::value;
@@ -724,7 +739,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                         lds_cell<P>(win + c * P, um);
                         lds_cell<P>(win + (c + 1) * P, u0);
                         lds_cell<P>(win + (c + 2) * P, up);
-                        tr[cc] = post_flag<P, FMA>(a.post, a.basis, um, u0, up);
+                        tr[cc] = post_flag_t<P, FMA, MODE>(a.post, a.basis, um, u0, up);
                     }
                 }
                 __syncwarp();
@@ -2056,7 +2071,7 @@ __device__ __forceinline__ double* post_other(const PostArgs& a, int sp) {
 }
 
 // v flag pass: one thread per x dof walks kVChunk v cells (in place)
-template <int P, bool FAST>
+template <int P, bool FAST, int IND>
 __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant__ PostArgs a) {
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
@@ -2071,7 +2086,7 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
         vload<P>(f, a.ld, xd, j0, lo, hi, a.periodic, a.nv, u0);
         for (int j = j0; j < j1; ++j) {
             vload<P>(f, a.ld, xd, j + 1, lo, hi, a.periodic, a.nv, up);
-            const bool tr[1] = {post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)};
+            const bool tr[1] = {post_flag_t<P, FAST, IND>(a.cfg, a.basis, um, u0, up)};
             const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
                                                  ((unsigned long long)j << 32) | (unsigned)xd};
             defer_push_n<1>(a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
@@ -2253,7 +2268,7 @@ static cudaError_t configure_xsweep() {
 template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out) {
     using Cf = XCfg<P>;
-    constexpr int TT = MODE == 1 ? Cf::T - 1 : Cf::T;
+    constexpr int TT = MODE >= 1 ? Cf::T - 1 : Cf::T;
     if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA, MODE>()) return e;
     b = a;
     b.tile_start[0] = 0;
@@ -2664,8 +2679,13 @@ static cudaError_t launch_post_x_t(const PostArgs& a, cudaStream_t s) {
     x.post = a.cfg;
     XSweepArgs b;
     int grid = 0;
-    if (cudaError_t e = xsweep_plan<P, false, false, FAST, 1>(x, b, grid)) return e;
-    if (grid > 0) xsweep_kernel<P, false, false, FAST, 1><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
+    if (a.cfg.indicator == 1) {
+        if (cudaError_t e = xsweep_plan<P, false, false, FAST, 1>(x, b, grid)) return e;
+        if (grid > 0) xsweep_kernel<P, false, false, FAST, 1><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
+    } else {
+        if (cudaError_t e = xsweep_plan<P, false, false, FAST, 2>(x, b, grid)) return e;
+        if (grid > 0) xsweep_kernel<P, false, false, FAST, 2><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
+    }
     launch_post_tail<P, 0, FAST>(a, s);
     return cudaGetLastError();
 }
@@ -2673,7 +2693,10 @@ static cudaError_t launch_post_x_t(const PostArgs& a, cudaStream_t s) {
 template <int P, bool FAST>
 static cudaError_t launch_post_v_t(const PostArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
-    post_v_kernel<P, FAST><<<grid, kVThreads, 0, s>>>(a);
+    if (a.cfg.indicator == 1)
+        post_v_kernel<P, FAST, 1><<<grid, kVThreads, 0, s>>>(a);
+    else
+        post_v_kernel<P, FAST, 2><<<grid, kVThreads, 0, s>>>(a);
     launch_post_tail<P, 1, FAST>(a, s);
     return cudaGetLastError();
 }

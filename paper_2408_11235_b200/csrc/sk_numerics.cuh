@@ -549,9 +549,12 @@ SK_HD int inline_limit(const Basis& b, double alpha, double threshold, const dou
 
 // ---------------- post limiters (limiters.cpp:47-165) ----------------
 SK_HD double minmod(double a, double b, double c) {
-    if (a > 0 && b > 0 && c > 0) return dmin2(a, dmin2(b, c));
-    if (a < 0 && b < 0 && c < 0) return -dmin2(-a, dmin2(-b, -c));
-    return 0.0;
+    // branch-free, same values: one of the three sign cases is selected
+    const double mpos = dmin2(a, dmin2(b, c));
+    const double mneg = -dmin2(-a, dmin2(-b, -c));
+    const bool pos = (a > 0) & (b > 0) & (c > 0);
+    const bool neg = (a < 0) & (b < 0) & (c < 0);
+    return pos ? mpos : (neg ? mneg : 0.0);
 }
 
 template <int P>
@@ -725,8 +728,8 @@ SK_HD bool indicator_minmod_fast(const Basis& b, const PostCfg& c, const double*
     double scale = fmax(fmax(fmax(fabs(mean_m), fabs(mean_0)), fmax(fabs(mean_p), fabs(u0_plus))),
                         fmax(fmax(fabs(u0_minus), fabs(d_plus)), fabs(d_minus)));
     const double guard = 1e-13 * scale;
-    return fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard ||
-           fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard;
+    return (fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard) |
+           (fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard);
 }
 template <int P>
 SK_HD double integrate_fast(const Basis& b, const double (*t)[SK_MAXP], const double* rc, const double* u) {
