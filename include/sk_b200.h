@@ -136,6 +136,12 @@ sk_status sk_stats_reset(sk_ctx* ctx);
 /* Grid1D::three_block (grid.cpp:36-46) with the reference's arithmetic */
 sk_status sk_grid_three_block(double left, double right, int fine_cells, int coarse_cells, int m,
                               double* block_left, int* block_cells, double* block_dx);
+/* build_shift_matrices(ReferenceBasis::get(k), alpha) (advection.cpp:27-66):
+ * the p x p shift matrices A, B (row-major, p = k+1) the sweeps apply, from the
+ * host copy of the same constants (bitwise the reference's). k in 0..6, alpha in
+ * [0,1). Host only -- no context or GPU needed (the `solkin matrices` table,
+ * tools/solkin_main.cpp:43-57). */
+sk_status sk_shift_matrices(int k, double alpha, double* A, double* B);
 
 /* ---- fields: NodalField(species, x, v, k) (field.cpp:9-16) ---- */
 sk_status sk_field_create(sk_ctx* ctx, int species, double v_left, double v_right, int v_cells,

@@ -454,6 +454,34 @@ class Ref(_Lib):
         fails = self.lib.ref_self_checks()
         return fails, self.last_error()
 
+    def config_eval(self, preset="", file="", kv=(), resolve=False):
+        """RunConfig layered as cmd_run does (solkin_main.cpp:20-28): returns
+        ("ok", echo, [violations], nsteps) or ("error", message)."""
+        L = self.lib
+        L.ref_config_eval.restype = C.c_int
+        L.ref_config_eval.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p,
+                                      C.c_long, C.c_char_p, C.c_long, C.POINTER(C.c_long)]
+        echo = C.create_string_buffer(1 << 14)
+        viol = C.create_string_buffer(1 << 14)
+        n = C.c_long(0)
+        kvs = "".join(f"{k}\t{v}\n" for k, v in kv).encode()
+        rc = L.ref_config_eval(preset.encode(), str(file).encode(), kvs, int(resolve), echo,
+                               len(echo), viol, len(viol), C.byref(n))
+        if rc:
+            return ("error", self.last_error())
+        lines = viol.value.decode().split("\n")
+        return ("ok", echo.value.decode(), [x for x in lines if x], n.value)
+
+    def matrices_text(self, alpha, order):
+        """the `solkin matrices` table (solkin_main.cpp:43-57)"""
+        L = self.lib
+        L.ref_matrices_text.restype = C.c_int
+        L.ref_matrices_text.argtypes = [C.c_double, C.c_int, C.c_char_p, C.c_long]
+        out = C.create_string_buffer(1 << 14)
+        if L.ref_matrices_text(float(alpha), int(order), out, len(out)):
+            raise RuntimeError(self.last_error())
+        return out.value.decode()
+
     def gauss_legendre(self, k):
         n = np.zeros(k + 1)
         w = np.zeros(k + 1)

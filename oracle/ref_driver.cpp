@@ -14,6 +14,7 @@
 // reference-LAPACK algorithm; the image has no LAPACK development package).
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -417,6 +418,55 @@ int ref_self_checks() {
     int failures = run_self_checks(out);
     g_error = out.str();
     return failures;
+}
+
+// config.cpp:58-218 -- RunConfig as cmd_run layers it (solkin_main.cpp:20-28):
+// preset (empty: defaults) -> file (empty: none) -> kv overrides ("key\tvalue"
+// lines, applied verbatim through apply_kv) -> resolve() when asked. Writes
+// echo() and violations() (one per line); 1 + ref_last_error() on a throw.
+int ref_config_eval(const char* preset, const char* file, const char* kv, int resolve, char* echo,
+                    long echo_cap, char* viol, long viol_cap, long* nsteps) {
+    return guarded([&] {
+        RunConfig c;
+        if (preset && *preset) c = RunConfig::preset(preset);
+        if (file && *file) c.apply_file(file);
+        std::istringstream lines(kv ? kv : "");
+        std::string line;
+        while (std::getline(lines, line)) {
+            if (line.empty()) continue;
+            const size_t tab = line.find('\t');
+            c.apply_kv(line.substr(0, tab), tab == std::string::npos ? "" : line.substr(tab + 1));
+        }
+        if (resolve) c.resolve();
+        std::string v;
+        for (const auto& s : c.violations()) v += s + "\n";
+        std::snprintf(echo, echo_cap, "%s", c.echo().c_str());
+        std::snprintf(viol, viol_cap, "%s", v.c_str());
+        *nsteps = c.nsteps();
+    });
+}
+// tools/solkin_main.cpp:43-57 -- the `solkin matrices` table, from the reference basis
+int ref_matrices_text(double alpha, int order, char* out, long cap) {
+    return guarded([&] {
+        const auto& basis = ReferenceBasis::get(order);
+        auto M = build_shift_matrices(basis, alpha);
+        std::string s;
+        char buf[64];
+        auto table = [&](const char* name, const std::vector<double>& mat) {
+            std::snprintf(buf, sizeof(buf), "%s(alpha=%.17g), order %d:\n", name, alpha, order);
+            s += buf;
+            for (int m = 0; m < M.p; ++m) {
+                for (int n = 0; n < M.p; ++n) {
+                    std::snprintf(buf, sizeof(buf), " % .17e", mat[m * M.p + n]);
+                    s += buf;
+                }
+                s += "\n";
+            }
+        };
+        table("A", M.A);
+        table("B", M.B);
+        std::snprintf(out, cap, "%s", s.c_str());
+    });
 }
 
 }  // extern "C"

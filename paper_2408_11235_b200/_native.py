@@ -68,6 +68,7 @@ SIGNATURES = {
     "sk_last_error_step": (C.c_long, []),
     "sk_version": (C.c_char_p, []),
     "sk_grid_three_block": (_i, [_d, _d, _i, _i, _i, _dp, _ip, _dp]),
+    "sk_shift_matrices": (_i, [_i, _d, _dp, _dp]),
     "sk_ctx_create": (_i, [_i, _i, _i, _dp, _ip, _dp, _d, C.POINTER(_vp)]),
     "sk_ctx_destroy": (_i, [_vp]),
     "sk_ctx_set_stream": (_i, [_vp, _vp]),

@@ -618,6 +618,12 @@ sk_status moments(sk_field* f, double* out4) {
 }  // namespace
 
 // ===========================================================================
+template <int P>
+static void shift_matrices_host(double alpha, double* A, double* B) {
+    const Basis b = make_basis(P - 1);
+    shift_matrices<P>(b, alpha, A, B);
+}
+
 extern "C" {
 
 const char* sk_last_error(void) { return g_err.c_str(); }
@@ -641,6 +647,23 @@ sk_status sk_grid_three_block(double left, double right, int nf, int nc, int m, 
     bl[2] = bl[1] + nc * dxc;
     bc[2] = nf;
     bd[2] = dxf;
+    return SK_OK;
+}
+
+sk_status sk_shift_matrices(int k, double alpha, double* A, double* B) {
+    if (k < 0 || k > 6) return fail(SK_ERR_RUNTIME, "k must be in 0..6");
+    if (!(alpha >= 0.0 && alpha < 1.0))
+        return fail(SK_ERR_RUNTIME, "build_shift_matrices: alpha must be in [0,1)");
+    if (!A || !B) return fail(SK_ERR_RUNTIME, "sk_shift_matrices: null output");
+    switch (k + 1) {
+        case 1: shift_matrices_host<1>(alpha, A, B); break;
+        case 2: shift_matrices_host<2>(alpha, A, B); break;
+        case 3: shift_matrices_host<3>(alpha, A, B); break;
+        case 4: shift_matrices_host<4>(alpha, A, B); break;
+        case 5: shift_matrices_host<5>(alpha, A, B); break;
+        case 6: shift_matrices_host<6>(alpha, A, B); break;
+        default: shift_matrices_host<7>(alpha, A, B); break;
+    }
     return SK_OK;
 }
 

@@ -28,6 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
+from . import runconfig as RC
 
 
 class SimulationError(RuntimeError):
@@ -155,7 +156,8 @@ class SpeciesParams:
 
 @dataclass
 class RunConfig:
-    """config.hpp:11-41 (defaults) -- the keys that shape the step."""
+    """RunConfig (config.hpp:11-59): keys, defaults, presets, key = value files,
+    validation and echo as the reference (config.cpp:58-221)."""
 
     scenario: str = "blob"
     t0: float = 2000.0  # injection source window (config.hpp:18)
@@ -178,6 +180,137 @@ class RunConfig:
     adapt_gamma: float = 0.05
     adapt_tol: float = 1e-14
     penalty_scale: float = 10.0
+    out_dir: str = "out"
+    cadence: int = 10           # flux row every N steps
+    snapshot_cadence: int = 0   # 0 = off
+    profile_cadence: int = 0    # 0 = off
+    threads: int = 1            # accepted for parity; the device ignores it
+
+    # (key, attribute, kind) in echo order (config.cpp:111-137, 196-224)
+    KEYS = (("scenario", "scenario", "s"), ("L", "L", "d"), ("dt", "dt", "d"), ("k", "k", "i"),
+            ("mu", "mu", "d"), ("t_final", "t_final", "d"), ("sigma", "sigma", "d"),
+            ("t0", "t0", "d"), ("vmax_e", "vmax_e", "d"), ("vmax_i", "vmax_i", "d"),
+            ("mesh.fine_block_cells", "fine_block_cells", "i"),
+            ("mesh.coarse_block_cells", "coarse_block_cells", "i"),
+            ("mesh.refinement_ratio", "refinement_ratio", "i"), ("v_cells", "v_cells", "i"),
+            ("limiter", "limiter", "s"), ("limiter.threshold", "limiter_threshold", "d"),
+            ("adaptivity.v_adjust", "v_adjust", "b"), ("adaptivity.p", "adapt_p", "d"),
+            ("adaptivity.gamma", "adapt_gamma", "d"), ("adaptivity.tol", "adapt_tol", "d"),
+            ("poisson.penalty_scale", "penalty_scale", "d"), ("output.dir", "out_dir", "s"),
+            ("output.cadence", "cadence", "i"), ("output.snapshot_cadence", "snapshot_cadence", "i"),
+            ("output.profile_cadence", "profile_cadence", "i"), ("threads", "threads", "i"))
+    # name -> (scenario, fine, coarse, m, v_cells or None to keep the defaults, t_final)
+    PRESETS = {"blob-desk": ("blob", None, 400.0), "injection-desk": ("injection", None, 400.0),
+               "blob-paper": ("blob", (100, 100, 1, 150), 4000.0),
+               "injection-paper": ("injection", (100, 100, 8, 150), 8000.0)}
+
+    @staticmethod
+    def preset(name: str) -> "RunConfig":
+        """config.cpp:58-86"""
+        if name not in RunConfig.PRESETS:
+            raise RuntimeError(f"unknown preset '{name}' (expected blob-paper, injection-paper, "
+                               "blob-desk, injection-desk)")
+        scenario, mesh, t_final = RunConfig.PRESETS[name]
+        c = RunConfig(scenario=scenario, t_final=t_final)
+        if mesh:
+            c.fine_block_cells, c.coarse_block_cells, c.refinement_ratio, c.v_cells = mesh
+        return c
+
+    @staticmethod
+    def from_file(path: str) -> "RunConfig":
+        c = RunConfig()
+        c.apply_file(path)
+        return c
+
+    def apply_file(self, path: str) -> None:
+        """flat key = value lines with '#' comments (config.cpp:93-109)"""
+        try:
+            with open(path, "rb") as fh:
+                data = fh.read().decode("utf-8", "surrogateescape")
+        except OSError:
+            raise RuntimeError(f"cannot read config file '{path}'") from None
+        for lineno, line in enumerate(data.split("\n")[: data.count("\n") + (not data.endswith("\n"))], 1):
+            line = RC.trim(line.split("#", 1)[0])
+            if not line:
+                continue
+            if "=" not in line:
+                raise RuntimeError(f"{path}:{lineno}: expected key = value")
+            key, value = line.split("=", 1)
+            self.apply_kv(RC.trim(key), RC.trim(value))
+
+    def apply_kv(self, key: str, value: str) -> None:
+        """config.cpp:111-138"""
+        for name, attr, kind in self.KEYS:
+            if name != key:
+                continue
+            if kind == "d":
+                setattr(self, attr, RC.stod_full(key, value))
+            elif kind == "i":
+                setattr(self, attr, RC.stoi_full(key, value))
+            elif kind == "b":
+                setattr(self, attr, RC.onoff(key, value))
+            else:
+                setattr(self, attr, value)
+            return
+        raise RuntimeError(f"unknown config key '{key}'")
+
+    def resolve(self) -> None:
+        """sigma < 0 -> 0.1 L (config.cpp:140-142)"""
+        if self.sigma < 0:
+            self.sigma = 0.1 * self.L
+
+    def violations(self) -> list:
+        """'key: message' lines in the reference's order (config.cpp:144-185)"""
+        out = []
+
+        def need(ok, key, msg):
+            if not ok:
+                out.append(f"{key}: {msg}")
+
+        need(self.scenario in ("blob", "injection"), "scenario", "must be blob or injection")
+        need(self.L > 0, "L", "must be positive")
+        need(self.dt > 0, "dt", "must be positive")
+        need(0 <= self.k <= 6, "k", "must be in 0..6")
+        need(self.mu > 0, "mu", "must be positive")
+        need(not self.t_final < 0, "t_final", "must be >= 0")
+        need(self.sigma > 0, "sigma", "must be positive (call resolve() to default to 0.1*L)")
+        need(self.t0 > 0, "t0", "must be positive")
+        need(self.vmax_e > 0, "vmax_e", "must be positive")
+        need(self.vmax_i > 0, "vmax_i", "must be positive")
+        need(self.fine_block_cells >= 1, "mesh.fine_block_cells", "must be >= 1")
+        need(self.coarse_block_cells >= 1, "mesh.coarse_block_cells", "must be >= 1")
+        need(self.refinement_ratio >= 1, "mesh.refinement_ratio", "must be >= 1")
+        need(self.v_cells >= 1, "v_cells", "must be >= 1")
+        try:
+            LimiterConfig.parse(self.limiter)
+            ok = True
+        except RuntimeError:
+            ok = False
+        need(ok, "limiter", "must be one of " + ", ".join(LimiterConfig.MODES))
+        need(self.limiter_threshold > 0, "limiter.threshold", "must be positive")
+        need(self.adapt_p > 0 and not self.adapt_gamma < 0 and not self.adapt_p + self.adapt_gamma >= 1,
+             "adaptivity.p/gamma", "need 0 < p, 0 <= gamma, p + gamma < 1")
+        need(self.adapt_tol > 0, "adaptivity.tol", "must be positive")
+        need(self.penalty_scale > 0, "poisson.penalty_scale", "must be positive")
+        need(self.cadence >= 1, "output.cadence", "must be >= 1")
+        need(self.snapshot_cadence >= 0, "output.snapshot_cadence", "must be >= 0")
+        need(self.profile_cadence >= 0, "output.profile_cadence", "must be >= 0")
+        need(self.threads >= 1, "threads", "must be >= 1")
+        return out
+
+    def validate(self) -> None:
+        v = self.violations()
+        if v:
+            raise RuntimeError("invalid configuration:" + "".join("\n  " + s for s in v))
+
+    def echo(self) -> str:
+        """re-ingestible key = value echo (config.cpp:187-218)"""
+        fmt = {"d": RC.g17, "i": str, "b": lambda b: "on" if b else "off", "s": str}
+        return "".join(f"{name} = {fmt[kind](getattr(self, attr))}\n" for name, attr, kind in self.KEYS)
+
+    def nsteps(self) -> int:
+        """std::lround(t_final / dt) (config.cpp:220)"""
+        return RC.lround(self.t_final / self.dt)
 
     @property
     def nx(self) -> int:
@@ -673,14 +806,23 @@ def run_step(state: SimulationState):
     state.run_step()
 
 
-def run(cfg: RunConfig, nsteps: int | None = None, cadence: int = 10, snapshot_cadence: int = 0,
-        profile_cadence: int = 0, out_dir: str | None = "out", device: int = 0,
-        exact: bool = False) -> dict:
-    """run() (run.cpp:60-169): nsteps (default t_final/dt, config.cpp:220) run()
+_FROM_CFG = object()
+
+
+def run(cfg: RunConfig, nsteps: int | None = None, cadence: int | None = None,
+        snapshot_cadence: int | None = None, profile_cadence: int | None = None,
+        out_dir=_FROM_CFG, device: int = 0, exact: bool = False) -> dict:
+    """run() (run.cpp:60-169): nsteps (default cfg.nsteps(), config.cpp:220) run()
     loop bodies with flux.csv rows every `cadence` steps, snapshots / profiles
-    at their cadences, run.log -- into out_dir (None: no files)."""
+    at their cadences, run.log -- into out_dir (None: no files). Cadences and
+    out_dir default to the config's output.* keys."""
     if nsteps is None:
-        nsteps = int(math.floor(cfg.t_final / cfg.dt + 0.5))  # std::lround
+        nsteps = cfg.nsteps()
+    cadence = cfg.cadence if cadence is None else cadence
+    snapshot_cadence = cfg.snapshot_cadence if snapshot_cadence is None else snapshot_cadence
+    profile_cadence = cfg.profile_cadence if profile_cadence is None else profile_cadence
+    if out_dir is _FROM_CFG:
+        out_dir = cfg.out_dir
     grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
                               cfg.refinement_ratio)
     ctx = Context(grid, cfg.k, cfg.penalty_scale, device)
@@ -698,3 +840,28 @@ def run(cfg: RunConfig, nsteps: int | None = None, cadence: int = 10, snapshot_c
                     error=N.lib().sk_last_error().decode() if res.exit_code else "")
     finally:
         ctx.close()
+
+
+# ----------------------------------------------------------------------------
+# shift matrices / the `solkin matrices` table
+# ----------------------------------------------------------------------------
+def build_shift_matrices(k: int, alpha: float):
+    """build_shift_matrices(ReferenceBasis::get(k), alpha) (advection.cpp:27-66):
+    (A, B) as p x p arrays from the library's host constants. No GPU needed."""
+    p = k + 1
+    A = np.zeros((max(p, 1), max(p, 1)))
+    B = np.zeros_like(A)
+    _check(N.lib().sk_shift_matrices(int(k), float(alpha), A.ctypes.data_as(N._dp),
+                                     B.ctypes.data_as(N._dp)))
+    return A, B
+
+
+def matrices_text(alpha: float, order: int) -> str:
+    """the text `solkin matrices --alpha a --order k` prints (tools/solkin_main.cpp:43-57)"""
+    A, B = build_shift_matrices(order, alpha)
+    out = []
+    for name, mat in (("A", A), ("B", B)):
+        out.append(f"{name}(alpha={RC.g17(alpha)}), order {order}:\n")
+        for row in mat:
+            out.append("".join(RC.e17(x) for x in row) + "\n")
+    return "".join(out)
