@@ -100,6 +100,47 @@ __device__ __forceinline__ void defer_push_n(unsigned int* count, unsigned int c
     }
 }
 
+// the same queue staged per warp in shared memory: flagged entries collect in
+// the warp's kQCap-slot slice and reach the global list in one atomic + one
+// coalesced copy per flush, so a warp stalls on the contended counter once per
+// kQCap entries instead of once per flagged tile. n is warp-uniform.
+constexpr int kQCap = 64;
+__device__ __forceinline__ void wq_flush(unsigned long long* q, int& n, unsigned int* count,
+                                         unsigned int cap, unsigned long long* list,
+                                         unsigned members = 0xffffffffu) {
+    if (n == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(members) - 1;
+    __syncwarp(members);
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned)n);
+    base = __shfl_sync(members, base, leader);
+    const int step = __popc(members);  // members' ranks cover the entries
+    for (int i = __popc(members & ((1u << lane) - 1u)); i < n; i += step)
+        if (base + i < cap) list[base + i] = q[i];
+    __syncwarp(members);
+    n = 0;
+}
+template <int N>
+__device__ __forceinline__ void wq_push(unsigned long long* q, int& n, unsigned int* count, unsigned int cap,
+                                        unsigned long long* list, const bool (&want)[N],
+                                        const unsigned long long (&entry)[N],
+                                        unsigned members = 0xffffffffu) {
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < N; ++i) any |= want[i];
+    if (!__any_sync(members, any)) return;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const unsigned m = __ballot_sync(members, want[i]);
+        if (!m) continue;
+        if (n + __popc(m) > kQCap) wq_flush(q, n, count, cap, list, members);
+        if (want[i]) q[n + __popc(m & ((1u << lane) - 1u))] = entry[i];
+        n += __popc(m);
+    }
+}
+
 // per-species limiter counters of a whole block: warp reduce -> shared ->
 // one global atomic per nonzero counter per block (the fixup kernels' per-warp
 // atomics all hit the same six words)
@@ -464,7 +505,7 @@ struct XCfg {
     static constexpr int STAGE = ((WIN + NF + HDR + 1) / 2) * 2;
     static constexpr int S = 5;                     // input stages (outputs go straight to HBM)
     static constexpr int RACC = 0;                  // (fused-moment accumulators live in registers)
-    static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + RACC) + 8 * 2 * S;
+    static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + RACC) + 8 * 2 * S + 8 * NC * kQCap;
 };
 
 struct XTile {
@@ -541,6 +582,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     double* racc = smem + C::S * C::STAGE;                   // [T][P] this CTA's column (RHO)
     unsigned long long* full = reinterpret_cast<unsigned long long*>(racc + C::RACC);
     unsigned long long* empty = full + C::S;
+    unsigned long long* wqueue = empty + C::S;  // [NC][kQCap] deferred entries per consumer warp
     const Grid& g = a.grid;
     const int ntot = a.nspecies * a.nlines * a.tile_start[g.nblocks];
     const int G = gridDim.x;
@@ -691,6 +733,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     [[maybe_unused]] const ThrCut cut{a.threshold, a.thr_hi, a.thr_lo};
     unsigned nt_t = 0, nt_c = 0, nt_o = 0;
     bool bad = false;
+    unsigned long long* wq = wqueue + warp * kQCap;
+    int wq_n = 0;
     // fused moment: the grid is a multiple of the tiles per line, so this CTA
     // always sees the same tile column and each thread the same cells -- the
     // accumulators live in registers
@@ -744,7 +788,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stg]);
-                defer_push_n<NCC>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+                wq_push<NCC>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry);
             };
             if (C::CPT == 2 && ncc == 2) {
                 flags(std::integral_constant<int, C::CPT>{});
@@ -818,7 +862,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
             // troubled cells are queued for the fixup kernel (on overflow it rescans)
-            if constexpr (INLINE) defer_push_n<NCC>(a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+            if constexpr (INLINE) wq_push<NCC>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry);
             double* dline = dstp(sp) + lbase + (long long)(g.start[b] + c0) * P;
 #pragma unroll
             for (int cc = 0; cc < NCC; ++cc) {
@@ -867,6 +911,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             }
         }
     }
+    if constexpr (INLINE || MODE >= 1) wq_flush(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list);
     if constexpr (INLINE) count_flags(a.st->stats[a.nspecies == 1 ? a.species0 : 0], nt_t, nt_c, nt_o);
     if (a.check_finite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.st->nonfinite, 1);
 }
@@ -2077,6 +2122,9 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
     const int sp = a.species0 + blockIdx.z;
     const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
     const unsigned members = __ballot_sync(0xffffffffu, xd < a.nxd);
+    __shared__ unsigned long long wqueue[kVThreads / 32][kQCap];
+    unsigned long long* wq = wqueue[threadIdx.x >> 5];
+    int wq_n = 0;
     if (xd < a.nxd) {
         const double* f = post_live(a, sp);
         double um[P], u0[P], up[P];
@@ -2089,13 +2137,14 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
             const bool tr[1] = {post_flag_t<P, FAST, IND>(a.cfg, a.basis, um, u0, up)};
             const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
                                                  ((unsigned long long)j << 32) | (unsigned)xd};
-            defer_push_n<1>(a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
+            wq_push<1>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
 #pragma unroll
             for (int n = 0; n < P; ++n) {
                 um[n] = u0[n];
                 u0[n] = up[n];
             }
         }
+        wq_flush(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, members);
     }
 }
 
