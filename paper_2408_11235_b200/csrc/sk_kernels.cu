@@ -870,7 +870,19 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 if (c < nt) {
                     // straight to HBM: the warp's lanes cover 32 contiguous cells
                     double* dp = dline + (long long)c * P;
-                    if constexpr (P % 2 == 0) {
+                    if constexpr (P == 4) {
+                        // one 256-bit store per cell: the warp writes 32 whole
+                        // sectors per instruction (two 128-bit stores would each
+                        // touch every sector half-full and double the L1 traffic)
+                        if ((((unsigned long long)dp) & 31) == 0) {
+                            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dp), "d"(o[cc][0]),
+                                         "d"(o[cc][1]), "d"(o[cc][2]), "d"(o[cc][3])
+                                         : "memory");
+                        } else {
+#pragma unroll
+                            for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
+                        }
+                    } else if constexpr (P % 2 == 0) {
                         if ((((unsigned long long)dp) & 15) == 0) {
 #pragma unroll
                             for (int i = 0; i < P / 2; ++i)
