@@ -553,6 +553,24 @@ __device__ __forceinline__ void lds_cell(const double* p, double* u) {
         for (int n = 0; n < P; ++n) u[n] = p[n];
     }
 }
+// the same for a warp reading 32 consecutive cells (lane L: cell base + L):
+// for P = 4 lanes 4..7 of every 8 fetch their two 16-byte halves in swapped
+// order, so each 128-bit load instruction hits all 32 banks once per 8 lanes
+// (4 wavefronts instead of 8)
+template <int P>
+__device__ __forceinline__ void lds_cell_w(const double* p, double* u) {
+    if constexpr (P == 4) {
+        const int h = (threadIdx.x >> 2) & 1;
+        const double2* q = reinterpret_cast<const double2*>(p);
+        const double2 a = q[h], b = q[h ^ 1];
+        u[0] = h ? b.x : a.x;
+        u[1] = h ? b.y : a.y;
+        u[2] = h ? a.x : b.x;
+        u[3] = h ? a.y : b.y;
+    } else {
+        lds_cell<P>(p, u);
+    }
+}
 template <int P>
 __device__ __forceinline__ void sts_cell(double* p, const double* u) {
     if constexpr (P % 2 == 0) {
@@ -806,8 +824,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 #pragma unroll
             for (int cc = 0; cc < NCC; ++cc) {
                 const int c = min(tid + cc * C::NT, nt - 1);
-                lds_cell<P>(win + c * P, ul[cc]);
-                lds_cell<P>(win + (c + 1) * P, ur[cc]);
+                lds_cell_w<P>(win + c * P, ul[cc]);
+                lds_cell_w<P>(win + (c + 1) * P, ur[cc]);
             }
             // advection.cpp:95-101, both cells share each broadcast matrix load
 #pragma unroll
