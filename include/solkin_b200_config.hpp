@@ -305,11 +305,21 @@ inline RunConfig resolve_run_config(const std::string& config_path, const std::s
     return cfg;
 }
 
+// the device context run() builds for a config: Grid1D::three_block over
+// [-L, L] (run.cpp:31), degree k, the SIPG penalty
+inline Context make_context(const RunConfig& cfg, int device = 0) {
+    return Context(GridBlocks::three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
+                                           cfg.refinement_ratio),
+                   cfg.k, cfg.penalty_scale, device);
+}
+
 // run(cfg) (run.cpp:60-169): nsteps, cadences and out_dir from the config
 inline sk_run_result run(const Context& ctx, const RunConfig& cfg) {
     return run(ctx, cfg.to_c(), cfg.nsteps(), cfg.cadence, cfg.snapshot_cadence, cfg.profile_cadence,
                cfg.out_dir);
 }
+// run(const RunConfig&) (run.hpp) with the context built here
+inline sk_run_result run(const RunConfig& cfg, int device = 0) { return run(make_context(cfg, device), cfg); }
 
 // build_shift_matrices (advection.cpp:27-66) from the library's constants
 struct ShiftMatrices {

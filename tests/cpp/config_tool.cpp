@@ -8,6 +8,7 @@
 //   config_tool matrices <alpha> <order>   -> the `solkin matrices` table
 //   config_tool layered <file|-> <preset|-> <limiter|-> <out|-> <threads>
 //       -> resolve_run_config (cmd_run's layering + validate), as eval
+//   config_tool run <file|-> <preset|->   -> `solkin run` on the device (GPU only)
 #include <cstdio>
 #include <cstdlib>
 #include <iostream>
@@ -41,6 +42,12 @@ int main(int argc, char** argv) {
         if (cmd == "layered" && argc == 7) {
             report(solkin_b200::resolve_run_config(arg(argv[2]), arg(argv[3]), arg(argv[4]),
                                                    arg(argv[5]), std::atoi(argv[6])));
+            return 0;
+        }
+        if (cmd == "run" && argc == 4) {
+            const RunConfig cfg = solkin_b200::resolve_run_config(arg(argv[2]), arg(argv[3]));
+            const sk_run_result r = solkin_b200::run(cfg);
+            std::cout << "exit " << r.exit_code << " steps " << r.steps_done << "\n";
             return 0;
         }
         if (cmd == "matrices" && argc == 4) {

@@ -718,3 +718,45 @@ def test_post_limiters_conserve_mass(sk, mode):
             before = f.mass()
             sk.apply_post_limiter(f, direction, lim)
             assert abs(f.mass() - before) <= 1e-13 * abs(before), (sp, direction)
+
+
+@pytest.mark.gpu
+def test_run_from_config_file(sk, ref, tmp_path):
+    """§8f N4: `solkin run --config` through the C++ mirror (resolve_run_config +
+    run(const RunConfig&)) and the Python RunConfig write the same files (same
+    library, bitwise), and match the reference's run() on that config"""
+    import shutil
+    import subprocess
+
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    from paper_2408_11235_b200 import _native
+
+    tool = str(tmp_path / "config_tool")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), "-o", tool,
+                        os.path.join(ROOT, "tests", "cpp", "config_tool.cpp"), _native.LIB,
+                        "-Wl,-rpath," + os.path.dirname(_native.LIB)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    cpp_dir, py_dir, ref_dir = tmp_path / "cpp", tmp_path / "py", tmp_path / "ref"
+    text = ("# small injection-free blob run\nk = 2\nmu = 1836\nmesh.fine_block_cells = 16\n"
+            "mesh.coarse_block_cells = 32\nv_cells = 40\nlimiter = sldg\nt_final = 1.2\n"
+            "output.cadence = 3\noutput.snapshot_cadence = 6\noutput.profile_cadence = 6\n")
+    cfg_path = tmp_path / "run.cfg"
+    cfg_path.write_text(text + f"output.dir = {cpp_dir}\n")
+    r = subprocess.run([tool, "run", str(cfg_path), "-"], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.startswith("exit 0 steps 12"), r.stdout + r.stderr
+    cfg = sk.RunConfig.from_file(str(cfg_path))
+    cfg.out_dir = str(py_dir)
+    cfg.resolve()
+    cfg.validate()
+    out = sk.run(cfg)
+    assert out["exit_code"] == 0 and out["steps_done"] == cfg.nsteps() == 12
+    for name in ("flux.csv", "snapshot_6.bin", "snapshot_12.bin", "profiles_12.csv"):
+        assert (cpp_dir / name).read_bytes() == (py_dir / name).read_bytes(), name
+    ref.state(**cfg.oracle_kwargs()).run_files(cfg.t_final, cfg.cadence, cfg.snapshot_cadence,
+                                               cfg.profile_cadence, ref_dir)
+    ga = np.loadtxt(py_dir / "flux.csv", delimiter=",", skiprows=1)
+    gb = np.loadtxt(ref_dir / "flux.csv", delimiter=",", skiprows=1)
+    assert ga.shape == gb.shape == (5, 12)
+    scale = np.maximum(np.abs(gb).max(axis=0), 1e-300)
+    assert (np.abs(ga - gb) / scale).max() <= 1e-12
