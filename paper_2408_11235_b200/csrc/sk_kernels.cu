@@ -1947,61 +1947,128 @@ __global__ void shrink_table_kernel(const __grid_constant__ ShrinkArgs a) {
     for (int q = np; q < 4; ++q) cellv[q] = -1;
 }
 
-// per x dof, new cell j: dst[m] = sum_pieces (sum_n T[m][n] src[n]) (adaptivity.cpp:109-124)
+// wait until at most n cp.async groups are pending (n < 8, run time value)
+__device__ __forceinline__ void cp_wait_dyn(int n) {
+    switch (n) {
+        case 0: cp_wait<0>(); break;
+        case 1: cp_wait<1>(); break;
+        case 2: cp_wait<2>(); break;
+        case 3: cp_wait<3>(); break;
+        case 4: cp_wait<4>(); break;
+        case 5: cp_wait<5>(); break;
+        case 6: cp_wait<6>(); break;
+        default: cp_wait<7>(); break;
+    }
+}
+
+// per x dof, new cell j: dst[m] = sum_pieces (sum_n T[m][n] src[n]) (adaptivity.cpp:109-124).
+// The old cells of a chunk of new cells form one increasing run [olo, ohi];
+// they stream through the v sweep's per-thread cp.async ring (old cell c in
+// slot (c - olo) % R, one commit group per cell), so R*P loads stay in flight
+// per thread. Consecutive new cells share their boundary old cell, and the
+// rounded new-cell edges (aa_{j+1} vs bb_j) can send cell j+1 one old cell
+// back: a slot is refilled only once the current new cell starts two old
+// cells past it. A cell outside the ring window is read from global directly.
 template <int P>
-__global__ void shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
+__global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
+    // the block's threads share the chunk: its transfer matrices are staged
+    // once per item (coalesced) instead of each warp re-reading them per cell;
+    // a 4-deep ring then keeps the CTA at 32 KB (7 CTAs, 28 warps per SM)
+    constexpr bool TS = P <= 4;
+    constexpr int R = TS ? 4 : vring<P>();
+    static_assert(R <= 8, "cp_wait_dyn covers 8 groups");
+    __shared__ double ring[R * P * kVThreads];
+    constexpr int TN = 4 * P * P;  // doubles per new cell
+    __shared__ __align__(16) double tsh[TS ? kVChunk * TN : 2];
     const int sp = blockIdx.z;
     // bounded grid, (x block, v chunk) items by grid stride: on the (usual)
     // steps without a shrink the whole launch is a few hundred early exits
     if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
-    const int nxb = (a.nxd + blockDim.x - 1) / blockDim.x;
+    const int nxb = (a.nxd + kVThreads - 1) / kVThreads;
     const long long nitems = (long long)nxb * ((a.nv + kVChunk - 1) / kVChunk);
     const bool fl = field_flipped(a.flip[sp]);
     const double* f = fl ? a.out[sp] : a.f[sp];
     double* out = fl ? a.f[sp] : a.out[sp];
+    double* my = ring + threadIdx.x;
+    const long long ld = a.ld;
     for (long long w = blockIdx.x; w < nitems; w += gridDim.x) {
-        const int xd = (int)(w % nxb) * blockDim.x + threadIdx.x;
-        if (xd >= a.nxd) continue;
+        const int xd = (int)(w % nxb) * kVThreads + threadIdx.x;
         const int j0 = (int)(w / nxb) * kVChunk, j1 = min(j0 + kVChunk, a.nv);
-        // old cells come in increasing order and consecutive new cells share
-        // their boundary old cell: keep the last one in registers (halves the
-        // DRAM reads of a shrink)
-        int last = -1;
-        double lastv[P];
+        if constexpr (TS) {
+            const double* tg = a.ttab[sp] + ((long long)a.cell0 + j0) * TN;
+            __syncthreads();  // the previous item's readers are done
+            for (int i = threadIdx.x; i < (j1 - j0) * TN; i += kVThreads) tsh[i] = tg[i];
+            __syncthreads();
+        }
+        if (xd >= a.nxd) continue;
+        const int* cv0 = a.tcell[sp] + ((long long)a.cell0 + j0) * 4;
+        const int* cv1 = a.tcell[sp] + ((long long)a.cell0 + j1 - 1) * 4;
+        const int olo = cv0[0] - a.cell0;
+        int ohi = olo;
+        for (int pc = 0; pc < 4 && cv1[pc] >= 0; ++pc) ohi = cv1[pc] - a.cell0;
+        // old cells outside the allocated rows are reported when consumed
+        auto issue = [&](int c) {
+            const bool ok = c >= -a.halo && c < a.nv + a.halo;
+            const double* g = f + xd + (ok ? (long long)c * P * ld : 0);
+            double* slot = my + ((c - olo) % R) * P * kVThreads;
+#pragma unroll
+            for (int n = 0; n < P; ++n) cp_async8(slot + n * kVThreads, g + n * ld, ok);
+            cp_commit();
+        };
+        int iss = olo;  // next old cell to issue; groups committed = iss - olo
+        for (; iss <= ohi && iss < olo + R; ++iss) issue(iss);
         for (int j = j0; j < j1; ++j) {
             double dst[P];
 #pragma unroll
             for (int m = 0; m < P; ++m) dst[m] = 0.0;
             const long long jg = (long long)a.cell0 + j;  // global new cell
-            const double* T = a.ttab[sp] + jg * 4 * P * P;
+            const double* T = TS ? tsh + (j - j0) * TN : a.ttab[sp] + jg * TN;
             const int* cellv = a.tcell[sp] + jg * 4;
+            int oc = olo;
             for (int pc = 0; pc < 4; ++pc) {
-                int oc = cellv[pc];
-                if (oc < 0) break;
-                oc -= a.cell0;  // local old cell; a shard reads up to `halo` beyond its range
+                const int c = cellv[pc];
+                if (c < 0) break;
+                oc = c - a.cell0;  // local old cell; a shard reads up to `halo` beyond its range
                 if (oc < -a.halo || oc >= a.nv + a.halo) {
                     raise_error(a.st, 1, 6, oc, a.halo, a.st->step);
                     break;
                 }
-                if (oc != last) {
-#pragma unroll
-                    for (int n = 0; n < P; ++n) lastv[n] = f[((long long)oc * P + n) * a.ld + xd];
-                    last = oc;
-                }
                 double src[P];
+                if (oc >= iss - R && oc < iss && oc >= olo) {
+                    cp_wait_dyn(iss - 1 - oc);
+                    const double* sl = my + ((oc - olo) % R) * P * kVThreads;
 #pragma unroll
-                for (int n = 0; n < P; ++n) src[n] = lastv[n];
+                    for (int n = 0; n < P; ++n) src[n] = sl[n * kVThreads];
+                } else {
+#pragma unroll
+                    for (int n = 0; n < P; ++n) src[n] = f[((long long)oc * P + n) * ld + xd];
+                }
 #pragma unroll
                 for (int m = 0; m < P; ++m) {
+                    double tr[P];  // row m of piece pc (16-byte shared loads when staged)
+                    if constexpr (TS && P % 2 == 0) {
+#pragma unroll
+                        for (int n = 0; n < P; n += 2) {
+                            const double2 t2 = *reinterpret_cast<const double2*>(T + pc * P * P + m * P + n);
+                            tr[n] = t2.x;
+                            tr[n + 1] = t2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int n = 0; n < P; ++n) tr[n] = T[pc * P * P + m * P + n];
+                    }
                     double acc = 0.0;
 #pragma unroll
-                    for (int n = 0; n < P; ++n) acc += T[pc * P * P + m * P + n] * src[n];
+                    for (int n = 0; n < P; ++n) acc += tr[n] * src[n];
                     dst[m] += acc;
                 }
             }
 #pragma unroll
-            for (int m = 0; m < P; ++m) out[((long long)j * P + m) * a.ld + xd] = dst[m];
+            for (int m = 0; m < P; ++m) out[((long long)j * P + m) * ld + xd] = dst[m];
+            // cells below oc - 1 are done: their slots take cells up to oc - 2 + R
+            for (; iss <= ohi && iss < oc - 1 + R; ++iss) issue(iss);
         }
+        cp_wait<0>();
     }
 }
 
@@ -2708,7 +2775,7 @@ cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s) {
         SK_DISPATCH_P(P, (shrink_check_kernel<PP><<<dim3((a.nxd + 255) / 256, 2), 256, 0, s>>>(a)));
     if (a.force < 0) return cudaGetLastError();
     SK_DISPATCH_P(P, (shrink_table_kernel<PP><<<dim3((a.nv_global + 127) / 128, 2), 128, 0, s>>>(a)));
-    SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3(sm_count() * 16, 1, 2), 128, 0, s>>>(a)));
+    SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3(sm_count() * 8, 1, 2), kVThreads, 0, s>>>(a)));
     shrink_finalize_kernel<<<1, 32, 0, s>>>(a);
     return cudaGetLastError();
 }

@@ -133,8 +133,11 @@ def test_post_limiters_bitwise(sk, ora, mode, m):
             assert np.array_equal(f.download(), o.field(sp)), f"{mode} dir{d} sp{sp}"
 
 
-def test_velocity_cutoff_bitwise(sk, ora):
-    cfg, o, st = _pair(sk, ora, dict(k=3, nf=8, nc=16, m=1, nv=24, mu=1836.0))
+@pytest.mark.parametrize("k,nv", [(3, 24), (3, 200), (2, 131), (6, 70)])
+def test_velocity_cutoff_bitwise(sk, ora, k, nv):
+    """one and several v chunks per thread (the projection's cp.async ring:
+    8 slots for p <= 4, 4 for p > 4), ragged last chunk"""
+    cfg, o, st = _pair(sk, ora, dict(k=k, nf=8, nc=16, m=1, nv=nv, mu=1836.0))
     pol = sk.VAdjustPolicy(cfg.adapt_p, cfg.adapt_gamma, cfg.adapt_tol)
     for sp in (0, 1):
         f = st.field(sp)
@@ -144,7 +147,9 @@ def test_velocity_cutoff_bitwise(sk, ora):
             r = sk.shrink_velocity_domain(f, pol)
             ro = o.shrink(sp)
             assert np.array_equal(f.download(), o.field(sp))
-            assert r["vmax_after"] == o.vmax(sp) == ro["vmax_after"]
+            # vmax_after is new_vmax (adaptivity.cpp:103,127); vmax() is the new
+            # grid's right() = left + cells*dx, which can differ in the last bit
+            assert r["vmax_after"] == ro["vmax_after"] and f.vmax() == o.vmax(sp)
             assert abs(r["mass_after"] - ro["mass_after"]) <= 1e-12 * abs(ro["mass_after"])
     # a field with mass at the probe velocity must not shrink
     f = st.field(0)
@@ -755,8 +760,24 @@ def test_run_from_config_file(sk, ref, tmp_path):
         assert (cpp_dir / name).read_bytes() == (py_dir / name).read_bytes(), name
     ref.state(**cfg.oracle_kwargs()).run_files(cfg.t_final, cfg.cadence, cfg.snapshot_cadence,
                                                cfg.profile_cadence, ref_dir)
-    ga = np.loadtxt(py_dir / "flux.csv", delimiter=",", skiprows=1)
     gb = np.loadtxt(ref_dir / "flux.csv", delimiter=",", skiprows=1)
+    ga = np.loadtxt(py_dir / "flux.csv", delimiter=",", skiprows=1)
     assert ga.shape == gb.shape == (5, 12)
-    scale = np.maximum(np.abs(gb).max(axis=0), 1e-300)
-    assert (np.abs(ga - gb) / scale).max() <= 1e-12
+    # fast mode: t, masses and v_max to 1e-12 relative; the wall fluxes and the
+    # E energy follow E's absolute contract, 1e-12 * max(1, scale) (early E is
+    # ~1e-5 and carries the rho cancellation: 3e-11 relative even between two
+    # CPU builds -- SURVEY §8c)
+    rel, ab = [0, 7, 8, 10, 11], [1, 2, 3, 4, 5, 6, 9]
+    scale = np.maximum(np.abs(gb[:, rel]).max(axis=0), 1e-300)
+    assert (np.abs(ga[:, rel] - gb[:, rel]) / scale).max() <= 1e-12
+    tol = 1e-12 * np.maximum(1.0, np.abs(gb[:, ab]).max(axis=0))
+    assert (np.abs(ga[:, ab] - gb[:, ab]) <= tol).all()
+    # exact mode on the same config reproduces the reference's rows (t, fluxes,
+    # E energy, v_max bitwise; the masses come from a parallel reduction)
+    ex_dir = tmp_path / "exact"
+    out = sk.run(cfg, out_dir=str(ex_dir), exact=True)
+    assert out["exit_code"] == 0 and out["steps_done"] == 12
+    ge = np.loadtxt(ex_dir / "flux.csv", delimiter=",", skiprows=1)
+    cols = [0, 1, 2, 3, 4, 5, 6, 9, 10, 11]
+    assert np.array_equal(ge[:, cols], gb[:, cols])
+    assert np.abs(ge[:, 7:9] - gb[:, 7:9]).max() <= 1e-12 * np.abs(gb[:, 7:9]).max()
