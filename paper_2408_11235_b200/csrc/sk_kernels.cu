@@ -1980,6 +1980,7 @@ __global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_
     __shared__ double ring[R * P * kVThreads];
     constexpr int TN = 4 * P * P;  // doubles per new cell
     __shared__ __align__(16) double tsh[TS ? kVChunk * TN : 2];
+    __shared__ int csh[TS ? kVChunk * 4 : 1];  // the chunk's old-cell lists
     const int sp = blockIdx.z;
     // bounded grid, (x block, v chunk) items by grid stride: on the (usual)
     // steps without a shrink the whole launch is a few hundred early exits
@@ -1998,11 +1999,13 @@ __global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_
             const double* tg = a.ttab[sp] + ((long long)a.cell0 + j0) * TN;
             __syncthreads();  // the previous item's readers are done
             for (int i = threadIdx.x; i < (j1 - j0) * TN; i += kVThreads) tsh[i] = tg[i];
+            const int* cg = a.tcell[sp] + ((long long)a.cell0 + j0) * 4;
+            for (int i = threadIdx.x; i < (j1 - j0) * 4; i += kVThreads) csh[i] = cg[i];
             __syncthreads();
         }
         if (xd >= a.nxd) continue;
-        const int* cv0 = a.tcell[sp] + ((long long)a.cell0 + j0) * 4;
-        const int* cv1 = a.tcell[sp] + ((long long)a.cell0 + j1 - 1) * 4;
+        const int* cv0 = TS ? csh : a.tcell[sp] + ((long long)a.cell0 + j0) * 4;
+        const int* cv1 = cv0 + (j1 - 1 - j0) * 4;
         const int olo = cv0[0] - a.cell0;
         int ohi = olo;
         for (int pc = 0; pc < 4 && cv1[pc] >= 0; ++pc) ohi = cv1[pc] - a.cell0;
@@ -2023,7 +2026,7 @@ __global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_
             for (int m = 0; m < P; ++m) dst[m] = 0.0;
             const long long jg = (long long)a.cell0 + j;  // global new cell
             const double* T = TS ? tsh + (j - j0) * TN : a.ttab[sp] + jg * TN;
-            const int* cellv = a.tcell[sp] + jg * 4;
+            const int* cellv = cv0 + (j - j0) * 4;
             int oc = olo;
             for (int pc = 0; pc < 4; ++pc) {
                 const int c = cellv[pc];
