@@ -11,7 +11,8 @@ Bar:
     (The charge-density reduction order differs from the serial reference,
     so full steps are tolerance-level, App. A item 6.)
   * full size (C3): sampled x and v lines of one GPU sweep, bitwise in exact
-    mode, <= 1e-12 in fast mode.
+    mode, <= 1e-12 in fast mode; 11 whole run() loop bodies in exact mode
+    bitwise against the reference's own loop (oracle/_ref).
 """
 import os
 import subprocess
@@ -781,3 +782,27 @@ def test_run_from_config_file(sk, ref, tmp_path):
     cols = [0, 1, 2, 3, 4, 5, 6, 9, 10, 11]
     assert np.array_equal(ge[:, cols], gb[:, cols])
     assert np.abs(ge[:, 7:9] - gb[:, 7:9]).max() <= 1e-12 * np.abs(gb[:, 7:9]).max()
+
+
+def test_c3_full_size_run_matches_reference(sk, ref):
+    """C3 at BASELINE size (2048x4096 cells per species, k=3, mu=1836, sldg,
+    cut-off on): 11 run() loop bodies (run.cpp:124-131) in exact mode against
+    the reference's own loop (oracle/_ref, all host threads). f of both
+    species, E, v_max and the shrink counts must be bitwise the reference's;
+    11 steps put the first cut-off check past its 10-step cooldown."""
+    cfg = sk.named_config("C3")
+    n = 11
+    st = sk.SimulationState(cfg, exact=True)
+    st.run_steps(n)
+    st.ctx.synchronize()
+    r = ref.state(threads=os.cpu_count() or 1, **cfg.oracle_kwargs())
+    r.run(n)
+    assert st.step_index() == r.step_index() == n
+    assert np.array_equal(st.E(), r.E())
+    for sp in (0, 1):
+        assert st.shrinks(sp)[0] == r.shrinks(sp), f"shrinks sp{sp}"
+        assert st.field(sp).vmax() == r.vmax(sp), f"v_max sp{sp}"
+        got, want = st.field(sp).download(), r.field(sp)
+        assert got.shape == want.shape and np.array_equal(got, want), \
+            f"sp{sp}: max rel diff {rel(got, want):.3e}"
+    st.close()
