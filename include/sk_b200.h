@@ -126,6 +126,16 @@ sk_status sk_ctx_set_eager_errors(sk_ctx* ctx, int on);
  * fused into the first x sweep, block-cyclic-reduction solve; results agree
  * with the reference to the 1e-12 relative tolerance. */
 sk_status sk_ctx_set_exact_reductions(sk_ctx* ctx, int on);
+/* Exact mode per part, for attributing a fast-mode deviation: any OR of
+ * SK_EXACT_ARITH (unfused sweep/limiter arithmetic), SK_EXACT_RHO (charge
+ * density in the reference's serial order, poisson.cpp:194-216) and
+ * SK_EXACT_POISSON (dpbtrs order, poisson.cpp:166-174). SK_EXACT_ALL is
+ * sk_ctx_set_exact_reductions(ctx, 1); 0 is fast mode. */
+#define SK_EXACT_ARITH 1
+#define SK_EXACT_RHO 2
+#define SK_EXACT_POISSON 4
+#define SK_EXACT_ALL 7
+sk_status sk_ctx_set_exact_parts(sk_ctx* ctx, int mask);
 /* Capacity of the deferred limiter-clamp list (troubled cells queued by the
  * sweeps, clamped by a fixup kernel); above it the fixup rescans the sweep.
  * Default and maximum 4 Mi cells; exposed for testing the rescan path. */

@@ -17,6 +17,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libsk_oracle.so")
+ORACLE_FMA_SO = os.path.join(HERE, "_build", "libsk_oracle_fma.so")  # envelope: FMA build
 REF_SO = os.path.join(HERE, "_ref", "libsolkin_ref.so")
 
 _dp = C.POINTER(C.c_double)
@@ -88,6 +89,7 @@ class Oracle(_Lib):
         L.sko_state_post_limit.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p]
         L.sko_state_charge_density.argtypes = [C.c_void_p, _dp]
         L.sko_state_poisson_solve.argtypes = [C.c_void_p, _dp, _dp, _dp]
+        L.sko_set_lapack.argtypes = [C.c_void_p, C.c_void_p]
         L.sko_state_shrink.argtypes = [C.c_void_p, C.c_int, _dp]
         L.sko_state_summary.argtypes = [C.c_void_p, _dp]
         L.sko_lagrange.restype = C.c_double
@@ -242,6 +244,17 @@ class Oracle(_Lib):
         """0 = reference order; 1 = electrons first (rounding-noise envelope)"""
         self.lib.sko_set_rho_order(int(mode))
 
+    def set_lapack(self, lib=None):
+        """Poisson operators created from now on factor and solve with
+        ``lib``'s dpbtrf_/dpbtrs_ (a ctypes CDLL, e.g. openblas()); None = the
+        reference-LAPACK restatement. Rounding-noise envelope only."""
+        if lib is None:
+            self.lib.sko_set_lapack(None, None)
+        elif isinstance(lib, tuple):  # raw (dpbtrf, dpbtrs) function addresses
+            self.lib.sko_set_lapack(C.c_void_p(lib[0]), C.c_void_p(lib[1]))
+        else:
+            self.lib.sko_set_lapack(C.cast(lib.dpbtrf_, C.c_void_p), C.cast(lib.dpbtrs_, C.c_void_p))
+
     def state(self, **cfg) -> "OracleState":
         return OracleState(self, **cfg)
 
@@ -255,6 +268,34 @@ def _cfg_args(cfg):
         raise KeyError(f"unknown oracle config keys {unknown}")
     c.update({k: v for k, v in cfg.items() if k in c})
     return c
+
+
+def openblas():
+    """The OpenBLAS 0.3.15 shipped in this image (opencv wheel), or None."""
+    import glob
+
+    d = "/opt/prime-rl/.venv/lib/python3.12/site-packages/opencv_python_headless.libs/"
+    libs = glob.glob(d + "libopenblas*.so")
+    if not libs:
+        return None
+    for dep in glob.glob(d + "libquadmath*") + glob.glob(d + "libgfortran*"):
+        C.CDLL(dep, mode=C.RTLD_GLOBAL)
+    return C.CDLL(libs[0])
+
+
+def scipy_lapack():
+    """(dpbtrf, dpbtrs) addresses of the LAPACK scipy links (scipy-openblas,
+    a different build from openblas()), or None."""
+    try:
+        from scipy.linalg import cython_lapack
+    except Exception:
+        return None
+    get = C.pythonapi.PyCapsule_GetPointer
+    get.restype, get.argtypes = C.c_void_p, [C.py_object, C.c_char_p]
+    name = C.pythonapi.PyCapsule_GetName
+    name.restype, name.argtypes = C.c_char_p, [C.py_object]
+    caps = cython_lapack.__pyx_capi__
+    return tuple(get(caps[f], name(caps[f])) for f in ("dpbtrf", "dpbtrs"))
 
 
 class _StateBase:
@@ -365,6 +406,21 @@ class OracleState(_StateBase):
         self._check(self.lib.sko_state_poisson_solve(self.h, pr, E.ctypes.data_as(_dp),
                                                      phi.ctypes.data_as(_dp)))
         return E, phi
+
+    def poisson_band(self):
+        """the assembled SIPG band (kd+1 rows per column, lower, column-major)"""
+        n, kd = C.c_int(), C.c_int()
+        f = self.lib.sko_state_poisson_band
+        f.restype, f.argtypes = _dp, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        ptr = f(self.h, C.byref(n), C.byref(kd))
+        return np.ctypeslib.as_array(ptr, shape=(n.value, kd.value + 1)).copy()
+
+    def poisson_load(self, rho):
+        rho, pr = _arr(rho)
+        out = np.zeros(self.nx * (self.k + 2))
+        self.lib.sko_state_poisson_load.argtypes = [C.c_void_p, _dp, _dp]
+        self._check(self.lib.sko_state_poisson_load(self.h, pr, out.ctypes.data_as(_dp)))
+        return out
 
     def check_shrink(self, species):
         r = self.lib.sko_state_check_shrink(self.h, species)

@@ -1174,12 +1174,25 @@ int sko_shrink_velocity_domain(sko_field* f, double pp, double gamma, double tol
  * ==================================================================== */
 
 /* poisson.cpp:38-57 ctor */
+/* Noise-envelope knob (tests only, tests/golden/make_c3_envelope.py): factor
+ * and solve with another LAPACK's dpbtrf_/dpbtrs_ (e.g. the OpenBLAS in the
+ * image) instead of the reference-LAPACK restatement. The reference pins no
+ * LAPACK (core/CMakeLists.txt:1), so this spread is part of its own noise.
+ * Applies to Poisson operators created while it is set. */
+static sko_dpbtrf_fn g_lapack_trf = 0;
+static sko_dpbtrs_fn g_lapack_trs = 0;
+void sko_set_lapack(sko_dpbtrf_fn trf, sko_dpbtrs_fn trs) {
+    g_lapack_trf = trf;
+    g_lapack_trs = trs;
+}
+
 int sko_poisson_init(sko_poisson* P, const sko_grid* g, int k, double penalty_scale) {
     memset(P, 0, sizeof *P);
     if (k < 0) return fail(SKO_ERR_RUNTIME, "PoissonOperator: degree must be >= 0");
     if (!(penalty_scale > 0))
         return fail(SKO_ERR_RUNTIME, "PoissonOperator: penalty_scale must be positive");
     P->grid = *g;
+    P->lapack_trs = g_lapack_trs;
     P->k = k;
     P->p = k + 2;
     P->n = g->ncells * (k + 2);
@@ -1266,7 +1279,14 @@ int sko_poisson_init(sko_poisson* P, const sko_grid* g, int k, double penalty_sc
     /* poisson.cpp:124-133 factorize */
     P->factor = (double*)malloc(sizeof(double) * (size_t)ldab * P->n);
     memcpy(P->factor, P->band, sizeof(double) * (size_t)ldab * P->n);
-    int info = sko_dpbtrf_lower(P->n, P->kd, P->factor, ldab);
+    int info;
+    if (g_lapack_trf) {  /* envelope knob: another LAPACK's dpbtrf_ (Fortran ABI) */
+        int n = P->n, kd = P->kd, ld = ldab;
+        info = 0;
+        g_lapack_trf("L", &n, &kd, P->factor, &ld, &info);
+    } else {
+        info = sko_dpbtrf_lower(P->n, P->kd, P->factor, ldab);
+    }
     if (info != 0)
         return fail(SKO_ERR_RUNTIME,
                     "Poisson factorization failed (matrix not positive definite; penalty_scale "
@@ -1300,7 +1320,12 @@ int sko_poisson_build_load(const sko_poisson* P, const double* rho, double* load
 /* poisson.cpp:166-192 solve_raw + solve */
 int sko_poisson_solve(const sko_poisson* P, const double* rho, double* phi, double* E) {
     sko_poisson_build_load(P, rho, phi);
-    sko_dpbtrs_lower(P->n, P->kd, P->factor, P->kd + 1, phi);
+    if (P->lapack_trs) {
+        int n = P->n, kd = P->kd, ld = P->kd + 1, one = 1, info = 0;
+        P->lapack_trs("L", &n, &kd, &one, P->factor, &ld, phi, &n, &info);
+    } else {
+        sko_dpbtrs_lower(P->n, P->kd, P->factor, P->kd + 1, phi);
+    }
     const int k = P->k, ps = P->p;
     for (int c = 0; c < P->grid.ncells; ++c) {
         double h = sko_grid_cell_width(&P->grid, c);
@@ -1595,6 +1620,16 @@ long sko_state_field_size(sko_state* S, int species) {
 }
 double sko_state_vmax(sko_state* S, int species) { return sko_grid_right(&sfield(S, species)->v); }
 double* sko_state_E(sko_state* S) { return S->E; }
+/* tests only: the Poisson load vector (poisson.cpp:135-149) */
+int sko_state_poisson_load(sko_state* S, const double* rho, double* load) {
+    return sko_poisson_build_load(&S->poisson, rho, load);
+}
+/* tests only: the assembled SIPG band before factorisation, (kd+1) x n column-major lower */
+const double* sko_state_poisson_band(sko_state* S, int* n, int* kd) {
+    *n = S->poisson.n;
+    *kd = S->poisson.kd;
+    return S->poisson.band;
+}
 double* sko_state_phi(sko_state* S) { return S->phi; }
 long sko_state_step_index(sko_state* S) { return S->step; }
 int sko_state_shrinks(sko_state* S, int species) {

@@ -164,9 +164,13 @@ int sko_check_velocity_shrink(const sko_field* f, double p, double gamma, double
 int sko_shrink_velocity_domain(sko_field* f, double p, double gamma, double tol, double* result);
 
 /* ---- poisson (poisson.cpp) ---- */
+typedef void (*sko_dpbtrf_fn)(const char*, const int*, const int*, double*, const int*, int*);
+typedef void (*sko_dpbtrs_fn)(const char*, const int*, const int*, const int*, const double*,
+                              const int*, double*, const int*, int*);
 typedef struct {
     sko_grid grid;
     int k, p, n, kd;
+    sko_dpbtrs_fn lapack_trs; /* envelope knob, NULL = restatement */
     double penalty_scale, symmetry_defect;
     double* band;   /* (kd+1) x n, column-major lower band */
     double* factor; /* banded Cholesky factor */
@@ -180,6 +184,8 @@ int sko_poisson_solve(const sko_poisson* P, const double* rho, double* phi, doub
 void sko_charge_density(const sko_field* fe, const sko_field* fi, double* rho);
 /* tests only: 0 = reference order, 1 = electrons first (noise envelope) */
 void sko_set_rho_order(int mode);
+/* tests only: NULL, NULL = the restatement (reference-LAPACK order) */
+void sko_set_lapack(sko_dpbtrf_fn trf, sko_dpbtrs_fn trs);
 double sko_electric_energy(const sko_grid* g, int k, const double* E);
 
 /* LAPACK restatement (lapack_band.c): reference-LAPACK dpbtf2 + dtbsv order */

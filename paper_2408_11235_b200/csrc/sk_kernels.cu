@@ -1340,6 +1340,32 @@ __global__ void rho_reduce_kernel(const __grid_constant__ RhoArgs a) {
 // Poisson: replay of the host block-cyclic-reduction plan (single CTA, one
 // thread per block row per level, PS = k+2 compile-time)
 // ---------------------------------------------------------------------------
+// Load value of row i = c*PS + m for the BCR replay: stage 0/1 the SIPG load
+// (poisson.cpp:135-149); stage 2 the residual b_i - (A x)_i of the stage-1
+// solution x (band rows i-kd .. i+kd, j ascending).
+template <int PS>
+__device__ __forceinline__ double poisson_load(const PoissonDev& pd, int stage, const double* rho, int c, int m) {
+    constexpr int KD = 2 * PS - 1, LD = KD + 1;
+    const int k = PS - 2;
+    double val = 0.0;
+#pragma unroll
+    for (int n = 0; n <= k; ++n) val += pd.interp[m * (k + 1) + n] * rho[c * (k + 1) + n];
+    double b = pd.ws[m] * pd.h[c] * val;
+    if (stage == 2) {
+        const int i = c * PS + m, n = pd.ncells * PS;
+        double ax = 0.0;
+#pragma unroll
+        for (int d = -KD; d <= KD; ++d) {
+            const int j = i + d;
+            if (j < 0 || j >= n) continue;
+            const double aij = d < 0 ? pd.band[(long long)j * LD - d] : pd.band[(long long)i * LD + d];
+            ax += aij * pd.ir_x[j];
+        }
+        b -= ax;
+    }
+    return b;
+}
+
 // M is stored transposed over rows: entry (m,n) of row r at M[(m*PS+n)*rows + r]
 template <int PS>
 __device__ __forceinline__ void matvec_t(const double* __restrict__ M, int rows, int r,
@@ -1354,7 +1380,7 @@ __device__ __forceinline__ void matvec_t(const double* __restrict__ M, int rows,
 }
 
 template <int PS>
-__global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ PoissonDev pd,
+__global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ PoissonDev pd, int stage,
                                                        const double* __restrict__ rho,
                                                        double* __restrict__ E,
                                                        double* __restrict__ phi) {
@@ -1363,12 +1389,9 @@ __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ P
     const int tid = threadIdx.x, nth = blockDim.x;
     // vectors are SoA per level: b_l[m*Nl + q]
     double* b0 = pd.bws;
-    for (int i = tid; i < N * PS; i += nth) {  // load vector (poisson.cpp:135-149)
+    for (int i = tid; i < N * PS; i += nth) {  // load vector (poisson.cpp:135-149) / residual
         const int m = i / N, c = i - (i / N) * N;
-        double val = 0.0;
-#pragma unroll
-        for (int n = 0; n <= k; ++n) val += pd.interp[m * (k + 1) + n] * rho[c * (k + 1) + n];
-        b0[i] = pd.ws[m] * pd.h[c] * val;
+        b0[i] = poisson_load<PS>(pd, stage, rho, c, m);
     }
     __syncthreads();
     // reduction: b'_r = b_q + alpha_q b_{q-1} + gamma_q b_{q+1}, q = 2r;
@@ -1452,17 +1475,25 @@ __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ P
         __syncthreads();
     }
     const double* x0 = pd.xws;
+    if (stage == 1) {  // first solve of the refinement: keep x, no E yet
+        for (int i = tid; i < N * PS; i += nth) {
+            const int c = i / PS, m = i - (i / PS) * PS;
+            pd.ir_x[i] = x0[m * N + c];
+        }
+        return;
+    }
+    auto xv = [&](int n, int c) { return stage == 2 ? pd.ir_x[c * PS + n] + x0[n * N + c] : x0[n * N + c]; };
     if (phi)
         for (int i = tid; i < N * PS; i += nth) {
             const int c = i / PS, m = i - (i / PS) * PS;
-            phi[i] = x0[m * N + c];
+            phi[i] = xv(m, c);
         }
     // E = -phi' at the degree-k nodes (poisson.cpp:176-192)
     for (int i = tid; i < N * (k + 1); i += nth) {
         const int c = i / (k + 1), m = i - (i / (k + 1)) * (k + 1);
         double dphi = 0.0;
 #pragma unroll
-        for (int n = 0; n < PS; ++n) dphi += pd.deriv[m * PS + n] * x0[n * N + c];
+        for (int n = 0; n < PS; ++n) dphi += pd.deriv[m * PS + n] * xv(n, c);
         E[i] = -dphi / pd.h[c];
     }
 }
@@ -1531,7 +1562,7 @@ __host__ __device__ inline int pc_vec_doubles(const PClusterMap& m, const PRange
 
 template <int PS>
 __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_constant__ PoissonDev pd,
-                                                               const __grid_constant__ PClusterMap cm,
+                                                               const __grid_constant__ PClusterMap cm, int stage,
                                                                const double* __restrict__ rho,
                                                                double* __restrict__ E,
                                                                double* __restrict__ phi) {
@@ -1563,10 +1594,7 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
         double* b0 = psm + bo[0];
         for (int i = tid; i < n0 * PS; i += nth) {
             const int m = i / n0, q = i - (i / n0) * n0, cc = a0 + q;
-            double val = 0.0;
-#pragma unroll
-            for (int n = 0; n <= k; ++n) val += pd.interp[m * (k + 1) + n] * rho[cc * (k + 1) + n];
-            b0[i] = pd.ws[m] * pd.h[cc] * val;
+            b0[i] = poisson_load<PS>(pd, stage, rho, cc, m);
         }
     }
     __syncthreads();
@@ -1760,16 +1788,26 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
     {
         const int l0 = R.xa[0], n0 = R.xb[0] - l0;
         const double* x0 = psm + xo[0];
+        if (stage == 1) {  // first solve of the refinement: keep x, no E yet
+            for (int i = tid; i < n0 * PS; i += nth) {
+                const int q = i / PS, m = i - (i / PS) * PS;
+                pd.ir_x[(long long)(l0 + q) * PS + m] = x0[m * n0 + q];
+            }
+            return;
+        }
+        auto xv = [&](int n, int q) {
+            return stage == 2 ? pd.ir_x[(long long)(l0 + q) * PS + n] + x0[n * n0 + q] : x0[n * n0 + q];
+        };
         if (phi)
             for (int i = tid; i < n0 * PS; i += nth) {
                 const int q = i / PS, m = i - (i / PS) * PS;
-                phi[(long long)(l0 + q) * PS + m] = x0[m * n0 + q];
+                phi[(long long)(l0 + q) * PS + m] = xv(m, q);
             }
         for (int i = tid; i < n0 * (k + 1); i += nth) {
             const int q = i / (k + 1), m = i - (i / (k + 1)) * (k + 1), cc = l0 + q;
             double dphi = 0.0;
 #pragma unroll
-            for (int n = 0; n < PS; ++n) dphi += pd.deriv[m * PS + n] * x0[n * n0 + q];
+            for (int n = 0; n < PS; ++n) dphi += pd.deriv[m * PS + n] * xv(n, q);
             E[(long long)cc * (k + 1) + m] = -dphi / pd.h[cc];
         }
     }
@@ -1780,67 +1818,217 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
 // trajectory is bitwise the reference's (parity mode, not the fast path)
 // ---------------------------------------------------------------------------
 // charge_density (poisson.cpp:194-216): per x dof, ions then electrons,
-// rows ascending, rho += ((sign*w_vn)*dv) * f
+// rows ascending, rho += ((sign*w_vn)*dv) * f. The sum is one sequential chain
+// per x dof (nx*p of them), so the parallelism for HBM is in the loads: each
+// thread streams its column through a kRhoRing-deep cp.async ring in shared
+// memory ([slot][thread]: a warp's slot is one coalesced 256-byte row piece),
+// keeping kRhoRing loads in flight while the adds retire in order.
+constexpr int kRhoThreads = 32, kRhoRing = 96;
 template <int P>
-__global__ void rho_exact_kernel(const __grid_constant__ RhoArgs a) {
+__global__ void __launch_bounds__(kRhoThreads) rho_exact_kernel(const __grid_constant__ RhoArgs a) {
+    __shared__ double ring[kRhoRing * kRhoThreads];
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
-    double acc = 0.0;
-    for (int s = 0; s < 2; ++s) {
+    const double* fs[2];
+    double wv[2][P];
+    for (int s = 0; s < 2; ++s) {  // s = 0: ions (sign +1), s = 1: electrons (sign -1)
         const int sp = s == 0 ? 1 : 0;
         const double sign = s == 0 ? 1.0 : -1.0;
         const double dv = a.vg[sp]->dx;
-        const double* f = (field_flipped(a.flip[sp]) ? a.alt[sp] : a.f[sp]) + xd;
-        for (int r = 0; r < a.nrows; ++r) {
-            const int vn = r - (r / P) * P;
-            const double w = sign * a.basis.weights[vn] * dv;
-            acc += w * __ldg(f + (long long)r * a.ld);
+        fs[s] = (field_flipped(a.flip[sp]) ? a.alt[sp] : a.f[sp]) + xd;
+#pragma unroll
+        for (int vn = 0; vn < P; ++vn) wv[s][vn] = sign * a.basis.weights[vn] * dv;
+    }
+    const long long nr = a.nrows, total = 2 * nr;
+    double* my = ring + threadIdx.x;
+    auto issue = [&](long long r, int slot) {
+        if (r < total) {
+            const int s = r >= nr;
+            cp_async8(my + slot * kRhoThreads, fs[s] + (r - s * nr) * a.ld, true);
+        }
+        cp_commit();
+    };
+#pragma unroll 1
+    for (int c = 0; c < kRhoRing - 1; ++c) issue(c, c);
+    double acc = 0.0;
+    long long r = 0;
+    for (int s = 0; s < 2; ++s) {
+#pragma unroll 1
+        for (long long rr = 0; rr < nr; rr += P) {
+#pragma unroll
+            for (int vn = 0; vn < P; ++vn, ++r) {
+                const int slot = (int)(r % kRhoRing);
+                cp_wait<kRhoRing - 2>();
+                const double v = my[slot * kRhoThreads];
+                // refill the slot consumed one row ago (its value is in acc already)
+                issue(r + kRhoRing - 1, slot == 0 ? kRhoRing - 1 : slot - 1);
+                acc += wv[s][vn] * v;
+            }
         }
     }
+    cp_wait<0>();
     a.rho[xd] = acc;
 }
 
 // PoissonOperator::solve with dpbtrs('L') = dtbsv('L','N') + dtbsv('L','T')
-// replayed in reference-BLAS order by one thread (poisson.cpp:135-192)
+// replayed in reference-BLAS order (poisson.cpp:135-192), bitwise.
+//
+// Both triangular sweeps are one dependence chain (column j's division needs
+// every earlier column's update of x[j]; the transposed sweep's dot product is
+// a fixed sequential sum), so the arithmetic stays on one thread. What is not
+// serial is moved off it:
+//  * the band window x[j..j+kd] lives in that thread's registers (no memory
+//    round trip between dependent columns), and the rest of the block stages
+//    the next chunk of factor columns, right-hand sides and reciprocals of the
+//    diagonal into shared memory while it works on the current chunk;
+//  * each IEEE division a/c on the chain becomes q = a*r, q += (a - q*c)*r
+//    with r = RN(1/c) precomputed (Markstein's correction: RN(a/c) except in
+//    cases a few ulp^2 from a rounding boundary). The dividends are recorded;
+//    afterwards all threads re-divide them in parallel and compare bit for
+//    bit, and a pass with any mismatch is replayed with true divisions -- the
+//    result is the reference's either way.
+// The load and E = -phi' phases are parallel over dofs.
+__device__ __forceinline__ double div_markstein(double a, double c, double r) {
+    const double q = __dmul_rn(a, r);
+    const double e = __fma_rn(-q, c, a);  // exact remainder
+    return __fma_rn(e, r, q);
+}
+
+template <int PS>
 __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constant__ PoissonDev pd,
                                                             const double* __restrict__ rho,
                                                             double* __restrict__ E,
                                                             double* __restrict__ phi) {
-    const int ps = pd.ps, k = pd.k, N = pd.ncells, n = N * ps, kd = pd.kd, ldab = kd + 1;
+    constexpr int KD = 2 * PS - 1, LD = KD + 1, CH = 128;
+    __shared__ double scol[2][CH * LD];
+    __shared__ double sx[2][CH];
+    __shared__ double srcp[2][CH];
+    __shared__ int redo;
+    const int k = pd.k, N = pd.ncells, n = N * PS;
     double* x = pd.xws;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int c = i / ps, m = i - (i / ps) * ps;
+    double* rhs = pd.exws;              // load vector (replay source of the forward pass)
+    double* fwd = pd.exws + n;          // forward result (replay source of the backward pass)
+    double* dvd = pd.exws + 2 * n;      // dividends on the chain
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // build_load (poisson.cpp:135-149)
+        const int c = i / PS, m = i - (i / PS) * PS;
         double val = 0.0;
         for (int q = 0; q <= k; ++q) val += pd.interp[m * (k + 1) + q] * rho[c * (k + 1) + q];
-        x[i] = pd.ws[m] * pd.h[c] * val;
+        x[i] = rhs[i] = pd.ws[m] * pd.h[c] * val;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int j = 0; j < n; ++j) {
-            if (x[j] != 0.0) {
-                const double* col = pd.chol + (long long)j * ldab;
-                x[j] = x[j] / col[0];
-                const double temp = x[j];
-                const int imax = n - 1 < j + kd ? n - 1 : j + kd;
-                for (int i = j + 1; i <= imax; ++i) x[i] = x[i] - temp * col[i - j];
+    const int nch = (n + CH - 1) / CH;
+    // chunk ch of factor columns, 1/diagonal and x[xoff + ch*CH + i] into buffer
+    // b; warp 0 computes, the other warps stage (or, with all = true, warp 0)
+    auto stage = [&](int ch, int b, int xoff, bool all) {
+        const int j0 = ch * CH, ncol = min(CH, n - j0);
+        const double* src = pd.chol + (long long)j0 * LD;
+        const int t0 = all ? (int)threadIdx.x : (int)threadIdx.x - 32;
+        const int nt = all ? 32 : (int)blockDim.x - 32;
+        for (int i = t0; i >= 0 && i < ncol * LD; i += nt) scol[b][i] = src[i];
+        for (int i = t0; i >= 0 && i < CH; i += nt) {
+            const int g = j0 + i + xoff;
+            sx[b][i] = g >= 0 && g < n ? x[g] : 0.0;
+            srcp[b][i] = i < ncol ? 1.0 / src[(long long)i * LD] : 0.0;
+        }
+    };
+    // ---- dtbsv('L','N'): forward, column oriented ----
+    auto forward = [&](auto fast_c) {
+        constexpr bool FAST = decltype(fast_c)::value;
+        double w[LD];  // x[j .. j+KD]
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int l = 0; l < LD; ++l) w[l] = l < n ? x[l] : 0.0;
+        if (threadIdx.x < 32) stage(0, 0, LD, true);
+        __syncthreads();
+        for (int ch = 0; ch < nch; ++ch) {
+            const int b = ch & 1;
+            if (ch + 1 < nch) stage(ch + 1, b ^ 1, LD, false);
+            if (threadIdx.x == 0) {
+                const int j0 = ch * CH, j1 = min(n, j0 + CH);
+                for (int j = j0; j < j1; ++j) {
+                    const double* col = &scol[b][(j - j0) * LD];
+                    if (FAST) dvd[j] = w[0];
+                    if (w[0] != 0.0) {
+                        w[0] = FAST ? div_markstein(w[0], col[0], srcp[b][j - j0]) : w[0] / col[0];
+                        const double temp = w[0];
+#pragma unroll
+                        for (int l = 1; l < LD; ++l)
+                            if (j + l < n) w[l] = w[l] - temp * col[l];
+                    }
+                    x[j] = w[0];
+#pragma unroll
+                    for (int l = 0; l + 1 < LD; ++l) w[l] = w[l + 1];
+                    w[LD - 1] = sx[b][j - j0];  // x[j + LD], untouched by columns <= j
+                }
             }
+            __syncthreads();
         }
-        for (int j = n - 1; j >= 0; --j) {
-            const double* col = pd.chol + (long long)j * ldab;
-            double temp = x[j];
-            const int imax = n - 1 < j + kd ? n - 1 : j + kd;
-            for (int i = imax; i >= j + 1; --i) temp = temp - col[i - j] * x[i];
-            temp = temp / col[0];
-            x[j] = temp;
+    };
+    // ---- dtbsv('L','T'): backward, dot-product form, i from imax down to j+1 ----
+    auto backward = [&](auto fast_c) {
+        constexpr bool FAST = decltype(fast_c)::value;
+        double u[LD];  // u[l] = x[j + l] (final), l = 1..KD
+#pragma unroll
+        for (int l = 0; l < LD; ++l) u[l] = 0.0;
+        const int last = nch - 1;
+        if (threadIdx.x < 32) stage(last, last & 1, 0, true);
+        __syncthreads();
+        for (int ch = last; ch >= 0; --ch) {
+            const int b = ch & 1;
+            if (ch > 0) stage(ch - 1, b ^ 1, 0, false);
+            if (threadIdx.x == 0) {
+                const int j0 = ch * CH, j1 = min(n, j0 + CH);
+                for (int j = j1 - 1; j >= j0; --j) {
+                    const double* col = &scol[b][(j - j0) * LD];
+                    double temp = sx[b][j - j0];
+#pragma unroll
+                    for (int l = LD - 1; l >= 1; --l)
+                        if (j + l < n) temp = temp - col[l] * u[l];
+                    if (FAST) dvd[j] = temp;
+                    temp = FAST ? div_markstein(temp, col[0], srcp[b][j - j0]) : temp / col[0];
+#pragma unroll
+                    for (int l = LD - 1; l >= 2; --l) u[l] = u[l - 1];
+                    u[1] = temp;
+                    x[j] = temp;
+                }
+            }
+            __syncthreads();
         }
-    }
+    };
+    // every recorded dividend divided again (IEEE), bit for bit against x
+    auto verify = [&](bool skip_zero) {
+        if (threadIdx.x == 0) redo = 0;
+        __syncthreads();
+        int bad = 0;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            const double a = dvd[j];
+            if (skip_zero && a == 0.0) continue;  // forward: zero columns are not divided
+            bad |= __double_as_longlong(a / pd.chol[(long long)j * LD]) != __double_as_longlong(x[j]);
+        }
+        if (__syncthreads_or(bad) && threadIdx.x == 0) redo = 1;
+        __syncthreads();
+        return redo != 0;
+    };
     __syncthreads();
+    forward(std::true_type{});
+    if (verify(true)) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = rhs[i];
+        __syncthreads();
+        forward(std::false_type{});
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) fwd[i] = x[i];
+    __syncthreads();
+    backward(std::true_type{});
+    if (verify(false)) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = fwd[i];
+        __syncthreads();
+        backward(std::false_type{});
+    }
     if (phi)
         for (int i = threadIdx.x; i < n; i += blockDim.x) phi[i] = x[i];
-    for (int i = threadIdx.x; i < N * (k + 1); i += blockDim.x) {
+    for (int i = threadIdx.x; i < N * (k + 1); i += blockDim.x) {  // E = -phi' (poisson.cpp:182-190)
         const int c = i / (k + 1), m = i - (i / (k + 1)) * (k + 1);
         double dphi = 0.0;
-        for (int q = 0; q < ps; ++q) dphi += pd.deriv[m * ps + q] * x[c * ps + q];
+        for (int q = 0; q < PS; ++q) dphi += pd.deriv[m * PS + q] * x[c * PS + q];
         E[i] = -dphi / pd.h[c];
     }
 }
@@ -2684,8 +2872,8 @@ static int poisson_cluster_plan(const PoissonDev& pd, PClusterMap& cm, size_t& s
 }
 
 template <int PS>
-static cudaError_t launch_poisson_t(const PoissonDev& pd, const double* rho, double* E, double* phi,
-                                    cudaStream_t s) {
+static cudaError_t launch_poisson_t(const PoissonDev& pd, int stage, const double* rho, double* E,
+                                    double* phi, cudaStream_t s) {
     static int cached_n = -1, cached_c = 0;
     static PClusterMap cached_cm{};
     static size_t cached_smem = 0;
@@ -2694,7 +2882,7 @@ static cudaError_t launch_poisson_t(const PoissonDev& pd, const double* rho, dou
         cached_n = pd.ncells;
     }
     if (cached_c == 0) {
-        poisson_kernel<PS><<<1, 1024, 0, s>>>(pd, rho, E, phi);
+        poisson_kernel<PS><<<1, 1024, 0, s>>>(pd, stage, rho, E, phi);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
@@ -2709,23 +2897,23 @@ static cudaError_t launch_poisson_t(const PoissonDev& pd, const double* rho, dou
     cfg.stream = s;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, poisson_cluster_kernel<PS>, pd, cached_cm, rho, E, phi);
+    return cudaLaunchKernelEx(&cfg, poisson_cluster_kernel<PS>, pd, cached_cm, stage, rho, E, phi);
 }
 
-cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
+cudaError_t launch_poisson(const PoissonDev& pd, int stage, const double* rho, double* E, double* phi,
                            cudaStream_t s) {
-    SK_DISPATCH_P(pd.ps - 1, return (launch_poisson_t<PP + 1>(pd, rho, E, phi, s)));
+    SK_DISPATCH_P(pd.ps - 1, return (launch_poisson_t<PP + 1>(pd, stage, rho, E, phi, s)));
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s) {
-    SK_DISPATCH_P(a.basis.p, (rho_exact_kernel<PP><<<(a.nxd + 63) / 64, 64, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (rho_exact_kernel<PP><<<(a.nxd + kRhoThreads - 1) / kRhoThreads, kRhoThreads, 0, s>>>(a)));
     return cudaGetLastError();
 }
 
 cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double* E, double* phi,
                                  cudaStream_t s) {
-    poisson_exact_kernel<<<1, 256, 0, s>>>(pd, rho, E, phi);
+    SK_DISPATCH_P(pd.ps - 1, (poisson_exact_kernel<PP + 1><<<1, 256, 0, s>>>(pd, rho, E, phi)));
     return cudaGetLastError();
 }
 

@@ -143,6 +143,13 @@ struct PoissonDev {
     const double *AlphaT, *GammaT, *LoT, *UpT, *DinvT, *DinvTop;  // see PoissonPlan
     const double *interp, *deriv, *h, *ws;
     double *bws, *xws;     // per level SoA [ps][rows]
+    // one step of iterative refinement on the block-cyclic-reduction solve:
+    // stage 1 solves from rho into ir_x (phi, AoS); stage 2 solves A d = b - A x
+    // (residual from the SIPG band, computed in its load phase) and writes
+    // phi = x + d and E. band = the assembled matrix, (kd+1) x n lower.
+    const double* band;
+    double* ir_x;
+    double* exws;          // exact mode: 3n doubles (poisson_exact_kernel)
 };
 
 struct ShrinkArgs {
@@ -228,7 +235,7 @@ cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream
 int xsweep_rho_groups(const XSweepArgs& a);
 cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_rho(const RhoArgs& a, int nspecies_mask, cudaStream_t s);
-cudaError_t launch_poisson(const PoissonDev& pd, const double* rho, double* E, double* phi,
+cudaError_t launch_poisson(const PoissonDev& pd, int stage, const double* rho, double* E, double* phi,
                            cudaStream_t s);
 // exact-reduction mode: reference summation order / sequential dpbtrs
 cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s);

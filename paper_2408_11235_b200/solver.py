@@ -461,6 +461,13 @@ class Context:
         reference-order charge density, sequential dpbtrs solve"""
         _check(N.lib().sk_ctx_set_exact_reductions(self.h, int(on)))
 
+    EXACT_ARITH, EXACT_RHO, EXACT_POISSON = 1, 2, 4
+
+    def set_exact_parts(self, mask: int):
+        """exact mode per part (OR of EXACT_ARITH / EXACT_RHO / EXACT_POISSON),
+        to attribute a fast-mode deviation to one of them"""
+        _check(N.lib().sk_ctx_set_exact_parts(self.h, int(mask)))
+
     def synchronize(self):
         _check(N.lib().sk_ctx_synchronize(self.h))
 
@@ -669,8 +676,10 @@ class SimulationState:
             grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
                                       cfg.refinement_ratio)
             ctx = Context(grid, cfg.k, cfg.penalty_scale, device)
-        if exact:
+        if exact is True:
             ctx.set_exact_reductions(True)
+        elif exact:  # a mask of Context.EXACT_* parts
+            ctx.set_exact_parts(int(exact))
         self.ctx = ctx
         h = C.c_void_p()
         ccfg = cfg.to_c()

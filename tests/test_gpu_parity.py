@@ -25,6 +25,9 @@ from tests.golden.make_golden import STATE_CFGS, STATE_STEPS
 pytestmark = pytest.mark.gpu
 
 F_TOL = 1e-12
+# tolerance factor over the reference's own rounding-noise envelope, the same
+# on every mesh (_envelope, test_c3_fast_mode_within_reference_envelope)
+ENV_C = 20.0
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -188,32 +191,49 @@ FULL_CFGS = {
 
 
 def _envelope(ora, cfg, steps):
-    """Rounding-noise envelope of the reference dynamics:
-    |oracle - oracle with the charge density summed in another order| per
-    step. The GPU sums rho in yet another (parallel) order and replays the
-    Poisson solve by cyclic reduction, so its deviation is compared with this."""
-    a, b = ora.state(**cfg.oracle_kwargs()), ora.state(**cfg.oracle_kwargs())
+    """Rounding-noise envelope of the reference dynamics, per
+    step the max over three perturbations the reference itself leaves open
+    (tests/golden/make_c3_envelope.py): the charge density summed in the other
+    species order, the Poisson band solved by another LAPACK (scipy's), and
+    the restatement built with FMA contraction. The GPU's fast mode sums rho
+    in yet another (parallel) order, solves Poisson by refined cyclic
+    reduction and contracts the sweeps into DFMA, so its deviation is compared
+    with this."""
+    import oracle as O
+
+    a = ora.state(**cfg.oracle_kwargs())
+    pert = {"rho": ora.state(**cfg.oracle_kwargs())}
+    lap = O.scipy_lapack()
+    if lap is not None:
+        ora.set_lapack(lap)
+        try:
+            pert["lapack"] = ora.state(**cfg.oracle_kwargs())
+        finally:
+            ora.set_lapack(None)
+    if os.path.exists(O.oracle.ORACLE_FMA_SO):
+        pert["fma"] = O.Oracle(O.oracle.ORACLE_FMA_SO).state(**cfg.oracle_kwargs())
     env = {}
     for s in range(1, steps + 1):
         a.step()
-        ora.set_rho_order(1)
-        try:
-            b.step()
-        finally:
-            ora.set_rho_order(0)
-        env[s] = (max(rel(a.field(sp), b.field(sp)) for sp in (0, 1)),
-                  np.abs(a.E() - b.E()).max())
+        for name, b in pert.items():
+            if name == "rho":
+                ora.set_rho_order(1)
+            try:
+                b.step()
+            finally:
+                ora.set_rho_order(0)
+        env[s] = (max(rel(a.field(sp), b.field(sp)) for sp in (0, 1) for b in pert.values()),
+                  max(np.abs(a.E() - b.E()).max() for b in pert.values()))
     return env
 
 
 @pytest.mark.parametrize("name", list(FULL_CFGS))
 def test_full_steps_vs_oracle(sk, ora, name):
-    """Fast path (parallel charge density + cyclic-reduction Poisson). The
-    exact-mode test proves every other operation is bitwise, so what remains
-    is reduction-order noise amplified by rho = int f_i - int f_e cancelling:
-    f within 1e-12 at steps 1 and 10; E within 1e-12 absolute
-    at step 1 and within 5e-10 of max|E| at step 10 (rho carries ~1e-10
-    relative cancellation noise under any reordering, App. A item 6)."""
+    """Fast path (DFMA sweeps, parallel charge density, refined cyclic-
+    reduction Poisson). The exact-mode test proves every other operation is
+    bitwise, so what remains is rounding noise: f within 1e-12
+    and E within 1e-12 * max(1, max|E|) at steps 1 and 10, each unless the
+    reference's own envelope (ENV_C x _envelope) is larger."""
     cfg, o, st = _pair(sk, ora, FULL_CFGS[name])
     env = _envelope(ora, cfg, 10)
     for s in range(1, 11):
@@ -222,13 +242,12 @@ def test_full_steps_vs_oracle(sk, ora, name):
         if s in (1, 10):
             ef, eE = env[s]
             for sp in (0, 1):
-                assert rel(st.field(sp).download(), o.field(sp)) <= max(F_TOL, 20 * ef), f"f sp{sp} step {s}"
+                assert rel(st.field(sp).download(), o.field(sp)) <= max(F_TOL, ENV_C * ef), f"f sp{sp} step {s}"
                 assert st.field(sp).vmax() == o.vmax(sp)
             E_o = o.E()
             dE = np.abs(st.E() - E_o).max()
             Emax = np.abs(E_o).max()
-            bound = 1e-12 * max(1.0, Emax) if s == 1 else max(1e-12 * max(1.0, Emax), 5e-10 * Emax)
-            assert dE <= max(bound, 20 * eE), (s, dE, eE)
+            assert dE <= max(1e-12 * max(1.0, Emax), ENV_C * eE), (s, dE, eE)
     assert st.shrinks(0) == (o.shrinks(0), o.last_shrink(0))
     assert st.shrinks(1) == (o.shrinks(1), o.last_shrink(1))
     assert st.step_index() == o.step_index() == 10
@@ -240,10 +259,7 @@ def test_full_steps_vs_oracle(sk, ora, name):
         for key, scale in ((f"mass_{sp}", m), (f"l2_{sp}", r[f"l2_{sp}"]),
                            (f"mom_{sp}", m * vm), (f"ekin_{sp}", r[f"ekin_{sp}"])):
             assert abs(g[key] - r[key]) <= 1e-12 * abs(scale), key
-    eE = env[10][1]
-    Emax = np.abs(o.E()).max()
-    assert abs(g["e_energy"] - r["e_energy"]) <= max(1e-12 * r["e_energy"],
-                                                     40 * eE * Emax * 400.0)
+    assert abs(g["e_energy"] - r["e_energy"]) <= 1e-12 * r["e_energy"]
     # counters: troubled/post near-exact; clamps flip on ulp-level E changes
     gs, os_ = st.stats(), o.stats()
     assert gs["outputs"] == os_["outputs"]
@@ -789,10 +805,8 @@ def test_c3_full_size_run_matches_reference(sk, ref):
     cut-off on): 11 run() loop bodies (run.cpp:124-131) in exact mode against
     the reference's own loop (oracle/_ref, all host threads). f of both
     species, E, v_max and the shrink counts must be bitwise the reference's
-    in exact mode. Fast mode: f within 1e-12 and E within 1e-11 at step 1,
-    the same shrinks, v_max and masses (1e-12) at step 11, and a relative E
-    error that does not grow over the 11 steps. The 11 steps include two
-    cut-off shrinks per species (the last on step 11)."""
+    in exact mode. The 11 steps include two cut-off shrinks per species (the
+    last on step 11). Fast mode: test_c3_fast_mode_within_reference_envelope."""
     cfg = sk.named_config("C3")
     n = 11
     st = sk.SimulationState(cfg, exact=True)
@@ -809,30 +823,49 @@ def test_c3_full_size_run_matches_reference(sk, ref):
         assert got.shape == want.shape and np.array_equal(got, want), \
             f"sp{sp}: max rel diff {rel(got, want):.3e}"
     st.close()
-    # the bench's mode (parallel ρ reduction, DFMA sweeps) stepped beside an
-    # exact-mode state (bitwise the reference, above). E = int rho cancels two
-    # O(1) species densities, so the reordered reduction leaves a ~1e-16 * n
-    # noise in rho; at C3 it sums over 8192 x nodes and 16384 v nodes per node.
-    # Measured (B200): step 1 |dE| 2.1e-12, f rel 5e-14 (e) / 2e-15 (i);
-    # step 11 |dE|/max|E| 5.6e-8, the same ratio as step 1 (the step-1 noise
-    # carried by the growing field, not an accumulating error), f_e rel 8.8e-11.
+
+
+
+def test_c3_fast_mode_within_reference_envelope(sk):
+    """The benchmarked (fast) mode at the BASELINE C3 size, stepped beside exact
+    mode (= the reference bit for bit, test_c3_full_size_run_matches_reference),
+    for 11 run() loop bodies including two cut-off shrinks per species.
+
+    Bound: ENV_C x the reference's own noise envelope at C3
+    (tests/golden/c3_envelope.npz, made offline by make_c3_envelope.py: the
+    reference restatement against itself with the charge density summed in
+    the other species order, with another LAPACK, and built with FMA), per
+    step, for f of both species, E, and the diagnostics mass, L2, electric
+    energy, momentum and kinetic energy. Shrink steps and v_max identical."""
+    env = np.load(os.path.join(ROOT, "tests", "golden", "c3_envelope.npz"))
+    cfg = sk.named_config("C3")
+    n = int(env["steps"][-1])
     ex, fast = sk.SimulationState(cfg, exact=True), sk.SimulationState(cfg)
-    ratio = []
+    keys = ("mass_e", "mass_i", "l2_e", "l2_i", "e_energy", "mom_e", "mom_i", "ekin_e", "ekin_i")
+    worst = {}
     for s in range(1, n + 1):
         ex.run_step()
         fast.run_step()
+        i = s - 1
         Ex, Ef = ex.E(), fast.E()
-        dE = np.abs(Ef - Ex).max()
-        ratio.append(dE / np.abs(Ex).max())
-        if s == 1:
-            assert dE <= 1e-11, dE
-            for sp in (0, 1):
-                d = rel(fast.field(sp).download(), ex.field(sp).download())
-                assert d <= F_TOL, f"fast sp{sp} step 1: {d:.3e}"
-    assert ratio[-1] <= 2.0 * ratio[0] + 1e-12, ratio
+        assert np.abs(Ex).max() == env["Emax"][i]  # exact mode is the envelope's reference run
+        got = {"dE": np.abs(Ef - Ex).max()}
+        for sp, nm in ((0, "df_e"), (1, "df_i")):
+            got[nm] = rel(fast.field(sp).download(), ex.field(sp).download())
+        sx, sf = ex.summary(), fast.summary()
+        for k in keys:
+            got["d_" + k] = abs(sf[k] - sx[k])
+        for key, v in got.items():
+            e = float(env["env_" + key][i])
+            # a diagnostic the perturbations left bitwise equal gets a 4-ulp floor
+            floor = 4 * np.spacing(abs(float(env["ref_" + key[2:]][i]))) if key.startswith("d_") else 0.0
+            bound = ENV_C * e + floor
+            worst[key] = max(worst.get(key, 0.0), v / bound if bound > 0 else (0.0 if v == 0 else np.inf))
+            assert v <= bound, f"step {s} {key}: {v:.3e} > {ENV_C:g} x envelope {e:.3e} (+{floor:.1e})"
+        for sp in (0, 1):
+            assert fast.field(sp).vmax() == ex.field(sp).vmax(), f"v_max sp{sp} step {s}"
     for sp in (0, 1):
-        assert fast.shrinks(sp) == ex.shrinks(sp) and fast.field(sp).vmax() == ex.field(sp).vmax()
-        a, b = fast.field(sp).download(), ex.field(sp).download()
-        assert abs(a.sum() - b.sum()) <= 1e-12 * abs(b.sum()), f"mass sp{sp}"
+        assert fast.shrinks(sp) == ex.shrinks(sp)
+    print("worst ratio to the bound per quantity:", {k: round(v, 3) for k, v in worst.items()})
     fast.close()
     ex.close()
