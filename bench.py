@@ -1,17 +1,24 @@
 #!/usr/bin/env python
 """Benchmark: phase-space DoF updates/s of the full sLdG run() loop body.
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl b200|reference]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl b200|reference]
 
 One "step" = one run() loop body (core/src/run.cpp:124-131): x half-sweep
 (+inline sLdG limiter, + 3-block transfer), charge density, Poisson solve, v
 sweep, x half-sweep, nonfinite check, velocity cut-off check (and shrink when
 it fires) for BOTH species. value = 2*(nx*p)*(nv*p)*K / device time.
 
-N == 1: the whole state on one B200. N > 1 (torchrun): the phase space is
-sharded along v (paper_2408_11235_b200.sharding), max-over-ranks device time.
+Default workload: C5 (BASELINE.json configs[4]: 16384x16384 cells/species,
+k=3, mu=1836, sLdG limiter, cut-off on; 137 GB resident on one B200), the
+largest configuration that fits one GPU and the one the metric's 1/2/4/8 GPU
+sweep is quoted on. N == 1: the whole state on one B200. N > 1 (torchrun):
+the phase space is sharded along v (paper_2408_11235_b200.sharding),
+max-over-ranks device time.
+
 --impl reference: the reference itself (oracle/_ref, compiled from
-/root/reference) on this host's cores, same config and metric.
+/root/reference) on this host's cores, same metric, timing the same step
+window (W warm-up run() loop bodies, then K), on a bounded sample of the
+workload when the full shape would not finish in minutes (cpu_sample_cfg).
 """
 from __future__ import annotations
 
@@ -89,39 +96,72 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_reference_run(cfg, steps: int, warmup: int, budget_s: float):
-    """Time the reference (oracle/_ref) on this host: returns (DoF/s, info)."""
+# phase-space DoF of the largest CPU sample: the reference runs a C3-sized
+# problem (2.7e8 DoF) at ~5 s per run() loop body on 16 cores, and a full C5
+# state would need a ~2 min serial fill plus ~6 min per species for the
+# serial cut-off shrink every blob run fires at step 1 (adaptivity.cpp:94-130)
+CPU_SAMPLE_DOF = 2.7e8
+
+
+def cpu_sample_cfg(cfg):
+    """The workload the CPU reference times: the config itself when it is at
+    most CPU_SAMPLE_DOF, else the same x mesh, k, mu, limiter and cut-off with
+    fewer v cells over the same v extent (the per-DoF work of every phase --
+    x lines of full length, v lines, serial shrink -- is the same kind; the
+    1D Poisson solve is the full one). Returns (cfg, description)."""
+    import dataclasses
+
+    if cfg.dof_total <= CPU_SAMPLE_DOF * 1.01:
+        return cfg, "the full workload"
+    nv = cfg.v_cells
+    while nv > 64 and cfg.dof_total * (nv / cfg.v_cells) > CPU_SAMPLE_DOF * 1.01:
+        nv //= 2
+    sc = dataclasses.replace(cfg, v_cells=nv)
+    return sc, (f"a v slab: {cfg.nx}x{nv} cells/species ({cfg.v_cells // nv}x fewer v cells over the "
+                f"same v extent, {sc.dof_total:.3g} DoF), x mesh/k/mu/limiter/cut-off as the workload")
+
+
+def cpu_reference_run(cfg, steps: int, warmup: int, budget_s: float | None):
+    """Time the reference (oracle/_ref) on this host over run() loop bodies
+    W+1..W+K (budget_s None: exactly K; else until budget_s is spent, at least
+    one). Returns (DoF/s of the sample, info)."""
     import oracle
 
     if not oracle.ref_available():
         raise RuntimeError("oracle/_ref/libsolkin_ref.so not built")
     threads = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    scfg, what = cpu_sample_cfg(cfg)
     t0 = time.perf_counter()
-    st = oracle.Ref().state(threads=threads, **cfg.oracle_kwargs())
+    st = oracle.Ref().state(threads=threads, **scfg.oracle_kwargs())
     t_init = time.perf_counter() - t0
-    st.run(max(warmup, 1))
-    # time single loop bodies until the budget is spent (a shrink event, 10x a
-    # plain step on the CPU, must not size the sample)
+    w = max(warmup, 1)
+    st.run(w)
     k, t = 0, 0.0
-    while k < max(steps, 1) and (k == 0 or t < budget_s):
+    while k < max(steps, 1) and (budget_s is None or k == 0 or t < budget_s):
         t += st.run(1)
         k += 1
-    rate = cfg.dof_total * k / t
-    sample = (f"{cfg.nx}x{cfg.v_cells} k={cfg.k} {cfg.limiter}: {k} timed run() loop bodies "
-              f"after {max(warmup, 1)} warm-up (init {t_init:.1f}s), {threads} threads, "
-              f"{t:.2f}s timed")
-    return rate, dict(threads=threads, steps=k, seconds=t, sample=sample, timers=st.timers())
+    rate = scfg.dof_total * k / t
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+    except (ValueError, OSError):
+        mem = float("nan")
+    sample = (f"{what}; run() loop bodies {w + 1}..{w + k} after {w} warm-up (init {t_init:.1f}s), "
+              f"{threads} threads, {t:.2f}s timed, host RAM {mem:.0f} GiB")
+    return rate, dict(threads=threads, steps=k, seconds=t, sample=sample, timers=st.timers(),
+                      sample_cfg=scfg)
 
 
 def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rate, info = cpu_reference_run(cfg, args.steps, args.warmup, budget_s=args.cpu_budget)
+    # the same window as the GPU arm: W warm-up bodies, then exactly K
+    rate, info = cpu_reference_run(cfg, args.steps, args.warmup, budget_s=None)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": info["steps"],
         "warmup": args.warmup, "ms_per_step": 1e3 * info["seconds"] / info["steps"],
+        "ms_per_step_note": "wall time per run() loop body of the CPU sample (cpu_baseline.sample)",
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (blob initial condition, run.cpp:41-46)", "impl": "reference",
         "config": config_dict(args, cfg),
@@ -153,13 +193,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--limiter", default=None)
+    ap.add_argument("--refinement", type=int, default=None,
+                    help="sheath refinement ratio m of the three-block x mesh (default: the config's)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--exact-steps", type=int, default=4,
+                    help="steps of the exact-mode sub-measurement (0: skip)")
     ap.add_argument("--exact", action="store_true",
                     help="exact-reduction (bitwise parity) mode for rho and Poisson")
     args = ap.parse_args()
@@ -167,6 +211,8 @@ def main():
     import paper_2408_11235_b200 as sk
 
     over = {"limiter": args.limiter} if args.limiter else {}
+    if args.refinement:
+        over["refinement_ratio"] = args.refinement
     cfg = sk.named_config(args.config, **over)
 
     if args.impl == "reference":
@@ -264,6 +310,24 @@ def main():
         "limiter_stats": st.stats(),
         "clocks": clk,
     }
+
+    # ---- exact (bitwise-parity) mode on the same state: the reference's
+    # serial charge-density order and dpbtrs chain on the device ----
+    if not args.exact and args.exact_steps > 0:
+        st.ctx.set_exact_reductions(True)
+        st.run_steps(2)  # capture
+        torch.cuda.synchronize()
+        t0.record(stream)
+        st.run_steps(args.exact_steps)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        st.ctx.synchronize()
+        ems = t0.elapsed_time(t1) / args.exact_steps
+        st.ctx.set_exact_reductions(False)
+        line["exact_mode"] = {"ms_per_step": ems, "value": cfg.dof_total / (ems / 1e3), "unit": UNIT,
+                              "steps": args.exact_steps,
+                              "what": "the same run() loop body with sk_ctx_set_exact_reductions(1): "
+                                      "trajectory bitwise the reference's (tests/test_gpu_parity.py)"}
 
     # ---- e2e: the drop-in C-ABI call over pinned HOST buffers ----
     if not args.no_e2e:

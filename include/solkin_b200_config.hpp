@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <sys/stat.h>
+
 #include "solkin_b200.hpp"
 
 namespace solkin_b200 {
@@ -313,8 +315,20 @@ inline Context make_context(const RunConfig& cfg, int device = 0) {
                    cfg.k, cfg.penalty_scale, device);
 }
 
-// run(cfg) (run.cpp:60-169): nsteps, cadences and out_dir from the config
-inline sk_run_result run(const Context& ctx, const RunConfig& cfg) {
+// run(cfg) (run.cpp:60-169): nsteps, cadences and out_dir from the config,
+// resolved and validated first (run.cpp:61-63), its echo written to
+// <out_dir>/config_resolved.cfg (run.cpp:70-73)
+inline sk_run_result run(const Context& ctx, const RunConfig& cfg_in) {
+    RunConfig cfg = cfg_in;
+    cfg.resolve();
+    cfg.validate();
+    if (!cfg.out_dir.empty()) {
+        const std::string& dir = cfg.out_dir;
+        ::mkdir(dir.c_str(), 0755);  // OutputWriter's directory (diagnostics.cpp:118-126)
+        std::ofstream out(dir + "/config_resolved.cfg", std::ios::trunc);
+        if (!out.good()) throw std::runtime_error("cannot open '" + dir + "/config_resolved.cfg' for writing");
+        out << cfg.echo();
+    }
     return run(ctx, cfg.to_c(), cfg.nsteps(), cfg.cadence, cfg.snapshot_cadence, cfg.profile_cadence,
                cfg.out_dir);
 }

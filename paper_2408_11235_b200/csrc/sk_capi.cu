@@ -523,6 +523,7 @@ sk_status enq_rho(sk_field* fe, sk_field* fi, double* rho) {
     sk_ctx* c = fe->ctx;
     RhoArgs a{};
     a.basis = c->basis;
+    a.st = c->st;
     a.vg[0] = fe->vg;
     a.vg[1] = fi->vg;
     a.f[0] = fe->cur_ptr();
@@ -621,14 +622,16 @@ sk_status validate_policy(const sk_vadjust* p) {
     return SK_OK;
 }
 
-sk_status moments(sk_field* f, double* out4) {
+// other = true: the buffer that is NOT live (after a cut-off shrink it still
+// holds the field before the projection)
+sk_status moments(sk_field* f, double* out4, bool other = false) {
     sk_ctx* c = f->ctx;
     DiagArgs a{};
     a.basis = c->basis;
     a.grid = c->grid;
     a.vg = f->vg;
-    a.f = f->cur_ptr();
-    a.alt = f->other_ptr();
+    a.f = other ? f->other_ptr() : f->cur_ptr();
+    a.alt = other ? f->cur_ptr() : f->other_ptr();
     a.flip = f->dflip;
     a.nxd = c->grid.ncells * c->P;
     a.ld = a.nxd;
@@ -771,6 +774,7 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(dalloc(&c->st, 1));
     CK(cudaMemset(c->st, 0, sizeof(DevStatus)));
+    d.st = c->st;
     {
         DevStatus init{};
         init.last_shrink[0] = init.last_shrink[1] = -10;  // run.cpp:124-125
@@ -2039,6 +2043,12 @@ sk_status sk_run(sk_ctx* c, const sk_run_config* cfg, long nsteps, int cadence, 
     sk_status rc = sample();
     if (!rc) rc = outputs(0);
     int seen[2] = {0, 0};
+    long last_shrink[2] = {-10, -10};
+    const double shrink_p = cfg->policy.p;
+    // with files, per-phase CUDA events stand in for the reference's StepTimers
+    // (stepper.hpp:24-32) and the loop body is enqueued eagerly
+    if (files) sk_state_set_phase_timing(s, 1);
+    double ph_ms[PH_N] = {};
     long step = 0;
     while (!rc && step < nsteps) {
         // run the steps up to the next output event as graph replays
@@ -2049,14 +2059,23 @@ sk_status sk_run(sk_ctx* c, const sk_run_config* cfg, long nsteps, int cadence, 
         upto(cadence);
         upto(snapshot_cadence);
         upto(profile_cadence);
+        // with files, a batch also ends at each step that may shrink (cooldown
+        // over, run.cpp:100): right after it the other buffer still holds the
+        // pre-shrink field, whose mass the shrink log line reports
+        if (files && cfg->v_adjust)
+            for (int sp = 0; sp < 2; ++sp) next = std::min(next, std::max(step + 1, last_shrink[sp] + 10));
         sk_status r = sk_run_steps(s, (int)(next - step));
         if (r == SK_OK) r = collect_errors(c);
         if (r == SK_ERR_SIMULATION) {
             res->exit_code = 1;
             log += std::string("ABORT: ") + sk_last_error() + "\n";
+            // kernels halt at the first error, so the device step counter is the
+            // failing step (nonfinite: incremented, stepper.cpp:99-102) or the
+            // last completed one (ghost width: raised inside the step)
+            const bool after_step = c->st_host->err_kind == 3;
             long at = 0;
             sk_state_step_index(s, &at);
-            res->steps_done = at;
+            res->steps_done = after_step ? at - 1 : at;
             if (files) {
                 sk_state_write_snapshot(s, dir.c_str());
                 sk_state_write_profiles(s, dir.c_str());
@@ -2071,10 +2090,28 @@ sk_status sk_run(sk_ctx* c, const sk_run_config* cfg, long nsteps, int cadence, 
             long last = 0;
             sk_state_shrinks(s, sp, &cnt, &last);
             if (cnt > seen[sp] && files) {
-                log += "step " + std::to_string(last) + ": " + species_name(sp) + " v domain shrink " +
-                       g17(c->st_host->vmax_before[sp]) + " -> " + g17(field_vmax(s->f[sp])) + "\n";
+                // one event per line: the batch ended at the shrink step, the
+                // live buffer holds the projected field, the other one the
+                // field before it (on the old v grid: its mass is rescaled by
+                // dv_old/dv_new = vmax_before/vmax_after)
+                const double vb = c->st_host->vmax_before[sp];
+                const double va = vb * (1.0 - shrink_p);  // adaptivity.cpp:103
+                double mb[4], ma[4];
+                if ((rc = moments(s->f[sp], ma)) || (rc = moments(s->f[sp], mb, true))) break;
+                const double mass_before = mb[0] * (vb / va);
+                char buf[256];
+                std::snprintf(buf, sizeof buf, "step %ld: %s v domain shrink %g -> %g (mass delta %g)\n", last,
+                              species_name(sp), vb, va, ma[0] - mass_before);
+                log += buf;
             }
             seen[sp] = cnt;
+            last_shrink[sp] = cnt > 0 ? last : -10;
+        }
+        if (rc) break;
+        if (files) {
+            double ms[PH_N];
+            sk_state_phase_times(s, ms, nullptr, PH_N);
+            for (int i = 0; i < PH_N; ++i) ph_ms[i] += ms[i];
         }
         if (step % cadence == 0) {
             if ((rc = sample())) break;
@@ -2095,7 +2132,16 @@ sk_status sk_run(sk_ctx* c, const sk_run_config* cfg, long nsteps, int cadence, 
     res->shrinks_i = seen[1];
     sk_stats_get(c, &res->stats);
     if (files) {
-        log += "wall=" + g17(res->wall_seconds) + " s\n";
+        // run.cpp:159-167 (device phase times from CUDA events)
+        const double sec = 1e-3;
+        const double ax = (ph_ms[PH_XTAB] + ph_ms[PH_X1] + ph_ms[PH_X1_FIX] + ph_ms[PH_X2] + ph_ms[PH_X2_FIX]) * sec;
+        const double av = (ph_ms[PH_VTAB] + ph_ms[PH_V] + ph_ms[PH_V_FIX]) * sec;
+        const double po = (ph_ms[PH_RHO] + ph_ms[PH_POISSON]) * sec;
+        const double pl = (ph_ms[PH_POST_X1] + ph_ms[PH_POST_V] + ph_ms[PH_POST_X2]) * sec;
+        char buf[512];
+        std::snprintf(buf, sizeof buf, "phase timings [s]: source=%g advect_x=%g advect_v=%g poisson=%g "
+                      "post_limiter=%g wall=%g\n", 0.0, ax, av, po, pl, res->wall_seconds);
+        log += buf;
         write_file(dir + "/run.log", log);
     }
     sk_state_destroy(s);

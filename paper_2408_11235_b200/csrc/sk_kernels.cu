@@ -60,6 +60,14 @@ __device__ __forceinline__ void raise_error(DevStatus* st, int code, int kind, i
     }
 }
 
+// A raised error halts the run: every later kernel of the step sequence
+// returns at entry, so the state stays as the failing step left it (the
+// reference's exception unwinds out of run(): run.cpp:147-155) until the host
+// collects and clears the error.
+__device__ __forceinline__ bool halted(const DevStatus* st) {
+    return st && *reinterpret_cast<const volatile int*>(&st->err_code) != 0;
+}
+
 __device__ __forceinline__ void count_flags(unsigned long long* dst, unsigned t, unsigned c,
                                             unsigned o) {
     const unsigned full = 0xffffffffu;
@@ -179,6 +187,7 @@ __device__ __forceinline__ bool all_finite(const double* o) {
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void xtab_kernel(const __grid_constant__ XTabArgs a) {
+    if (halted(a.st)) return;
     const int line = blockIdx.x * blockDim.x + threadIdx.x;
     if (line >= a.nlines) return;
     const int sp = a.species0 + blockIdx.y;
@@ -324,6 +333,16 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 // ---------------------------------------------------------------------------
+// fp64 tensor-core MMA (SASS DMMA): D(8x8) = A(8x4, row) * B(4x8, col) + C.
+// Lane l holds A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4) + {0,1}].
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
 // TMA bulk copy / mbarrier helpers (sm_90+; SASS UBLKCP / SYNCS)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -399,6 +418,7 @@ __device__ __forceinline__ bool xghost_side(const Grid& g, int b, int side) {
 // lanes load the blocks' shifts together and share the line's ghost values.
 template <int P>
 __global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ XSweepArgs a) {
+    if (halted(a.st)) return;
     const Grid& g = a.grid;
     const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     const int nb = g.nblocks;
@@ -592,6 +612,9 @@ template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
+    // fast mode at k = 3: the projection and indicator on the fp64 tensor cores
+    constexpr bool kDmma = P == 4 && FMA && MODE == 0 && C::T % (C::NC * 8) == 0;
+    if (halted(a.st)) return;
     static_assert(MODE == 0 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
     constexpr int TT = MODE >= 1 ? C::T - 1 : C::T;  // cells per tile
     constexpr int WX = MODE >= 1 ? 2 : 1;            // window cells beyond the tile
@@ -756,12 +779,14 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     // fused moment: the grid is a multiple of the tiles per line, so this CTA
     // always sees the same tile column and each thread the same cells -- the
     // accumulators live in registers
-    [[maybe_unused]] double rreg[RHO ? C::CPT : 1][RHO ? P : 1];
+    // (DMMA path: [8-cell group][2 nodes] per lane, see below)
+    constexpr int RA = kDmma ? C::T / C::NC / 8 : C::CPT, RB = kDmma ? 1 : P;
+    [[maybe_unused]] double rreg[RHO ? RA : 1][RHO ? RB : 1];
     if constexpr (RHO)
 #pragma unroll
-        for (int cc = 0; cc < C::CPT; ++cc)
+        for (int cc = 0; cc < RA; ++cc)
 #pragma unroll
-            for (int m = 0; m < P; ++m) rreg[cc][m] = 0.0;
+            for (int m = 0; m < RB; ++m) rreg[cc][m] = 0.0;
     (void)racc;
     int rcol_nt = 0, rcol_base = 0;
     int it = 0;
@@ -818,6 +843,91 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             }
             continue;
         }
+        if constexpr (kDmma) {
+            // Fast mode, k = 3: the tile as 8-cell groups on the fp64 tensor
+            // cores. Per cell the 8 inputs (left source cell, right source
+            // cell) map to 8 outputs with one 8x8 matrix constant along the
+            // line: the projection (advection.cpp:95-101) and, for the inline
+            // indicator, the two source means and the two extension moments of
+            // the projected cell (limiters.cpp:175-188), which are linear in
+            // the inputs too. Two m8n8k4 MMAs per 8 cells replace ~80 DFMA and
+            // shared loads per cell; quad lanes 0/1 hold nodes 0-1 / 2-3 of a
+            // cell, lanes 2/3 its means / extension moments.
+            const int kq = lane & 3, nq = lane >> 2;
+            const double* Am = row + 2;
+            const double* Bm = row + 2 + P * P;
+            double b0, b1;  // W[kq][nq], W[4 + kq][nq]
+            if (nq < P) {
+                b0 = Am[nq * P + kq];
+                b1 = Bm[nq * P + kq];
+            } else if (nq == P) {
+                b0 = a.basis.weights[kq];
+                b1 = 0.0;
+            } else if (nq == P + 1) {
+                b0 = 0.0;
+                b1 = a.basis.weights[kq];
+            } else {
+                const double* e = row + 2 + 2 * P * P + (nq == P + 2 ? 0 : P);
+                b0 = 0.0;
+                b1 = 0.0;
+                if (INLINE)
+#pragma unroll
+                    for (int m = 0; m < P; ++m) {
+                        b0 = fma(e[m], Am[m * P + kq], b0);
+                        b1 = fma(e[m], Bm[m * P + kq], b1);
+                    }
+            }
+            constexpr int G = C::T / C::NC / 8;  // 8-cell groups per warp
+            const int wbase = warp * (C::T / C::NC);
+            double fa[G][2];  // A fragments: this lane's input of the left / right source cell
+#pragma unroll
+            for (int gi = 0; gi < G; ++gi) {
+                const int c = wbase + 8 * gi;
+                fa[gi][0] = fa[gi][1] = 0.0;
+                if (c < nt) {  // warp-uniform
+                    fa[gi][0] = win[(c + nq) * P + kq];
+                    fa[gi][1] = win[(c + 1 + nq) * P + kq];
+                }
+            }
+            // the window stage is consumed
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+            double wdv = 0.0;
+            if constexpr (RHO) wdv = reinterpret_cast<const double*>(hdr)[4];
+            double* dline = dstp(sp) + lbase + (long long)(g.start[b] + c0) * P;
+#pragma unroll
+            for (int gi = 0; gi < G; ++gi) {
+                if (wbase + 8 * gi >= nt) break;  // warp-uniform
+                double d0 = 0.0, d1 = 0.0;
+                dmma884(d0, d1, fa[gi][0], b0);
+                dmma884(d0, d1, fa[gi][1], b1);
+                const int cell = wbase + 8 * gi + nq;
+                const bool valid = cell < nt;
+                if constexpr (INLINE) {
+                    // lane kq = 2 takes the extension moments from its neighbour
+                    const double ex = __shfl_down_sync(0xffffffffu, d0, 1);
+                    const double ey = __shfl_down_sync(0xffffffffu, d1, 1);
+                    const bool tr[1] = {kq == 2 && valid &&
+                                        over_threshold(fabs(ex - d0) + fabs(ey - d1), dmax2(fabs(d0), fabs(d1)), cut)};
+                    const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
+                                                         ((unsigned long long)line << 32) |
+                                                         (unsigned)(g.start[b] + c0 + cell)};
+                    wq_push<1>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry);
+                }
+                if constexpr (RHO) {
+                    // node kq of the cell to lane kq: one accumulator per lane
+                    const int src = (lane & ~3) | (kq >> 1);
+                    const double x0 = __shfl_sync(0xffffffffu, d0, src), x1 = __shfl_sync(0xffffffffu, d1, src);
+                    if (valid) rreg[gi][0] = fma(wdv, (kq & 1) ? x1 : x0, rreg[gi][0]);
+                }
+                if (kq < 2 && valid) {
+                    if (a.check_finite) bad |= !(isfinite(d0) && isfinite(d1));
+                    *reinterpret_cast<double2*>(dline + (long long)cell * P + 2 * kq) = make_double2(d0, d1);
+                }
+            }
+            continue;
+        }
+        if constexpr (!kDmma) {
         auto cells = [&](auto ncc_c) {
             constexpr int NCC = decltype(ncc_c)::value;
             double ul[NCC][P], ur[NCC][P], o[NCC][P];
@@ -926,18 +1036,28 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
         }
+        }
     }
     if (RHO && rcol_nt > 0) {
         // this CTA always saw the same tile column (grid is a multiple of the
         // tiles per line): one partial row per (column, CTA group)
         const int ntl = a.tile_start[g.nblocks];
         double* prow = a.rho_partial + (long long)(vb / ntl) * g.ncells * P;
+        if constexpr (kDmma) {
+            const int kq = lane & 3, nq = lane >> 2, wbase = warp * (C::T / C::NC);
 #pragma unroll
-        for (int cc = 0; cc < C::CPT; ++cc) {
-            const int c = tid + cc * C::NT;
-            if (c < rcol_nt) {
+            for (int gi = 0; gi < RA; ++gi) {
+                const int c = wbase + 8 * gi + nq;
+                if (c < rcol_nt) prow[(long long)(rcol_base + c) * P + kq] = rreg[gi][0];
+            }
+        } else {
 #pragma unroll
-                for (int n = 0; n < P; ++n) prow[(long long)(rcol_base + c) * P + n] = rreg[cc][n];
+            for (int cc = 0; cc < C::CPT; ++cc) {
+                const int c = tid + cc * C::NT;
+                if (c < rcol_nt) {
+#pragma unroll
+                    for (int n = 0; n < P; ++n) prow[(long long)(rcol_base + c) * P + n] = rreg[cc][n];
+                }
             }
         }
     }
@@ -951,6 +1071,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void vtab_kernel(const __grid_constant__ VTabArgs a) {
+    if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
     const int sp = a.species0 + blockIdx.y;
@@ -1015,6 +1136,7 @@ __device__ __forceinline__ void vissue(const double* gp, long long ld, bool vali
 
 template <int P, bool INLINE, bool PERIODIC, bool FMA>
 __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant__ VSweepArgs a) {
+    if (halted(a.st)) return;
     constexpr int R = vring<P>();
     static_assert(kVChunk % R == 0, "chunk must be a multiple of the ring depth");
     __shared__ double ring[R * P * kVThreads];
@@ -1223,6 +1345,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
 
 template <int P, bool FMA>
 __global__ void __launch_bounds__(128, 8) xfix_kernel(const __grid_constant__ XSweepArgs a) {
+    if (halted(a.st)) return;
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1283,6 +1406,7 @@ __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, in
 
 template <int P, bool FMA>
 __global__ void __launch_bounds__(128, 8) vfix_kernel(const __grid_constant__ VSweepArgs a) {
+    if (halted(a.st)) return;
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1312,6 +1436,7 @@ __global__ void __launch_bounds__(128, 8) vfix_kernel(const __grid_constant__ VS
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void rho_partial_kernel(const __grid_constant__ RhoArgs a) {
+    if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
     const int sp = blockIdx.z;
@@ -1328,6 +1453,7 @@ __global__ void rho_partial_kernel(const __grid_constant__ RhoArgs a) {
 }
 
 __global__ void rho_reduce_kernel(const __grid_constant__ RhoArgs a) {
+    if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
     double acc = 0.0;
@@ -1384,6 +1510,7 @@ __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ P
                                                        const double* __restrict__ rho,
                                                        double* __restrict__ E,
                                                        double* __restrict__ phi) {
+    if (halted(pd.st)) return;
     constexpr int pp = PS * PS;
     const int k = PS - 2, N = pd.ncells;
     const int tid = threadIdx.x, nth = blockDim.x;
@@ -1566,6 +1693,7 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
                                                                const double* __restrict__ rho,
                                                                double* __restrict__ E,
                                                                double* __restrict__ phi) {
+    if (halted(pd.st)) return;
     constexpr int pp = PS * PS;
     extern __shared__ double psm[];
     cg::cluster_group cl = cg::this_cluster();
@@ -1826,6 +1954,7 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
 constexpr int kRhoThreads = 32, kRhoRing = 96;
 template <int P>
 __global__ void __launch_bounds__(kRhoThreads) rho_exact_kernel(const __grid_constant__ RhoArgs a) {
+    if (halted(a.st)) return;
     __shared__ double ring[kRhoRing * kRhoThreads];
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
@@ -1899,6 +2028,7 @@ __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constan
                                                             const double* __restrict__ rho,
                                                             double* __restrict__ E,
                                                             double* __restrict__ phi) {
+    if (halted(pd.st)) return;
     constexpr int KD = 2 * PS - 1, LD = KD + 1, CH = 128;
     __shared__ double scol[2][CH * LD];
     __shared__ double sx[2][CH];
@@ -2038,6 +2168,7 @@ __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constan
 // shrink cooldown gate (run.cpp:98-101)
 // ---------------------------------------------------------------------------
 __global__ void step_end_kernel(DevStatus* st, double dt, int v_adjust, long long cooldown, int mask) {
+    if (halted(st)) return;  // no step after a failed one (the step counter stays at it)
     st->time += dt;  // stepper.cpp:98
     st->step += 1;
     if (st->nonfinite) raise_error(st, 2, 3, 0, 0, st->step);
@@ -2051,6 +2182,7 @@ __global__ void step_end_kernel(DevStatus* st, double dt, int v_adjust, long lon
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void shrink_check_kernel(const __grid_constant__ ShrinkArgs a) {
+    if (halted(a.st)) return;
     const int sp = blockIdx.y;
     if (!((a.species_mask >> sp) & 1)) return;
     if (a.st->shrink_flag[sp] == 0) return;
@@ -2081,6 +2213,7 @@ __global__ void shrink_check_kernel(const __grid_constant__ ShrinkArgs a) {
 // build_v_transfer (adaptivity.cpp:52-90): one thread per new cell
 template <int P>
 __global__ void shrink_table_kernel(const __grid_constant__ ShrinkArgs a) {
+    if (halted(a.st)) return;
     const int sp = blockIdx.y;
     if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;  // global new cell
@@ -2159,6 +2292,7 @@ __device__ __forceinline__ void cp_wait_dyn(int n) {
 // cells past it. A cell outside the ring window is read from global directly.
 template <int P>
 __global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
+    if (halted(a.st)) return;
     // the block's threads share the chunk: its transfer matrices are staged
     // once per item (coalesced) instead of each warp re-reading them per cell;
     // a 4-deep ring then keeps the CTA at 32 KB (7 CTAs, 28 warps per SM)
@@ -2266,6 +2400,7 @@ __global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_
 // commit the new v grid (field.cpp:96-101); the projection already sits in
 // the field's other buffer, so the buffers exchange roles instead of copying
 __global__ void shrink_finalize_kernel(const __grid_constant__ ShrinkArgs a) {
+    if (halted(a.st)) return;
     const int sp = threadIdx.x;
     if (sp >= 2 || !((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
     DevVGrid ov = *a.vg[sp];
@@ -2406,6 +2541,7 @@ __device__ __forceinline__ double* post_other(const PostArgs& a, int sp) {
 // v flag pass: one thread per x dof walks kVChunk v cells (in place)
 template <int P, bool FAST, int IND>
 __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant__ PostArgs a) {
+    if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
     const int j0 = blockIdx.y * kVChunk, j1 = min(j0 + kVChunk, a.nv);
@@ -2438,6 +2574,7 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
 
 // overflow only: the field (with its readable v halo rows) into the other buffer
 __global__ void post_copy_kernel(const __grid_constant__ PostArgs a, int P) {
+    if (halted(a.st)) return;
     if (*a.fix_count <= a.fix_cap) return;
     const long long r0 = -(long long)a.gl * P, r1 = (long long)(a.nv + a.gr) * P;
     const long long n = (r1 - r0) * a.ld;
@@ -2454,6 +2591,7 @@ __global__ void post_copy_kernel(const __grid_constant__ PostArgs a, int P) {
 // re-flagged cell from the copy straight into the field)
 template <int P, int DIR, bool FAST>
 __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ PostArgs a) {
+    if (halted(a.st)) return;
     const unsigned cnt = *a.fix_count;
     const bool rescan = cnt > a.fix_cap;
     const Grid& g = a.grid;
@@ -2522,6 +2660,7 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
 // the queued modifications into the field (list mode only)
 template <int P, int DIR>
 __global__ void __launch_bounds__(128) post_scatter_kernel(const __grid_constant__ PostArgs a) {
+    if (halted(a.st)) return;
     const unsigned cnt = *a.fix_count;
     if (cnt > a.fix_cap) return;
     const Grid& g = a.grid;
@@ -2686,7 +2825,8 @@ int xsweep_rho_groups(const XSweepArgs& a) {
 constexpr int kRhoRedParts = 8;
 __global__ void __launch_bounds__(32 * kRhoRedParts)
     rho_fused_reduce_kernel(const double* partial, const unsigned long long* corr, int groups, int nxd,
-                            double* rho) {
+                            double* rho, const DevStatus* st) {
+    if (halted(st)) return;
     __shared__ double sp[kRhoRedParts][32];
     __shared__ unsigned long long sh[kRhoRedParts][32], sl[kRhoRedParts][32];
     const int l = threadIdx.x & 31, q = threadIdx.x >> 5;
@@ -2722,7 +2862,7 @@ cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream
     const int nxd = a.grid.ncells * a.basis.p;
     const int groups = xsweep_rho_groups(a);
     rho_fused_reduce_kernel<<<(nxd + 31) / 32, 32 * kRhoRedParts, 0, s>>>(a.rho_partial, a.rho_corr, groups,
-                                                                        nxd, rho);
+                                                                        nxd, rho, a.st);
     return cudaGetLastError();
 }
 
@@ -2929,6 +3069,7 @@ cudaError_t launch_step_end(DevStatus* st, double dt, int v_adjust, long long co
 // indexed by the species' v-grid level (its shrink count), so the increment
 // is bitwise the reference's.
 __global__ void source_kernel(const __grid_constant__ SourceArgs a) {
+    if (halted(a.st)) return;
     const int sp = blockIdx.y;
     const double t = a.second ? a.st->time + a.half : a.st->time;
     if (!(t <= a.t0)) return;  // SourceTerm::active (stepper.hpp:19-21)

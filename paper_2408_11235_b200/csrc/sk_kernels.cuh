@@ -121,6 +121,7 @@ struct VSweepArgs {
 
 struct RhoArgs {
     Basis basis;
+    const DevStatus* st;
     const DevVGrid* vg[2];
     const double* f[2];
     const double* alt[2];  // the fields' other buffers (used when flipped)
@@ -150,6 +151,7 @@ struct PoissonDev {
     const double* band;
     double* ir_x;
     double* exws;          // exact mode: 3n doubles (poisson_exact_kernel)
+    const DevStatus* st;   // halts on a raised error
 };
 
 struct ShrinkArgs {

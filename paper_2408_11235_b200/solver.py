@@ -22,6 +22,7 @@ libsk_b200.so. There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -825,6 +826,11 @@ def run(cfg: RunConfig, nsteps: int | None = None, cadence: int | None = None,
     loop bodies with flux.csv rows every `cadence` steps, snapshots / profiles
     at their cadences, run.log -- into out_dir (None: no files). Cadences and
     out_dir default to the config's output.* keys."""
+    import dataclasses
+
+    cfg = dataclasses.replace(cfg)  # run.cpp:61-63: resolve + validate a copy
+    cfg.resolve()
+    cfg.validate()
     if nsteps is None:
         nsteps = cfg.nsteps()
     cadence = cfg.cadence if cadence is None else cadence
@@ -832,6 +838,10 @@ def run(cfg: RunConfig, nsteps: int | None = None, cadence: int | None = None,
     profile_cadence = cfg.profile_cadence if profile_cadence is None else profile_cadence
     if out_dir is _FROM_CFG:
         out_dir = cfg.out_dir
+    if out_dir is not None:  # run.cpp:70-73
+        os.makedirs(out_dir, exist_ok=True)
+        with open(os.path.join(out_dir, "config_resolved.cfg"), "w") as f:
+            f.write(cfg.echo())
     grid = Grid1D.three_block(-cfg.L, cfg.L, cfg.fine_block_cells, cfg.coarse_block_cells,
                               cfg.refinement_ratio)
     ctx = Context(grid, cfg.k, cfg.penalty_scale, device)

@@ -398,6 +398,35 @@ def test_errors_map_to_reference_exceptions(sk):
     assert ei.value.step == 1
 
 
+def test_nonfinite_mid_batch_halts_at_the_failing_step(sk):
+    """A nonfinite state raised inside a graph-replayed batch halts every later
+    kernel: the step counter stays at the failing step and the fields are the
+    ones that step left -- the reference's run() unwinds at the throw
+    (stepper.cpp:99-102, run.cpp:147-155) -- identical to stepping one loop
+    body at a time; after the error is collected the context is usable."""
+    cfg = cfg_of(sk, k=2, nf=8, nc=16, m=1, nv=32, limiter="sldg", mu=400.0)
+    a, b = sk.SimulationState(cfg), sk.SimulationState(cfg)
+    a.ctx.set_eager_errors(False)
+    a.run_steps(3)
+    b.run_steps(3)
+    f = a.f_e.download()
+    f[len(f) // 2 + 7] = np.nan
+    a.f_e.upload(f)
+    b.f_e.upload(f)
+    with pytest.raises(sk.SimulationError, match="nonfinite") as ea:
+        a.run_steps(6)  # graph pairs: the failure is in the first body of the first pair
+        a.ctx.synchronize()
+    with pytest.raises(sk.SimulationError, match="nonfinite") as eb:
+        b.run_step()
+    assert ea.value.step == eb.value.step == 4
+    assert a.step_index() == b.step_index() == 4
+    for sp in (0, 1):
+        fa, fb = a.field(sp).download(), b.field(sp).download()
+        assert np.array_equal(fa, fb, equal_nan=True), f"sp{sp}"
+        assert a.field(sp).vmax() == b.field(sp).vmax()
+    assert np.array_equal(a.E(), b.E(), equal_nan=True)
+
+
 def test_periodic_sweep_conserves_mass(sk):
     """test_advection.cpp:194-225 (CFL up to 50, mass conserved to 1e-13)"""
     grid = sk.Grid1D.uniform(-1.0, 1.0, 64)
@@ -720,6 +749,21 @@ def test_diagnostics_and_outputs_match_reference(sk, ref, tmp_path):
     for step in (0, 10, 20):
         assert (ra / f"snapshot_{step}.bin").read_bytes() == (rb / f"snapshot_{step}.bin").read_bytes()
         assert (ra / f"profiles_{step}.csv").read_text() == (rb / f"profiles_{step}.csv").read_text()
+    # run.log (run.cpp:103-112,135-143,159-167): the same lines; the shrink
+    # mass deltas are rounding-level differences of two sums (1e-13), compared
+    # to 1e-11; the phase-timing line has the reference's keys
+    la, lb = (ra / "run.log").read_text().splitlines(), (rb / "run.log").read_text().splitlines()
+    assert len(la) == len(lb)
+    for x, y in zip(la, lb):
+        if y.startswith("phase timings [s]:"):
+            assert [t.split("=")[0] for t in x.split()] == [t.split("=")[0] for t in y.split()]
+        elif "(mass delta " in y:
+            px, dx = x.split("(mass delta ")
+            py, dy = y.split("(mass delta ")
+            assert px == py
+            assert abs(float(dx.rstrip(")")) - float(dy.rstrip(")"))) <= 1e-11
+        else:
+            assert x == y
 
 
 @pytest.mark.parametrize("mode", ["minmod+simple", "minmod+line", "meanerr+simple", "meanerr+line"])
@@ -777,6 +821,13 @@ def test_run_from_config_file(sk, ref, tmp_path):
         assert (cpp_dir / name).read_bytes() == (py_dir / name).read_bytes(), name
     ref.state(**cfg.oracle_kwargs()).run_files(cfg.t_final, cfg.cadence, cfg.snapshot_cadence,
                                                cfg.profile_cadence, ref_dir)
+    # config_resolved.cfg (run.cpp:70-73): both mirrors write the reference's echo
+    ea = (cpp_dir / "config_resolved.cfg").read_text().splitlines()
+    eb = (py_dir / "config_resolved.cfg").read_text().splitlines()
+    assert [x for x in ea if not x.startswith("output.dir")] == [x for x in eb if not x.startswith("output.dir")]
+    if (ref_dir / "config_resolved.cfg").exists():
+        er = (ref_dir / "config_resolved.cfg").read_text().splitlines()
+        assert [x.split(" = ")[0] for x in er] == [x.split(" = ")[0] for x in eb]
     gb = np.loadtxt(ref_dir / "flux.csv", delimiter=",", skiprows=1)
     ga = np.loadtxt(py_dir / "flux.csv", delimiter=",", skiprows=1)
     assert ga.shape == gb.shape == (5, 12)
