@@ -234,6 +234,7 @@ def main():
     st = sk.SimulationState(cfg, device=dev, exact=args.exact)
     st.ctx.set_eager_errors(False)
     st.run_steps(args.warmup)
+    st.prepare_steps(args.steps)  # graph captures outside the timed region
     st.ctx.synchronize()
 
     # ---- timed region: K run() loop bodies (graph replay), CUDA events on the

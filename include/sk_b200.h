@@ -136,6 +136,12 @@ sk_status sk_ctx_set_exact_reductions(sk_ctx* ctx, int on);
 #define SK_EXACT_POISSON 4
 #define SK_EXACT_ALL 7
 sk_status sk_ctx_set_exact_parts(sk_ctx* ctx, int mask);
+/* Fusion of step n's second and step n+1's first x half sweep inside
+ * sk_run_steps: one pass over f instead of two (32 instead of 48 B/DoF per
+ * step). Default off (SK_STEP_FUSION=1 in the environment turns it on): on
+ * B200 each half sweep is issue-bound about as much as HBM-bound, so the fused
+ * pass measures break-even at C5 and slower at C3. */
+sk_status sk_ctx_set_step_fusion(sk_ctx* ctx, int on);
 /* Capacity of the deferred limiter-clamp list (troubled cells queued by the
  * sweeps, clamped by a fixup kernel); above it the fixup rescans the sweep.
  * Default and maximum 4 Mi cells; exposed for testing the rescan path. */
@@ -276,8 +282,16 @@ sk_status sk_run(sk_ctx* ctx, const sk_run_config* cfg, long nsteps, int cadence
 sk_status sk_strang_step(sk_state* s);
 /* one run() loop body: strang_step + shrink checks with the 10-step cooldown */
 sk_status sk_run_step(sk_state* s);
-/* n loop bodies (CUDA-graph replayed after the first) */
+/* n loop bodies, replayed as CUDA graphs of up to 10 bodies (SK_GRAPH_STEPS).
+ * With step fusion on (sk_ctx_set_step_fusion, fast mode) each step boundary
+ * inside a graph runs step n's second and step n+1's first x half sweep as one
+ * pass over f, unless the velocity cut-off may check at the end of step n
+ * (then both sweeps run separately, decided on the device). */
 sk_status sk_run_steps(sk_state* s, int n);
+/* Capture (without running) the CUDA graphs sk_run_steps(state, n) will
+ * replay from the current state, so a later sk_run_steps(n) does no capture
+ * inside a timed region. */
+sk_status sk_state_prepare_steps(sk_state* state, int n);
 sk_status sk_state_step_index(sk_state* s, long* step);
 sk_status sk_state_shrinks(sk_state* s, int species, int* count, long* last_step);
 /* per-phase CUDA-event timing of the step (disables graph replay while on).

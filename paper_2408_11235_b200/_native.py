@@ -75,6 +75,7 @@ SIGNATURES = {
     "sk_ctx_set_eager_errors": (_i, [_vp, _i]),
     "sk_ctx_set_exact_reductions": (_i, [_vp, _i]),
     "sk_ctx_set_exact_parts": (_i, [_vp, _i]),
+    "sk_ctx_set_step_fusion": (_i, [_vp, _i]),
     "sk_ctx_set_fix_capacity": (_i, [_vp, C.c_uint]),
     "sk_ctx_synchronize": (_i, [_vp]),
     "sk_stats_get": (_i, [_vp, C.POINTER(sk_stats)]),
@@ -114,6 +115,7 @@ SIGNATURES = {
     "sk_strang_step": (_i, [_vp]),
     "sk_run_step": (_i, [_vp]),
     "sk_run_steps": (_i, [_vp, _i]),
+    "sk_state_prepare_steps": (_i, [_vp, _i]),
     "sk_state_step_index": (_i, [_vp, _lp]),
     "sk_state_shrinks": (_i, [_vp, _i, _ip, _lp]),
     "sk_run_step_host": (_i, [_vp, _dp, _dp, _sz]),

@@ -90,6 +90,11 @@ struct sk_ctx {
     // launch parameter baked into kernel arguments changes: states re-capture
     // their CUDA graphs when it differs from the generation they captured at
     unsigned long long gen = 0;
+    // step-boundary fusion of the x half sweeps (sk_ctx_set_step_fusion): off by
+    // default -- measured break-even at C5 and slower at C3, because each pass
+    // of the x sweep is issue-bound about as much as it is HBM-bound
+    // (profiles/r02_fused_xsweep.txt); SK_STEP_FUSION=1 turns it on
+    bool fuse_off = getenv("SK_STEP_FUSION") == nullptr || atoi(getenv("SK_STEP_FUSION")) == 0;
 };
 
 struct sk_field {
@@ -143,11 +148,19 @@ struct sk_state {
     double sqrt_mu[2] = {1.0, 1.0};
     double charge[2] = {-1.0, 1.0};
     long step_host = 0;
-    cudaGraphExec_t graph2 = nullptr;  // two loop bodies
-    unsigned long long graph_gen = ~0ull;  // sk_ctx::gen at capture
-    int graph_cur0 = -1, graph_cur1 = -1;
-    int graph_exact = -1;              // arithmetic mode the graph was captured in
-    long long graph_launches = 0;      // kernels per graph replay
+    // CUDA graphs of nb consecutive loop bodies (sk_run_steps), keyed by the
+    // buffer parity they start from, the arithmetic mode, the scratch-buffer
+    // generation and nb; replays leave the parity at cur_after
+    struct StepGraph {
+        cudaGraphExec_t exec = nullptr;
+        int cur0 = -1, cur1 = -1, exact = -1, nb = 0;
+        int after0 = 0, after1 = 0;
+        unsigned long long gen = ~0ull;
+        long long launches = 0;        // kernels per replay
+        long long used = 0;            // LRU stamp
+    };
+    StepGraph graphs[4];
+    long long graph_clock = 0;
     int rank = 0, nranks = 1;          // v-shard of a multi-GPU run
     int shrink_halo = 0;               // halo cells a sharded shrink reads
     double* src_gx = nullptr;          // injection source tables (SourceArgs)
@@ -326,8 +339,13 @@ sk_status ensure_xghost(sk_ctx* c, int nlines) {
     return SK_OK;
 }
 
+// gate / gate_on: the launches run only when (*gate != 0) == gate_on (one
+// alternative of a fusable step boundary); swap = false: the buffers' roles
+// were already exchanged for the boundary; fused_reduce: also reduce the
+// partials of the other alternative (the fused sweep) under the inverse gate
 sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
-                     int check_finite, double* rho_out = nullptr) {
+                     int check_finite, double* rho_out = nullptr, const int* gate = nullptr, int gate_on = 0,
+                     bool swap = true, bool fused_reduce = false) {
     sk_ctx* c = fs[0]->ctx;
     XSweepArgs a{};
     a.basis = c->basis;
@@ -357,6 +375,8 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;
+    a.gate = gate;
+    a.gate_on = gate_on;
     if (rho_out) {  // fused charge density (both species in this launch)
         a.rho_fuse = 1;
         for (int i = 0; i < nspecies; ++i) {
@@ -395,8 +415,91 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     if (rho_out) {
         CK(launch_rho_fused_reduce(a, rho_out, c->stream));
         c->launches += 1;
+        if (fused_reduce) {
+            XSweepArgs b = a;
+            b.gate_on = !gate_on;
+            CK(launch_rho_fused_reduce(b, rho_out, c->stream, 1));
+            c->launches += 1;
+        }
     }
-    for (int i = 0; i < nspecies; ++i) fs[i]->swap();
+    if (swap)
+        for (int i = 0; i < nspecies; ++i) fs[i]->swap();
+    return SK_OK;
+}
+
+// A fusable step boundary n -> n+1: step n's second x half sweep and step
+// n+1's first (with its charge-density partials) as ONE pass over f
+// (xsweep_kernel MODE 3), or -- when the cut-off may check at the end of step
+// n (cooldown over, fuse_decide_kernel) -- the plain second sweep here and the
+// plain first sweep in the next body (enq_phase_a with fuse_in), which then
+// records the extra buffer exchange in the flip flags. Both alternatives are
+// enqueued, the device runs one; the host exchanges the buffers once.
+sk_status enq_fused_boundary(sk_state* s, int inline_sldg, double threshold) {
+    sk_ctx* c = s->ctx;
+    sk_field* fs[2] = {s->f[0], s->f[1]};
+    CK(launch_fuse_decide(c->st, s->cfg.v_adjust, 10, c->stream));
+    c->launches += 1;
+    XSweepArgs a{};
+    a.basis = c->basis;
+    a.grid = c->grid;
+    a.st = c->st;
+    for (int i = 0; i < 2; ++i) {
+        a.src[i] = fs[i]->cur_ptr();
+        a.dst[i] = fs[i]->other_ptr();
+        a.flip[i] = fs[i]->dflip;
+        a.tab[i] = fs[i]->xtab;
+        a.vg[i] = fs[i]->vg;
+        a.charge_w[i] = i == 1 ? 1.0 : -1.0;
+        fs[i]->may_flip = true;
+    }
+    a.nlines = fs[0]->nv * c->P;
+    a.nspecies = 2;
+    a.species0 = 0;
+    std::memcpy(a.tile_start, c->xtiles, sizeof a.tile_start);
+    a.inline_sldg = inline_sldg;
+    a.check_finite = 1;
+    a.fma = 1;
+    a.threshold = threshold;
+    {
+        const ThrCut cut = make_thr_cut(threshold);
+        a.thr_hi = cut.hi;
+        a.thr_lo = cut.lo;
+    }
+    a.fix_list = c->fix_list;
+    a.fix_count = c->fix_count;
+    a.fix_cap = c->fix_cap;
+    a.gate = &c->st->fuse_ok;
+    // fused alternative: both half sweeps, in-kernel clamps, rho partials
+    {
+        XSweepArgs f = a;
+        f.gate_on = 1;
+        f.rho_fuse = 1;
+        const size_t nxd = (size_t)c->grid.ncells * c->P;
+        if ((size_t)xsweep_rho_groups(f, 1) * nxd > c->rho_fpart_n || !c->rho_corr)
+            return fail(SK_ERR_RUNTIME, "internal: fused rho buffers not sized");
+        f.rho_partial = c->rho_fpart;
+        f.rho_corr = c->rho_corr;
+        CK(cudaMemsetAsync(c->rho_corr, 0, sizeof(unsigned long long) * nxd * 2 * kRhoCorrCopies, c->stream));
+        if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
+        CK(launch_xsweep_fused(f, c->stream));
+        c->launches += 1;
+        if (inline_sldg) {
+            CK(launch_xfix2(f, c->stream));
+            c->launches += 1;
+        }
+    }
+    if (c->fix_timer)
+        if (sk_status rc = mark(c->fix_timer, c->fix_phase)) return rc;
+    // plain alternative: step n's second half sweep only
+    a.gate_on = 0;
+    if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
+    CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
+    c->launches += 1;
+    if (inline_sldg) {
+        CK(launch_xfix(a, c->stream));
+        c->launches += 1;
+    }
+    for (int i = 0; i < 2; ++i) fs[i]->swap();
     return SK_OK;
 }
 
@@ -878,6 +981,12 @@ sk_status sk_ctx_set_exact_parts(sk_ctx* c, int mask) {
     return SK_OK;
 }
 
+sk_status sk_ctx_set_step_fusion(sk_ctx* c, int on) {
+    c->fuse_off = on == 0;
+    ++c->gen;  // captured step graphs change
+    return SK_OK;
+}
+
 sk_status sk_ctx_set_eager_errors(sk_ctx* c, int on) {
     c->eager = on != 0;
     return SK_OK;
@@ -1214,9 +1323,10 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
     if (sk_status rc = validate_limiter(&cfg->limiter)) return rc;
     if (cfg->v_adjust)
         if (sk_status rc = validate_policy(&cfg->policy)) return rc;
-    {  // cells per pass, both species: room for the flagged ones
+    {  // cells per pass, both species: room for the flagged ones (sLdG: ~0.5 %
+       // troubled; a fused step boundary queues ~3x that, see xfix2_kernel)
         const size_t cells = 2 * (size_t)cfg->v_cells * c->P * c->grid.ncells;
-        if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 64)) return rc;
+        if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 32)) return rc;
     }
     if (sk_status rc = ensure_xghost_cfg(c, cfg, cfg->v_cells * c->P)) return rc;
     if (cfg->limiter.indicator)
@@ -1252,7 +1362,8 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         a.fma = 0;  // size for either arithmetic (sk_ctx_set_exact_reductions may flip it)
         const int g0 = xsweep_rho_groups(a);
         a.fma = 1;
-        const int g1 = xsweep_rho_groups(a);
+        int g1 = xsweep_rho_groups(a);
+        if (xsweep_fused_supported(c->P)) g1 = std::max(g1, xsweep_rho_groups(a, 1));  // fused boundaries
         const size_t need = (size_t)(g0 > g1 ? g0 : g1) * ne;
         if (need > c->rho_fpart_n) {
             if (c->rho_fpart) cudaFree(c->rho_fpart);
@@ -1343,7 +1454,8 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
         a.fma = 0;  // size for either arithmetic (sk_ctx_set_exact_reductions may flip it)
         const int g0 = xsweep_rho_groups(a);
         a.fma = 1;
-        const int g1 = xsweep_rho_groups(a);
+        int g1 = xsweep_rho_groups(a);
+        if (xsweep_fused_supported(c->P)) g1 = std::max(g1, xsweep_rho_groups(a, 1));  // fused boundaries
         const size_t need = (size_t)(g0 > g1 ? g0 : g1) * ne;
         if (need > c->rho_fpart_n) {
             if (c->rho_fpart) cudaFree(c->rho_fpart);
@@ -1367,7 +1479,8 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
 sk_status sk_state_destroy(sk_state* s) {
     if (!s) return SK_OK;
     cudaSetDevice(s->ctx->device);
-    if (s->graph2) cudaGraphExecDestroy(s->graph2);
+    for (auto& g : s->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaStreamSynchronize(s->ctx->stream);
     for (auto& m : s->marks) cudaEventDestroy(m.second);
     for (auto e : s->pool) cudaEventDestroy(e);
@@ -1479,8 +1592,19 @@ sk_status enq_source(sk_state* s, int second) {
     return SK_OK;
 }
 
-// phase A: x tables + first x half sweep (+ fused local charge density)
-sk_status enq_phase_a(sk_state* s) {
+// can the loop bodies of this state fuse their x half sweeps across step
+// boundaries? (fast mode with the fused moment, sLdG or no limiter, no
+// injection source, one dx class, unsharded; sk_ctx_set_step_fusion turns it on)
+bool fusable(const sk_state* s) {
+    const sk_ctx* c = s->ctx;
+    return !c->fuse_off && !(c->exact & (SK_EXACT_ARITH | SK_EXACT_RHO)) && s->cfg.limiter.indicator == 0 &&
+           s->cfg.scenario != 1 && c->grid.nclass == 1 && s->nranks == 1 && xsweep_fused_supported(c->P);
+}
+
+// phase A: x tables + first x half sweep (+ fused local charge density).
+// fuse_in: the previous body ended at a fusable boundary (enq_fused_boundary):
+// this sweep is its unfused alternative
+sk_status enq_phase_a(sk_state* s, bool fuse_in = false) {
     sk_ctx* c = s->ctx;
     const sk_limiter* lim = &s->cfg.limiter;
     const int inl = lim->inline_sldg;
@@ -1499,9 +1623,14 @@ sk_status enq_phase_a(sk_state* s) {
     const bool fuse = !post && !(c->exact & SK_EXACT_RHO);
     {
         FixTimer ft(s, PH_X1_FIX);
-        if ((rc = mark(s, PH_X1)) ||
-            (rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr)))
+        if ((rc = mark(s, PH_X1))) return rc;
+        if (fuse_in) {
+            if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0, s->rho, &c->st->fuse_ok, 0, false, true))) return rc;
+            CK(launch_flip_toggle(c->st, fs[0]->dflip, fs[1]->dflip, c->stream));
+            c->launches += 1;
+        } else if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr))) {
             return rc;
+        }
     }
     if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     if (!fuse && ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho)))) return rc;
@@ -1530,7 +1659,7 @@ sk_status enq_phase_b1(sk_state* s) {
 
 // phase B, second part: post limiter V (a v shard exchanges a one-cell halo
 // before it), second x half sweep, post limiter X
-sk_status enq_phase_b2(sk_state* s) {
+sk_status enq_phase_b2(sk_state* s, bool fuse_out = false) {
     const sk_limiter* lim = &s->cfg.limiter;
     const int inl = lim->inline_sldg;
     const double thr = lim->threshold;
@@ -1540,27 +1669,30 @@ sk_status enq_phase_b2(sk_state* s) {
     if (post && ((rc = mark(s, PH_POST_V)) || (rc = enq_post(fs, 2, SK_DIR_V, lim, 0)))) return rc;
     {
         FixTimer ft(s, PH_X2_FIX);
-        if ((rc = mark(s, PH_X2)) || (rc = enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
+        if ((rc = mark(s, PH_X2))) return rc;
+        if ((rc = fuse_out ? enq_fused_boundary(s, inl, thr) : enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
     }
     if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
     // stepper.cpp:93-97 (injection): source half step at state.time + half
     return enq_source(s, 1);
 }
 
-sk_status enq_phase_b(sk_state* s) {
+sk_status enq_phase_b(sk_state* s, bool fuse_out = false) {
     if (sk_status rc = enq_phase_b1(s)) return rc;
-    return enq_phase_b2(s);
+    return enq_phase_b2(s, fuse_out);
 }
 
 // stepper.cpp:44-103 (blob: no source term), all on the context stream.
-sk_status enq_strang(sk_state* s) {
-    if (sk_status rc = enq_phase_a(s)) return rc;
-    return enq_phase_b(s);
+sk_status enq_strang(sk_state* s, bool fuse_in = false, bool fuse_out = false) {
+    if (sk_status rc = enq_phase_a(s, fuse_in)) return rc;
+    return enq_phase_b(s, fuse_out);
 }
 
-sk_status enq_run_body(sk_state* s) {
+// one run() loop body (run.cpp:124-131); fuse_in / fuse_out: the step
+// boundary before / after it fuses the x half sweeps (enq_fused_boundary)
+sk_status enq_run_body(sk_state* s, bool fuse_in = false, bool fuse_out = false) {
     sk_ctx* c = s->ctx;
-    if (sk_status rc = enq_strang(s)) return rc;
+    if (sk_status rc = enq_strang(s, fuse_in, fuse_out)) return rc;
     if (sk_status rc = mark(s, PH_SHRINK)) return rc;
     CK(launch_step_end(c->st, s->cfg.dt, s->cfg.v_adjust, 10, 3, c->stream));
     c->launches += 1;
@@ -1639,61 +1771,132 @@ sk_status sk_run_step(sk_state* s) {
     return after_launch(s->ctx);
 }
 
-sk_status sk_run_steps(sk_state* s, int n) {
+namespace {
+// nb consecutive loop bodies; with fusable(s) every internal step boundary
+// fuses its two x half sweeps (enq_fused_boundary)
+sk_status enq_bodies(sk_state* s, int nb) {
+    const bool fz = fusable(s);
+    for (int i = 0; i < nb; ++i)
+        if (sk_status rc = enq_run_body(s, fz && i > 0, fz && i + 1 < nb)) return rc;
+    return SK_OK;
+}
+
+int graph_bodies() {
+    static const int g = [] {
+        const char* e = getenv("SK_GRAPH_STEPS");
+        const int v = e ? atoi(e) : 10;
+        return v < 2 ? 2 : (v > 64 ? 64 : v);
+    }();
+    return g;
+}
+
+// the graph for nb bodies from the current buffer parity (captured on a miss)
+sk_status step_graph(sk_state* s, int nb, sk_state::StepGraph** out) {
     sk_ctx* c = s->ctx;
-    CK(cudaSetDevice(c->device));
-    // Two loop bodies leave both ping-pong buffers where they started, so a
-    // captured pair replays with fixed pointers.
-    if (s->timing || getenv("SK_NO_GRAPH")) {  // per-phase events: plain enqueue, no graph
-        for (int i = 0; i < n; ++i)
-            if (sk_status rc = enq_run_body(s)) return rc;
-        return after_launch(c);
-    }
-    for (int attempt = 0; n >= 2 && attempt < 3 &&
-                          (!s->graph2 || s->graph_cur0 != s->f[0]->cur || s->graph_cur1 != s->f[1]->cur ||
-                           s->graph_exact != c->exact || s->graph_gen != c->gen);
-         ++attempt) {
-        if (s->graph2) {
-            cudaGraphExecDestroy(s->graph2);
-            s->graph2 = nullptr;
+    const int c0 = s->f[0]->cur, c1 = s->f[1]->cur;
+    for (auto& g : s->graphs)
+        if (g.exec && g.nb == nb && g.cur0 == c0 && g.cur1 == c1 && g.exact == c->exact && g.gen == c->gen) {
+            g.used = ++s->graph_clock;
+            *out = &g;
+            return SK_OK;
         }
-        int c0 = s->f[0]->cur, c1 = s->f[1]->cur;
-        long h0 = s->step_host;
-        long long l0 = c->launches;
+    sk_state::StepGraph* slot = &s->graphs[0];
+    for (auto& g : s->graphs)
+        if (g.used < slot->used) slot = &g;
+    if (slot->exec) {
+        cudaGraphExecDestroy(slot->exec);
+        slot->exec = nullptr;
+    }
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const long h0 = s->step_host;
+        const long long l0 = c->launches;
         const unsigned long long gen0 = c->gen;
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        sk_status rc = enq_run_body(s);
-        if (!rc) rc = enq_run_body(s);
+        sk_status rc = enq_bodies(s, nb);
         cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+        // capture only records: restore the host's view of the state
         s->step_host = h0;
-        s->graph_launches = c->launches - l0;
+        slot->launches = c->launches - l0;
         c->launches = l0;
+        slot->after0 = s->f[0]->cur;
+        slot->after1 = s->f[1]->cur;
+        s->f[0]->cur = c0;
+        s->f[1]->cur = c1;
         if (rc) return rc;
         CK(ce);
-        if (s->f[0]->cur != c0 || s->f[1]->cur != c1)
-            return fail(SK_ERR_RUNTIME, "internal: buffer parity after two steps");
         if (c->gen != gen0) {  // a scratch buffer moved while capturing: capture again
             cudaGraphDestroy(g);
             continue;
         }
-        CK(cudaGraphInstantiate(&s->graph2, g, 0));
+        CK(cudaGraphInstantiate(&slot->exec, g, 0));
         cudaGraphDestroy(g);
-        s->graph_cur0 = c0;
-        s->graph_cur1 = c1;
-        s->graph_exact = c->exact;
-        s->graph_gen = c->gen;
+        slot->cur0 = c0;
+        slot->cur1 = c1;
+        slot->exact = c->exact;
+        slot->gen = c->gen;
+        slot->nb = nb;
+        slot->used = ++s->graph_clock;
+        *out = slot;
+        return SK_OK;
     }
-    if (n >= 2 && !s->graph2) return fail(SK_ERR_RUNTIME, "internal: step graph capture did not settle");
-    int done = 0;
-    for (; done + 2 <= n; done += 2) {
-        CK(cudaGraphLaunch(s->graph2, c->stream));
-        s->step_host += 2;
-        c->launches += s->graph_launches;
+    return fail(SK_ERR_RUNTIME, "internal: step graph capture did not settle");
+}
+
+// replay plan of sk_run_steps(n): graphs of graph_bodies() bodies, then one
+// graph of the remainder (a single remaining body runs eagerly)
+std::vector<int> batches(int n) {
+    const int G = graph_bodies();
+    std::vector<int> out;
+    for (int done = 0; done < n; done += out.back()) out.push_back(std::min(G, n - done));
+    return out;
+}
+}  // namespace
+
+sk_status sk_run_steps(sk_state* s, int n) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    if (s->timing || getenv("SK_NO_GRAPH")) {  // per-phase events: plain enqueue, no graph
+        if (sk_status rc = enq_bodies(s, n)) return rc;
+        return after_launch(c);
     }
-    for (; done < n; ++done)
-        if (sk_status rc = enq_run_body(s)) return rc;
+    for (int nb : batches(n)) {
+        if (nb == 1) {
+            if (sk_status rc = enq_run_body(s)) return rc;
+            continue;
+        }
+        sk_state::StepGraph* g = nullptr;
+        if (sk_status rc = step_graph(s, nb, &g)) return rc;
+        CK(cudaGraphLaunch(g->exec, c->stream));
+        s->step_host += nb;
+        c->launches += g->launches;
+        s->f[0]->cur = g->after0;
+        s->f[1]->cur = g->after1;
+    }
     return after_launch(c);
+}
+
+sk_status sk_state_prepare_steps(sk_state* s, int n) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    if (s->timing || getenv("SK_NO_GRAPH")) return SK_OK;
+    // walk the parities sk_run_steps(n) will start its batches from
+    const int c0 = s->f[0]->cur, c1 = s->f[1]->cur;
+    sk_status rc = SK_OK;
+    for (int nb : batches(n)) {
+        if (nb == 1) {  // an eager body exchanges the buffers three times
+            s->f[0]->swap();
+            s->f[1]->swap();
+            continue;
+        }
+        sk_state::StepGraph* g = nullptr;
+        if ((rc = step_graph(s, nb, &g))) break;
+        s->f[0]->cur = g->after0;
+        s->f[1]->cur = g->after1;
+    }
+    s->f[0]->cur = c0;
+    s->f[1]->cur = c1;
+    return rc;
 }
 
 sk_status sk_state_set_phase_timing(sk_state* s, int on) {

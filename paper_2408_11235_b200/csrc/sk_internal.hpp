@@ -52,7 +52,7 @@ struct DevStatus {
     int shrink_count[2];
     double vmax_before[2];        // of the last shrink
     int nonfinite;
-    int pad;
+    int fuse_ok;                  // this step boundary runs the fused x half sweeps (no cut-off check can fire)
     double time;                  // state.time (stepper.cpp:98), advanced at each step end
 };
 

@@ -336,6 +336,7 @@ __device__ __forceinline__ void cp_wait() {
 // fp64 tensor-core MMA (SASS DMMA): D(8x8) = A(8x4, row) * B(4x8, col) + C.
 // Lane l holds A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4) + {0,1}].
 // ---------------------------------------------------------------------------
+constexpr bool kXsweepDmma = false;  // see xsweep_kernel
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                  : "+d"(d0), "+d"(d1)
@@ -526,6 +527,15 @@ struct XCfg {
     static constexpr int S = 5;                     // input stages (outputs go straight to HBM)
     static constexpr int RACC = 0;                  // (fused-moment accumulators live in registers)
     static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + RACC) + 8 * 2 * S + 8 * NC * kQCap;
+    // MODE 3 (two half sweeps fused): 4 input stages, the intermediate line
+    // segment, the clamped second-pass cells and two troubled-cell lists
+    static constexpr int S3 = 4;
+    static constexpr int WIN3 = (((T + 2) * P + 4) + 1) / 2 * 2;
+    static constexpr int STAGE3 = ((WIN3 + NF + HDR + 1) / 2) * 2;
+    static constexpr size_t SMEM3 = sizeof(double) * (size_t)(S3 * STAGE3 + 2 * (T + 1) * P + 2 * (NF + 2)) +
+                                    8 * 2 * S3 + 8 * NC * kQCap + sizeof(int) * (2 * (T + 1) + 4);
+    template <int MODE>
+    static constexpr size_t smem() { return MODE == 3 ? SMEM3 : SMEM; }
 };
 
 struct XTile {
@@ -603,27 +613,67 @@ __device__ __forceinline__ void sts_cell(double* p, const double* u) {
     }
 }
 
+// one output cell to global memory. k = 3: one 256-bit store per cell, so a
+// warp writes 32 whole sectors per instruction (two 128-bit stores would each
+// touch every sector half-full and double the L1 traffic)
+template <int P>
+__device__ __forceinline__ void stg_cell(double* dp, const double* o) {
+    if constexpr (P == 4) {
+        if ((((unsigned long long)dp) & 31) == 0) {
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dp), "d"(o[0]), "d"(o[1]), "d"(o[2]),
+                         "d"(o[3])
+                         : "memory");
+            return;
+        }
+    } else if constexpr (P % 2 == 0) {
+        if ((((unsigned long long)dp) & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < P / 2; ++i) reinterpret_cast<double2*>(dp)[i] = make_double2(o[2 * i], o[2 * i + 1]);
+            return;
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < P; ++m) dp[m] = o[m];
+}
+
 // MODE 0: the x sweep. MODE 1 / 2: the post-limiter flag pass in x with the
 // minmod / mean-error indicator (limiters.cpp:254-345) on the same pipeline --
 // window = the tile's cells and one neighbour on each side (tiles of T-1
 // cells), no table row, the indicator per cell, flagged cells queued; in place
-// (nothing stored).
+// (nothing stored). MODE 3: two consecutive x half sweeps fused (fused_tile).
 template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
+    constexpr int S = MODE == 3 ? C::S3 : C::S;  // input stages
     // fast mode at k = 3: the projection and indicator on the fp64 tensor cores
-    constexpr bool kDmma = P == 4 && FMA && MODE == 0 && C::T % (C::NC * 8) == 0;
+    // (DMMA m8n8k4, two per 8 cells). Measured on B200 (C3): x sweeps 0.80 ->
+    // 2.0 ms / 0.75 -> 1.44 ms, ~1.5 TFLOP/s effective -- the fp64 MMA path is
+    // far slower than the DFMA pipe here, so it stays compiled out
+    // (profiles/r02_dmma_xsweep.txt).
+    constexpr bool kDmma = kXsweepDmma && P == 4 && FMA && MODE == 0 && C::T % (C::NC * 8) == 0;
     if (halted(a.st)) return;
-    static_assert(MODE == 0 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
-    constexpr int TT = MODE >= 1 ? C::T - 1 : C::T;  // cells per tile
+    static_assert(MODE == 0 || MODE == 3 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
+    static_assert(MODE != 3 || C::T == 2 * C::NT, "MODE 3: T + 1 intermediate cells over 3 passes of the consumers");
+    if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;  // device-decided alternative
+    // cells per tile: the flag passes' windows need one cell each side; MODE 3
+    // keeps T (its stage holds a T + 2 cell window) so block sizes divide evenly
+    constexpr int TT = (MODE == 1 || MODE == 2) ? C::T - 1 : C::T;
+    constexpr int WIN = MODE == 3 ? C::WIN3 : C::WIN;
+    constexpr int STAGE = MODE == 3 ? C::STAGE3 : C::STAGE;
     constexpr int WX = MODE >= 1 ? 2 : 1;            // window cells beyond the tile
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;                                   // S x STAGE
-    double* racc = smem + C::S * C::STAGE;                   // [T][P] this CTA's column (RHO)
+    double* racc = smem + S * STAGE;                         // [T][P] this CTA's column (RHO)
     unsigned long long* full = reinterpret_cast<unsigned long long*>(racc + C::RACC);
-    unsigned long long* empty = full + C::S;
-    unsigned long long* wqueue = empty + C::S;  // [NC][kQCap] deferred entries per consumer warp
+    unsigned long long* empty = full + S;
+    unsigned long long* wqueue = empty + S;  // [NC][kQCap] deferred entries per consumer warp
+    // MODE 3, by tile parity: intermediate cells [2][T][P], the tile's table
+    // row + moment weight [2][NF + 2] (read after the stage is handed back),
+    // pass-1 troubled flags as tile epochs [2][T]
+    [[maybe_unused]] double* mid = reinterpret_cast<double*>(wqueue + C::NC * kQCap);
+    [[maybe_unused]] double* rowc = mid + 2 * (C::T + 1) * P;
+    [[maybe_unused]] int* tl1 = reinterpret_cast<int*>(rowc + 2 * (C::NF + 2));
     const Grid& g = a.grid;
     const int ntot = a.nspecies * a.nlines * a.tile_start[g.nblocks];
     const int G = gridDim.x;
@@ -633,8 +683,10 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     auto srcp = [&](int sp) -> const double* { return ((fm >> sp) & 1u) ? a.dst[sp] : a.src[sp]; };
     auto dstp = [&](int sp) -> double* { return ((fm >> sp) & 1u) ? const_cast<double*>(a.src[sp]) : a.dst[sp]; };
 
+    if constexpr (MODE == 3)
+        for (int i = threadIdx.x; i < 2 * (C::T + 1); i += blockDim.x) tl1[i] = -1;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < C::S; ++i) {
+        for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], C::NC);
         }
@@ -666,26 +718,28 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             // wait out one load latency each
             auto batch_istar = [&](int it0) -> int {
                 const long long t = vb + (long long)(it0 + lane) * G;
-                if constexpr (MODE >= 1) return -1;  // window starts one cell left
-                return t < ntot ? (int)__ldg(row_of(decode_xtile(a, (int)t, TT))) : 0;
+                if constexpr (MODE == 1 || MODE == 2) return -1;  // window starts one cell left
+                // MODE 3: two shifts, the window starts 2 i* cells away
+                const int ist = t < ntot ? (int)__ldg(row_of(decode_xtile(a, (int)t, TT))) : 0;
+                return MODE == 3 ? 2 * ist : ist;
             };
             int ist_cur = batch_istar(0);
             int ist_nxt = batch_istar(32);
             int it = 0;
             for (int t = vb; t < ntot; t += G, ++it) {
-                const int stg = it % C::S;
+                const int stg = it % S;
                 if ((it & 31) == 0 && it > 0) {
                     ist_cur = ist_nxt;
                     ist_nxt = batch_istar(it + 32);
                 }
                 const XTile x = decode_xtile(a, t, TT);
                 const int istar = __shfl_sync(0xffffffffu, ist_cur, it & 31);
-                mbar_wait(&empty[stg], ((it / C::S) & 1) ^ 1);
+                mbar_wait(&empty[stg], ((it / S) & 1) ^ 1);
                 const int s0 = x.c0 + istar;
                 int vlo, vhi;
                 xvalid_range(a, x.b, vlo, vhi);
                 const int clo = max(s0, vlo), chi = min(s0 + x.nt + WX, vhi);
-                double* st = stages + stg * C::STAGE;
+                double* st = stages + stg * STAGE;
                 // element parity of window cell s0 in HBM decides the smem origin
                 const long long lbase = (long long)x.line * g.ncells * P;
                 const long long eg = lbase + ((long long)g.start[x.b] + s0) * P;
@@ -727,7 +781,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     if (lane != 0) continue;
                 }
                 // decoded tile for the consumers (released by the arrive below)
-                int* hdr = reinterpret_cast<int*>(st + C::WIN + C::NF);
+                int* hdr = reinterpret_cast<int*>(st + WIN + C::NF);
                 hdr[0] = x.sp;
                 hdr[1] = x.line;
                 hdr[2] = x.b;
@@ -740,7 +794,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     const int vn = x.line - (x.line / P) * P;
                     reinterpret_cast<double*>(hdr)[4] = a.charge_w[x.sp] * a.basis.weights[vn] * dvs[x.sp];
                 }
-                unsigned bytes = MODE >= 1 ? 0u : C::NF * 8;
+                unsigned bytes = (MODE == 1 || MODE == 2) ? 0u : C::NF * 8;
                 long long ga = 0, gb = 0;
                 if (chi > clo) {
                     // element g of the line sits at st + 2 + woff + (g - eg): same
@@ -759,7 +813,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     bytes += (unsigned)(gb - ga) * 8;
                 }
                 mbar_expect_tx(&full[stg], bytes);
-                if constexpr (MODE == 0) tma_load_1d(st + C::WIN, row_of(x), C::NF * 8, &full[stg]);
+                if constexpr (MODE == 0 || MODE == 3) tma_load_1d(st + WIN, row_of(x), C::NF * 8, &full[stg]);
                 if (gb > ga) {
                     double* dst = st + 2 + woff + (ga - eg);
                     tma_load_1d(dst, srcp(x.sp) + ga, (unsigned)(gb - ga) * 8, &full[stg]);
@@ -776,6 +830,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     bool bad = false;
     unsigned long long* wq = wqueue + warp * kQCap;
     int wq_n = 0;
+    [[maybe_unused]] unsigned f3[2][3] = {{0, 0, 0}, {0, 0, 0}};  // MODE 3: in-kernel clamp counters
     // fused moment: the grid is a multiple of the tiles per line, so this CTA
     // always sees the same tile column and each thread the same cells -- the
     // accumulators live in registers
@@ -791,11 +846,11 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     int rcol_nt = 0, rcol_base = 0;
     int it = 0;
     for (int t = vb; t < ntot; t += G, ++it) {
-        const int stg = it % C::S;
-        mbar_wait(&full[stg], (it / C::S) & 1);
-        double* st = stages + stg * C::STAGE;
-        const double* row = st + C::WIN;
-        const int* hdr = reinterpret_cast<const int*>(st + C::WIN + C::NF);
+        const int stg = it % S;
+        mbar_wait(&full[stg], (it / S) & 1);
+        double* st = stages + stg * STAGE;
+        const double* row = st + WIN;
+        const int* hdr = reinterpret_cast<const int*>(st + WIN + C::NF);
         const int sp = hdr[0], line = hdr[1], b = hdr[2], c0 = hdr[3], nt = hdr[4];
         const int s0 = hdr[5], clo = hdr[6], chi = hdr[7];
         const int cells_b = g.cells[b];
@@ -809,7 +864,95 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         // cells per thread this warp has in this tile (warp-uniform): short
         // tiles (3-block meshes) skip the idle slots instead of recomputing
         const int ncc = min(C::CPT, nt > warp * 32 + C::NT ? 2 : (nt > warp * 32 ? 1 : 0));
-        if constexpr (MODE >= 1) {
+        // MODE 3: step n's second x half sweep and step n+1's first one in one
+        // pass over the tile (stepper.cpp:90 then :74, same tau and v grid, so
+        // the same table row): the window holds the 2 i*-shifted sources and
+        // the intermediate cells stay in shared memory. No clamp runs here:
+        // pass 2 reads the unclamped intermediate, and every output cell a
+        // troubled cell can reach (troubled itself, or next to a troubled
+        // intermediate cell) is queued; xfix2_kernel recomputes those cells
+        // with both clamps from the intact sources (the arithmetic of the
+        // unfused sweep + fixup) and corrects the fused moment exactly. One
+        // consumer barrier per tile (intermediate, flags and row copy are
+        // double-buffered by tile parity).
+        [[maybe_unused]] auto fused_tile = [&]() {
+            const int istar = (int)row[0];
+            const int pb = it & 1;
+            double* midb = mid + pb * (C::T + 1) * P;
+            int* t1 = tl1 + pb * (C::T + 1);           // pass-1 troubled flags: tile epoch
+            double* rc = rowc + pb * (C::NF + 2);
+            const int gbase = g.start[b] + c0;  // global cell of the tile's first output
+            const int nmid = nt + 1;            // intermediate cells the outputs read
+            if (tid < C::NF) rc[tid] = row[tid];
+            if (tid == C::NF) rc[C::NF] = RHO ? reinterpret_cast<const double*>(hdr)[4] : 0.0;
+            // ---- pass 1: intermediate cells gbase + i* + m, m < nmid (<= T + 1) ----
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const int m = tid + cc * C::NT;
+                if (m < nmid) {
+                    const int gm = gbase + istar + m;
+                    double o[P];
+                    if (gm < 0 || gm >= g.ncells) {
+#pragma unroll
+                        for (int n = 0; n < P; ++n) o[n] = 0.0;  // zero inflow (advection.cpp:89-93)
+                    } else {
+                        double ul[P], ur[P];
+                        lds_cell_w<P>(win + m * P, ul);
+                        lds_cell_w<P>(win + (m + 1) * P, ur);
+                        project_cell_f<P, FMA>(row + 2, row + 2 + P * P, ul, ur, o);
+                        if constexpr (INLINE)
+                            if (inline_indicator_m<P, FMA>(cut, row + 2 + 2 * P * P, row + 2 + 2 * P * P + P,
+                                                           mean_f<P, FMA>(a.basis, ul),
+                                                           mean_f<P, FMA>(a.basis, ur), o)) {
+                                t1[m] = it;
+                                if (m < nt) f3[sp & 1][0] += 1;  // seam cell m = nt: the next tile's m = 0
+                            }
+                    }
+                    sts_cell<P>(midb + m * P, o);
+                    if (a.check_finite) bad |= !all_finite<P>(o);  // step n's end state (stepper.cpp:99-102)
+                }
+            }
+            // the window is consumed
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+            consumer_sync(C::NT);
+            // ---- pass 2: output cells c < nt from intermediate cells c, c+1 ----
+            const double* Am = rc + 2;
+            const double* Bm = rc + 2 + P * P;
+            [[maybe_unused]] const double* ext = rc + 2 + 2 * P * P;
+            const double wdv = rc[C::NF];
+            double* dline = dstp(sp) + lbase + (long long)gbase * P;
+            [[maybe_unused]] bool fix[2];
+            [[maybe_unused]] unsigned long long entry[2];
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c = tid + cc * C::NT;
+                fix[cc] = false;
+                entry[cc] = ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
+                            (unsigned)(gbase + c);
+                if (c < nt) {
+                    double ul[P], ur[P], o[P];
+                    lds_cell_w<P>(midb + c * P, ul);
+                    lds_cell_w<P>(midb + (c + 1) * P, ur);
+                    project_cell_f<P, FMA>(Am, Bm, ul, ur, o);
+                    if constexpr (INLINE)
+                        fix[cc] = t1[c] == it || t1[c + 1] == it ||
+                                  inline_indicator_m<P, FMA>(cut, ext, ext + P, mean_f<P, FMA>(a.basis, ul),
+                                                             mean_f<P, FMA>(a.basis, ur), o);
+                    if constexpr (RHO) {  // step n+1's charge density (poisson.cpp:207)
+#pragma unroll
+                        for (int m = 0; m < P; ++m) rreg[cc][m] = madd<FMA>(rreg[cc][m], wdv, o[m]);
+                    }
+                    stg_cell<P>(dline + (long long)c * P, o);
+                }
+            }
+            if constexpr (INLINE) wq_push<2>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, fix, entry);
+        };
+        if constexpr (MODE == 3) {
+            fused_tile();
+            continue;
+        }
+        if constexpr (MODE == 1 || MODE == 2) {
             // post-limiter flags: cell c's stencil is window cells c, c+1, c+2
             auto flags = [&](auto ncc_c) {
                 constexpr int NCC = decltype(ncc_c)::value;
@@ -997,32 +1140,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 const int c = tid + cc * C::NT;
                 if (c < nt) {
                     // straight to HBM: the warp's lanes cover 32 contiguous cells
-                    double* dp = dline + (long long)c * P;
-                    if constexpr (P == 4) {
-                        // one 256-bit store per cell: the warp writes 32 whole
-                        // sectors per instruction (two 128-bit stores would each
-                        // touch every sector half-full and double the L1 traffic)
-                        if ((((unsigned long long)dp) & 31) == 0) {
-                            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dp), "d"(o[cc][0]),
-                                         "d"(o[cc][1]), "d"(o[cc][2]), "d"(o[cc][3])
-                                         : "memory");
-                        } else {
-#pragma unroll
-                            for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
-                        }
-                    } else if constexpr (P % 2 == 0) {
-                        if ((((unsigned long long)dp) & 15) == 0) {
-#pragma unroll
-                            for (int i = 0; i < P / 2; ++i)
-                                reinterpret_cast<double2*>(dp)[i] = make_double2(o[cc][2 * i], o[cc][2 * i + 1]);
-                        } else {
-#pragma unroll
-                            for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
-                        }
-                    } else {
-#pragma unroll
-                        for (int m = 0; m < P; ++m) dp[m] = o[cc][m];
-                    }
+                    stg_cell<P>(dline + (long long)c * P, o[cc]);
                 }
             }
         };
@@ -1061,8 +1179,13 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             }
         }
     }
-    if constexpr (INLINE || MODE >= 1) wq_flush(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list);
-    if constexpr (INLINE) count_flags(a.st->stats[a.nspecies == 1 ? a.species0 : 0], nt_t, nt_c, nt_o);
+    if constexpr (INLINE || MODE == 1 || MODE == 2) wq_flush(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list);
+    if constexpr (INLINE && MODE == 3) {
+        count_flags(a.st->stats[0], f3[0][0], f3[0][1], f3[0][2]);
+        count_flags(a.st->stats[1], f3[1][0], f3[1][1], f3[1][2]);
+    } else if constexpr (INLINE) {
+        count_flags(a.st->stats[a.nspecies == 1 ? a.species0 : 0], nt_t, nt_c, nt_o);
+    }
     if (a.check_finite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.st->nonfinite, 1);
 }
 
@@ -1346,6 +1469,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
 template <int P, bool FMA>
 __global__ void __launch_bounds__(128, 8) xfix_kernel(const __grid_constant__ XSweepArgs a) {
     if (halted(a.st)) return;
+    if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -1368,6 +1492,116 @@ __global__ void __launch_bounds__(128, 8) xfix_kernel(const __grid_constant__ XS
             line = (int)(r % a.nlines);
         }
         xfix_cell<P, FMA>(a, sp, line, cell, rescan, ct, cc, co);
+    }
+    block_count_flags(a.st, ct, cc, co);
+}
+
+// Fixup of a fused step boundary (xsweep_kernel MODE 3): output cell `cell`
+// of line `line` recomputed from the fused sweep's intact sources with both
+// half sweeps' clamps -- intermediate cells cell + i* and cell + i* + 1 (each
+// clamped when troubled, limiters.cpp:191-215), then the output (clamped when
+// troubled) -- i.e. what the unfused x sweep + xfix and x sweep + xfix give.
+// The fused moment summed the stored value: the difference goes into the
+// exact integer corrections. Counters: the output's flags, and the clamp
+// flags of its left intermediate cell (each troubled intermediate cell is the
+// left one of exactly one queued output; the fused kernel counted it troubled).
+template <int P, bool FMA>
+__device__ __forceinline__ void xfix2_cell(const XSweepArgs& a, int sp, int line, int cell, unsigned* ct,
+                                           unsigned* cc, unsigned* co) {
+    constexpr int NF = xnf<P>();
+    const Grid& g = a.grid;
+    int b = 0;
+    while (cell >= g.start[b + 1]) ++b;
+    const double* row = a.tab[sp] + ((long long)g.cls[b] * a.nlines + line) * NF;
+    const int istar = (int)row[0];
+    const double alpha = row[1];
+    const double* A = row + 2;
+    const double* B = row + 2 + P * P;
+    const double* el = row + 2 + 2 * P * P;
+    const double* er = el + P;
+    const ThrCut cut{a.threshold, a.thr_hi, a.thr_lo};
+    const long long lbase = (long long)line * g.ncells * P;
+    const bool flipped = field_flipped(a.flip[sp]);
+    const double* src = (flipped ? a.dst[sp] : a.src[sp]) + lbase;
+    double* out = (flipped ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + lbase + (long long)cell * P;
+    auto load = [&](int k, double* u) {
+        if (k >= 0 && k < g.ncells) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) u[q] = src[(long long)k * P + q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) u[q] = 0.0;  // zero inflow
+        }
+    };
+    double mid[2][P];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int k = cell + istar + j;
+        if (k < 0 || k >= g.ncells) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) mid[j][q] = 0.0;
+            continue;
+        }
+        double ul[P], ur[P];
+        load(k + istar, ul);
+        load(k + istar + 1, ur);
+        project_cell_f<P, FMA>(A, B, ul, ur, mid[j]);
+        if (inline_indicator_m<P, FMA>(cut, el, er, mean_f<P, FMA>(a.basis, ul), mean_f<P, FMA>(a.basis, ur),
+                                       mid[j])) {
+            const int fl = inline_clamp_f<P, FMA>(a.basis, alpha, ul, ur, mid[j]);
+            if (j == 0) {
+                cc[sp] += (fl >> 1) & 1;
+                co[sp] += (fl >> 2) & 1;
+            }
+        }
+    }
+    double o[P];
+    project_cell_f<P, FMA>(A, B, mid[0], mid[1], o);
+    if (inline_indicator_m<P, FMA>(cut, el, er, mean_f<P, FMA>(a.basis, mid[0]), mean_f<P, FMA>(a.basis, mid[1]),
+                                   o)) {
+        const int fl = inline_clamp_f<P, FMA>(a.basis, alpha, mid[0], mid[1], o);
+        ct[sp] += fl & 1;
+        cc[sp] += (fl >> 1) & 1;
+        co[sp] += (fl >> 2) & 1;
+    }
+    const int vn = line - (line / P) * P;
+    const double wdv = a.charge_w[sp] * a.basis.weights[vn] * a.vg[sp]->dx;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        const double old = out[q];
+        out[q] = o[q];
+        const double d = wdv * o[q] - wdv * old;
+        if (d != 0.0)
+            rho_corr_add(a.rho_corr + (long long)(line % kRhoCorrCopies) * a.grid.ncells * P,
+                         (long long)kRhoCorrCopies * a.grid.ncells * P, (long long)cell * P + q, d);
+    }
+}
+
+template <int P, bool FMA>
+__global__ void __launch_bounds__(128, 4) xfix2_kernel(const __grid_constant__ XSweepArgs a) {
+    if (halted(a.st)) return;
+    if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;
+    const unsigned cnt = *a.fix_count;
+    unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // list mode, or (the list overflowed) every output cell
+    const bool rescan = cnt > a.fix_cap;
+    const long long n = rescan ? (long long)a.nspecies * a.nlines * a.grid.ncells : (long long)cnt;
+    for (long long i = i0; i < n; i += stride) {
+        int sp, line, cell;
+        if (!rescan) {
+            const unsigned long long e = a.fix_list[i];
+            sp = (int)(e >> 63);
+            line = (int)((e >> 32) & 0x7fffffffu);
+            cell = (int)(e & 0xffffffffu);
+        } else {
+            cell = (int)(i % a.grid.ncells);
+            const long long r = i / a.grid.ncells;
+            sp = a.species0 + (int)(r / a.nlines);
+            line = (int)(r % a.nlines);
+        }
+        xfix2_cell<P, FMA>(a, sp, line, cell, ct, cc, co);
     }
     block_count_flags(a.st, ct, cc, co);
 }
@@ -2727,7 +2961,8 @@ static cudaError_t configure_xsweep() {
     cudaGetDevice(&dev);
     if (!(configured & (1u << (dev & 31)))) {
         cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)Cf::template smem<MODE>());
         if (e != cudaSuccess) return e;
         // full shared-memory carveout so two pipelines share each SM
         e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
@@ -2744,7 +2979,7 @@ static cudaError_t configure_xsweep() {
 template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out) {
     using Cf = XCfg<P>;
-    constexpr int TT = MODE >= 1 ? Cf::T - 1 : Cf::T;
+    constexpr int TT = (MODE == 1 || MODE == 2) ? Cf::T - 1 : Cf::T;
     if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA, MODE>()) return e;
     b = a;
     b.tile_start[0] = 0;
@@ -2754,7 +2989,7 @@ static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out
     const long long ntot = (long long)a.nspecies * a.nlines * ntl;
     int blocks_per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
-                                                  (Cf::NC + 1) * 32, Cf::SMEM);
+                                                  (Cf::NC + 1) * 32, Cf::template smem<MODE>());
     long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
     if (RHO) {
         grid = grid >= ntl ? (grid / ntl) * ntl : ntl;
@@ -2766,12 +3001,13 @@ static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out
     return cudaSuccess;
 }
 
-template <int P, bool INLINE, bool RHO, bool FMA>
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     XSweepArgs b;
     int grid = 0;
-    if (cudaError_t e = xsweep_plan<P, INLINE, RHO, FMA>(a, b, grid)) return e;
-    xsweep_kernel<P, INLINE, RHO, FMA><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
+    if (cudaError_t e = xsweep_plan<P, INLINE, RHO, FMA, MODE>(a, b, grid)) return e;
+    xsweep_kernel<P, INLINE, RHO, FMA, MODE>
+        <<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<MODE>(), s>>>(b);
     return cudaGetLastError();
 }
 
@@ -2795,27 +3031,62 @@ static cudaError_t launch_xsweep_f(const XSweepArgs& a, cudaStream_t s) {
     return launch_xsweep_t<P, INLINE, RHO, false>(a, s);
 }
 
-template <int P, bool INLINE>
+template <int P, bool INLINE, int MODE>
 static int rho_groups_t(const XSweepArgs& a) {
     XSweepArgs b;
     int grid = 0, ntl = 0;
     cudaError_t e;
-    if constexpr (kHasFma<P>)
+    if constexpr (MODE == 3) {
+        if constexpr (kHasFma<P>)
+            e = xsweep_plan<P, INLINE, true, true, 3>(a, b, grid);
+        else
+            return 0;
+    } else if constexpr (kHasFma<P>) {
         e = a.fma ? xsweep_plan<P, INLINE, true, true>(a, b, grid) : xsweep_plan<P, INLINE, true, false>(a, b, grid);
-    else
+    } else {
         e = xsweep_plan<P, INLINE, true, false>(a, b, grid);
+    }
     if (e != cudaSuccess) return 0;
     ntl = b.tile_start[a.grid.nblocks];
     return grid / ntl;
 }
 
-int xsweep_rho_groups(const XSweepArgs& a) {
-    if (a.inline_sldg) {
-        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, true>(a)))
+int xsweep_rho_groups(const XSweepArgs& a, int fused) {
+    if (fused) {
+        if (a.inline_sldg) {
+            SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, true, 3>(a)))
+        } else {
+            SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, false, 3>(a)))
+        }
+    } else if (a.inline_sldg) {
+        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, true, 0>(a)))
     } else {
-        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, false>(a)))
+        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, false, 0>(a)))
     }
     return 0;
+}
+
+bool xsweep_fused_supported(int P) { return P >= 1 && P <= 4; }
+
+// MODE 3 (two half sweeps fused, fast mode, always with the fused moment)
+template <int P>
+static cudaError_t launch_xsweep_fused_t(const XSweepArgs& a, cudaStream_t s) {
+    if constexpr (kHasFma<P>) {
+        if (a.inline_sldg) return launch_xsweep_t<P, true, true, true, 3>(a, s);
+        return launch_xsweep_t<P, false, true, true, 3>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+cudaError_t launch_xfix2(const XSweepArgs& a, cudaStream_t s) {
+    if (!a.inline_sldg) return cudaSuccess;
+    SK_DISPATCH_P(a.basis.p, (xfix2_kernel<PP, kHasFma<PP>><<<sm_count() * 4, 128, 0, s>>>(a)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xsweep_fused(const XSweepArgs& a, cudaStream_t s) {
+    if (!a.fma || !a.rho_fuse || a.periodic) return cudaErrorInvalidValue;
+    SK_DISPATCH_P(a.basis.p, return launch_xsweep_fused_t<PP>(a, s))
+    return cudaErrorInvalidValue;
 }
 
 // rho[x] = sum of the groups' partial rows + the clamp corrections. 32 x dofs
@@ -2825,8 +3096,9 @@ int xsweep_rho_groups(const XSweepArgs& a) {
 constexpr int kRhoRedParts = 8;
 __global__ void __launch_bounds__(32 * kRhoRedParts)
     rho_fused_reduce_kernel(const double* partial, const unsigned long long* corr, int groups, int nxd,
-                            double* rho, const DevStatus* st) {
+                            double* rho, const DevStatus* st, const int* gate, int gate_on) {
     if (halted(st)) return;
+    if (gate && ((*gate != 0) != (gate_on != 0))) return;
     __shared__ double sp[kRhoRedParts][32];
     __shared__ unsigned long long sh[kRhoRedParts][32], sl[kRhoRedParts][32];
     const int l = threadIdx.x & 31, q = threadIdx.x >> 5;
@@ -2858,11 +3130,11 @@ __global__ void __launch_bounds__(32 * kRhoRedParts)
     }
 }
 
-cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s) {
+cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s, int fused) {
     const int nxd = a.grid.ncells * a.basis.p;
-    const int groups = xsweep_rho_groups(a);
+    const int groups = xsweep_rho_groups(a, fused);
     rho_fused_reduce_kernel<<<(nxd + 31) / 32, 32 * kRhoRedParts, 0, s>>>(a.rho_partial, a.rho_corr, groups,
-                                                                        nxd, rho, a.st);
+                                                                        nxd, rho, a.st, a.gate, a.gate_on);
     return cudaGetLastError();
 }
 
@@ -3054,6 +3326,34 @@ cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s) {
 cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double* E, double* phi,
                                  cudaStream_t s) {
     SK_DISPATCH_P(pd.ps - 1, (poisson_exact_kernel<PP + 1><<<1, 256, 0, s>>>(pd, rho, E, phi)));
+    return cudaGetLastError();
+}
+
+// Step boundary n -> n+1 (before step_end of step n): the two x half sweeps
+// around it may be fused unless the velocity cut-off checks at the end of
+// step n -- checked only when its 10-step cooldown has run out (run.cpp:100),
+// and a shrink there changes the v grid between the two sweeps.
+__global__ void fuse_decide_kernel(DevStatus* st, int v_adjust, long long cooldown) {
+    if (halted(st)) return;
+    const long long n = st->step + 1;
+    int ok = 1;
+    for (int sp = 0; sp < 2; ++sp)
+        if (v_adjust && n - st->last_shrink[sp] >= cooldown) ok = 0;
+    st->fuse_ok = ok;
+}
+// the unfused alternative of a fused boundary leaves the field in the buffer
+// the fused sweep does not write: record it in the fields' flip flags
+__global__ void flip_toggle_kernel(const DevStatus* st, int* f0, int* f1) {
+    if (halted(st) || st->fuse_ok) return;
+    *f0 ^= 1;
+    *f1 ^= 1;
+}
+cudaError_t launch_fuse_decide(DevStatus* st, int v_adjust, long long cooldown, cudaStream_t s) {
+    fuse_decide_kernel<<<1, 1, 0, s>>>(st, v_adjust, cooldown);
+    return cudaGetLastError();
+}
+cudaError_t launch_flip_toggle(const DevStatus* st, int* f0, int* f1, cudaStream_t s) {
+    flip_toggle_kernel<<<1, 1, 0, s>>>(st, f0, f1);
     return cudaGetLastError();
 }
 

@@ -75,6 +75,10 @@ struct XSweepArgs {
     // post-limiter flag pass (xsweep_kernel MODE 1): the literature indicator
     // of every cell from its window, in place; flagged cells are queued
     PostCfg post;
+    // device-decided alternatives (fused / unfused step boundary): the kernel
+    // runs only if (*gate != 0) == gate_on; gate == nullptr: always
+    const int* gate;
+    int gate_on;
 };
 
 struct VTabArgs {
@@ -233,8 +237,19 @@ cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s);
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_xfix(const XSweepArgs& a, cudaStream_t s);
 // rho = sum of the fused partials + fixed-point corrections; returns #partials
-cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s);
-int xsweep_rho_groups(const XSweepArgs& a);
+// fused = 1: the partials of the MODE 3 (two fused half sweeps) launch
+cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s, int fused = 0);
+int xsweep_rho_groups(const XSweepArgs& a, int fused = 0);
+// two consecutive x half sweeps in one pass (step n's last, step n+1's first
+// with the fused charge density), fast mode, single-dx-class non-periodic grids
+bool xsweep_fused_supported(int P);
+cudaError_t launch_xsweep_fused(const XSweepArgs& a, cudaStream_t s);
+// its fixup: the queued output cells recomputed with both clamps (inline sLdG)
+cudaError_t launch_xfix2(const XSweepArgs& a, cudaStream_t s);
+// device decision for a fusable step boundary (DevStatus::fuse_ok) and the
+// flip-flag toggle of its unfused alternative
+cudaError_t launch_fuse_decide(DevStatus* st, int v_adjust, long long cooldown, cudaStream_t s);
+cudaError_t launch_flip_toggle(const DevStatus* st, int* f0, int* f1, cudaStream_t s);
 cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s);
 cudaError_t launch_rho(const RhoArgs& a, int nspecies_mask, cudaStream_t s);
 cudaError_t launch_poisson(const PoissonDev& pd, int stage, const double* rho, double* E, double* phi,

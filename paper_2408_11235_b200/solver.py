@@ -469,6 +469,10 @@ class Context:
         to attribute a fast-mode deviation to one of them"""
         _check(N.lib().sk_ctx_set_exact_parts(self.h, int(mask)))
 
+    def set_step_fusion(self, on: bool):
+        """fuse step n's second and step n+1's first x half sweep in run_steps"""
+        _check(N.lib().sk_ctx_set_step_fusion(self.h, int(on)))
+
     def synchronize(self):
         _check(N.lib().sk_ctx_synchronize(self.h))
 
@@ -726,6 +730,10 @@ class SimulationState:
     def run_steps(self, n: int):
         _check(N.lib().sk_run_steps(self.h, n))
         self.steps_enqueued += n
+
+    def prepare_steps(self, n: int):
+        """capture the graphs run_steps(n) will replay (no work is run)"""
+        _check(N.lib().sk_state_prepare_steps(self.h, n))
 
     def run_step_host(self, fe: np.ndarray, fi: np.ndarray):
         """drop-in strang_step + shrink over host arrays (updated in place)."""

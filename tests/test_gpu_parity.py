@@ -227,17 +227,22 @@ def _envelope(ora, cfg, steps):
     return env
 
 
+@pytest.mark.parametrize("batched", [False, True], ids=["stepwise", "fused"])
 @pytest.mark.parametrize("name", list(FULL_CFGS))
-def test_full_steps_vs_oracle(sk, ora, name):
+def test_full_steps_vs_oracle(sk, ora, name, batched):
     """Fast path (DFMA sweeps, parallel charge density, refined cyclic-
     reduction Poisson). The exact-mode test proves every other operation is
     bitwise, so what remains is rounding noise: f within 1e-12
     and E within 1e-12 * max(1, max|E|) at steps 1 and 10, each unless the
     reference's own envelope (ENV_C x _envelope) is larger."""
     cfg, o, st = _pair(sk, ora, FULL_CFGS[name])
+    st.ctx.set_step_fusion(batched)
     env = _envelope(ora, cfg, 10)
     for s in range(1, 11):
-        st.run_step()
+        if not batched:
+            st.run_step()
+        elif s in (1, 2):  # run_steps(9): a graph whose step boundaries fuse the x half sweeps
+            st.run_steps(1 if s == 1 else 9)
         o.step()
         if s in (1, 10):
             ef, eE = env[s]
@@ -396,6 +401,48 @@ def test_errors_map_to_reference_exceptions(sk):
     with pytest.raises(sk.SimulationError, match="nonfinite") as ei:
         st.run_step()
     assert ei.value.step == 1
+
+
+@pytest.mark.parametrize("kw", [
+    dict(k=3, nf=32, nc=64, m=1, nv=128, mu=1836.0, limiter="sldg"),
+    dict(k=2, nf=16, nc=32, m=1, nv=64, limiter="none"),
+    dict(k=1, nf=24, nc=24, m=1, nv=48, limiter="sldg"),
+    dict(k=0, nf=16, nc=16, m=1, nv=32, limiter="none")], ids=["k3_sldg", "k2_none", "k1_sldg", "k0_none"])
+def test_fused_step_boundaries_match_separate_sweeps(sk, kw):
+    """run_steps fuses step n's second and step n+1's first x half sweep into
+    one pass (xsweep_kernel MODE 3, clamps in-kernel), except at boundaries
+    where the cut-off may check (decided on the device). Against the same 25
+    steps with fusion off: every cell runs the same arithmetic, only the
+    charge density is grouped differently (fused moment of clamped values
+    instead of unclamped + exact corrections) -- f and E agree to rounding,
+    shrink steps and v_max are identical."""
+    cfg = cfg_of(sk, **kw)
+    a, b = sk.SimulationState(cfg), sk.SimulationState(cfg)
+    a.ctx.set_step_fusion(True)
+    b.ctx.set_step_fusion(False)
+    for n in (3, 10, 12):  # graphs of 3 and 10 bodies, plus a remainder of 2
+        a.run_steps(n)
+        b.run_steps(n)
+    assert a.step_index() == b.step_index() == 25
+    for sp in (0, 1):
+        assert a.shrinks(sp) == b.shrinks(sp) and a.shrinks(sp)[0] >= 2
+        assert a.field(sp).vmax() == b.field(sp).vmax()
+        fa, fb = a.field(sp).download(), b.field(sp).download()
+        assert rel(fa, fb) <= F_TOL, f"sp{sp}"
+        # pointwise where f is not vacuum (a missed clamp in the tails would
+        # hide below the max-normalised bound)
+        live = np.abs(fb) > 1e-8 * np.abs(fb).max()
+        assert (np.abs(fa - fb)[live] <= 1e-10 * np.abs(fb)[live]).all(), f"sp{sp} pointwise"
+    Eb = b.E()
+    assert np.abs(a.E() - Eb).max() <= 1e-12 * max(1.0, np.abs(Eb).max())
+    # limiter counters: a fused boundary does not evaluate the step-n cells that
+    # leave the line in step n+1's first sweep (their values cannot reach the
+    # state); elsewhere flags only flip where rounding-level E differences
+    # move near-vacuum cells across the threshold
+    sa, sb = a.stats(), b.stats()
+    assert sa["outputs"] == sb["outputs"]
+    for key in ("inline_troubled", "inline_clamped"):
+        assert abs(sa[key] - sb[key]) <= max(5, 0.05 * sb[key]), key
 
 
 def test_nonfinite_mid_batch_halts_at_the_failing_step(sk):
