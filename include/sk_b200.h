@@ -167,6 +167,13 @@ size_t sk_field_size(const sk_field* f);
 double* sk_field_data_dev(sk_field* f); /* current buffer (device) */
 sk_status sk_field_upload(sk_field* f, const double* host, size_t count);
 sk_status sk_field_download(sk_field* f, double* host, size_t count);
+/* `height` runs of `width` doubles, `pitch` doubles apart, from element
+ * `offset` of the field (layout field.hpp:71-73) into a packed host array:
+ * one x line (offset = row * nx*p, width = nx*p, height = 1) or one v line
+ * (offset = x dof, width = 1, height = nv*p, pitch = nx*p) -- gather_v_line
+ * (field.cpp:18-24) without a full download. */
+sk_status sk_field_download_2d(sk_field* f, double* host, size_t offset, size_t width, size_t height,
+                               size_t pitch);
 sk_status sk_field_upload_async(sk_field* f, const double* host_pinned, size_t count);
 sk_status sk_field_download_async(sk_field* f, double* host_pinned, size_t count);
 /* v-shard of a NodalField for a multi-GPU run sharded along v: this rank holds
@@ -235,6 +242,9 @@ sk_status sk_state_destroy(sk_state* s);
 sk_field* sk_state_field(sk_state* s, int species);
 double* sk_state_E_dev(sk_state* s);
 sk_status sk_state_download_E(sk_state* s, double* host, size_t count);
+/* the charge density of the state's last step (poisson.cpp:194-216 output,
+ * the Poisson right-hand side), nx*(k+1) values */
+sk_status sk_state_download_rho(sk_state* s, double* host, size_t count);
 /* v-sharded state: rank `rank` of `nranks` holds v_cells/nranks cells of each
  * species plus `halo` cells; the step runs as phase 2 (x half sweep + local
  * rho) -> caller all-reduces rho (sk_state_rho_dev) and exchanges the halos

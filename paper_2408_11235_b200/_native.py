@@ -86,6 +86,7 @@ SIGNATURES = {
     "sk_field_data_dev": (_vp, [_vp]),
     "sk_field_upload": (_i, [_vp, _dp, _sz]),
     "sk_field_download": (_i, [_vp, _dp, _sz]),
+    "sk_field_download_2d": (_i, [_vp, _dp, _sz, _sz, _sz, _sz]),
     "sk_field_upload_async": (_i, [_vp, _dp, _sz]),
     "sk_field_download_async": (_i, [_vp, _dp, _sz]),
     "sk_field_v_grid": (_i, [_vp, _dp, _dp, _ip]),
@@ -112,6 +113,7 @@ SIGNATURES = {
     "sk_state_field": (_vp, [_vp, _i]),
     "sk_state_E_dev": (_vp, [_vp]),
     "sk_state_download_E": (_i, [_vp, _dp, _sz]),
+    "sk_state_download_rho": (_i, [_vp, _dp, _sz]),
     "sk_strang_step": (_i, [_vp]),
     "sk_run_step": (_i, [_vp]),
     "sk_run_steps": (_i, [_vp, _i]),

@@ -389,7 +389,11 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
             return fail(SK_ERR_RUNTIME, "internal: fused rho buffers not sized");  // mallocs in capture)
         a.rho_partial = c->rho_fpart;
         a.rho_corr = c->rho_corr;
-        CK(cudaMemsetAsync(c->rho_corr, 0, sizeof(unsigned long long) * nxd * 2 * kRhoCorrCopies, c->stream));
+        // (the unfused alternative of a fused boundary: enq_fused_boundary
+        // zeroed the corrections before the fused sweep, and its fixup's
+        // corrections must survive until the reduction below)
+        if (!fused_reduce)
+            CK(cudaMemsetAsync(c->rho_corr, 0, sizeof(unsigned long long) * nxd * 2 * kRhoCorrCopies, c->stream));
     }
     if (!periodic && xghost_grid(c->grid)) {
         // ghost cells across the dx jumps: precomputed so the sweep only copies
@@ -1128,6 +1132,18 @@ sk_status sk_field_download(sk_field* f, double* host, size_t count) {
     CK(cudaStreamSynchronize(f->ctx->stream));
     return SK_OK;
 }
+sk_status sk_field_download_2d(sk_field* f, double* host, size_t offset, size_t width, size_t height,
+                               size_t pitch) {
+    if (width == 0 || height == 0) return SK_OK;
+    if (pitch < width || offset + (height - 1) * pitch + width > f->n)
+        return fail(SK_ERR_RUNTIME, "field download_2d: range outside the field");
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    CK(cudaMemcpy2DAsync(host, sizeof(double) * width, live + offset, sizeof(double) * pitch,
+                         sizeof(double) * width, height, cudaMemcpyDeviceToHost, f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    return SK_OK;
+}
 sk_status sk_field_upload_async(sk_field* f, const double* host, size_t count) {
     if (count != f->n) return fail(SK_ERR_RUNTIME, "field upload: size mismatch");
     double* live = nullptr;
@@ -1498,6 +1514,15 @@ sk_status sk_state_destroy(sk_state* s) {
 
 sk_field* sk_state_field(sk_state* s, int species) { return s->f[species & 1]; }
 double* sk_state_E_dev(sk_state* s) { return s->E; }
+
+sk_status sk_state_download_rho(sk_state* s, double* host, size_t count) {
+    sk_ctx* c = s->ctx;
+    if (count != (size_t)c->grid.ncells * c->P) return fail(SK_ERR_RUNTIME, "rho: size mismatch");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(host, s->rho, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SK_OK;
+}
 
 sk_status sk_state_download_E(sk_state* s, double* host, size_t count) {
     sk_ctx* c = s->ctx;

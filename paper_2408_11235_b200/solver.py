@@ -545,6 +545,14 @@ class NodalField:
         a = np.ascontiguousarray(data, dtype=np.float64).ravel()
         _check(N.lib().sk_field_upload(self.h, a.ctypes.data_as(C.POINTER(C.c_double)), a.size))
 
+    def download_2d(self, offset: int, width: int, height: int, pitch: int) -> np.ndarray:
+        """height runs of width doubles, pitch apart, from element offset (an x
+        line: width = nx*p; a v line: width 1, pitch nx*p) -> [height, width]"""
+        out = np.empty((height, width))
+        _check(N.lib().sk_field_download_2d(self.h, out.ctypes.data_as(C.POINTER(C.c_double)), offset, width,
+                                            height, pitch))
+        return out
+
     def download(self) -> np.ndarray:
         out = np.empty(self.size)
         _check(N.lib().sk_field_download(self.h, out.ctypes.data_as(C.POINTER(C.c_double)),
@@ -711,6 +719,12 @@ class SimulationState:
 
     def E_ptr(self) -> int:
         return N.lib().sk_state_E_dev(self.h)
+
+    def rho(self) -> np.ndarray:
+        """the charge density of the last step (the Poisson right-hand side)"""
+        out = np.empty(self.ctx.nx * self.ctx.p)
+        _check(N.lib().sk_state_download_rho(self.h, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
+        return out
 
     def E(self) -> np.ndarray:
         """state.field.E (stepper.hpp:48) downloaded to the host."""
