@@ -142,6 +142,10 @@ sk_status sk_ctx_set_exact_parts(sk_ctx* ctx, int mask);
  * B200 each half sweep is issue-bound about as much as HBM-bound, so the fused
  * pass measures break-even at C5 and slower at C3. */
 sk_status sk_ctx_set_step_fusion(sk_ctx* ctx, int on);
+/* Out-of-bounds write check: with SK_GUARD=1 in the environment when the
+ * context is created, fields, tables, E, rho and phi are allocated with
+ * sentinel guard zones; *bad = guard words overwritten since (0 = clean). */
+sk_status sk_ctx_check_guards(sk_ctx* ctx, long long* bad);
 /* Capacity of the deferred limiter-clamp list (troubled cells queued by the
  * sweeps, clamped by a fixup kernel); above it the fixup rescans the sweep.
  * Default and maximum 4 Mi cells; exposed for testing the rescan path. */

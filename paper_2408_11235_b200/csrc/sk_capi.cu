@@ -45,6 +45,9 @@ cudaError_t dalloc(T** p, size_t n) {
     return cudaMalloc((void**)p, sizeof(T) * (n ? n : 1));
 }
 
+constexpr size_t kGuard = 4096;                        // doubles per side
+constexpr unsigned long long kGuardWord = 0x7ff4dead5a5a5a5aull;  // a NaN no kernel writes
+
 }  // namespace
 
 struct sk_ctx {
@@ -95,7 +98,45 @@ struct sk_ctx {
     // of the x sweep is issue-bound about as much as it is HBM-bound
     // (profiles/r02_fused_xsweep.txt); SK_STEP_FUSION=1 turns it on
     bool fuse_off = getenv("SK_STEP_FUSION") == nullptr || atoi(getenv("SK_STEP_FUSION")) == 0;
+    // out-of-bounds write detection (compute-sanitizer is unavailable on the
+    // GPU pool): with SK_GUARD=1 the fields, tables, E, rho and phi get
+    // kGuard-double guard zones of a sentinel pattern on both sides;
+    // sk_ctx_check_guards counts overwritten guard words
+    bool guard_on = getenv("SK_GUARD") != nullptr && atoi(getenv("SK_GUARD")) != 0;
+    struct Guarded {
+        double* base;
+        size_t n;
+    };
+    std::vector<Guarded> guarded;
 };
+
+namespace {
+// n doubles, with guard zones when c->guard_on (see sk_ctx::guard_on)
+cudaError_t gdalloc(sk_ctx* c, double** p, size_t n) {
+    if (!c->guard_on) return dalloc(p, n);
+    double* base = nullptr;
+    cudaError_t e = dalloc(&base, n + 2 * kGuard);
+    if (e != cudaSuccess) return e;
+    std::vector<unsigned long long> g(kGuard, kGuardWord);
+    if ((e = cudaMemcpy(base, g.data(), sizeof(double) * kGuard, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMemcpy(base + kGuard + n, g.data(), sizeof(double) * kGuard, cudaMemcpyHostToDevice)) !=
+            cudaSuccess)
+        return e;
+    c->guarded.push_back({base, n});
+    *p = base + kGuard;
+    return cudaSuccess;
+}
+void gdfree(sk_ctx* c, double* p) {
+    if (!p) return;
+    for (size_t i = 0; i < c->guarded.size(); ++i)
+        if (c->guarded[i].base + kGuard == p) {
+            cudaFree(c->guarded[i].base);
+            c->guarded.erase(c->guarded.begin() + (long)i);
+            return;
+        }
+    cudaFree(p);
+}
+}  // namespace
 
 struct sk_field {
     sk_ctx* ctx = nullptr;
@@ -904,6 +945,7 @@ sk_status sk_ctx_destroy(sk_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (void* p : c->pbufs) cudaFree(p);
+    for (const auto& g : c->guarded) cudaFree(g.base);  // buffers of states not destroyed first
     cudaFree(c->st);
     cudaFreeHost(c->st_host);
     cudaFree(c->rho_partial);
@@ -985,6 +1027,21 @@ sk_status sk_ctx_set_exact_parts(sk_ctx* c, int mask) {
     return SK_OK;
 }
 
+sk_status sk_ctx_check_guards(sk_ctx* c, long long* bad) {
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    long long nbad = 0;
+    std::vector<unsigned long long> g(kGuard);
+    for (const auto& e : c->guarded)
+        for (int side = 0; side < 2; ++side) {
+            CK(cudaMemcpy(g.data(), side ? e.base + kGuard + e.n : e.base, sizeof(double) * kGuard,
+                          cudaMemcpyDeviceToHost));
+            for (unsigned long long w : g) nbad += w != kGuardWord;
+        }
+    *bad = nbad;
+    return c->guard_on ? SK_OK : fail(SK_ERR_RUNTIME, "guards are off (set SK_GUARD=1 before the context)");
+}
+
 sk_status sk_ctx_set_step_fusion(sk_ctx* c, int on) {
     c->fuse_off = on == 0;
     ++c->gen;  // captured step graphs change
@@ -1050,8 +1107,8 @@ sk_status sk_field_create_shard(sk_ctx* c, int species, double v_left, double v_
     f->n = (size_t)ncell * P * row;
     f->halo_off = (size_t)halo * P * row;
     const size_t total = f->n + 2 * f->halo_off;
-    CK(dalloc(&f->buf[0], total + 8));  // +8: bulk copies may round up past the end
-    CK(dalloc(&f->buf[1], total + 8));
+    CK(gdalloc(c, &f->buf[0], total + 8));  // +8: bulk copies may round up past the end
+    CK(gdalloc(c, &f->buf[1], total + 8));
     CK(cudaMemsetAsync(f->buf[0], 0, sizeof(double) * total, c->stream));
     CK(cudaMemsetAsync(f->buf[1], 0, sizeof(double) * total, c->stream));
     CK(dalloc(&f->vg, 1));
@@ -1059,8 +1116,8 @@ sk_status sk_field_create_shard(sk_ctx* c, int species, double v_left, double v_
     CK(cudaMemsetAsync(f->dflip, 0, sizeof(int), c->stream));
     DevVGrid vg{v_left, dv, v_cells_global, cell0};
     CK(cudaMemcpy(f->vg, &vg, sizeof vg, cudaMemcpyHostToDevice));
-    CK(dalloc(&f->xtab, (size_t)c->grid.nclass * ncell * P * xtab_nf(P)));
-    CK(dalloc(&f->vtab, (size_t)vtab_nf(P) * c->grid.ncells * P));
+    CK(gdalloc(c, &f->xtab, (size_t)c->grid.nclass * ncell * P * xtab_nf(P)));
+    CK(gdalloc(c, &f->vtab, (size_t)vtab_nf(P) * c->grid.ncells * P));
     CK(dalloc(&f->ttab, (size_t)v_cells_global * 4 * P * P));
     CK(dalloc(&f->tcell, (size_t)v_cells_global * 4));
     CK(cudaStreamSynchronize(c->stream));
@@ -1096,12 +1153,12 @@ sk_status sk_field_destroy(sk_field* f) {
     if (!f) return SK_OK;
     cudaSetDevice(f->ctx->device);
     cudaStreamSynchronize(f->ctx->stream);
-    cudaFree(f->buf[0]);
-    cudaFree(f->buf[1]);
+    gdfree(f->ctx, f->buf[0]);
+    gdfree(f->ctx, f->buf[1]);
     cudaFree(f->vg);
     cudaFree(f->dflip);
-    cudaFree(f->xtab);
-    cudaFree(f->vtab);
+    gdfree(f->ctx, f->xtab);
+    gdfree(f->ctx, f->vtab);
     cudaFree(f->ttab);
     cudaFree(f->tcell);
     delete f;
@@ -1389,9 +1446,9 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         }
         if (!c->rho_corr) CK(dalloc(&c->rho_corr, 2 * ne * kRhoCorrCopies));
     }
-    CK(dalloc(&s->E, ne));
-    CK(dalloc(&s->rho, ne));
-    CK(dalloc(&s->phi, (size_t)c->grid.ncells * (c->P + 1)));
+    CK(gdalloc(c, &s->E, ne));
+    CK(gdalloc(c, &s->rho, ne));
+    CK(gdalloc(c, &s->phi, (size_t)c->grid.ncells * (c->P + 1)));
     // run.cpp:56 initial field
     if ((rc = enq_rho(s->f[0], s->f[1], s->rho))) return rc;
     if ((rc = enq_poisson(c, s->rho, s->E, s->phi))) return rc;
@@ -1481,9 +1538,9 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
         }
         if (!c->rho_corr) CK(dalloc(&c->rho_corr, 2 * ne * kRhoCorrCopies));
     }
-    CK(dalloc(&s->E, ne));
-    CK(dalloc(&s->rho, ne));
-    CK(dalloc(&s->phi, (size_t)c->grid.ncells * (c->P + 1)));
+    CK(gdalloc(c, &s->E, ne));
+    CK(gdalloc(c, &s->rho, ne));
+    CK(gdalloc(c, &s->phi, (size_t)c->grid.ncells * (c->P + 1)));
     // local charge density of the initial data; the caller sums it over the
     // ranks and calls sk_state_phase(s, 1) for the initial field (run.cpp:56)
     if ((rc = enq_rho(s->f[0], s->f[1], s->rho))) return rc;
@@ -1505,9 +1562,9 @@ sk_status sk_state_destroy(sk_state* s) {
     cudaFree(s->src_gv[1]);
     sk_field_destroy(s->f[0]);
     sk_field_destroy(s->f[1]);
-    cudaFree(s->E);
-    cudaFree(s->rho);
-    cudaFree(s->phi);
+    gdfree(s->ctx, s->E);
+    gdfree(s->ctx, s->rho);
+    gdfree(s->ctx, s->phi);
     delete s;
     return SK_OK;
 }

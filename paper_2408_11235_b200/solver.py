@@ -469,6 +469,12 @@ class Context:
         to attribute a fast-mode deviation to one of them"""
         _check(N.lib().sk_ctx_set_exact_parts(self.h, int(mask)))
 
+    def check_guards(self) -> int:
+        """guard words overwritten around the state buffers (needs SK_GUARD=1)"""
+        bad = C.c_longlong()
+        _check(N.lib().sk_ctx_check_guards(self.h, C.byref(bad)))
+        return bad.value
+
     def set_step_fusion(self, on: bool):
         """fuse step n's second and step n+1's first x half sweep in run_steps"""
         _check(N.lib().sk_ctx_set_step_fusion(self.h, int(on)))

@@ -1105,3 +1105,16 @@ def test_c5_full_size_sampled_lines(sk, ora, exact):
     st.close()
     st.ctx.close()
     _free_gpu()
+
+
+def test_no_out_of_bounds_writes(sk):
+    """Memory-safety stand-in for compute-sanitizer (closed on the GPU pool,
+    SURVEY.md §5): every state buffer between sentinel guard zones, 12 run()
+    loop bodies of five small configurations touching every kernel family in
+    both arithmetic modes, not one guard word overwritten."""
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "sanitize_steps.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
