@@ -268,6 +268,17 @@ sk_status sk_state_create_shard(sk_ctx* ctx, const sk_run_config* cfg, int rank,
 double* sk_state_rho_dev(sk_state* s);
 int* sk_state_shrink_flags_dev(sk_state* s); /* int[2], device: 1 = shrink this step */
 int sk_state_shrink_halo(sk_state* s);        /* halo cells a sharded shrink reads */
+/* Adaptive v-halo exchange of a shard (phases 6-9 of sk_state_phase): phase 6
+ * (Poisson + v tables) records the cells this step's v sweep reads beyond the
+ * shard -- max over x dofs of |i*|+1 (advection.cpp:14-25, :226) -- into a
+ * pinned word read by sk_state_vhalo_need once phase 6 has completed; the
+ * caller exchanges that many cells (sk_state_set_vhalo, then sk_field_halo)
+ * while phase 7 sweeps the v chunks that read no halo cell for shifts up to
+ * `bound`, and phase 8 sweeps the rest (phase 9: all chunks, when the shift
+ * exceeded `bound`). Width and bound are at most sk_state_vhalo_capacity. */
+sk_status sk_state_vhalo_need(sk_state* s, int* need);
+sk_status sk_state_set_vhalo(sk_state* s, int width, int bound);
+int sk_state_vhalo_capacity(sk_state* s);
 sk_status sk_state_phase(sk_state* s, int phase);
 /* ---- diagnostics and output (diagnostics.cpp, run.cpp:60-169).
  * Single-GPU states; all synchronise. */

@@ -98,6 +98,9 @@ SIGNATURES = {
     "sk_state_rho_dev": (_vp, [_vp]),
     "sk_state_shrink_flags_dev": (_vp, [_vp]),
     "sk_state_shrink_halo": (_i, [_vp]),
+    "sk_state_vhalo_need": (_i, [_vp, C.POINTER(C.c_int)]),
+    "sk_state_set_vhalo": (_i, [_vp, _i, _i]),
+    "sk_state_vhalo_capacity": (_i, [_vp]),
     "sk_state_phase": (_i, [_vp, _i]),
     "sk_field_fill_blob": (_i, [_vp, _d]),
     "sk_advect_x": (_i, [_vp, _d, _d, _i, C.POINTER(sk_limiter), _i, C.c_long]),

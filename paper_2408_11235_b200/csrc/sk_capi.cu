@@ -160,6 +160,11 @@ struct sk_field {
     // resolve it themselves; host-side buffer access goes through live_ptr().
     int* dflip = nullptr;
     bool may_flip = false;             // a shrink projection was ever enqueued
+    // v shards: dflip as of the end of phase 6, copied to pinned memory there;
+    // valid (flip_known) from sk_state_vhalo_need until phase 8/9, so the halo
+    // exchange between them resolves buffers without a stream synchronisation
+    int* flip_pin = nullptr;
+    bool flip_known = false;
     double* cur_ptr() { return buf[cur] + halo_off; }
     double* other_ptr() { return buf[cur ^ 1] + halo_off; }
     void swap() { cur ^= 1; }
@@ -167,6 +172,10 @@ struct sk_field {
     cudaError_t live_ptr(double** p) {
         if (!may_flip) {
             *p = cur_ptr();
+            return cudaSuccess;
+        }
+        if (flip_known) {
+            *p = buf[cur ^ (*reinterpret_cast<volatile int*>(flip_pin) & 1)] + halo_off;
             return cudaSuccess;
         }
         int fl = 0;
@@ -204,6 +213,12 @@ struct sk_state {
     long long graph_clock = 0;
     int rank = 0, nranks = 1;          // v-shard of a multi-GPU run
     int shrink_halo = 0;               // halo cells a sharded shrink reads
+    // adaptive v-halo exchange of a shard (phases 6-9): cells this step's v
+    // sweep reads beyond the shard (device, pinned mirror) and the bound that
+    // classified the v chunks run before the exchange as interior
+    int* vneed_dev = nullptr;
+    int* vneed_host = nullptr;
+    int vbound = 0;
     double* src_gx = nullptr;          // injection source tables (SourceArgs)
     double* src_gv[2] = {nullptr, nullptr};
     // optional per-phase CUDA-event timing (sk_state_set_phase_timing)
@@ -548,8 +563,11 @@ sk_status enq_fused_boundary(sk_state* s, int inline_sldg, double threshold) {
     return SK_OK;
 }
 
+// halo_need: a v shard sizing its exchange from this step's E -- the tables
+// report the cells read beyond the shard into it, checked against the
+// allocated halo instead of the exchanged one
 sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, const double* charge,
-                   const double* sqrt_mu, int inline_sldg, double threshold) {
+                   const double* sqrt_mu, int inline_sldg, double threshold, int* halo_need = nullptr) {
     sk_ctx* c = fs[0]->ctx;
     VTabArgs a{};
     a.basis = c->basis;
@@ -565,6 +583,12 @@ sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, con
     a.st = c->st;
     a.halo_lo = fs[0]->gl() > 0 ? fs[0]->gl() : -1;
     a.halo_hi = fs[0]->gr() > 0 ? fs[0]->gr() : -1;
+    if (halo_need) {
+        a.halo_need = halo_need;
+        if (a.halo_lo >= 0) a.halo_lo = fs[0]->halo;
+        if (a.halo_hi >= 0) a.halo_hi = fs[0]->halo;
+        CK(cudaMemsetAsync(halo_need, 0, sizeof(int), c->stream));
+    }
     a.nxd = c->grid.ncells * c->P;
     a.nspecies = nspecies;
     a.species0 = nspecies == 2 ? 0 : fs[0]->species;
@@ -575,8 +599,12 @@ sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, con
     return SK_OK;
 }
 
+// chunk0 / nchunks: only v chunks [chunk0, chunk0 + nchunks) of kVChunk cells
+// (nchunks 0: all, < 0: none); part = 1: first part of a split sweep (fix list
+// reset, no fixup, no exchange of the buffers' roles), 3: a middle part, 2: the
+// last part (fixup and exchange, no reset), 0: the whole sweep
 sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
-                     int check_finite) {
+                     int check_finite, int chunk0 = 0, int nchunks = 0, int part = 0) {
     sk_ctx* c = fs[0]->ctx;
     VSweepArgs a{};
     a.basis = c->basis;
@@ -611,12 +639,20 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.fix_list = c->fix_list;
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;
-    if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
-    CK(launch_vsweep(a, c->stream));
-    c->launches += 1;
+    a.chunk0 = chunk0;
+    a.nchunks = nchunks;
+    if (inline_sldg && (part == 0 || part == 1))
+        CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
+    if (nchunks >= 0) {
+        CK(launch_vsweep(a, c->stream));
+        c->launches += 1;
+    }
+    if (part == 1 || part == 3) return SK_OK;
     if (c->fix_timer)
         if (sk_status rc = mark(c->fix_timer, c->fix_phase)) return rc;
     if (inline_sldg) {
+        a.chunk0 = 0;
+        a.nchunks = 0;
         CK(launch_vfix(a, c->stream));
         c->launches += 1;
     }
@@ -1157,6 +1193,7 @@ sk_status sk_field_destroy(sk_field* f) {
     gdfree(f->ctx, f->buf[1]);
     cudaFree(f->vg);
     cudaFree(f->dflip);
+    cudaFreeHost(f->flip_pin);
     gdfree(f->ctx, f->xtab);
     gdfree(f->ctx, f->vtab);
     cudaFree(f->ttab);
@@ -1510,6 +1547,16 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
     }
     s->f[0]->xhalo = s->f[1]->xhalo = h;
     s->shrink_halo = hs;
+    if (nranks > 1) {
+        CK(dalloc(&s->vneed_dev, 1));
+        CK(cudaMallocHost((void**)&s->vneed_host, sizeof(int)));
+        *s->vneed_host = 0;
+        s->vbound = halloc;
+        for (int sp = 0; sp < 2; ++sp) {
+            CK(cudaMallocHost((void**)&s->f[sp]->flip_pin, sizeof(int)));
+            *s->f[sp]->flip_pin = 0;
+        }
+    }
     double sigma = cfg->sigma < 0 ? 0.1 * cfg->L : cfg->sigma;
     if (cfg->scenario == 1 ? (rc = build_source_tables(s))
                            : ((rc = sk_field_fill_blob(s->f[0], sigma)) || (rc = sk_field_fill_blob(s->f[1], sigma)))) {
@@ -1560,6 +1607,8 @@ sk_status sk_state_destroy(sk_state* s) {
     cudaFree(s->src_gx);
     cudaFree(s->src_gv[0]);
     cudaFree(s->src_gv[1]);
+    cudaFree(s->vneed_dev);
+    cudaFreeHost(s->vneed_host);
     sk_field_destroy(s->f[0]);
     sk_field_destroy(s->f[1]);
     gdfree(s->ctx, s->E);
@@ -1793,6 +1842,26 @@ double* sk_state_rho_dev(sk_state* s) { return s->rho; }
 int* sk_state_shrink_flags_dev(sk_state* s) { return s->ctx->st->shrink_flag; }
 int sk_state_shrink_halo(sk_state* s) { return s->shrink_halo; }
 
+sk_status sk_state_vhalo_need(sk_state* s, int* need) {
+    if (!s->vneed_host) return fail(SK_ERR_RUNTIME, "vhalo_need: not a v shard");
+    *need = *reinterpret_cast<volatile int*>(s->vneed_host);
+    s->f[0]->flip_known = s->f[1]->flip_known = true;  // phase 6 copied them with it
+    return SK_OK;
+}
+
+sk_status sk_state_set_vhalo(sk_state* s, int width, int bound) {
+    sk_field* f0 = s->f[0];
+    if (!s->vneed_dev) return fail(SK_ERR_RUNTIME, "set_vhalo: not a v shard");
+    if (width < 1 || width > f0->halo || width > f0->nv || bound < 1 || bound > f0->halo)
+        return fail(SK_ERR_RUNTIME, "set_vhalo: width and bound must be in 1..allocated halo (" +
+                                        std::to_string(f0->halo) + " cells)");
+    s->f[0]->xhalo = s->f[1]->xhalo = width;
+    s->vbound = bound;
+    return SK_OK;
+}
+
+int sk_state_vhalo_capacity(sk_state* s) { return s->f[0]->halo; }
+
 // step end + the local part of the cut-off decision (v-sharded phases)
 static sk_status enq_shard_step_end(sk_state* s) {
     sk_ctx* c = s->ctx;
@@ -1809,6 +1878,7 @@ static sk_status enq_shard_step_end(sk_state* s) {
 sk_status sk_state_phase(sk_state* s, int phase) {
     sk_ctx* c = s->ctx;
     CK(cudaSetDevice(c->device));
+    if (phase != 7) s->f[0]->flip_known = s->f[1]->flip_known = false;
     sk_status rc = SK_OK;
     switch (phase) {
         case 0: rc = enq_rho(s->f[0], s->f[1], s->rho); break;
@@ -1826,6 +1896,56 @@ sk_status sk_state_phase(sk_state* s, int phase) {
         case 5:  // post-limited shards: post V, x half sweep, post X, step end, check
             if (!(rc = enq_phase_b2(s))) rc = enq_shard_step_end(s);
             break;
+        case 6: {  // Poisson, v tables sizing this step's v-halo exchange (sk_state_vhalo_need)
+            if (!s->vneed_dev) return fail(SK_ERR_RUNTIME, "phase 6: not a v shard");
+            sk_field* fs[2] = {s->f[0], s->f[1]};
+            const sk_limiter* lim = &s->cfg.limiter;
+            if ((rc = mark(s, PH_POISSON)) || (rc = enq_poisson(c, s->rho, s->E, s->phi))) break;
+            if ((rc = mark(s, PH_VTAB)) || (rc = enq_vtab(fs, 2, s->E, s->cfg.dt, s->charge, s->sqrt_mu,
+                                                          lim->inline_sldg, lim->threshold, s->vneed_dev)))
+                break;
+            CK(cudaMemcpyAsync(s->vneed_host, s->vneed_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            for (int sp = 0; sp < 2; ++sp) {
+                s->f[sp]->flip_known = false;
+                CK(cudaMemcpyAsync(s->f[sp]->flip_pin, s->f[sp]->dflip, sizeof(int), cudaMemcpyDeviceToHost,
+                                   c->stream));
+            }
+            break;
+        }
+        case 7: {  // v sweep of the chunks that read no halo cell for shifts up to vbound
+            sk_field* fs[2] = {s->f[0], s->f[1]};
+            const sk_limiter* lim = &s->cfg.limiter;
+            const int n = fs[0]->nv, nch = (n + kVChunk - 1) / kVChunk;
+            const int lo = fs[0]->cell0 > 0 ? (s->vbound + kVChunk - 1) / kVChunk : 0;
+            const int hi = fs[0]->cell0 + n < fs[0]->nv_global ? (n - s->vbound) / kVChunk : nch;
+            if ((rc = mark(s, PH_V))) break;
+            rc = enq_vsweep(fs, 2, 0, lim->inline_sldg, lim->threshold, 0, lo, hi > lo ? hi - lo : -1, 1);
+            break;
+        }
+        case 8:    // the remaining v chunks after the halo exchange, then as phase 3 (or stop: post V)
+        case 9: {  // (9: every v chunk again -- the step's shift exceeded vbound)
+            sk_field* fs[2] = {s->f[0], s->f[1]};
+            fs[0]->flip_known = fs[1]->flip_known = false;
+            const sk_limiter* lim = &s->cfg.limiter;
+            const int n = fs[0]->nv, nch = (n + kVChunk - 1) / kVChunk;
+            int lo = fs[0]->cell0 > 0 ? (s->vbound + kVChunk - 1) / kVChunk : 0;
+            int hi = fs[0]->cell0 + n < fs[0]->nv_global ? (n - s->vbound) / kVChunk : nch;
+            if (hi < lo) hi = lo;
+            {
+                FixTimer ft(s, PH_V_FIX);
+                if (phase == 9) {
+                    rc = enq_vsweep(fs, 2, 0, lim->inline_sldg, lim->threshold, 0);
+                } else {
+                    rc = enq_vsweep(fs, 2, 0, lim->inline_sldg, lim->threshold, 0, 0, lo > 0 ? lo : -1, 3);
+                    if (!rc)
+                        rc = enq_vsweep(fs, 2, 0, lim->inline_sldg, lim->threshold, 0, hi, nch > hi ? nch - hi : -1,
+                                        2);
+                }
+            }
+            if (rc || (s->nranks > 1 && lim->indicator)) break;  // post limited: phase 5 continues
+            if (!(rc = enq_phase_b2(s))) rc = enq_shard_step_end(s);
+            break;
+        }
         case 4:  // shrink with the (all-reduced) decision in sk_state_shrink_flags_dev
             if (s->cfg.v_adjust) {
                 sk_field* fs[2] = {s->f[0], s->f[1]};

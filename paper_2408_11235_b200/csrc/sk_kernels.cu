@@ -1205,8 +1205,11 @@ __global__ void vtab_kernel(const __grid_constant__ VTabArgs a) {
     decompose_shift(speed, a.tau, dv, istar, alpha);
     double A[P * P], B[P * P];
     shift_matrices<P>(a.basis, alpha, A, B);
-    if ((a.halo_lo >= 0 && -istar > a.halo_lo) || (a.halo_hi >= 0 && istar + 1 > a.halo_hi))
+    if (a.halo_need) {  // the shard's exchange width is sized from this (sk_state_vhalo_need)
+        atomicMax(a.halo_need, max(-istar, istar + 1));
+    } else if ((a.halo_lo >= 0 && -istar > a.halo_lo) || (a.halo_hi >= 0 && istar + 1 > a.halo_hi)) {
         raise_error(a.st, 2, 5, max(-istar, istar + 1), max(a.halo_lo, a.halo_hi), a.st->step);
+    }
     double* t = a.tab[sp];
     const int n = a.nxd;
     t[xd] = (double)istar;
@@ -1267,7 +1270,7 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
     // share an x range (and its table rows, ~1/3 of the bytes a chunk reads)
     // run back to back -- chosen when the tables would not stay in L2
     const int xb = a.chunk_major ? blockIdx.y : blockIdx.x;
-    const int jb = a.chunk_major ? blockIdx.x : blockIdx.y;
+    const int jb = a.chunk0 + (a.chunk_major ? blockIdx.x : blockIdx.y);
     const int xd = xb * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
     const int j0 = jb * kVChunk;
@@ -3196,7 +3199,8 @@ static void launch_vsweep_f(const VSweepArgs& a, dim3 grid, cudaStream_t s) {
 }
 
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
-    const int nxb = (a.nxd + kVThreads - 1) / kVThreads, nch = (a.n + kVChunk - 1) / kVChunk;
+    const int nxb = (a.nxd + kVThreads - 1) / kVThreads;
+    const int nch = a.nchunks > 0 ? a.nchunks : (a.n + kVChunk - 1) / kVChunk;
     dim3 grid = a.chunk_major ? dim3(nch, nxb, a.nspecies) : dim3(nxb, nch, a.nspecies);
     if (a.periodic)
         SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, true, false><<<grid, kVThreads, 0, s>>>(a)))

@@ -96,6 +96,7 @@ struct VTabArgs {
     double threshold;
     DevStatus* st;
     int halo_lo, halo_hi;  // v-shard: max readable cells below/above (-1: wall)
+    int* halo_need;        // v-shard: max over x dofs of the cells read beyond the shard (atomicMax)
 };
 
 struct VSweepArgs {
@@ -121,6 +122,7 @@ struct VSweepArgs {
     unsigned long long* fix_list;
     unsigned int* fix_count;
     unsigned int fix_cap;
+    int chunk0, nchunks;  // v chunks [chunk0, chunk0 + nchunks) of kVChunk cells (nchunks 0: all)
 };
 
 struct RhoArgs {

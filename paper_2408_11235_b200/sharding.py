@@ -7,8 +7,11 @@ of each species for all x, plus `halo` cells below and above. Then
   * the charge density is a local partial (fused into the first x sweep)
     followed by an all-reduce(sum) of nx*(k+1) doubles;
   * the Poisson solve is replicated (every rank gets the same E);
-  * the v sweep reads `halo` cells from the neighbouring ranks, exchanged
-    point-to-point right after the first x sweep;
+  * the v sweep reads up to `halo` cells from the neighbouring ranks. The
+    exchange is sized per step from this step's E: the v tables (after the
+    replicated Poisson solve) record max |i*|+1 over the x dofs, and exactly
+    that many cells move point-to-point while the v chunks that read no halo
+    cell are already being swept (interior first, edges after the exchange);
   * the velocity cut-off (adaptivity.cpp:16-130, run.cpp:98-114): the ranks
     holding the probe cells decide locally, an all-reduce(MIN) of two ints
     makes the decision global, and on a shrink step each rank exchanges the
@@ -156,6 +159,8 @@ class ShardedState:
         from .solver import LimiterConfig
 
         self._post = LimiterConfig.parse(cfg.limiter).to_c().indicator != 0
+        self._vbound = int(L.sk_state_vhalo_capacity(h)) if nranks > 1 else 0
+        self.halo_widths = []  # exchanged v-halo cells per step (adaptive)
         # initial field: local moment (created) -> all-reduce -> Poisson
         self._reduce_rho()
         self._phase(1)
@@ -172,12 +177,13 @@ class ShardedState:
         allreduce_rho(self.rho, self.group)
         self.ctx.enter()
 
-    def _exchange(self, cells=None, species=(0, 1)):
+    def _exchange(self, cells=None, species=(0, 1), enter_leave=True):
         if self.plan.nranks == 1:
             return
         from .solver import _check
 
-        self.ctx.leave()
+        if enter_leave:
+            self.ctx.leave()
         for sp in species:
             f = self.f[sp]
             views = []
@@ -190,7 +196,8 @@ class ShardedState:
                         _check(N.lib().sk_field_halo_n(f.h, side, send, cells, C.byref(ptr), C.byref(cnt)))
                     views.append(_dev_tensor(ptr.value, cnt.value, self.device))
             exchange_halos(views[0], views[1], views[2], views[3], self.plan, self.group)
-        self.ctx.enter()
+        if enter_leave:
+            self.ctx.enter()
 
     def _cutoff(self):
         """run.cpp:98-114 across ranks: global decision, halo fill, shrink"""
@@ -215,17 +222,47 @@ class ShardedState:
         self._phase(4)
 
     def step(self):
-        """one run() loop body: x half sweep (+ local rho) | all-reduce rho,
-        halo exchange | Poisson, v sweep, x half sweep, step end, local cut-off
-        check | all-reduce decision, shrink halos | shrink"""
+        """one run() loop body: x half sweep (+ local rho) | all-reduce rho |
+        Poisson, v tables | [halo exchange of this step's width, overlapped
+        with the interior v chunks] | edge v chunks, x half sweep, step end,
+        local cut-off check | all-reduce decision, shrink halos | shrink"""
         self._phase(2)
         self._reduce_rho()
-        self._exchange()
-        self._phase(3)
+        if self.plan.nranks == 1:
+            self._phase(3)
+        else:
+            self._v_sweep_adaptive()
         if self._post and self.plan.nranks > 1:
             self._exchange(1)  # post limiter V reads one cell across each shard edge
             self._phase(5)
         self._cutoff()
+
+    def _v_sweep_adaptive(self):
+        import torch
+
+        from .solver import _check
+
+        L = N.lib()
+        self._phase(6)  # Poisson + v tables: this step's halo width -> pinned word
+        ev = torch.cuda.Event()
+        ev.record(self.ctx.stream)
+        self._phase(7)  # v chunks that read no halo cell (shifts <= bound), runs on
+        ev.synchronize()  # the library stream while the halos move below
+        need = C.c_int()
+        _check(L.sk_state_vhalo_need(self.h, C.byref(need)))
+        need = max(1, need.value)
+        cap = int(L.sk_state_vhalo_capacity(self.h))
+        width = min(need, cap)  # (need > cap: the v tables raised "insufficient v halo")
+        _check(L.sk_state_set_vhalo(self.h, width, self._vbound))
+        torch.cuda.current_stream(self.device).wait_event(ev)
+        self._exchange(enter_leave=False)
+        self.ctx.enter()
+        self._phase(8 if need <= self._vbound else 9)
+        self.halo_widths.append(width)
+        # interior bound of the next step: twice this step's width (E varies
+        # slowly from step to step; a faster change only costs a re-sweep)
+        self._vbound = min(cap, max(2 * need, need + 4))
+        _check(L.sk_state_set_vhalo(self.h, width, self._vbound))
 
     def close(self):
         if getattr(self, "h", None):
@@ -251,8 +288,11 @@ def bench_sharded(args, cfg, metric, unit, config):
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    # halo capacity: the exchanged width follows this step's E (adaptive, from
+    # the v tables); the capacity only bounds it -- |E| up to 2, or the
+    # cut-off's shrink halo (ceil(p nv / 2) + 3 cells) when that is wider
     dv = 2 * cfg.vmax_e / cfg.v_cells
-    halo = max(4, min(cfg.v_cells // world, halo_cells_needed(0.5, cfg.dt, dv)))
+    halo = max(4, min(cfg.v_cells // world, halo_cells_needed(2.0, cfg.dt, dv)))
     st = ShardedState(cfg, rank, world, halo=halo, device=local)
     st.ctx.set_eager_errors(False)
     for _ in range(args.warmup):
@@ -275,6 +315,23 @@ def bench_sharded(args, cfg, metric, unit, config):
     ms = torch.tensor([t0.elapsed_time(t1)], device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    widths = list(st.halo_widths[-args.steps:])
+    # second K-step window with per-phase CUDA events on every rank: the
+    # per-kernel durations behind the roofline (max over ranks per phase)
+    from .solver import _check
+
+    _check(N.lib().sk_state_set_phase_timing(st.h, 1))
+    nph = len(N.PHASES)
+    msa, cnt = (C.c_double * nph)(), (C.c_long * nph)()
+    _check(N.lib().sk_state_phase_times(st.h, msa, cnt, nph))  # clears
+    for _ in range(args.steps):
+        st.step()
+    st.ctx.synchronize()
+    _check(N.lib().sk_state_phase_times(st.h, msa, cnt, nph))
+    _check(N.lib().sk_state_set_phase_timing(st.h, 0))
+    ph = torch.tensor([msa[i] for i in range(nph)], device=f"cuda:{local}", dtype=torch.float64)
+    dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+    phases = {N.PHASES[i]: (float(ph[i]), int(cnt[i])) for i in range(nph) if cnt[i]}
     # e2e: every step moves this rank's shard host -> device and back
     e2e = None
     if not getattr(args, "no_e2e", False):
@@ -305,14 +362,36 @@ def bench_sharded(args, cfg, metric, unit, config):
         cfgd = dict(config)
         cfgd["parallelism"] = f"v-shard x{world} (halo {halo} cells, NCCL all-reduce + P2P)"
         cfgd["v_cutoff"] = "on (sharded: all-reduced decision, halo on shrink steps)" if cfg.v_adjust else "off"
+        cfgd["v_halo_exchanged_cells"] = {"max": max(widths) if widths else None,
+                                          "mean": sum(widths) / len(widths) if widths else None,
+                                          "capacity": int(N.lib().sk_state_vhalo_capacity(st.h))}
+        # dominant kernel: per-rank sweep over 1/world of the DoF, 16 B/DoF
+        sweeps = {"x_sweep_1", "x_sweep_2", "v_sweep"}
+        dom = max((k for k in phases if k in sweeps), key=lambda k: phases[k][0])
+        per_launch = phases[dom][0] / max(phases[dom][1], 1)
+        alg = bench.BYTES_PER_DOF_SWEEP * cfg.dof_total / world
+        achieved = alg / (per_launch / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "profiles", "ncu_traffic.json")) as f:
+                t = json.load(f).get(getattr(args, "config", ""), {}).get(dom)
+            traffic = t / world if t else None  # (single-GPU capture; a shard moves 1/world of it)
+        except Exception:
+            pass
         line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (blob initial condition, run.cpp:41-46)",
                 "config": cfgd,
-                "roofline": {"bound": "hbm", "kernel": "whole step (48 B/DoF)", "achieved": step_gbs,
-                             "peak": peak * world, "peak_kind": peak_kind, "unit": "GB/s",
-                             "frac": step_gbs / (peak * world), "traffic": None},
+                "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                             "traffic": traffic, "alg_bytes_per_launch": alg, "ms_per_launch": per_launch,
+                             "step_achieved_gbs": step_gbs, "step_peak_gbs": peak * world,
+                             "step_frac": step_gbs / (peak * world),
+                             "timing": "kernel ms: per-phase CUDA events over a second K-step window, "
+                                       "max over ranks; achieved per GPU"},
+                "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
                 "gpu_launches": launches, "clocks": clk}
         if e2e:
             line["e2e"] = e2e

@@ -571,13 +571,18 @@ def test_cpp_mirror_runs_against_oracle():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("adaptive", [False, True], ids=["fixed_halo", "adaptive_halo"])
 @pytest.mark.parametrize("v_adjust,limiter", [(False, "sldg"), (True, "sldg"), (True, "minmod+line")],
                          ids=["no_cutoff", "cutoff", "cutoff_post"])
-def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust, limiter):
+def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust, limiter, adaptive):
     """The CUDA v-shard path (global cell offsets in the x tables, halo reads in
     the v sweep, local fused charge density, sharded velocity cut-off) driven
     like two ranks, with the all-reduces and the halo exchanges done by device
-    copies in one process; 12 run() loop bodies cover two shrink events."""
+    copies in one process; 12 run() loop bodies cover two shrink events.
+    adaptive: phases 6-9 -- the exchange width from this step's E (v tables),
+    interior v chunks swept before the exchange, the edges after; the
+    interior bound alternates between the last width + 1 and 1, and every
+    third step re-sweeps all chunks (phase 9)."""
     import ctypes as C
 
     import torch
@@ -640,7 +645,8 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust, limiter):
     for ctx, h, *_ in shards:
         _check(L.sk_state_phase(h, 1))
     shrinks = 0
-    for _ in range(12):
+    last_need, widths, resweeps = 1, set(), 0
+    for step in range(12):
         if v_adjust:
             ref.run_step()
         else:
@@ -648,9 +654,32 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust, limiter):
         for ctx, h, *_ in shards:
             _check(L.sk_state_phase(h, 2))
         reduce_rho()
-        exchange()
-        for ctx, h, *_ in shards:
-            _check(L.sk_state_phase(h, 3))
+        if not adaptive:
+            exchange()
+            for ctx, h, *_ in shards:
+                _check(L.sk_state_phase(h, 3))
+        else:
+            bound = 1 if step % 2 else last_need + 1
+            for ctx, h, *_ in shards:
+                _check(L.sk_state_set_vhalo(h, 1, bound))
+                _check(L.sk_state_phase(h, 6))
+                _check(L.sk_state_phase(h, 7))
+            sync()
+            needs = []
+            for ctx, h, *_ in shards:
+                nd = C.c_int()
+                _check(L.sk_state_vhalo_need(h, C.byref(nd)))
+                needs.append(nd.value)
+            assert needs[0] == needs[1] >= 1  # E is replicated: the same width on both sides
+            last_need = needs[0]
+            widths.add(last_need)
+            for ctx, h, *_ in shards:
+                _check(L.sk_state_set_vhalo(h, last_need, bound))
+            exchange()
+            resweep = last_need > bound or step % 3 == 2  # (also on purpose: phase 9 is exact too)
+            for ctx, h, *_ in shards:
+                _check(L.sk_state_phase(h, 9 if resweep else 8))
+            resweeps += resweep
         if post:  # post limiter V reads one cell across the shard edge
             exchange(1)
             for ctx, h, *_ in shards:
@@ -668,6 +697,8 @@ def test_two_v_shards_on_one_gpu_match_unsharded(sk, v_adjust, limiter):
                     _check(L.sk_state_phase(h, 4))
     if v_adjust:
         assert shrinks >= 2
+    if adaptive:
+        assert resweeps >= 1 and max(widths) < halo, (widths, resweeps)
     for sp in (0, 1):
         parts = []
         for ctx, h, _, plan, _ in shards:
