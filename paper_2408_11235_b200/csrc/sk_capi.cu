@@ -399,9 +399,12 @@ sk_status ensure_xghost(sk_ctx* c, int nlines) {
 // alternative of a fusable step boundary); swap = false: the buffers' roles
 // were already exchanged for the boundary; fused_reduce: also reduce the
 // partials of the other alternative (the fused sweep) under the inverse gate
+// src / src_mode: the injection source half step fused into this sweep
+// (XSweepArgs::src_mode: 1 on the sources read, 2 on the outputs)
 sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
                      int check_finite, double* rho_out = nullptr, const int* gate = nullptr, int gate_on = 0,
-                     bool swap = true, bool fused_reduce = false) {
+                     bool swap = true, bool fused_reduce = false, const sk_state* src = nullptr,
+                     int src_mode = 0) {
     sk_ctx* c = fs[0]->ctx;
     XSweepArgs a{};
     a.basis = c->basis;
@@ -433,6 +436,14 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.fix_cap = c->fix_cap;
     a.gate = gate;
     a.gate_on = gate_on;
+    if (src && src_mode) {
+        a.src_mode = src_mode;
+        a.src_gx = src->src_gx;
+        a.src_gv[0] = src->src_gv[0];
+        a.src_gv[1] = src->src_gv[1];
+        a.src_half = 0.5 * src->cfg.dt;
+        a.src_t0 = src->cfg.t0;
+    }
     if (rho_out) {  // fused charge density (both species in this launch)
         a.rho_fuse = 1;
         for (int i = 0; i < nspecies; ++i) {
@@ -1732,6 +1743,14 @@ bool fusable(const sk_state* s) {
            s->cfg.scenario != 1 && c->grid.nclass == 1 && s->nranks == 1 && xsweep_fused_supported(c->P);
 }
 
+// the injection source rides in the x sweeps (XSweepArgs::src_mode); the
+// 3-block ghosts across a dx jump are transferred from neighbour cells with
+// the source added, as the reference transfers them after its source pass
+bool source_fusable(const sk_state* s) {
+    static const bool off = getenv("SK_SOURCE_SEPARATE") != nullptr;
+    return !off && s->cfg.scenario == 1;
+}
+
 // phase A: x tables + first x half sweep (+ fused local charge density).
 // fuse_in: the previous body ended at a fusable boundary (enq_fused_boundary):
 // this sweep is its unfused alternative
@@ -1744,8 +1763,11 @@ sk_status enq_phase_a(sk_state* s, bool fuse_in = false) {
     sk_field* fs[2] = {s->f[0], s->f[1]};
     sk_status rc;
     const bool post = lim->indicator != 0;
-    // stepper.cpp:68-72 (injection): source half step at state.time
-    if ((rc = enq_source(s, 0))) return rc;
+    // stepper.cpp:68-72 (injection): source half step at state.time -- fused
+    // into the first x sweep's reads on grids without dx jumps (no transferred
+    // ghosts to which it would have to be applied before the transfer)
+    const int src1 = source_fusable(s) ? 1 : 0;
+    if (!src1 && (rc = enq_source(s, 0))) return rc;
     // x tables serve both x half-sweeps (same tau, same v grid within a step)
     if ((rc = mark(s, PH_XTAB)) || (rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1)))
         return rc;
@@ -1759,7 +1781,8 @@ sk_status enq_phase_a(sk_state* s, bool fuse_in = false) {
             if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0, s->rho, &c->st->fuse_ok, 0, false, true))) return rc;
             CK(launch_flip_toggle(c->st, fs[0]->dflip, fs[1]->dflip, c->stream));
             c->launches += 1;
-        } else if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr))) {
+        } else if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr, nullptr, 0, true, false, s,
+                                    src1))) {
             return rc;
         }
     }
@@ -1798,14 +1821,18 @@ sk_status enq_phase_b2(sk_state* s, bool fuse_out = false) {
     sk_status rc;
     const bool post = lim->indicator != 0;
     if (post && ((rc = mark(s, PH_POST_V)) || (rc = enq_post(fs, 2, SK_DIR_V, lim, 0)))) return rc;
+    // stepper.cpp:93-97 (injection): source half step at state.time + half --
+    // fused into the second x sweep's stores unless a post limiter runs between
+    const int src2 = !post && source_fusable(s) ? 2 : 0;
     {
         FixTimer ft(s, PH_X2_FIX);
         if ((rc = mark(s, PH_X2))) return rc;
-        if ((rc = fuse_out ? enq_fused_boundary(s, inl, thr) : enq_xsweep(fs, 2, 0, inl, thr, 1))) return rc;
+        if ((rc = fuse_out ? enq_fused_boundary(s, inl, thr)
+                           : enq_xsweep(fs, 2, 0, inl, thr, 1, nullptr, nullptr, 0, true, false, s, src2)))
+            return rc;
     }
     if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
-    // stepper.cpp:93-97 (injection): source half step at state.time + half
-    return enq_source(s, 1);
+    return src2 ? SK_OK : enq_source(s, 1);
 }
 
 sk_status enq_phase_b(sk_state* s, bool fuse_out = false) {

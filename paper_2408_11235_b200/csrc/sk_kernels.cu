@@ -275,11 +275,54 @@ __global__ void xtab_kernel(const __grid_constant__ XTabArgs a) {
     }
 }
 
+// Injection source half step of one x line (stepper.cpp:29-42, run.cpp:47-53):
+// f += 0.5 half (S(t) + S(t + half)), S = H(t0 - t) blob(x, v) / t0, with the
+// blob's x and v factors from host libm tables (source_kernel's arithmetic).
+// t: the half step's start (state.time, or state.time + half for the second)
+struct LineSource {
+    bool on;
+    double gv, w, t, t2, t0;
+    const double* gx;
+};
+__device__ __forceinline__ LineSource line_source(const XSweepArgs& a, int sp, int line, int mode) {
+    LineSource s{};
+    if (a.src_mode != mode) return s;
+    const double t = mode == 2 ? a.st->time + a.src_half : a.st->time;
+    if (!(t <= a.src_t0)) return s;  // SourceTerm::active (stepper.hpp:19-21)
+    const int lev = a.st->shrink_count[sp];
+    if (lev >= kSourceLevels) {  // (as source_kernel)
+        raise_error(a.st, 1, 7, lev, kSourceLevels, a.st->step);
+        return s;
+    }
+    s.on = true;
+    s.gv = a.src_gv[sp][(long long)lev * a.nlines + line];
+    s.w = 0.5 * a.src_half;
+    s.t = t;
+    s.t2 = t + a.src_half;
+    s.t0 = a.src_t0;
+    s.gx = a.src_gx;
+    return s;
+}
+// u (the P nodes of global x cell xc) += the source increment, bitwise source_kernel
+template <int P>
+__device__ __forceinline__ void add_source(const LineSource& s, int xc, double* u) {
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        const double blob = s.gx[xc * P + n] * s.gv;
+        const double s1 = s.t > s.t0 ? 0.0 : blob / s.t0;
+        const double s2 = s.t2 > s.t0 ? 0.0 : blob / s.t0;
+        u[n] = u[n] + s.w * (s1 + s2);
+    }
+}
+
 // ghost cell value for block-local cell s outside [0, cells_b) (fill_ghost,
 // adaptivity.cpp:169-207): copy / coarse_to_fine piece / fine_to_coarse.
+// src (the first injection source half step, if on): the reference adds it
+// to every cell before the ghosts are transferred -- added to each
+// neighbour cell value read, in the same rounding
 template <int P, int MC = 0>
 __device__ double x_fetch_outside(const Basis& basis, const Grid& g, const double* line, int b,
-                                  int s, int n) {
+                                  int s, int n, const LineSource* src = nullptr) {
     const bool left = s < 0;
     int nb, j;
     if (left) {
@@ -293,10 +336,18 @@ __device__ double x_fetch_outside(const Basis& basis, const Grid& g, const doubl
     }
     const int iface = left ? g.start[b] : g.start[b] + g.cells[b];
     const int nb_begin = g.start[nb], nb_end = nb_begin + g.cells[nb];
+    const bool ws = src != nullptr && src->on;
     if (g.dx[nb] == g.dx[b]) {
-        int src = left ? iface - j : iface + (j - 1);
-        if (src < nb_begin || src >= nb_end) return 0.0;
-        return line[(long long)src * P + n];
+        int sc = left ? iface - j : iface + (j - 1);
+        if (sc < nb_begin || sc >= nb_end) return 0.0;
+        if (ws) {
+            double u[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) u[q] = line[(long long)sc * P + q];
+            add_source<P>(*src, sc, u);
+            return u[n];
+        }
+        return line[(long long)sc * P + n];
     }
     if (g.dx[nb] > g.dx[b]) {
         const int m = MC > 0 ? MC : (int)llround(g.dx[nb] / g.dx[b]);
@@ -306,11 +357,28 @@ __device__ double x_fetch_outside(const Basis& basis, const Grid& g, const doubl
         double u[P];
 #pragma unroll
         for (int q = 0; q < P; ++q) u[q] = line[(long long)coarse * P + q];
+        if (ws) add_source<P>(*src, coarse, u);
         return coarse_to_fine_node<P, MC>(basis, u, m, piece, n);
     }
     const int m = MC > 0 ? MC : (int)llround(g.dx[b] / g.dx[nb]);
     int lo = left ? iface - j * m : iface + (j - 1) * m;
     if (lo < nb_begin || lo + m > nb_end) return 0.0;
+    if (ws) {  // fine_to_coarse_node's arithmetic on the cells with the source added
+        double acc = 0.0;
+#pragma unroll (MC > 0 ? MC : 1)
+        for (int jj = 0; jj < m; ++jj) {
+            double u[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) u[q] = line[(long long)(lo + jj) * P + q];
+            add_source<P>(*src, lo + jj, u);
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                double xi_c = (jj + basis.nodes[q]) / m;
+                acc += basis.weights[q] / m * u[q] * lagrange<P>(basis, n, xi_c);
+            }
+        }
+        return acc / basis.weights[n];
+    }
     return fine_to_coarse_node<P, MC>(basis, line + (long long)lo * P, m, n);
 }
 
@@ -451,6 +519,7 @@ __global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ 
     const int m = rmax == rmin ? rmax : 0;
     const double* src = (field_flipped(a.flip[sp]) ? a.dst[sp] : a.src[sp]) + (long long)line * g.ncells * P;
     double* out = a.ghost + (long long)(sp * a.nlines + line) * nb * a.ghost_cap * P;
+    const LineSource lsrc = line_source(a, sp, line, 1);  // (first injection half step, if fused)
     auto fill = [&](auto mc) {
         constexpr int MC = decltype(mc)::value;
         for (int e = lane; e < total; e += 32) {
@@ -465,7 +534,7 @@ __global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ 
             const int l = e - base;
             const int j = l / P + 1, n = l - (l / P) * P;
             out[(long long)b * a.ghost_cap * P + l] =
-                x_fetch_outside<P, MC>(a.basis, g, src, b, sg == 0 ? -j : g.cells[b] - 1 + j, n);
+                x_fetch_outside<P, MC>(a.basis, g, src, b, sg == 0 ? -j : g.cells[b] - 1 + j, n, &lsrc);
         }
     };
     switch (m) {  // the usual refinement ratios unrolled; others at run time
@@ -772,7 +841,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                                 cp_async8(w + e, gh + (j - 1) * P + n, true);
                                 anyc = true;
                             } else {
-                                w[e] = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n);
+                                const LineSource lsrc = line_source(a, x.sp, x.line, 1);
+                                w[e] = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n, &lsrc);
                             }
                         }
                         if (anyc) mbar_cp_async_arrive(&full[stg]);
@@ -1080,6 +1150,20 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 lds_cell_w<P>(win + c * P, ul[cc]);
                 lds_cell_w<P>(win + (c + 1) * P, ur[cc]);
             }
+            if (a.src_mode == 1) {  // the step's first source half step, on the cells as read
+                const LineSource src = line_source(a, sp, line, 1);
+                if (src.on) {
+                    // raw line cells only (ghosts across a dx jump arrive with it)
+                    int vlo, vhi;
+                    xvalid_range(a, b, vlo, vhi);
+#pragma unroll
+                    for (int cc = 0; cc < NCC; ++cc) {
+                        const int wl = s0 + min(tid + cc * C::NT, nt - 1);  // block-local window cell c
+                        if (wl >= vlo && wl < vhi) add_source<P>(src, g.start[b] + wl, ul[cc]);
+                        if (wl + 1 >= vlo && wl + 1 < vhi) add_source<P>(src, g.start[b] + wl + 1, ur[cc]);
+                    }
+                }
+            }
             // advection.cpp:95-101, both cells share each broadcast matrix load
 #pragma unroll
             for (int m = 0; m < P; ++m) {
@@ -1135,6 +1219,17 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             // troubled cells are queued for the fixup kernel (on overflow it rescans)
             if constexpr (INLINE) wq_push<NCC>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry);
             double* dline = dstp(sp) + lbase + (long long)(g.start[b] + c0) * P;
+            if (a.src_mode == 2) {  // the step's second source half step, on the outputs; a troubled
+                const LineSource src = line_source(a, sp, line, 2);  // cell gets it after its clamp (xfix)
+                if (src.on)
+#pragma unroll
+                    for (int cc = 0; cc < NCC; ++cc) {
+                        const int c = tid + cc * C::NT;
+                        bool troubled = false;
+                        if constexpr (INLINE) troubled = tr[cc];
+                        if (c < nt && !troubled) add_source<P>(src, g.start[b] + c0 + c, o[cc]);
+                    }
+            }
 #pragma unroll
             for (int cc = 0; cc < NCC; ++cc) {
                 const int c = tid + cc * C::NT;
@@ -1408,8 +1503,8 @@ __device__ __forceinline__ bool rescan_indicator(const Basis& b, double thr, int
 // out-of-line ghost fetch for the fixup kernels (keeps their code small)
 template <int P>
 __device__ __noinline__ double x_fetch_outside_ool(const Basis& basis, const Grid& g, const double* line,
-                                                   int b, int s, int n) {
-    return x_fetch_outside<P>(basis, g, line, b, s, n);
+                                                   int b, int s, int n, const LineSource* src = nullptr) {
+    return x_fetch_outside<P>(basis, g, line, b, s, n, src);
 }
 
 template <int P, bool FMA>
@@ -1426,6 +1521,8 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
     const long long lbase = (long long)line * g.ncells * P;
     const bool flipped = field_flipped(a.flip[sp]);
     const double* src = (flipped ? a.dst[sp] : a.src[sp]) + lbase;
+    // the sweep read its sources with the first injection half step added (if fused)
+    const LineSource src1 = line_source(a, sp, line, 1);
     double uu[2][P];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1435,15 +1532,19 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
             const double* cp = src + (long long)(g.start[b] + ss) * P;
 #pragma unroll
             for (int q = 0; q < P; ++q) uu[h][q] = cp[q];
+            if (src1.on) add_source<P>(src1, g.start[b] + ss, uu[h]);
         } else {
 #pragma unroll
-            for (int q = 0; q < P; ++q) uu[h][q] = x_fetch_outside_ool<P>(a.basis, g, src, b, s, q);
+            for (int q = 0; q < P; ++q) uu[h][q] = x_fetch_outside_ool<P>(a.basis, g, src, b, s, q, &src1);
         }
     }
+    const LineSource src2 = line_source(a, sp, line, 2);
     double* up = (flipped ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + lbase + (long long)cell * P;
     double o[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) o[q] = up[q];
+    if (rescan && src2.on)  // untroubled cells hold projection + source: recompute the projection
+        project_cell_f<P, FMA>(row + 2, row + 2 + P * P, uu[0], uu[1], o);  // (the sweep's arithmetic)
     if (rescan && !rescan_indicator<P>(a.basis, a.threshold, a.fma, row + 2 + 2 * P * P,
                                        row + 2 + 2 * P * P + P, uu[0], uu[1], o))
         return;
@@ -1451,8 +1552,12 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
 #pragma unroll
     for (int q = 0; q < P; ++q) o0[q] = o[q];
     const int fl = inline_clamp_f<P, FMA>(a.basis, alpha, uu[0], uu[1], o);
+    double os[P];  // stored: with the second source half step after the clamp
 #pragma unroll
-    for (int q = 0; q < P; ++q) up[q] = o[q];
+    for (int q = 0; q < P; ++q) os[q] = o[q];
+    if (src2.on) add_source<P>(src2, cell, os);
+#pragma unroll
+    for (int q = 0; q < P; ++q) up[q] = os[q];
     if (a.rho_fuse && (fl & 2)) {  // the fused moment summed the unclamped values
         const int vn = line - (line / P) * P;
         const double wdv = a.charge_w[sp] * a.basis.weights[vn] * a.vg[sp]->dx;

@@ -79,6 +79,15 @@ struct XSweepArgs {
     // runs only if (*gate != 0) == gate_on; gate == nullptr: always
     const int* gate;
     int gate_on;
+    // injection source half step (stepper.cpp:29-42) fused into
+    // the sweep: 1 = added to the source cells as they are read (the half step
+    // at state.time before the first x sweep, stepper.cpp:68-72), 2 = added to
+    // the outputs (at state.time + half after the second, stepper.cpp:93-97);
+    // the fixup kernel applies it the same way to the cells it reloads / clamps
+    int src_mode;
+    const double* src_gx;      // [nxd] x factor of the source blob
+    const double* src_gv[2];   // [kSourceLevels][nlines] v factor per v-grid level
+    double src_half, src_t0;
 };
 
 struct VTabArgs {

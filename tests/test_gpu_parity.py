@@ -330,14 +330,20 @@ def test_exact_mode_trajectory_bitwise(sk, ora, name):
     assert gs == os_
 
 
-@pytest.mark.parametrize("limiter", ["sldg", "minmod+line", "meanerr+simple"])
+@pytest.mark.parametrize("limiter", ["sldg", "minmod+line", "meanerr+simple", "sldg_injection"])
 def test_deferred_clamp_overflow_rescan_is_identical(sk, limiter):
     """troubled (sLdG) / flagged (post limiter) cells are queued for a fixup
     kernel; when the queue overflows the fixup rescans the pass -- both paths
-    must give the same bits"""
+    must give the same bits. sldg_injection: the source half steps fused into
+    the x sweeps (the rescan recomputes what a queued cell would have held)"""
     from paper_2408_11235_b200 import _native as N
 
-    cfg = cfg_of(sk, k=2, nf=16, nc=16, m=8, nv=32, limiter=limiter)
+    if limiter == "sldg_injection":
+        cfg = cfg_of(sk, k=3, nf=16, nc=32, m=1, nv=32, limiter="sldg", scenario="injection", t0=0.45,
+                     mu=1836.0)
+        limiter = "sldg"
+    else:
+        cfg = cfg_of(sk, k=2, nf=16, nc=16, m=8, nv=32, limiter=limiter)
     a, b = sk.SimulationState(cfg), sk.SimulationState(cfg)
     assert N.lib().sk_ctx_set_fix_capacity(b.ctx.h, 7) == 0  # forces overflow
     for _ in range(6):
@@ -347,7 +353,7 @@ def test_deferred_clamp_overflow_rescan_is_identical(sk, limiter):
         assert np.array_equal(a.field(sp).download(), b.field(sp).download())
     st = a.stats()
     assert st == b.stats()
-    assert (st["inline_troubled"] if limiter == "sldg" else st["post_troubled"]) > 1000
+    assert (st["inline_troubled"] if limiter == "sldg" else st["post_troubled"]) > 300
 
 
 def test_graph_replay_equals_eager(sk):
@@ -768,20 +774,38 @@ def test_sharded_state_one_rank_matches_run_steps(sk):
 @pytest.mark.parametrize("kw", [
     dict(k=2, nf=8, nc=16, m=2, nv=32, limiter="sldg", scenario="injection", t0=0.35),
     dict(k=3, nf=16, nc=32, m=1, nv=48, mu=1836.0, limiter="sldg", scenario="injection", t0=1.05),
-    dict(k=3, nf=6, nc=12, m=1, nv=24, mu=1836.0, limiter="minmod+line", scenario="injection", t0=0.8)],
-    ids=["k2_m2", "k3_mu1836", "k3_post"])
-def test_injection_scenario(sk, ora, kw, exact):
+    dict(k=3, nf=6, nc=12, m=1, nv=24, mu=1836.0, limiter="minmod+line", scenario="injection", t0=0.8),
+    dict(k=2, nf=8, nc=16, m=8, nv=32, limiter="sldg", scenario="injection", t0=0.35, ghost_cap=1)],
+    ids=["k2_m2", "k3_mu1836", "k3_post", "k2_m8_ghosts_in_kernel"])
+def test_injection_scenario(sk, ora, kw, exact, monkeypatch):
     """§8f N2: the injection source half steps on the device (host exp tables
     per v-grid level) -- bitwise trajectories in exact mode, 1e-12 in fast
-    mode -- across the source window's end and velocity shrinks"""
+    mode -- across the source window's end and velocity shrinks. Both half
+    steps ride in the x sweeps (first: added to the cells as read, in the sweep,
+    its fixup and the transferred 3-block ghosts; second: added to the outputs,
+    after the clamp for troubled cells); k3_post keeps the second one separate
+    (post X runs between)."""
+    import dataclasses
+
+    kw = dict(kw)
+    if "ghost_cap" in kw:  # 3-block ghosts beyond the pre-pass buffer: evaluated in the sweep
+        monkeypatch.setenv("SK_XGHOST_CAP", str(kw.pop("ghost_cap")))
     cfg = cfg_of(sk, **kw)
     o = ora.state(**cfg.oracle_kwargs())
     st = sk.SimulationState(cfg, exact=exact)
     for sp in (0, 1):
         assert not st.field(sp).download().any()
+    # the fused path launches no separate source kernels: as many kernels per
+    # loop body as the blob scenario on the same grid (one more with a post limiter)
+    blob = sk.SimulationState(dataclasses.replace(cfg, scenario="blob"), exact=exact)
+    l0, b0 = st.launches(), blob.launches()
+    blob.run_step()
     for s in range(14):
         o.step()
         st.run_step()
+        if s == 0:
+            extra = (st.launches() - l0) - (blob.launches() - b0)
+            assert extra == (1 if "+" in kw["limiter"] else 0), extra
         for sp in (0, 1):
             got, want = st.field(sp).download(), o.field(sp)
             if exact:
