@@ -603,8 +603,10 @@ struct XCfg {
     static constexpr int STAGE3 = ((WIN3 + NF + HDR + 1) / 2) * 2;
     static constexpr size_t SMEM3 = sizeof(double) * (size_t)(S3 * STAGE3 + 2 * (T + 1) * P + 2 * (NF + 2)) +
                                     8 * 2 * S3 + 8 * NC * kQCap + sizeof(int) * (2 * (T + 1) + 4);
+    // MODE 1/2 (post-limiter flag passes): full T-cell tiles with a T + 2 cell window
+    static constexpr size_t SMEM12 = sizeof(double) * (size_t)(S * STAGE3) + 8 * 2 * S + 8 * NC * kQCap;
     template <int MODE>
-    static constexpr size_t smem() { return MODE == 3 ? SMEM3 : SMEM; }
+    static constexpr size_t smem() { return MODE == 3 ? SMEM3 : (MODE == 1 || MODE == 2) ? SMEM12 : SMEM; }
 };
 
 struct XTile {
@@ -725,11 +727,13 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     static_assert(MODE == 0 || MODE == 3 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
     static_assert(MODE != 3 || C::T == 2 * C::NT, "MODE 3: T + 1 intermediate cells over 3 passes of the consumers");
     if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;  // device-decided alternative
-    // cells per tile: the flag passes' windows need one cell each side; MODE 3
-    // keeps T (its stage holds a T + 2 cell window) so block sizes divide evenly
-    constexpr int TT = (MODE == 1 || MODE == 2) ? C::T - 1 : C::T;
-    constexpr int WIN = MODE == 3 ? C::WIN3 : C::WIN;
-    constexpr int STAGE = MODE == 3 ? C::STAGE3 : C::STAGE;
+    // cells per tile: T in every mode -- the flag passes (one neighbour cell
+    // each side) and MODE 3 (two shifts) stage a T + 2 cell window instead of
+    // shortening the tile, so power-of-two blocks split into full tiles (511-
+    // cell tiles left 1-2 cell remainder tiles in most lines)
+    constexpr int TT = C::T;
+    constexpr int WIN = MODE == 0 ? C::WIN : C::WIN3;
+    constexpr int STAGE = MODE == 0 ? C::STAGE : C::STAGE3;
     constexpr int WX = MODE >= 1 ? 2 : 1;            // window cells beyond the tile
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;                                   // S x STAGE
@@ -3087,7 +3091,7 @@ static cudaError_t configure_xsweep() {
 template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
 static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out) {
     using Cf = XCfg<P>;
-    constexpr int TT = (MODE == 1 || MODE == 2) ? Cf::T - 1 : Cf::T;
+    constexpr int TT = Cf::T;
     if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA, MODE>()) return e;
     b = a;
     b.tile_start[0] = 0;
@@ -3568,10 +3572,14 @@ static cudaError_t launch_post_x_t(const PostArgs& a, cudaStream_t s) {
     int grid = 0;
     if (a.cfg.indicator == 1) {
         if (cudaError_t e = xsweep_plan<P, false, false, FAST, 1>(x, b, grid)) return e;
-        if (grid > 0) xsweep_kernel<P, false, false, FAST, 1><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
+        if (grid > 0)
+            xsweep_kernel<P, false, false, FAST, 1>
+                <<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<1>(), s>>>(b);
     } else {
         if (cudaError_t e = xsweep_plan<P, false, false, FAST, 2>(x, b, grid)) return e;
-        if (grid > 0) xsweep_kernel<P, false, false, FAST, 2><<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::SMEM, s>>>(b);
+        if (grid > 0)
+            xsweep_kernel<P, false, false, FAST, 2>
+                <<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<2>(), s>>>(b);
     }
     launch_post_tail<P, 0, FAST>(a, s);
     return cudaGetLastError();
