@@ -712,7 +712,10 @@ __device__ __forceinline__ void stg_cell(double* dp, const double* o) {
 // window = the tile's cells and one neighbour on each side (tiles of T-1
 // cells), no table row, the indicator per cell, flagged cells queued; in place
 // (nothing stored). MODE 3: two consecutive x half sweeps fused (fused_tile).
-template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
+// SRC (MODE 0): the injection source half step fused into this sweep, 1 on the
+// cells read, 2 on the outputs (XSweepArgs::src_mode); a template argument so
+// the plain sweeps carry none of its registers
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0, int SRC = 0>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
     using C = XCfg<P>;
@@ -845,8 +848,12 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                                 cp_async8(w + e, gh + (j - 1) * P + n, true);
                                 anyc = true;
                             } else {
-                                const LineSource lsrc = line_source(a, x.sp, x.line, 1);
-                                w[e] = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n, &lsrc);
+                                if constexpr (SRC == 1) {
+                                    const LineSource lsrc = line_source(a, x.sp, x.line, 1);
+                                    w[e] = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n, &lsrc);
+                                } else {
+                                    w[e] = x_fetch_outside<P>(a.basis, g, src, x.b, sc, n);
+                                }
                             }
                         }
                         if (anyc) mbar_cp_async_arrive(&full[stg]);
@@ -1154,7 +1161,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                 lds_cell_w<P>(win + c * P, ul[cc]);
                 lds_cell_w<P>(win + (c + 1) * P, ur[cc]);
             }
-            if (a.src_mode == 1) {  // the step's first source half step, on the cells as read
+            if constexpr (SRC == 1) {  // the step's first source half step, on the cells as read
                 const LineSource src = line_source(a, sp, line, 1);
                 if (src.on) {
                     // raw line cells only (ghosts across a dx jump arrive with it)
@@ -1223,7 +1230,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             // troubled cells are queued for the fixup kernel (on overflow it rescans)
             if constexpr (INLINE) wq_push<NCC>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry);
             double* dline = dstp(sp) + lbase + (long long)(g.start[b] + c0) * P;
-            if (a.src_mode == 2) {  // the step's second source half step, on the outputs; a troubled
+            if constexpr (SRC == 2) {  // the step's second source half step, on the outputs; a troubled
                 const LineSource src = line_source(a, sp, line, 2);  // cell gets it after its clamp (xfix)
                 if (src.on)
 #pragma unroll
@@ -3065,19 +3072,19 @@ static int sm_count() {
 template <int P>
 constexpr bool kHasFma = kHasFmaDev<P>;
 
-template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0, int SRC = 0>
 static cudaError_t configure_xsweep() {
     using Cf = XCfg<P>;
     static unsigned configured = 0;  // per-device bit
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured & (1u << (dev & 31)))) {
-        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
+        cudaError_t e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE, SRC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)Cf::template smem<MODE>());
         if (e != cudaSuccess) return e;
         // full shared-memory carveout so two pipelines share each SM
-        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
+        e = cudaFuncSetAttribute(xsweep_kernel<P, INLINE, RHO, FMA, MODE, SRC>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         configured |= 1u << (dev & 31);
@@ -3088,11 +3095,15 @@ static cudaError_t configure_xsweep() {
 // persistent grid of one x-sweep variant: resident CTAs, and for the fused
 // moment a multiple of the tiles per line (each CTA then always sees the same
 // tile column, so the per-group partial rows sum in a fixed order)
-template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
+// (the grid is sized from the SRC = 0 variant, so a source-fused sweep lays out
+// the fused-moment partials exactly like xsweep_rho_groups expects)
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0, int SRC = 0>
 static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out) {
     using Cf = XCfg<P>;
     constexpr int TT = Cf::T;
-    if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA, MODE>()) return e;
+    if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA, MODE, SRC>()) return e;
+    if (SRC != 0)
+        if (cudaError_t e = configure_xsweep<P, INLINE, RHO, FMA, MODE, 0>()) return e;
     b = a;
     b.tile_start[0] = 0;
     for (int i = 0; i < a.grid.nblocks; ++i)
@@ -3100,7 +3111,7 @@ static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out
     const int ntl = b.tile_start[a.grid.nblocks];
     const long long ntot = (long long)a.nspecies * a.nlines * ntl;
     int blocks_per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO, FMA, MODE>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, xsweep_kernel<P, INLINE, RHO, FMA, MODE, 0>,
                                                   (Cf::NC + 1) * 32, Cf::template smem<MODE>());
     long long grid = (long long)sm_count() * (blocks_per_sm > 0 ? blocks_per_sm : 1);
     if (RHO) {
@@ -3113,12 +3124,12 @@ static cudaError_t xsweep_plan(const XSweepArgs& a, XSweepArgs& b, int& grid_out
     return cudaSuccess;
 }
 
-template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0>
+template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0, int SRC = 0>
 static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     XSweepArgs b;
     int grid = 0;
-    if (cudaError_t e = xsweep_plan<P, INLINE, RHO, FMA, MODE>(a, b, grid)) return e;
-    xsweep_kernel<P, INLINE, RHO, FMA, MODE>
+    if (cudaError_t e = xsweep_plan<P, INLINE, RHO, FMA, MODE, SRC>(a, b, grid)) return e;
+    xsweep_kernel<P, INLINE, RHO, FMA, MODE, SRC>
         <<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<MODE>(), s>>>(b);
     return cudaGetLastError();
 }
@@ -3136,11 +3147,18 @@ cudaError_t launch_xghost(const XSweepArgs& a, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
+template <int P, bool INLINE, bool RHO, bool FMA>
+static cudaError_t launch_xsweep_s(const XSweepArgs& a, cudaStream_t s) {
+    if (a.src_mode == 1) return launch_xsweep_t<P, INLINE, RHO, FMA, 0, 1>(a, s);
+    if constexpr (!RHO)  // (the second source half step rides in the second x sweep: no moment)
+        if (a.src_mode == 2) return launch_xsweep_t<P, INLINE, RHO, FMA, 0, 2>(a, s);
+    return launch_xsweep_t<P, INLINE, RHO, FMA>(a, s);
+}
 template <int P, bool INLINE, bool RHO>
 static cudaError_t launch_xsweep_f(const XSweepArgs& a, cudaStream_t s) {
     if constexpr (kHasFma<P>)
-        if (a.fma) return launch_xsweep_t<P, INLINE, RHO, true>(a, s);
-    return launch_xsweep_t<P, INLINE, RHO, false>(a, s);
+        if (a.fma) return launch_xsweep_s<P, INLINE, RHO, true>(a, s);
+    return launch_xsweep_s<P, INLINE, RHO, false>(a, s);
 }
 
 template <int P, bool INLINE, int MODE>
