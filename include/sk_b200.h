@@ -148,7 +148,9 @@ sk_status sk_ctx_set_step_fusion(sk_ctx* ctx, int on);
 sk_status sk_ctx_check_guards(sk_ctx* ctx, long long* bad);
 /* Capacity of the deferred limiter-clamp list (troubled cells queued by the
  * sweeps, clamped by a fixup kernel); above it the fixup rescans the sweep.
- * Default and maximum 4 Mi cells; exposed for testing the rescan path. */
+ * Sized when a state is created: at least 4 Mi entries, cells/32 of a pass
+ * for the inline limiter, cells/6 for the literature post limiters; cap may
+ * only lower it (for testing the rescan path). */
 sk_status sk_ctx_set_fix_capacity(sk_ctx* ctx, unsigned int cap);
 sk_status sk_ctx_synchronize(sk_ctx* ctx); /* also reports device-side errors */
 sk_status sk_stats_get(sk_ctx* ctx, sk_stats* out);

@@ -576,11 +576,12 @@ __device__ __forceinline__ bool post_flag_t(const PostCfg& cfg, const Basis& b, 
 //   tile = (species, x row, block, T cells); its source window is T+1 cells
 //   that are contiguous in HBM. One producer warp streams windows (and the
 //   tile's table row) into an S-stage smem ring with cp.async.bulk + mbarrier
-//   transaction counts; NC consumer warps compute two cells each (projection
-//   + inline indicator in registers, matrices as smem broadcasts), write the
-//   tile AoS into a triple-buffered output stage and one thread bulk-stores it.
-//   Window cells outside the contiguous valid range (walls, 3-block ghosts,
-//   periodic wrap) are filled by the consumers after the copy lands.
+//   transaction counts, and its lanes fill the window cells outside the
+//   contiguous valid range (walls, 3-block ghosts, periodic wrap) before the
+//   stage is armed; NC consumer warps compute two cells each (projection +
+//   inline indicator in registers, matrices as smem broadcasts), hand the stage
+//   back, queue troubled cells for the fixup and store each cell with one
+//   256-bit store straight to HBM.
 // ---------------------------------------------------------------------------
 template <int P>
 struct XCfg {
