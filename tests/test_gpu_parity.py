@@ -1173,3 +1173,33 @@ def test_no_out_of_bounds_writes(sk):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "sanitize_steps.py")],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_bench_sharded_one_rank_line(sk, monkeypatch, capsys):
+    """bench.py's torchrun path (sharding.bench_sharded) end to end on one NCCL
+    rank: the JSON line carries the contract keys, the per-kernel roofline from
+    the per-phase window, and e2e through the sharded API."""
+    import argparse
+    import json
+    import socket
+
+    import bench
+    from paper_2408_11235_b200 import sharding
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    for k, v in dict(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                     MASTER_PORT=str(port)).items():
+        monkeypatch.setenv(k, v)
+    cfg = cfg_of(sk, k=3, nf=64, nc=128, m=1, nv=128, mu=1836.0, limiter="sldg")
+    args = argparse.Namespace(steps=4, warmup=3, config="C3", no_e2e=False, e2e_steps=1)
+    sharding.bench_sharded(args, cfg, bench.METRIC, bench.UNIT, {"workload": "test"})
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "roofline",
+                "phases_ms_per_step", "gpu_launches", "clocks", "e2e"):
+        assert key in line, key
+    assert line["n_gpus"] == 1 and line["value"] > 0
+    assert line["roofline"]["kernel"] in ("x_sweep_1", "x_sweep_2", "v_sweep")
+    assert 0 < line["roofline"]["frac"] < 1.5
