@@ -899,6 +899,7 @@ sk_status sk_ctx_create(int device, int k, int nblocks, const double* left, cons
         return fail(SK_ERR_CUDA, "no CUDA device (the B200 path has no CPU fallback)");
     if (device < 0 || device >= ndev) return fail(SK_ERR_CUDA, "invalid device index");
     CK(cudaSetDevice(device));
+    CK(launch_init_device());
     auto* c = new sk_ctx;
     c->device = device;
     c->k = k;

@@ -22,6 +22,7 @@
 // reference's.
 #include <algorithm>
 #include <type_traits>
+#include <utility>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -66,6 +67,18 @@ __device__ __forceinline__ void raise_error(DevStatus* st, int code, int kind, i
 // collects and clears the error.
 __device__ __forceinline__ bool halted(const DevStatus* st) {
     return st && *reinterpret_cast<const volatile int*>(&st->err_code) != 0;
+}
+
+// Programmatic dependent launch: every kernel of the step is launched with
+// programmatic stream serialisation (pdl_launch), waits here for the previous
+// grid's completion and memory before touching anything, and at once lets the
+// next kernel's CTAs be scheduled as its own last wave retires -- the launch
+// and block-scheduling gaps between the ~15 kernels of a step overlap the
+// previous kernel's tail. (A no-op for kernels launched without the attribute.)
+__constant__ int c_pdl_trigger;  // 1: trigger at entry, 0: implicit trigger at CTA exit (SK_PDL)
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (c_pdl_trigger) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void count_flags(unsigned long long* dst, unsigned t, unsigned c,
@@ -187,6 +200,7 @@ __device__ __forceinline__ bool all_finite(const double* o) {
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void xtab_kernel(const __grid_constant__ XTabArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int line = blockIdx.x * blockDim.x + threadIdx.x;
     if (line >= a.nlines) return;
@@ -487,6 +501,7 @@ __device__ __forceinline__ bool xghost_side(const Grid& g, int b, int side) {
 // lanes load the blocks' shifts together and share the line's ghost values.
 template <int P>
 __global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ XSweepArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const Grid& g = a.grid;
     const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
@@ -719,6 +734,7 @@ __device__ __forceinline__ void stg_cell(double* dp, const double* o) {
 template <int P, bool INLINE, bool RHO, bool FMA, int MODE = 0, int SRC = 0>
 __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     xsweep_kernel(const __grid_constant__ XSweepArgs a) {
+    pdl_enter();
     using C = XCfg<P>;
     constexpr int S = MODE == 3 ? C::S3 : C::S;  // input stages
     // fast mode at k = 3: the projection and indicator on the fp64 tensor cores
@@ -1301,6 +1317,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void vtab_kernel(const __grid_constant__ VTabArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
@@ -1369,6 +1386,7 @@ __device__ __forceinline__ void vissue(const double* gp, long long ld, bool vali
 
 template <int P, bool INLINE, bool PERIODIC, bool FMA>
 __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant__ VSweepArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     constexpr int R = vring<P>();
     static_assert(kVChunk % R == 0, "chunk must be a multiple of the ring depth");
@@ -1588,6 +1606,7 @@ __device__ __forceinline__ void xfix_cell(const XSweepArgs& a, int sp, int line,
 
 template <int P, bool FMA>
 __global__ void __launch_bounds__(128, 8) xfix_kernel(const __grid_constant__ XSweepArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;
     const unsigned cnt = *a.fix_count;
@@ -1699,6 +1718,7 @@ __device__ __forceinline__ void xfix2_cell(const XSweepArgs& a, int sp, int line
 
 template <int P, bool FMA>
 __global__ void __launch_bounds__(128, 4) xfix2_kernel(const __grid_constant__ XSweepArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;
     const unsigned cnt = *a.fix_count;
@@ -1760,6 +1780,7 @@ __device__ __forceinline__ void vfix_cell(const VSweepArgs& a, int sp, int j, in
 
 template <int P, bool FMA>
 __global__ void __launch_bounds__(128, 8) vfix_kernel(const __grid_constant__ VSweepArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const unsigned cnt = *a.fix_count;
     unsigned ct[2] = {0, 0}, cc[2] = {0, 0}, co[2] = {0, 0};
@@ -1790,6 +1811,7 @@ __global__ void __launch_bounds__(128, 8) vfix_kernel(const __grid_constant__ VS
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void rho_partial_kernel(const __grid_constant__ RhoArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
@@ -1807,6 +1829,7 @@ __global__ void rho_partial_kernel(const __grid_constant__ RhoArgs a) {
 }
 
 __global__ void rho_reduce_kernel(const __grid_constant__ RhoArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
@@ -1864,6 +1887,7 @@ __global__ void __launch_bounds__(1024) poisson_kernel(const __grid_constant__ P
                                                        const double* __restrict__ rho,
                                                        double* __restrict__ E,
                                                        double* __restrict__ phi) {
+    pdl_enter();
     if (halted(pd.st)) return;
     constexpr int pp = PS * PS;
     const int k = PS - 2, N = pd.ncells;
@@ -2047,6 +2071,7 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
                                                                const double* __restrict__ rho,
                                                                double* __restrict__ E,
                                                                double* __restrict__ phi) {
+    pdl_enter();
     if (halted(pd.st)) return;
     constexpr int pp = PS * PS;
     extern __shared__ double psm[];
@@ -2308,6 +2333,7 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
 constexpr int kRhoThreads = 32, kRhoRing = 96;
 template <int P>
 __global__ void __launch_bounds__(kRhoThreads) rho_exact_kernel(const __grid_constant__ RhoArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     __shared__ double ring[kRhoRing * kRhoThreads];
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2382,6 +2408,7 @@ __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constan
                                                             const double* __restrict__ rho,
                                                             double* __restrict__ E,
                                                             double* __restrict__ phi) {
+    pdl_enter();
     if (halted(pd.st)) return;
     constexpr int KD = 2 * PS - 1, LD = KD + 1, CH = 128;
     __shared__ double scol[2][CH * LD];
@@ -2522,6 +2549,7 @@ __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constan
 // shrink cooldown gate (run.cpp:98-101)
 // ---------------------------------------------------------------------------
 __global__ void step_end_kernel(DevStatus* st, double dt, int v_adjust, long long cooldown, int mask) {
+    pdl_enter();
     if (halted(st)) return;  // no step after a failed one (the step counter stays at it)
     st->time += dt;  // stepper.cpp:98
     st->step += 1;
@@ -2536,6 +2564,7 @@ __global__ void step_end_kernel(DevStatus* st, double dt, int v_adjust, long lon
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void shrink_check_kernel(const __grid_constant__ ShrinkArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int sp = blockIdx.y;
     if (!((a.species_mask >> sp) & 1)) return;
@@ -2567,6 +2596,7 @@ __global__ void shrink_check_kernel(const __grid_constant__ ShrinkArgs a) {
 // build_v_transfer (adaptivity.cpp:52-90): one thread per new cell
 template <int P>
 __global__ void shrink_table_kernel(const __grid_constant__ ShrinkArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int sp = blockIdx.y;
     if (!((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
@@ -2646,6 +2676,7 @@ __device__ __forceinline__ void cp_wait_dyn(int n) {
 // cells past it. A cell outside the ring window is read from global directly.
 template <int P>
 __global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_constant__ ShrinkArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     // the block's threads share the chunk: its transfer matrices are staged
     // once per item (coalesced) instead of each warp re-reading them per cell;
@@ -2754,6 +2785,7 @@ __global__ void __launch_bounds__(kVThreads) shrink_project_kernel(const __grid_
 // commit the new v grid (field.cpp:96-101); the projection already sits in
 // the field's other buffer, so the buffers exchange roles instead of copying
 __global__ void shrink_finalize_kernel(const __grid_constant__ ShrinkArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int sp = threadIdx.x;
     if (sp >= 2 || !((a.species_mask >> sp) & 1) || a.st->shrink_flag[sp] == 0) return;
@@ -2769,6 +2801,7 @@ __global__ void shrink_finalize_kernel(const __grid_constant__ ShrinkArgs a) {
 }
 
 __global__ void shrink_force_kernel(DevStatus* st, int mask) {
+    pdl_enter();
     for (int sp = 0; sp < 2; ++sp) st->shrink_flag[sp] = (mask >> sp) & 1;
 }
 
@@ -2780,6 +2813,7 @@ constexpr int kDiagThreads = 256;
 
 template <int P>
 __global__ void __launch_bounds__(kDiagThreads) diag_partial_kernel(const __grid_constant__ DiagArgs a) {
+    pdl_enter();
     const DevVGrid vg = a.vg[0];
     const double* fb = field_flipped(a.flip) ? a.alt : a.f;
     const long long total = (long long)a.nrows * a.nxd;
@@ -2815,6 +2849,7 @@ __global__ void __launch_bounds__(kDiagThreads) diag_partial_kernel(const __grid
 }
 
 __global__ void diag_final_kernel(const double* partial, int nblk, double* out) {
+    pdl_enter();
     const int q = threadIdx.x;
     if (q >= 4) return;
     double acc = 0.0;
@@ -2824,6 +2859,7 @@ __global__ void diag_final_kernel(const double* partial, int nblk, double* out) 
 
 __global__ void fill_separable_kernel(double* f, const double* gx, const double* gv, long long ld,
                                       long long total) {
+    pdl_enter();
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
         const long long r = i / ld;
@@ -2833,6 +2869,7 @@ __global__ void fill_separable_kernel(double* f, const double* gx, const double*
 }
 
 __global__ void copy_kernel(double* dst, const double* src, long long n) {
+    pdl_enter();
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         dst[i] = src[i];
@@ -2895,6 +2932,7 @@ __device__ __forceinline__ double* post_other(const PostArgs& a, int sp) {
 // v flag pass: one thread per x dof walks kVChunk v cells (in place)
 template <int P, bool FAST, int IND>
 __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant__ PostArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     const int sp = a.species0 + blockIdx.z;
@@ -2928,6 +2966,7 @@ __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant
 
 // overflow only: the field (with its readable v halo rows) into the other buffer
 __global__ void post_copy_kernel(const __grid_constant__ PostArgs a, int P) {
+    pdl_enter();
     if (halted(a.st)) return;
     if (*a.fix_count <= a.fix_cap) return;
     const long long r0 = -(long long)a.gl * P, r1 = (long long)(a.nv + a.gr) * P;
@@ -2945,6 +2984,7 @@ __global__ void post_copy_kernel(const __grid_constant__ PostArgs a, int P) {
 // re-flagged cell from the copy straight into the field)
 template <int P, int DIR, bool FAST>
 __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ PostArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const unsigned cnt = *a.fix_count;
     const bool rescan = cnt > a.fix_cap;
@@ -3014,6 +3054,7 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
 // the queued modifications into the field (list mode only)
 template <int P, int DIR>
 __global__ void __launch_bounds__(128) post_scatter_kernel(const __grid_constant__ PostArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const unsigned cnt = *a.fix_count;
     if (cnt > a.fix_cap) return;
@@ -3033,6 +3074,7 @@ __global__ void __launch_bounds__(128) post_scatter_kernel(const __grid_constant
 }
 
 __global__ void post_v_count_kernel(DevStatus* st, int mask, unsigned long long per_species) {
+    pdl_enter();
     for (int sp = 0; sp < 2; ++sp)
         if ((mask >> sp) & 1) st->post_checked[sp] += per_species;
 }
@@ -3042,6 +3084,42 @@ __global__ void post_v_count_kernel(DevStatus* st, int mask, unsigned long long 
 // ===========================================================================
 // launchers
 // ===========================================================================
+constexpr int kPdlDefault = 0;  // measured: no gain (profiles/r02_pdl.txt)
+// Every launch of the step goes through here: programmatic stream serialisation
+// lets the next kernel's CTAs be scheduled while this one's last wave drains
+// (each kernel opens with pdl_enter(), which waits for the full completion and
+// memory flush of its predecessor before any access). SK_PDL selects the mode
+// (A/B measurement).
+static int pdl_mode() {
+    // SK_PDL: 0 off, 1 launch attribute + trigger at kernel entry, 2 attribute only
+    static const int mode = [] {
+        const char* e = std::getenv("SK_PDL");
+        return e && *e ? std::atoi(e) : kPdlDefault;
+    }();
+    return mode;
+}
+static bool pdl_on() { return pdl_mode() != 0; }
+// per device, before any launch or capture (sk_ctx_create)
+cudaError_t launch_init_device() {
+    const int trig = pdl_mode() == 1;
+    return cudaMemcpyToSymbol(c_pdl_trigger, &trig, sizeof(int));
+}
+template <typename... KP, typename... A>
+static cudaError_t pdl_launch(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 #define SK_DISPATCH_P(P_, CALL)                               \
     switch (P_) {                                             \
         case 1: { constexpr int PP = 1; CALL; } break;        \
@@ -3056,7 +3134,7 @@ __global__ void post_v_count_kernel(DevStatus* st, int mask, unsigned long long 
 
 cudaError_t launch_xtab(const XTabArgs& a, cudaStream_t s) {
     dim3 grid((a.nlines + 127) / 128, a.nspecies);
-    SK_DISPATCH_P(a.basis.p, (xtab_kernel<PP><<<grid, 128, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (pdl_launch(xtab_kernel<PP>, grid, 128, 0, s, a)));
     return cudaGetLastError();
 }
 
@@ -3130,8 +3208,7 @@ static cudaError_t launch_xsweep_t(const XSweepArgs& a, cudaStream_t s) {
     XSweepArgs b;
     int grid = 0;
     if (cudaError_t e = xsweep_plan<P, INLINE, RHO, FMA, MODE, SRC>(a, b, grid)) return e;
-    xsweep_kernel<P, INLINE, RHO, FMA, MODE, SRC>
-        <<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<MODE>(), s>>>(b);
+    pdl_launch(xsweep_kernel<P, INLINE, RHO, FMA, MODE, SRC>, grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<MODE>(), s, b);
     return cudaGetLastError();
 }
 
@@ -3139,7 +3216,7 @@ template <int P>
 static cudaError_t launch_xghost_t(const XSweepArgs& a, cudaStream_t s) {
     const long long warps = (long long)a.nspecies * a.nlines;
     const int grid = (int)((warps * 32 + 255) / 256);
-    if (grid > 0) xghost_kernel<P><<<grid, 256, 0, s>>>(a);
+    if (grid > 0) pdl_launch(xghost_kernel<P>, grid, 256, 0, s, a);
     return cudaGetLastError();
 }
 
@@ -3210,7 +3287,7 @@ static cudaError_t launch_xsweep_fused_t(const XSweepArgs& a, cudaStream_t s) {
 }
 cudaError_t launch_xfix2(const XSweepArgs& a, cudaStream_t s) {
     if (!a.inline_sldg) return cudaSuccess;
-    SK_DISPATCH_P(a.basis.p, (xfix2_kernel<PP, kHasFma<PP>><<<sm_count() * 4, 128, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (pdl_launch(xfix2_kernel<PP, kHasFma<PP>>, sm_count() * 4, 128, 0, s, a)));
     return cudaGetLastError();
 }
 
@@ -3228,6 +3305,7 @@ constexpr int kRhoRedParts = 8;
 __global__ void __launch_bounds__(32 * kRhoRedParts)
     rho_fused_reduce_kernel(const double* partial, const unsigned long long* corr, int groups, int nxd,
                             double* rho, const DevStatus* st, const int* gate, int gate_on) {
+    pdl_enter();
     if (halted(st)) return;
     if (gate && ((*gate != 0) != (gate_on != 0))) return;
     __shared__ double sp[kRhoRedParts][32];
@@ -3264,7 +3342,7 @@ __global__ void __launch_bounds__(32 * kRhoRedParts)
 cudaError_t launch_rho_fused_reduce(const XSweepArgs& a, double* rho, cudaStream_t s, int fused) {
     const int nxd = a.grid.ncells * a.basis.p;
     const int groups = xsweep_rho_groups(a, fused);
-    rho_fused_reduce_kernel<<<(nxd + 31) / 32, 32 * kRhoRedParts, 0, s>>>(a.rho_partial, a.rho_corr, groups,
+    pdl_launch(rho_fused_reduce_kernel, (nxd + 31) / 32, 32 * kRhoRedParts, 0, s, a.rho_partial, a.rho_corr, groups,
                                                                         nxd, rho, a.st, a.gate, a.gate_on);
     return cudaGetLastError();
 }
@@ -3285,19 +3363,19 @@ template <int P>
 static void launch_xfix_t(const XSweepArgs& a, cudaStream_t s) {
     if constexpr (kHasFma<P>)
         if (a.fma) {
-            xfix_kernel<P, true><<<sm_count() * 8, 128, 0, s>>>(a);
+            pdl_launch(xfix_kernel<P, true>, sm_count() * 8, 128, 0, s, a);
             return;
         }
-    xfix_kernel<P, false><<<sm_count() * 8, 128, 0, s>>>(a);
+    pdl_launch(xfix_kernel<P, false>, sm_count() * 8, 128, 0, s, a);
 }
 template <int P>
 static void launch_vfix_t(const VSweepArgs& a, cudaStream_t s) {
     if constexpr (kHasFma<P>)
         if (a.fma) {
-            vfix_kernel<P, true><<<sm_count() * 8, 128, 0, s>>>(a);
+            pdl_launch(vfix_kernel<P, true>, sm_count() * 8, 128, 0, s, a);
             return;
         }
-    vfix_kernel<P, false><<<sm_count() * 8, 128, 0, s>>>(a);
+    pdl_launch(vfix_kernel<P, false>, sm_count() * 8, 128, 0, s, a);
 }
 
 cudaError_t launch_xfix(const XSweepArgs& a, cudaStream_t s) {
@@ -3312,7 +3390,7 @@ cudaError_t launch_vfix(const VSweepArgs& a, cudaStream_t s) {
 
 cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + 127) / 128, a.nspecies);
-    SK_DISPATCH_P(a.basis.p, (vtab_kernel<PP><<<grid, 128, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (pdl_launch(vtab_kernel<PP>, grid, 128, 0, s, a)));
     return cudaGetLastError();
 }
 
@@ -3320,10 +3398,10 @@ template <int P, bool INLINE>
 static void launch_vsweep_f(const VSweepArgs& a, dim3 grid, cudaStream_t s) {
     if constexpr (kHasFma<P>)
         if (a.fma) {
-            vsweep_kernel<P, INLINE, false, true><<<grid, kVThreads, 0, s>>>(a);
+            pdl_launch(vsweep_kernel<P, INLINE, false, true>, grid, kVThreads, 0, s, a);
             return;
         }
-    vsweep_kernel<P, INLINE, false, false><<<grid, kVThreads, 0, s>>>(a);
+    pdl_launch(vsweep_kernel<P, INLINE, false, false>, grid, kVThreads, 0, s, a);
 }
 
 cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
@@ -3331,7 +3409,7 @@ cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
     const int nch = a.nchunks > 0 ? a.nchunks : (a.n + kVChunk - 1) / kVChunk;
     dim3 grid = a.chunk_major ? dim3(nch, nxb, a.nspecies) : dim3(nxb, nch, a.nspecies);
     if (a.periodic)
-        SK_DISPATCH_P(a.basis.p, (vsweep_kernel<PP, true, true, false><<<grid, kVThreads, 0, s>>>(a)))
+        SK_DISPATCH_P(a.basis.p, (pdl_launch(vsweep_kernel<PP, true, true, false>, grid, kVThreads, 0, s, a)))
     else if (a.inline_sldg)
         SK_DISPATCH_P(a.basis.p, (launch_vsweep_f<PP, true>(a, grid, s)))
     else
@@ -3341,8 +3419,8 @@ cudaError_t launch_vsweep(const VSweepArgs& a, cudaStream_t s) {
 
 cudaError_t launch_rho(const RhoArgs& a, int nspecies, cudaStream_t s) {
     dim3 grid((a.nxd + 127) / 128, a.nchunks, nspecies);
-    SK_DISPATCH_P(a.basis.p, (rho_partial_kernel<PP><<<grid, 128, 0, s>>>(a)));
-    rho_reduce_kernel<<<(a.nxd + 127) / 128, 128, 0, s>>>(a);
+    SK_DISPATCH_P(a.basis.p, (pdl_launch(rho_partial_kernel<PP>, grid, 128, 0, s, a)));
+    pdl_launch(rho_reduce_kernel, (a.nxd + 127) / 128, 128, 0, s, a);
     return cudaGetLastError();
 }
 
@@ -3426,21 +3504,23 @@ static cudaError_t launch_poisson_t(const PoissonDev& pd, int stage, const doubl
         cached_n = pd.ncells;
     }
     if (cached_c == 0) {
-        poisson_kernel<PS><<<1, 1024, 0, s>>>(pd, stage, rho, E, phi);
+        pdl_launch(poisson_kernel<PS>, 1, 1024, 0, s, pd, stage, rho, E, phi);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr{};
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = cached_c;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2]{};
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cached_c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.gridDim = dim3(cached_c);
     cfg.blockDim = dim3(1024);
     cfg.dynamicSmemBytes = cached_smem;
     cfg.stream = s;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, poisson_cluster_kernel<PS>, pd, cached_cm, stage, rho, E, phi);
 }
 
@@ -3451,13 +3531,13 @@ cudaError_t launch_poisson(const PoissonDev& pd, int stage, const double* rho, d
 }
 
 cudaError_t launch_rho_exact(const RhoArgs& a, cudaStream_t s) {
-    SK_DISPATCH_P(a.basis.p, (rho_exact_kernel<PP><<<(a.nxd + kRhoThreads - 1) / kRhoThreads, kRhoThreads, 0, s>>>(a)));
+    SK_DISPATCH_P(a.basis.p, (pdl_launch(rho_exact_kernel<PP>, (a.nxd + kRhoThreads - 1) / kRhoThreads, kRhoThreads, 0, s, a)));
     return cudaGetLastError();
 }
 
 cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double* E, double* phi,
                                  cudaStream_t s) {
-    SK_DISPATCH_P(pd.ps - 1, (poisson_exact_kernel<PP + 1><<<1, 256, 0, s>>>(pd, rho, E, phi)));
+    SK_DISPATCH_P(pd.ps - 1, (pdl_launch(poisson_exact_kernel<PP + 1>, 1, 256, 0, s, pd, rho, E, phi)));
     return cudaGetLastError();
 }
 
@@ -3466,6 +3546,7 @@ cudaError_t launch_poisson_exact(const PoissonDev& pd, const double* rho, double
 // step n -- checked only when its 10-step cooldown has run out (run.cpp:100),
 // and a shrink there changes the v grid between the two sweeps.
 __global__ void fuse_decide_kernel(DevStatus* st, int v_adjust, long long cooldown) {
+    pdl_enter();
     if (halted(st)) return;
     const long long n = st->step + 1;
     int ok = 1;
@@ -3476,22 +3557,23 @@ __global__ void fuse_decide_kernel(DevStatus* st, int v_adjust, long long cooldo
 // the unfused alternative of a fused boundary leaves the field in the buffer
 // the fused sweep does not write: record it in the fields' flip flags
 __global__ void flip_toggle_kernel(const DevStatus* st, int* f0, int* f1) {
+    pdl_enter();
     if (halted(st) || st->fuse_ok) return;
     *f0 ^= 1;
     *f1 ^= 1;
 }
 cudaError_t launch_fuse_decide(DevStatus* st, int v_adjust, long long cooldown, cudaStream_t s) {
-    fuse_decide_kernel<<<1, 1, 0, s>>>(st, v_adjust, cooldown);
+    pdl_launch(fuse_decide_kernel, 1, 1, 0, s, st, v_adjust, cooldown);
     return cudaGetLastError();
 }
 cudaError_t launch_flip_toggle(const DevStatus* st, int* f0, int* f1, cudaStream_t s) {
-    flip_toggle_kernel<<<1, 1, 0, s>>>(st, f0, f1);
+    pdl_launch(flip_toggle_kernel, 1, 1, 0, s, st, f0, f1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_step_end(DevStatus* st, double dt, int v_adjust, long long cooldown, int mask,
                             cudaStream_t s) {
-    step_end_kernel<<<1, 1, 0, s>>>(st, dt, v_adjust, cooldown, mask);
+    pdl_launch(step_end_kernel, 1, 1, 0, s, st, dt, v_adjust, cooldown, mask);
     return cudaGetLastError();
 }
 
@@ -3501,6 +3583,7 @@ cudaError_t launch_step_end(DevStatus* st, double dt, int v_adjust, long long co
 // indexed by the species' v-grid level (its shrink count), so the increment
 // is bitwise the reference's.
 __global__ void source_kernel(const __grid_constant__ SourceArgs a) {
+    pdl_enter();
     if (halted(a.st)) return;
     const int sp = blockIdx.y;
     const double t = a.second ? a.st->time + a.half : a.st->time;
@@ -3527,43 +3610,43 @@ __global__ void source_kernel(const __grid_constant__ SourceArgs a) {
 }
 
 cudaError_t launch_source(const SourceArgs& a, cudaStream_t s) {
-    source_kernel<<<dim3(sm_count() * 8, 2), 256, 0, s>>>(a);
+    pdl_launch(source_kernel, dim3(sm_count() * 8, 2), 256, 0, s, a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_shrink(const ShrinkArgs& a, cudaStream_t s) {
     const int P = a.basis.p;
     // force: see ShrinkArgs
-    if (a.force == 1 || a.force == -1) shrink_force_kernel<<<1, 1, 0, s>>>(a.st, a.species_mask);
+    if (a.force == 1 || a.force == -1) pdl_launch(shrink_force_kernel, 1, 1, 0, s, a.st, a.species_mask);
     if (a.force != 1 && a.force != 2)
-        SK_DISPATCH_P(P, (shrink_check_kernel<PP><<<dim3((a.nxd + 255) / 256, 2), 256, 0, s>>>(a)));
+        SK_DISPATCH_P(P, (pdl_launch(shrink_check_kernel<PP>, dim3((a.nxd + 255) / 256, 2), 256, 0, s, a)));
     if (a.force < 0) return cudaGetLastError();
-    SK_DISPATCH_P(P, (shrink_table_kernel<PP><<<dim3((a.nv_global + 127) / 128, 2), 128, 0, s>>>(a)));
-    SK_DISPATCH_P(P, (shrink_project_kernel<PP><<<dim3(sm_count() * 8, 1, 2), kVThreads, 0, s>>>(a)));
-    shrink_finalize_kernel<<<1, 32, 0, s>>>(a);
+    SK_DISPATCH_P(P, (pdl_launch(shrink_table_kernel<PP>, dim3((a.nv_global + 127) / 128, 2), 128, 0, s, a)));
+    SK_DISPATCH_P(P, (pdl_launch(shrink_project_kernel<PP>, dim3(sm_count() * 8, 1, 2), kVThreads, 0, s, a)));
+    pdl_launch(shrink_finalize_kernel, 1, 32, 0, s, a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_diag(const DiagArgs& a, double* out4, double* partial, cudaStream_t s) {
     DiagArgs b = a;
     b.partial = partial;
-    SK_DISPATCH_P(a.basis.p, (diag_partial_kernel<PP><<<kDiagBlocks, kDiagThreads, 0, s>>>(b)));
-    diag_final_kernel<<<1, 32, 0, s>>>(partial, kDiagBlocks, out4);
+    SK_DISPATCH_P(a.basis.p, (pdl_launch(diag_partial_kernel<PP>, kDiagBlocks, kDiagThreads, 0, s, b)));
+    pdl_launch(diag_final_kernel, 1, 32, 0, s, partial, kDiagBlocks, out4);
     return cudaGetLastError();
 }
 
 cudaError_t launch_fill_separable(double* f, const double* gx, const double* gv, long long ld,
                                   int nrows, cudaStream_t s) {
-    fill_separable_kernel<<<1184, 256, 0, s>>>(f, gx, gv, ld, (long long)nrows * ld);
+    pdl_launch(fill_separable_kernel, 1184, 256, 0, s, f, gx, gv, ld, (long long)nrows * ld);
     return cudaGetLastError();
 }
 
 // after a flag pass: overflow copy (device-gated), modifications, scatter
 template <int P, int DIR, bool FAST>
 static void launch_post_tail(const PostArgs& a, cudaStream_t s) {
-    post_copy_kernel<<<sm_count() * 4, 256, 0, s>>>(a, P);
-    post_fix_kernel<P, DIR, FAST><<<sm_count() * 8, 128, 0, s>>>(a);
-    post_scatter_kernel<P, DIR><<<sm_count() * 4, 128, 0, s>>>(a);
+    pdl_launch(post_copy_kernel, sm_count() * 4, 256, 0, s, a, P);
+    pdl_launch(post_fix_kernel<P, DIR, FAST>, sm_count() * 8, 128, 0, s, a);
+    pdl_launch(post_scatter_kernel<P, DIR>, sm_count() * 4, 128, 0, s, a);
 }
 
 template <int P, bool FAST>
@@ -3592,13 +3675,11 @@ static cudaError_t launch_post_x_t(const PostArgs& a, cudaStream_t s) {
     if (a.cfg.indicator == 1) {
         if (cudaError_t e = xsweep_plan<P, false, false, FAST, 1>(x, b, grid)) return e;
         if (grid > 0)
-            xsweep_kernel<P, false, false, FAST, 1>
-                <<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<1>(), s>>>(b);
+            pdl_launch(xsweep_kernel<P, false, false, FAST, 1>, grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<1>(), s, b);
     } else {
         if (cudaError_t e = xsweep_plan<P, false, false, FAST, 2>(x, b, grid)) return e;
         if (grid > 0)
-            xsweep_kernel<P, false, false, FAST, 2>
-                <<<grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<2>(), s>>>(b);
+            pdl_launch(xsweep_kernel<P, false, false, FAST, 2>, grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<2>(), s, b);
     }
     launch_post_tail<P, 0, FAST>(a, s);
     return cudaGetLastError();
@@ -3608,9 +3689,9 @@ template <int P, bool FAST>
 static cudaError_t launch_post_v_t(const PostArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
     if (a.cfg.indicator == 1)
-        post_v_kernel<P, FAST, 1><<<grid, kVThreads, 0, s>>>(a);
+        pdl_launch(post_v_kernel<P, FAST, 1>, grid, kVThreads, 0, s, a);
     else
-        post_v_kernel<P, FAST, 2><<<grid, kVThreads, 0, s>>>(a);
+        pdl_launch(post_v_kernel<P, FAST, 2>, grid, kVThreads, 0, s, a);
     launch_post_tail<P, 1, FAST>(a, s);
     return cudaGetLastError();
 }
@@ -3624,7 +3705,7 @@ cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s) {
     }
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
-    post_v_count_kernel<<<1, 1, 0, s>>>(a.st, mask, (unsigned long long)a.nrows * a.grid.ncells);
+    pdl_launch(post_v_count_kernel, 1, 1, 0, s, a.st, mask, (unsigned long long)a.nrows * a.grid.ncells);
     return cudaGetLastError();
 }
 
@@ -3636,12 +3717,12 @@ cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s) {
     }
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
-    post_v_count_kernel<<<1, 1, 0, s>>>(a.st, mask, (unsigned long long)a.nv * a.nxd);
+    pdl_launch(post_v_count_kernel, 1, 1, 0, s, a.st, mask, (unsigned long long)a.nv * a.nxd);
     return cudaGetLastError();
 }
 
 cudaError_t launch_scale_copy(double* dst, const double* src, size_t n, cudaStream_t s) {
-    copy_kernel<<<1184, 256, 0, s>>>(dst, src, (long long)n);
+    pdl_launch(copy_kernel, 1184, 256, 0, s, dst, src, (long long)n);
     return cudaGetLastError();
 }
 

@@ -234,6 +234,7 @@ struct PostArgs {
 };
 
 // launchers (P = k+1 dispatch inside)
+cudaError_t launch_init_device();
 cudaError_t launch_xtab(const XTabArgs& a, cudaStream_t s);
 cudaError_t launch_xsweep(const XSweepArgs& a, int ntiles, cudaStream_t s);
 // 3-block ghost pre-pass (a.ghost, a.ghost_cap set); needed only when adjacent
