@@ -142,6 +142,13 @@ sk_status sk_ctx_set_exact_parts(sk_ctx* ctx, int mask);
  * B200 each half sweep is issue-bound about as much as HBM-bound, so the fused
  * pass measures break-even at C5 and slower at C3. */
 sk_status sk_ctx_set_step_fusion(sk_ctx* ctx, int on);
+/* Post limiter V flags fused into the v sweep (default on; SK_POST_FUSION=0 in
+ * the environment turns it off at context creation): in the step, on walls
+ * without a v halo, the v sweep decides each cell's minmod / mean-error flag
+ * from the registers it stores (the stencil limiters.cpp's v pass reads back),
+ * so the post limiter V runs only its fixes -- one read of f less per step.
+ * The flags are bitwise those of the separate pass. */
+sk_status sk_ctx_set_post_fusion(sk_ctx* ctx, int on);
 /* Out-of-bounds write check: with SK_GUARD=1 in the environment when the
  * context is created, fields, tables, E, rho and phi are allocated with
  * sentinel guard zones; *bad = guard words overwritten since (0 = clean). */

@@ -76,6 +76,7 @@ SIGNATURES = {
     "sk_ctx_set_exact_reductions": (_i, [_vp, _i]),
     "sk_ctx_set_exact_parts": (_i, [_vp, _i]),
     "sk_ctx_set_step_fusion": (_i, [_vp, _i]),
+    "sk_ctx_set_post_fusion": (_i, [_vp, _i]),
     "sk_ctx_check_guards": (_i, [_vp, C.POINTER(C.c_longlong)]),
     "sk_ctx_set_fix_capacity": (_i, [_vp, C.c_uint]),
     "sk_ctx_synchronize": (_i, [_vp]),
@@ -154,10 +155,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise RuntimeError(f"{LIB} is not built: run __graft_entry__.build() "
+        path = os.environ.get("SK_B200_LIB") or LIB  # (another build of the same ABI, for A/B timing)
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is not built: run __graft_entry__.build() "
                                "(the sLdG step has no CPU fallback)")
-        L = C.CDLL(LIB)
+        L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
             fn.restype = res

@@ -103,6 +103,9 @@ struct sk_ctx {
     // kGuard-double guard zones of a sentinel pattern on both sides;
     // sk_ctx_check_guards counts overwritten guard words
     bool guard_on = getenv("SK_GUARD") != nullptr && atoi(getenv("SK_GUARD")) != 0;
+    // post limiter V flags fused into the v sweep (sk_ctx_set_post_fusion):
+    // saves the flag pass's read of f; SK_POST_FUSION=0 turns it off
+    bool post_fuse = getenv("SK_POST_FUSION") == nullptr || atoi(getenv("SK_POST_FUSION")) != 0;
     struct Guarded {
         double* base;
         size_t n;
@@ -198,6 +201,7 @@ struct sk_state {
     double sqrt_mu[2] = {1.0, 1.0};
     double charge[2] = {-1.0, 1.0};
     long step_host = 0;
+    bool post_v_queued = false;  // enq_phase_b1's v sweep queued the post limiter V's flags (for b2)
     // CUDA graphs of nb consecutive loop bodies (sk_run_steps), keyed by the
     // buffer parity they start from, the arithmetic mode, the scratch-buffer
     // generation and nb; replays leave the parity at cur_after
@@ -614,8 +618,19 @@ sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, con
 // (nchunks 0: all, < 0: none); part = 1: first part of a split sweep (fix list
 // reset, no fixup, no exchange of the buffers' roles), 3: a middle part, 2: the
 // last part (fixup and exchange, no reset), 0: the whole sweep
+// whether the post limiter V of this configuration can ride in the v sweep:
+// walls and no v halo (the extra neighbour outputs must be the stencil's
+// cells), and the indicator in the sweep's arithmetic (fast mode has DFMA
+// sweeps for k <= 3 only)
+bool post_v_fusable(sk_field** fs, const sk_limiter* lim, int periodic) {
+    const sk_ctx* c = fs[0]->ctx;
+    return lim && lim->indicator != 0 && c->post_fuse && !periodic && !lim->inline_sldg && fs[0]->gl() == 0 &&
+           fs[0]->gr() == 0 && ((c->exact & SK_EXACT_ARITH) || c->P <= 4);
+}
+
 sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
-                     int check_finite, int chunk0 = 0, int nchunks = 0, int part = 0) {
+                     int check_finite, int chunk0 = 0, int nchunks = 0, int part = 0,
+                     const sk_limiter* post_lim = nullptr) {
     sk_ctx* c = fs[0]->ctx;
     VSweepArgs a{};
     a.basis = c->basis;
@@ -652,6 +667,12 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     a.fix_cap = c->fix_cap;
     a.chunk0 = chunk0;
     a.nchunks = nchunks;
+    if (post_lim) {  // (caller checked post_v_fusable; one launch over all chunks)
+        a.post_v = post_lim->indicator;
+        a.post = post_cfg(post_lim);
+        post_cfg_points(c->basis, a.post);
+        CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
+    }
     if (inline_sldg && (part == 0 || part == 1))
         CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     if (nchunks >= 0) {
@@ -671,7 +692,8 @@ sk_status enq_vsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
     return SK_OK;
 }
 
-sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, int periodic) {
+sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, int periodic,
+                   bool flags_queued = false) {
     if (!lim || lim->indicator == 0) return SK_OK;
     sk_ctx* c = fs[0]->ctx;
     PostArgs a{};
@@ -704,12 +726,13 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;
     a.fix_vals = c->fix_vals;
-    CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
+    a.flags_queued = flags_queued && dir == SK_DIR_V;  // (the v sweep queued them: keep the list)
+    if (!a.flags_queued) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     if (dir == SK_DIR_X)
         CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
     else
         CK(launch_post_v(a, c->stream));
-    c->launches += 5;  // flag pass, overflow copy, fix, scatter, counter
+    c->launches += a.flags_queued ? 4 : 5;  // flag pass, overflow copy, fix, scatter, counter
     // in place: the field stays in its buffer
     return SK_OK;
 }
@@ -1093,6 +1116,12 @@ sk_status sk_ctx_check_guards(sk_ctx* c, long long* bad) {
 sk_status sk_ctx_set_step_fusion(sk_ctx* c, int on) {
     c->fuse_off = on == 0;
     ++c->gen;  // captured step graphs change
+    return SK_OK;
+}
+
+sk_status sk_ctx_set_post_fusion(sk_ctx* c, int on) {
+    c->post_fuse = on != 0;
+    ++c->gen;
     return SK_OK;
 }
 
@@ -1807,7 +1836,11 @@ sk_status enq_phase_b1(sk_state* s) {
         return rc;
     {
         FixTimer ft(s, PH_V_FIX);
-        if ((rc = mark(s, PH_V)) || (rc = enq_vsweep(fs, 2, 0, inl, thr, 0))) return rc;
+        // the post limiter V's flags ride in the v sweep where they can (enq_phase_b2 then runs its fixes)
+        const bool pv = post_v_fusable(fs, lim, 0);
+        if ((rc = mark(s, PH_V)) || (rc = enq_vsweep(fs, 2, 0, inl, thr, 0, 0, 0, 0, pv ? lim : nullptr)))
+            return rc;
+        s->post_v_queued = pv;
     }
     return SK_OK;
 }
@@ -1821,7 +1854,9 @@ sk_status enq_phase_b2(sk_state* s, bool fuse_out = false) {
     sk_field* fs[2] = {s->f[0], s->f[1]};
     sk_status rc;
     const bool post = lim->indicator != 0;
-    if (post && ((rc = mark(s, PH_POST_V)) || (rc = enq_post(fs, 2, SK_DIR_V, lim, 0)))) return rc;
+    const bool queued = s->post_v_queued;  // (set by enq_phase_b1's v sweep only)
+    s->post_v_queued = false;
+    if (post && ((rc = mark(s, PH_POST_V)) || (rc = enq_post(fs, 2, SK_DIR_V, lim, 0, queued)))) return rc;
     // stepper.cpp:93-97 (injection): source half step at state.time + half --
     // fused into the second x sweep's stores unless a post limiter runs between
     const int src2 = !post && source_fusable(s) ? 2 : 0;

@@ -561,15 +561,13 @@ __global__ void __launch_bounds__(256, 4) xghost_kernel(const __grid_constant__ 
 }
 
 // literature post-limiter indicator of one cell from its x or v stencil
+// (post_summary / post_decide: one arithmetic for the stencil passes and the
+// flags fused into the v sweep)
 template <int P, bool FAST = false>
 __device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, const double* um,
                                           const double* u0, const double* up) {
-    if constexpr (FAST)
-        return cfg.indicator == 1 ? indicator_minmod_fast<P>(b, cfg, um, u0, up)
-                                  : indicator_meanerr_fast<P>(b, cfg, um, u0, up);
-    else
-        return cfg.indicator == 1 ? indicator_minmod_pre<P>(b, um, u0, up)
-                                  : indicator_meanerr_pre<P>(b, cfg, um, u0, up);
+    return cfg.indicator == 1 ? post_flag_sum<P, FAST, 1>(b, cfg, um, u0, up)
+                              : post_flag_sum<P, FAST, 2>(b, cfg, um, u0, up);
 }
 
 // the same with the indicator fixed at compile time (flag passes: straight-line
@@ -577,13 +575,7 @@ __device__ __forceinline__ bool post_flag(const PostCfg& cfg, const Basis& b, co
 template <int P, bool FAST, int IND>
 __device__ __forceinline__ bool post_flag_t(const PostCfg& cfg, const Basis& b, const double* um,
                                             const double* u0, const double* up) {
-    if constexpr (FAST) {
-        if constexpr (IND == 1) return indicator_minmod_fast<P>(b, cfg, um, u0, up);
-        else return indicator_meanerr_fast<P>(b, cfg, um, u0, up);
-    } else {
-        if constexpr (IND == 1) return indicator_minmod_pre<P>(b, um, u0, up);
-        else return indicator_meanerr_pre<P>(b, cfg, um, u0, up);
-    }
+    return post_flag_sum<P, FAST, IND>(b, cfg, um, u0, up);
 }
 
 // ---------------------------------------------------------------------------
@@ -598,18 +590,27 @@ __device__ __forceinline__ bool post_flag_t(const PostCfg& cfg, const Basis& b, 
 //   back, queue troubled cells for the fixup and store each cell with one
 //   256-bit store straight to HBM.
 // ---------------------------------------------------------------------------
+#ifndef SK_X_CPT4
+#define SK_X_CPT4 2   // k = 3 x sweep: cells per consumer thread
+#endif
+#ifndef SK_X_STAGES
+#define SK_X_STAGES 5  // x sweep input ring depth
+#endif
+#ifndef SK_X_MINB4
+#define SK_X_MINB4 2  // k = 3 x sweep: resident CTAs per SM
+#endif
 template <int P>
 struct XCfg {
     static constexpr int NC = 8;                    // consumer warps
     static constexpr int NT = NC * 32;
-    static constexpr int CPT = P <= 4 ? 2 : 1;
-    static constexpr int MINB = 2;                  // CTAs per SM the registers must allow
+    static constexpr int CPT = P < 4 ? 2 : P == 4 ? SK_X_CPT4 : 1;
+    static constexpr int MINB = P == 4 ? SK_X_MINB4 : 2;  // CTAs per SM the registers must allow
     static constexpr int T = CPT * NT;              // output cells per tile
     static constexpr int WIN = (((T + 1) * P + 4) + 1) / 2 * 2;  // window doubles (+ slack), even
     static constexpr int NF = xnf<P>();
     static constexpr int HDR = 6;                   // tile header (8 ints + weight) from the producer
     static constexpr int STAGE = ((WIN + NF + HDR + 1) / 2) * 2;
-    static constexpr int S = 5;                     // input stages (outputs go straight to HBM)
+    static constexpr int S = SK_X_STAGES;           // input stages (outputs go straight to HBM)
     static constexpr int RACC = 0;                  // (fused-moment accumulators live in registers)
     static constexpr size_t SMEM = sizeof(double) * (size_t)(S * STAGE + RACC) + 8 * 2 * S + 8 * NC * kQCap;
     // MODE 3 (two half sweeps fused): 4 input stages, the intermediate line
@@ -745,7 +746,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     constexpr bool kDmma = kXsweepDmma && P == 4 && FMA && MODE == 0 && C::T % (C::NC * 8) == 0;
     if (halted(a.st)) return;
     static_assert(MODE == 0 || MODE == 3 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
-    static_assert(MODE != 3 || C::T == 2 * C::NT, "MODE 3: T + 1 intermediate cells over 3 passes of the consumers");
+    static_assert(MODE != 3 || C::T <= 2 * C::NT, "MODE 3: T + 1 intermediate cells over 3 passes of the consumers");
     if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;  // device-decided alternative
     // cells per tile: T in every mode -- the flag passes (one neighbour cell
     // each side) and MODE 3 (two shifts) stage a T + 2 cell window instead of
@@ -1384,13 +1385,23 @@ __device__ __forceinline__ void vissue(const double* gp, long long ld, bool vali
     for (int n = 0; n < P; ++n) cp_async8(slot + n * kVThreads, valid ? gp + n * ld : gp, valid);
 }
 
-template <int P, bool INLINE, bool PERIODIC, bool FMA>
+// PV (post limiter V fused, 1 minmod / 2 mean error): every output cell's
+// summary (post_summary) is formed from the registers it is stored from, and
+// cell j's flag is decided once cell j + 1's is known -- the stencil the post
+// pass would read back. A chunk also computes (without storing) its two
+// neighbour cells, so no flag waits for another block; outside [0, n) the
+// stencil sees the walls' zero cells like the post pass.
+template <int P, bool INLINE, bool PERIODIC, bool FMA, int PV = 0>
 __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant__ VSweepArgs a) {
     pdl_enter();
     if (halted(a.st)) return;
     constexpr int R = vring<P>();
     static_assert(kVChunk % R == 0, "chunk must be a multiple of the ring depth");
     __shared__ double ring[R * P * kVThreads];
+    // PV: flagged cells staged per warp (post limiters flag ~5-10 % of the cells)
+    __shared__ unsigned long long wqueue[PV ? kVThreads / 32 : 1][PV ? kQCap : 1];
+    [[maybe_unused]] unsigned long long* wq = wqueue[PV ? threadIdx.x >> 5 : 0];
+    [[maybe_unused]] int wq_n = 0;
     // chunk_major: v chunks are the fastest grid dimension, so the blocks that
     // share an x range (and its table rows, ~1/3 of the bytes a chunk reads)
     // run back to back -- chosen when the tables would not stay in L2
@@ -1400,6 +1411,9 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
     const int sp = a.species0 + blockIdx.z;
     const int j0 = jb * kVChunk;
     const int j1 = min(j0 + kVChunk, a.n);
+    static_assert(PV == 0 || (!INLINE && !PERIODIC), "fused post flags: no inline limiter, walls");
+    const int js = PV && j0 > 0 ? j0 - 1 : j0;   // outputs computed: [js, je) (PV: the neighbours too)
+    const int je = PV && j1 < a.n ? j1 + 1 : j1;
     bool bad = false;
     double* my = ring + threadIdx.x;
     [[maybe_unused]] const unsigned members = __ballot_sync(0xffffffffu, xd < a.nxd);
@@ -1412,9 +1426,9 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
         const long long ld = a.ld;
         const long long cstride = (long long)P * ld;  // one v cell
         const int lo = -a.gl, hi = a.n + a.gr;
-        const int ncells = (j1 - j0) + 1;              // source cells of this run
+        const int ncells = (je - js) + 1;              // source cells of this run
         // next source cell to issue and its row pointer (non-periodic: linear walk)
-        int s_iss = j0 + istar;
+        int s_iss = js + istar;
         auto src_of = [&](int s) -> const double* {
             if constexpr (PERIODIC) s = ((s % a.n) + a.n) % a.n;
             return f + (long long)s * cstride;
@@ -1457,12 +1471,14 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
         cp_commit();
         ++s_iss;
         g_iss = PERIODIC ? src_of(s_iss) : g_iss + cstride;
-        double* op = (fl ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + xd + (long long)j0 * cstride;
-        for (int jb = 0; jb < kVChunk; jb += R) {
+        double* op = (fl ? const_cast<double*>(a.src[sp]) : a.dst[sp]) + xd + (long long)js * cstride;
+        [[maybe_unused]] PostSum pa{0.0, 0.0, 0.0}, pb{0.0, 0.0, 0.0};  // cells j - 2, j - 1 (walls: zero)
+        constexpr int NOUT = kVChunk + (PV ? 2 : 0);
+        for (int jb = 0; jb < NOUT; jb += R) {
 #pragma unroll
             for (int u = 0; u < R; ++u) {
-                const int jj = jb + u;  // output cell j0 + jj; ur = ring cell jj+1
-                if (j0 + jj < j1) {
+                const int jj = jb + u;  // output cell js + jj; ur = ring cell jj+1
+                if (js + jj < je) {
                     cp_wait<R - 2>();
                     const double* sl = my + ((u + 1) % R) * P * kVThreads;
 #pragma unroll
@@ -1482,15 +1498,40 @@ __global__ void __launch_bounds__(kVThreads) vsweep_kernel(const __grid_constant
                         defer_push_n<1>(a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
                         mean_l = mean_r;
                     }
-                    if (check) bad |= !all_finite<P>(o);
+                    bool store = true;
+                    if constexpr (PV != 0) {
+                        const int j = js + jj;
+                        const PostSum sn = post_summary<P, FMA, PV>(a.basis, a.post, o);
+                        if (j - 1 >= j0) {  // cell j - 1's stencil is complete
+                            const bool tr[1] = {post_decide<FMA, PV>(a.post, pa, pb, sn)};
+                            const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
+                                                                 ((unsigned long long)(j - 1) << 32) |
+                                                                 (unsigned)xd};
+                            wq_push<1>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
+                        }
+                        pa = pb;
+                        pb = sn;
+                        store = j >= j0 && j < j1;
+                    }
+                    if (store) {
+                        if (check) bad |= !all_finite<P>(o);
 #pragma unroll
-                    for (int m = 0; m < P; ++m) op[m * ld] = o[m];
+                        for (int m = 0; m < P; ++m) op[m * ld] = o[m];
+                    }
                     op += cstride;
 #pragma unroll
                     for (int n = 0; n < P; ++n) ul[n] = ur[n];
                 }
             }
         }
+        if constexpr (PV != 0)
+            if (je == j1 && j1 - 1 >= j0) {  // the last cell against the upper wall's zero cell
+                const bool tr[1] = {post_decide<FMA, PV>(a.post, pa, pb, PostSum{0.0, 0.0, 0.0})};
+                const unsigned long long entry[1] = {((unsigned long long)(sp & 1) << 63) |
+                                                     ((unsigned long long)(j1 - 1) << 32) | (unsigned)xd};
+                wq_push<1>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry, members);
+            }
+        if constexpr (PV != 0) wq_flush(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, members);
         cp_wait<0>();
     }
     if (a.check_finite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
@@ -3396,6 +3437,18 @@ cudaError_t launch_vtab(const VTabArgs& a, cudaStream_t s) {
 
 template <int P, bool INLINE>
 static void launch_vsweep_f(const VSweepArgs& a, dim3 grid, cudaStream_t s) {
+    if constexpr (!INLINE) {
+        if (a.post_v == 1 || a.post_v == 2) {  // (the host fuses only where FAST == the sweep's FMA)
+            const bool f = kHasFma<P> && a.fma;
+            if (a.post_v == 1)
+                pdl_launch(f ? vsweep_kernel<P, false, false, kHasFma<P>, 1> : vsweep_kernel<P, false, false, false, 1>,
+                           grid, kVThreads, 0, s, a);
+            else
+                pdl_launch(f ? vsweep_kernel<P, false, false, kHasFma<P>, 2> : vsweep_kernel<P, false, false, false, 2>,
+                           grid, kVThreads, 0, s, a);
+            return;
+        }
+    }
     if constexpr (kHasFma<P>)
         if (a.fma) {
             pdl_launch(vsweep_kernel<P, INLINE, false, true>, grid, kVThreads, 0, s, a);
@@ -3688,10 +3741,12 @@ static cudaError_t launch_post_x_t(const PostArgs& a, cudaStream_t s) {
 template <int P, bool FAST>
 static cudaError_t launch_post_v_t(const PostArgs& a, cudaStream_t s) {
     dim3 grid((a.nxd + kVThreads - 1) / kVThreads, (a.nv + kVChunk - 1) / kVChunk, a.nspecies);
-    if (a.cfg.indicator == 1)
+    if (a.flags_queued) {
+    } else if (a.cfg.indicator == 1) {
         pdl_launch(post_v_kernel<P, FAST, 1>, grid, kVThreads, 0, s, a);
-    else
+    } else {
         pdl_launch(post_v_kernel<P, FAST, 2>, grid, kVThreads, 0, s, a);
+    }
     launch_post_tail<P, 1, FAST>(a, s);
     return cudaGetLastError();
 }

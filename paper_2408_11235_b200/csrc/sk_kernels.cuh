@@ -132,6 +132,10 @@ struct VSweepArgs {
     unsigned int* fix_count;
     unsigned int fix_cap;
     int chunk0, nchunks;  // v chunks [chunk0, chunk0 + nchunks) of kVChunk cells (nchunks 0: all)
+    // post limiter V flags fused into the sweep (1 minmod, 2 mean error; 0 off):
+    // flagged cells go to fix_list in the post pass's format (walls, no halo)
+    int post_v;
+    PostCfg post;
 };
 
 struct RhoArgs {
@@ -231,6 +235,7 @@ struct PostArgs {
     unsigned int* fix_count;
     unsigned int fix_cap;
     double* fix_vals;      // [fix_cap][P] modified values, scattered after all are computed
+    int flags_queued;      // v: the v sweep already queued the flags (VSweepArgs::post_v)
 };
 
 // launchers (P = k+1 dispatch inside)

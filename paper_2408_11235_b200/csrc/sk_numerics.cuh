@@ -668,44 +668,6 @@ SK_HD double integrate_pre(const Basis& b, const double (*t)[SK_MAXP], const dou
     return acc * 1.0;
 }
 
-// indicator_minmod / indicator_meanerr with the division-heavy evaluations
-// replaced by precomputed points (same operations, same results)
-template <int P>
-SK_HD bool indicator_minmod_pre(const Basis& b, const double* um, const double* u0, const double* up) {
-    double mean_m = mean<P>(b, um);
-    double mean_0 = mean<P>(b, u0);
-    double mean_p = mean<P>(b, up);
-    double u0_plus = eval_at<P>(basis_evalpt<P>(b, 1), u0) - mean_0;
-    double u0_minus = mean_0 - eval_at<P>(basis_evalpt<P>(b, 0), u0);
-    double d_plus = mean_p - mean_0;
-    double d_minus = mean_0 - mean_m;
-    double scale = fabs(mean_m);
-    double v;
-    v = fabs(mean_0); if (scale < v) scale = v;
-    v = fabs(mean_p); if (scale < v) scale = v;
-    v = fabs(u0_plus); if (scale < v) scale = v;
-    v = fabs(u0_minus); if (scale < v) scale = v;
-    v = fabs(d_plus); if (scale < v) scale = v;
-    v = fabs(d_minus); if (scale < v) scale = v;
-    double guard = 1e-13 * scale;
-    return fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard ||
-           fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard;
-}
-
-template <int P>
-SK_HD bool indicator_meanerr_pre(const Basis& b, const PostCfg& c, const double* um, const double* u0,
-                                 const double* up) {
-    double mean_m = mean<P>(b, um);
-    double mean_0 = mean<P>(b, u0);
-    double mean_p = mean<P>(b, up);
-    double denom = dmax2(fabs(mean_m), dmax2(fabs(mean_0), fabs(mean_p)));
-    if (denom <= 0.0) return false;
-    double ext_m = integrate_pre<P>(b, c.ipt, c.ipden, um);
-    double ext_p = integrate_pre<P>(b, c.imt, c.imden, up);
-    double ind = (fabs(ext_m - mean_0) + fabs(ext_p - mean_0)) / denom;
-    return ind > c.threshold;
-}
-
 // fast-mode indicators (tolerance mode): DFMA sums and multiplication by the
 // precomputed reciprocals instead of the exact-order divisions
 template <int P>
@@ -714,22 +676,6 @@ SK_HD double eval_end_fast(const Basis& b, const double* u, int one, double rc) 
 #pragma unroll
     for (int n = 0; n < P; ++n) num = fma(one ? b.ev1[n] : b.ev0[n], u[n], num);
     return num * rc;
-}
-template <int P>
-SK_HD bool indicator_minmod_fast(const Basis& b, const PostCfg& c, const double* um, const double* u0,
-                                 const double* up) {
-    const double mean_m = mean_f<P, true>(b, um);
-    const double mean_0 = mean_f<P, true>(b, u0);
-    const double mean_p = mean_f<P, true>(b, up);
-    const double u0_plus = eval_end_fast<P>(b, u0, 1, c.ev1rc) - mean_0;
-    const double u0_minus = mean_0 - eval_end_fast<P>(b, u0, 0, c.ev0rc);
-    const double d_plus = mean_p - mean_0;
-    const double d_minus = mean_0 - mean_m;
-    double scale = fmax(fmax(fmax(fabs(mean_m), fabs(mean_0)), fmax(fabs(mean_p), fabs(u0_plus))),
-                        fmax(fmax(fabs(u0_minus), fabs(d_plus)), fabs(d_minus)));
-    const double guard = 1e-13 * scale;
-    return (fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard) |
-           (fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard);
 }
 template <int P>
 SK_HD double integrate_fast(const Basis& b, const double (*t)[SK_MAXP], const double* rc, const double* u) {
@@ -743,17 +689,84 @@ SK_HD double integrate_fast(const Basis& b, const double (*t)[SK_MAXP], const do
     }
     return acc;
 }
-template <int P>
-SK_HD bool indicator_meanerr_fast(const Basis& b, const PostCfg& c, const double* um, const double* u0,
-                                  const double* up) {
-    const double mean_m = mean_f<P, true>(b, um);
-    const double mean_0 = mean_f<P, true>(b, u0);
-    const double mean_p = mean_f<P, true>(b, up);
-    const double denom = fmax(fabs(mean_m), fmax(fabs(mean_0), fabs(mean_p)));
-    if (!(denom > 0.0)) return false;
-    const double ext_m = integrate_fast<P>(b, c.ipt, c.iprc, um);
-    const double ext_p = integrate_fast<P>(b, c.imt, c.imrc, up);
-    return fabs(ext_m - mean_0) + fabs(ext_p - mean_0) > c.threshold * denom;
+// The post-limiter indicators split into a per-cell summary and a decision
+// from the three summaries of a stencil: indicator_minmod / indicator_meanerr
+// above with PostCfg's precomputed points (fast mode: DFMA sums and the
+// reciprocals), the same operations in the same order wherever a cell is
+// met, so a pass that meets every cell once (the v flags fused into the v
+// sweep) decides bitwise like the stencil passes.
+// minmod: (mean, value at xi = 1, value at xi = 0); meanerr: (mean, the cell's
+// extension over its right neighbour, over its left neighbour).
+struct PostSum {
+    double m, a, b;
+};
+template <int P, bool FAST, int IND>
+SK_HD PostSum post_summary(const Basis& b, const PostCfg& c, const double* u) {
+    PostSum s;
+    if constexpr (FAST) {
+        s.m = mean_f<P, true>(b, u);
+        if constexpr (IND == 1) {
+            s.a = eval_end_fast<P>(b, u, 1, c.ev1rc);
+            s.b = eval_end_fast<P>(b, u, 0, c.ev0rc);
+        } else {
+            s.a = integrate_fast<P>(b, c.ipt, c.iprc, u);
+            s.b = integrate_fast<P>(b, c.imt, c.imrc, u);
+        }
+    } else {
+        s.m = mean<P>(b, u);
+        if constexpr (IND == 1) {
+            s.a = eval_at<P>(basis_evalpt<P>(b, 1), u);
+            s.b = eval_at<P>(basis_evalpt<P>(b, 0), u);
+        } else {
+            s.a = integrate_pre<P>(b, c.ipt, c.ipden, u);
+            s.b = integrate_pre<P>(b, c.imt, c.imden, u);
+        }
+    }
+    return s;
+}
+template <bool FAST, int IND>
+SK_HD bool post_decide(const PostCfg& c, const PostSum& sm, const PostSum& s0, const PostSum& sp) {
+    if constexpr (IND == 1) {  // minmod
+        const double u0_plus = s0.a - s0.m;
+        const double u0_minus = s0.m - s0.b;
+        const double d_plus = sp.m - s0.m;
+        const double d_minus = s0.m - sm.m;
+        if constexpr (FAST) {
+            const double scale = fmax(fmax(fmax(fabs(sm.m), fabs(s0.m)), fmax(fabs(sp.m), fabs(u0_plus))),
+                                      fmax(fmax(fabs(u0_minus), fabs(d_plus)), fabs(d_minus)));
+            const double guard = 1e-13 * scale;
+            return (fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard) |
+                   (fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard);
+        } else {
+            double scale = fabs(sm.m);
+            double v;
+            v = fabs(s0.m); if (scale < v) scale = v;
+            v = fabs(sp.m); if (scale < v) scale = v;
+            v = fabs(u0_plus); if (scale < v) scale = v;
+            v = fabs(u0_minus); if (scale < v) scale = v;
+            v = fabs(d_plus); if (scale < v) scale = v;
+            v = fabs(d_minus); if (scale < v) scale = v;
+            const double guard = 1e-13 * scale;
+            return fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard ||
+                   fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard;
+        }
+    } else {  // mean error: ext_m = sm.a, ext_p = sp.b
+        if constexpr (FAST) {
+            const double denom = fmax(fabs(sm.m), fmax(fabs(s0.m), fabs(sp.m)));
+            if (!(denom > 0.0)) return false;
+            return fabs(sm.a - s0.m) + fabs(sp.b - s0.m) > c.threshold * denom;
+        } else {
+            const double denom = dmax2(fabs(sm.m), dmax2(fabs(s0.m), fabs(sp.m)));
+            if (denom <= 0.0) return false;
+            const double ind = (fabs(sm.a - s0.m) + fabs(sp.b - s0.m)) / denom;
+            return ind > c.threshold;
+        }
+    }
+}
+template <int P, bool FAST, int IND>
+SK_HD bool post_flag_sum(const Basis& b, const PostCfg& c, const double* um, const double* u0, const double* up) {
+    return post_decide<FAST, IND>(c, post_summary<P, FAST, IND>(b, c, um), post_summary<P, FAST, IND>(b, c, u0),
+                                  post_summary<P, FAST, IND>(b, c, up));
 }
 
 template <int P>

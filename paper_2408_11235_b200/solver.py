@@ -479,6 +479,10 @@ class Context:
         """fuse step n's second and step n+1's first x half sweep in run_steps"""
         _check(N.lib().sk_ctx_set_step_fusion(self.h, int(on)))
 
+    def set_post_fusion(self, on: bool):
+        """decide the post limiter V's flags inside the v sweep (default on)"""
+        _check(N.lib().sk_ctx_set_post_fusion(self.h, int(on)))
+
     def synchronize(self):
         _check(N.lib().sk_ctx_synchronize(self.h))
 

@@ -409,6 +409,44 @@ def test_errors_map_to_reference_exceptions(sk):
     assert ei.value.step == 1
 
 
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "fast"])
+@pytest.mark.parametrize("kw", [
+    dict(k=3, nf=16, nc=32, m=1, nv=64, mu=1836.0, limiter="minmod+line"),
+    dict(k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter="meanerr+simple"),
+    dict(k=2, nf=16, nc=16, m=1, nv=48, limiter="meanerr+line"),
+    dict(k=1, nf=12, nc=24, m=4, nv=40, limiter="minmod+simple"),
+    dict(k=5, nf=8, nc=8, m=1, nv=40, limiter="minmod+line")],
+    ids=["k3_minmod_line", "k3_meanerr_simple_m2", "k2_meanerr_line", "k1_minmod_simple_m4", "k5_minmod_line"])
+def test_post_v_flags_fused_into_v_sweep(sk, kw, exact):
+    """The step's v sweep decides the post limiter V's flags from the
+    registers it stores (each chunk also computes its two neighbour cells;
+    walls are zero cells) and the post pass only runs the fixes
+    (sk_ctx_set_post_fusion). Same summaries, same decisions as the separate
+    flag pass, so 12 steps through both shrinks agree bitwise with fusion
+    off: f, E, v_max, shrink steps and the limiter counters. v meshes of 2
+    chunks, a ragged last chunk; k = 5 in fast mode keeps the pass (no DFMA
+    sweep for k > 3)."""
+    cfg = cfg_of(sk, **kw)
+    a, b = sk.SimulationState(cfg, exact=exact), sk.SimulationState(cfg, exact=exact)
+    a.ctx.set_post_fusion(True)
+    b.ctx.set_post_fusion(False)
+    for st in (a, b):
+        st.run_step()  # (eager body: first-step shrink)
+        st.run_steps(11)
+    assert a.step_index() == b.step_index() == 12
+    for sp in (0, 1):
+        assert a.shrinks(sp) == b.shrinks(sp)
+        assert a.field(sp).vmax() == b.field(sp).vmax()
+        assert np.array_equal(a.field(sp).download(), b.field(sp).download()), f"sp{sp}"
+    assert np.array_equal(a.E(), b.E())
+    sa, sb = a.stats(), b.stats()
+    assert sa["post_checked"] == sb["post_checked"] > 0
+    assert sa["post_troubled"] == sb["post_troubled"] > 0
+    # the fused runs launched no v flag pass (one kernel less per step)
+    fused = exact or kw["k"] <= 3
+    assert b.launches() - a.launches() == (12 if fused else 0)
+
+
 @pytest.mark.parametrize("kw", [
     dict(k=3, nf=32, nc=64, m=1, nv=128, mu=1836.0, limiter="sldg"),
     dict(k=2, nf=16, nc=32, m=1, nv=64, limiter="none"),
