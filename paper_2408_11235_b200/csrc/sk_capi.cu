@@ -408,7 +408,7 @@ sk_status ensure_xghost(sk_ctx* c, int nlines) {
 sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg, double threshold,
                      int check_finite, double* rho_out = nullptr, const int* gate = nullptr, int gate_on = 0,
                      bool swap = true, bool fused_reduce = false, const sk_state* src = nullptr,
-                     int src_mode = 0) {
+                     int src_mode = 0, const sk_limiter* post_lim = nullptr) {
     sk_ctx* c = fs[0]->ctx;
     XSweepArgs a{};
     a.basis = c->basis;
@@ -478,7 +478,12 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
             c->launches += 1;
         }
     }
-    if (inline_sldg) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
+    if (post_lim) {  // (caller checked post_x_fusable): the post limiter X's flags of the outputs
+        a.post_x = post_lim->indicator;
+        a.post = post_cfg(post_lim);
+        post_cfg_points(c->basis, a.post);
+    }
+    if (inline_sldg || post_lim) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
     c->launches += 1;
     if (c->fix_timer)
@@ -622,6 +627,14 @@ sk_status enq_vtab(sk_field** fs, int nspecies, const double* E, double tau, con
 // walls and no v halo (the extra neighbour outputs must be the stencil's
 // cells), and the indicator in the sweep's arithmetic (fast mode has DFMA
 // sweeps for k <= 3 only)
+// the same for the post limiter X inside an x half sweep (no fused source or
+// moment in that sweep; block edges and tile edges go to the fix kernel as
+// candidates, so 3-block meshes fuse too)
+bool post_x_fusable(sk_field** fs, const sk_limiter* lim, int periodic, int src_mode) {
+    const sk_ctx* c = fs[0]->ctx;
+    return lim && lim->indicator != 0 && c->post_fuse && !periodic && !lim->inline_sldg && src_mode == 0 &&
+           ((c->exact & SK_EXACT_ARITH) || c->P <= 4);
+}
 bool post_v_fusable(sk_field** fs, const sk_limiter* lim, int periodic) {
     const sk_ctx* c = fs[0]->ctx;
     return lim && lim->indicator != 0 && c->post_fuse && !periodic && !lim->inline_sldg && fs[0]->gl() == 0 &&
@@ -726,7 +739,7 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     a.fix_count = c->fix_count;
     a.fix_cap = c->fix_cap;
     a.fix_vals = c->fix_vals;
-    a.flags_queued = flags_queued && dir == SK_DIR_V;  // (the v sweep queued them: keep the list)
+    a.flags_queued = flags_queued;  // (the sweep queued them: keep the list)
     if (!a.flags_queued) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     if (dir == SK_DIR_X)
         CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
@@ -1804,6 +1817,8 @@ sk_status enq_phase_a(sk_state* s, bool fuse_in = false) {
     // the charge-density moment rides along the first x sweep unless a post
     // limiter still has to modify f (or the parity mode wants the serial order)
     const bool fuse = !post && !(c->exact & SK_EXACT_RHO);
+    // the post limiter X's flags ride in the x sweep where they can
+    const bool px1 = !fuse_in && post_x_fusable(fs, lim, 0, src1);
     {
         FixTimer ft(s, PH_X1_FIX);
         if ((rc = mark(s, PH_X1))) return rc;
@@ -1812,11 +1827,11 @@ sk_status enq_phase_a(sk_state* s, bool fuse_in = false) {
             CK(launch_flip_toggle(c->st, fs[0]->dflip, fs[1]->dflip, c->stream));
             c->launches += 1;
         } else if ((rc = enq_xsweep(fs, 2, 0, inl, thr, 0, fuse ? s->rho : nullptr, nullptr, 0, true, false, s,
-                                    src1))) {
+                                    src1, px1 ? lim : nullptr))) {
             return rc;
         }
     }
-    if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
+    if (post && ((rc = mark(s, PH_POST_X1)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0, px1)))) return rc;
     if (!fuse && ((rc = mark(s, PH_RHO)) || (rc = enq_rho(fs[0], fs[1], s->rho)))) return rc;
     return SK_OK;
 }
@@ -1860,14 +1875,16 @@ sk_status enq_phase_b2(sk_state* s, bool fuse_out = false) {
     // stepper.cpp:93-97 (injection): source half step at state.time + half --
     // fused into the second x sweep's stores unless a post limiter runs between
     const int src2 = !post && source_fusable(s) ? 2 : 0;
+    const bool px2 = !fuse_out && post_x_fusable(fs, lim, 0, src2);
     {
         FixTimer ft(s, PH_X2_FIX);
         if ((rc = mark(s, PH_X2))) return rc;
         if ((rc = fuse_out ? enq_fused_boundary(s, inl, thr)
-                           : enq_xsweep(fs, 2, 0, inl, thr, 1, nullptr, nullptr, 0, true, false, s, src2)))
+                           : enq_xsweep(fs, 2, 0, inl, thr, 1, nullptr, nullptr, 0, true, false, s, src2,
+                                        px2 ? lim : nullptr)))
             return rc;
     }
-    if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0)))) return rc;
+    if (post && ((rc = mark(s, PH_POST_X2)) || (rc = enq_post(fs, 2, SK_DIR_X, lim, 0, px2)))) return rc;
     return src2 ? SK_OK : enq_source(s, 1);
 }
 

@@ -126,6 +126,9 @@ __device__ __forceinline__ void defer_push_n(unsigned int* count, unsigned int c
 // coalesced copy per flush, so a warp stalls on the contended counter once per
 // kQCap entries instead of once per flagged tile. n is warp-uniform.
 constexpr int kQCap = 64;
+// post-limiter list entries (sp << 63 | row << 32 | col): bit 62 marks a
+// candidate whose flag the fix kernel decides from the field (rows < 2^30)
+constexpr unsigned long long kPostCandidate = 1ull << 62;
 __device__ __forceinline__ void wq_flush(unsigned long long* q, int& n, unsigned int* count,
                                          unsigned int cap, unsigned long long* list,
                                          unsigned members = 0xffffffffu) {
@@ -622,8 +625,13 @@ struct XCfg {
                                     8 * 2 * S3 + 8 * NC * kQCap + sizeof(int) * (2 * (T + 1) + 4);
     // MODE 1/2 (post-limiter flag passes): full T-cell tiles with a T + 2 cell window
     static constexpr size_t SMEM12 = sizeof(double) * (size_t)(S * STAGE3) + 8 * 2 * S + 8 * NC * kQCap;
+    // MODE 4 / 5 (sweep + post-limiter flags): the tile's output summaries
+    // [2 tile parities][m, a, b][T] after the queues
+    static constexpr size_t SMEM45 = SMEM + sizeof(double) * 2 * 3 * T;
     template <int MODE>
-    static constexpr size_t smem() { return MODE == 3 ? SMEM3 : (MODE == 1 || MODE == 2) ? SMEM12 : SMEM; }
+    static constexpr size_t smem() {
+        return MODE == 3 ? SMEM3 : (MODE == 1 || MODE == 2) ? SMEM12 : MODE >= 4 ? SMEM45 : SMEM;
+    }
 };
 
 struct XTile {
@@ -746,6 +754,14 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     constexpr bool kDmma = kXsweepDmma && P == 4 && FMA && MODE == 0 && C::T % (C::NC * 8) == 0;
     if (halted(a.st)) return;
     static_assert(MODE == 0 || MODE == 3 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
+    static_assert(MODE < 4 || SRC == 0, "fused post flags: no fused source");
+    // MODE 4 / 5: the x sweep deciding the post limiter's x flags (minmod /
+    // mean error) of its own outputs -- summaries of the tile's cells in
+    // shared memory, one consumer barrier, each cell's decision from its
+    // neighbours' summaries; a tile's first and last cell (neighbour in
+    // another tile or block) go to the list as candidates the fix kernel
+    // re-decides from the field
+    constexpr int PX = MODE >= 4 ? MODE - 3 : 0;
     static_assert(MODE != 3 || C::T <= 2 * C::NT, "MODE 3: T + 1 intermediate cells over 3 passes of the consumers");
     if (a.gate && ((*a.gate != 0) != (a.gate_on != 0))) return;  // device-decided alternative
     // cells per tile: T in every mode -- the flag passes (one neighbour cell
@@ -753,9 +769,10 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     // shortening the tile, so power-of-two blocks split into full tiles (511-
     // cell tiles left 1-2 cell remainder tiles in most lines)
     constexpr int TT = C::T;
-    constexpr int WIN = MODE == 0 ? C::WIN : C::WIN3;
-    constexpr int STAGE = MODE == 0 ? C::STAGE : C::STAGE3;
-    constexpr int WX = MODE >= 1 ? 2 : 1;            // window cells beyond the tile
+    constexpr bool SWEEP = MODE == 0 || MODE >= 4;   // one plain half sweep per tile
+    constexpr int WIN = SWEEP ? C::WIN : C::WIN3;
+    constexpr int STAGE = SWEEP ? C::STAGE : C::STAGE3;
+    constexpr int WX = SWEEP ? 1 : 2;                // window cells beyond the tile
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;                                   // S x STAGE
     double* racc = smem + S * STAGE;                         // [T][P] this CTA's column (RHO)
@@ -768,6 +785,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     [[maybe_unused]] double* mid = reinterpret_cast<double*>(wqueue + C::NC * kQCap);
     [[maybe_unused]] double* rowc = mid + 2 * (C::T + 1) * P;
     [[maybe_unused]] int* tl1 = reinterpret_cast<int*>(rowc + 2 * (C::NF + 2));
+    [[maybe_unused]] double* psum = reinterpret_cast<double*>(wqueue + C::NC * kQCap);  // MODE 4 / 5
     const Grid& g = a.grid;
     const int ntot = a.nspecies * a.nlines * a.tile_start[g.nblocks];
     const int G = gridDim.x;
@@ -912,7 +930,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     bytes += (unsigned)(gb - ga) * 8;
                 }
                 mbar_expect_tx(&full[stg], bytes);
-                if constexpr (MODE == 0 || MODE == 3) tma_load_1d(st + WIN, row_of(x), C::NF * 8, &full[stg]);
+                if constexpr (SWEEP || MODE == 3) tma_load_1d(st + WIN, row_of(x), C::NF * 8, &full[stg]);
                 if (gb > ga) {
                     double* dst = st + 2 + woff + (ga - eg);
                     tma_load_1d(dst, srcp(x.sp) + ga, (unsigned)(gb - ga) * 8, &full[stg]);
@@ -1267,6 +1285,19 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
                     stg_cell<P>(dline + (long long)c * P, o[cc]);
                 }
             }
+            if constexpr (PX != 0) {  // the post limiter's summaries of the stored cells
+                double* q = psum + (it & 1) * 3 * C::T;
+#pragma unroll
+                for (int cc = 0; cc < NCC; ++cc) {
+                    const int c = tid + cc * C::NT;
+                    if (c < nt) {
+                        const PostSum ps = post_summary<P, FMA, PX>(a.basis, a.post, o[cc]);
+                        q[c] = ps.m;
+                        q[C::T + c] = ps.a;
+                        q[2 * C::T + c] = ps.b;
+                    }
+                }
+            }
         };
         // (the fused-moment variant keeps one body: its register accumulators
         // leave no room for a second)
@@ -1277,6 +1308,31 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
         } else {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+        if constexpr (PX != 0) {
+            // every summary of the tile is in (double-buffered by tile parity,
+            // so one barrier per tile orders both the reads and the next writes)
+            consumer_sync(C::NT);
+            const double* q = psum + (it & 1) * 3 * C::T;
+            auto sum_at = [&](int c) { return PostSum{q[c], q[C::T + c], q[2 * C::T + c]}; };
+            bool tr[C::CPT];
+            unsigned long long entry[C::CPT];
+#pragma unroll
+            for (int cc = 0; cc < C::CPT; ++cc) {
+                const int c = tid + cc * C::NT;
+                tr[cc] = false;
+                entry[cc] = ((unsigned long long)(sp & 1) << 63) | ((unsigned long long)line << 32) |
+                            (unsigned)(g.start[b] + c0 + c);
+                if (c < nt) {
+                    if (c == 0 || c == nt - 1) {  // neighbour outside the tile: a candidate
+                        tr[cc] = true;
+                        entry[cc] |= kPostCandidate;
+                    } else {
+                        tr[cc] = post_decide<FMA, PX>(a.post, sum_at(c - 1), sum_at(c), sum_at(c + 1));
+                    }
+                }
+            }
+            wq_push<C::CPT>(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list, tr, entry);
         }
         }
     }
@@ -1303,7 +1359,7 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
             }
         }
     }
-    if constexpr (INLINE || MODE == 1 || MODE == 2) wq_flush(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list);
+    if constexpr (INLINE || MODE == 1 || MODE == 2 || PX != 0) wq_flush(wq, wq_n, a.fix_count, a.fix_cap, a.fix_list);
     if constexpr (INLINE && MODE == 3) {
         count_flags(a.st->stats[0], f3[0][0], f3[0][1], f3[0][2]);
         count_flags(a.st->stats[1], f3[1][0], f3[1][1], f3[1][2]);
@@ -3036,10 +3092,12 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         int sp, row, col;  // x: row = line, col = cell; v: row = v cell, col = x dof
+        bool cand = false;  // queued by a sweep whose stencil crossed its tile: decide here
         if (!rescan) {
             const unsigned long long e = a.fix_list[i];
             sp = (int)(e >> 63);
-            row = (int)((e >> 32) & 0x7fffffffu);
+            cand = (e & kPostCandidate) != 0;
+            row = (int)((e >> 32) & 0x3fffffffu);
             col = (int)(e & 0xffffffffu);
         } else {
             sp = a.species0 + (int)(i / per_sp);
@@ -3067,7 +3125,12 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
             at = (long long)row * P * a.ld + col;
             ds = a.ld;
         }
-        if (rescan && !post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)) continue;
+        if ((rescan || cand) && !post_flag<P, FAST>(a.cfg, a.basis, um, u0, up)) {
+            if (cand)  // not flagged: the scatter writes the cell's own values back
+#pragma unroll
+                for (int m = 0; m < P; ++m) a.fix_vals[i * P + m] = u0[m];
+            continue;
+        }
         post_modify<P>(a.cfg, a.basis, um, u0, up, o);
         if (rescan) {
             double* out = post_live(a, sp);
@@ -3104,7 +3167,7 @@ __global__ void __launch_bounds__(128) post_scatter_kernel(const __grid_constant
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride) {
         const unsigned long long e = a.fix_list[i];
         const int sp = (int)(e >> 63);
-        const int row = (int)((e >> 32) & 0x7fffffffu);
+        const int row = (int)((e >> 32) & 0x3fffffffu);
         const int col = (int)(e & 0xffffffffu);
         double* out = post_live(a, sp);
         const long long at = DIR == 0 ? ((long long)row * g.ncells + col) * P : (long long)row * P * a.ld + col;
@@ -3268,6 +3331,12 @@ cudaError_t launch_xghost(const XSweepArgs& a, cudaStream_t s) {
 
 template <int P, bool INLINE, bool RHO, bool FMA>
 static cudaError_t launch_xsweep_s(const XSweepArgs& a, cudaStream_t s) {
+    if constexpr (!INLINE && !RHO)
+        if (a.post_x == 1 || a.post_x == 2) {  // (the host fuses only without a fused source)
+            if (a.src_mode) return cudaErrorInvalidValue;
+            return a.post_x == 1 ? launch_xsweep_t<P, false, false, FMA, 4, 0>(a, s)
+                                 : launch_xsweep_t<P, false, false, FMA, 5, 0>(a, s);
+        }
     if (a.src_mode == 1) return launch_xsweep_t<P, INLINE, RHO, FMA, 0, 1>(a, s);
     if constexpr (!RHO)  // (the second source half step rides in the second x sweep: no moment)
         if (a.src_mode == 2) return launch_xsweep_t<P, INLINE, RHO, FMA, 0, 2>(a, s);
@@ -3725,7 +3794,8 @@ static cudaError_t launch_post_x_t(const PostArgs& a, cudaStream_t s) {
     x.post = a.cfg;
     XSweepArgs b;
     int grid = 0;
-    if (a.cfg.indicator == 1) {
+    if (a.flags_queued) {  // the x sweep queued them (MODE 4 / 5)
+    } else if (a.cfg.indicator == 1) {
         if (cudaError_t e = xsweep_plan<P, false, false, FAST, 1>(x, b, grid)) return e;
         if (grid > 0)
             pdl_launch(xsweep_kernel<P, false, false, FAST, 1>, grid, (XCfg<P>::NC + 1) * 32, XCfg<P>::template smem<1>(), s, b);

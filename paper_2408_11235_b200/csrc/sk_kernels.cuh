@@ -75,6 +75,9 @@ struct XSweepArgs {
     // post-limiter flag pass (xsweep_kernel MODE 1): the literature indicator
     // of every cell from its window, in place; flagged cells are queued
     PostCfg post;
+    // sweep + post-limiter x flags of its outputs (1 minmod, 2 mean error;
+    // xsweep_kernel MODE 4 / 5; 0: plain sweep)
+    int post_x;
     // device-decided alternatives (fused / unfused step boundary): the kernel
     // runs only if (*gate != 0) == gate_on; gate == nullptr: always
     const int* gate;
@@ -235,7 +238,7 @@ struct PostArgs {
     unsigned int* fix_count;
     unsigned int fix_cap;
     double* fix_vals;      // [fix_cap][P] modified values, scattered after all are computed
-    int flags_queued;      // v: the v sweep already queued the flags (VSweepArgs::post_v)
+    int flags_queued;      // the sweep already queued the flags (VSweepArgs::post_v, XSweepArgs::post_x)
 };
 
 // launchers (P = k+1 dispatch inside)

@@ -417,15 +417,18 @@ def test_errors_map_to_reference_exceptions(sk):
     dict(k=1, nf=12, nc=24, m=4, nv=40, limiter="minmod+simple"),
     dict(k=5, nf=8, nc=8, m=1, nv=40, limiter="minmod+line")],
     ids=["k3_minmod_line", "k3_meanerr_simple_m2", "k2_meanerr_line", "k1_minmod_simple_m4", "k5_minmod_line"])
-def test_post_v_flags_fused_into_v_sweep(sk, kw, exact):
-    """The step's v sweep decides the post limiter V's flags from the
-    registers it stores (each chunk also computes its two neighbour cells;
-    walls are zero cells) and the post pass only runs the fixes
-    (sk_ctx_set_post_fusion). Same summaries, same decisions as the separate
-    flag pass, so 12 steps through both shrinks agree bitwise with fusion
-    off: f, E, v_max, shrink steps and the limiter counters. v meshes of 2
-    chunks, a ragged last chunk; k = 5 in fast mode keeps the pass (no DFMA
-    sweep for k > 3)."""
+def test_post_flags_fused_into_sweeps(sk, kw, exact):
+    """The step's sweeps decide the post limiter's flags of their own outputs
+    and the post passes only run the fixes (sk_ctx_set_post_fusion): the v
+    sweep from the registers it stores (each chunk also computes its two
+    neighbour cells; walls are zero cells), the x sweeps from the tile's
+    summaries in shared memory (a tile's first and last cell -- incl. every
+    block edge of the 3-block meshes -- re-decided by the fix kernel as
+    candidates). Same summaries, same decisions as the separate flag passes,
+    so 12 steps through both shrinks agree bitwise with fusion off: f, E,
+    v_max, shrink steps and the limiter counters. v meshes of 2 chunks, a
+    ragged last chunk; k = 5 in fast mode keeps the passes (no DFMA sweep
+    for k > 3)."""
     cfg = cfg_of(sk, **kw)
     a, b = sk.SimulationState(cfg, exact=exact), sk.SimulationState(cfg, exact=exact)
     a.ctx.set_post_fusion(True)
@@ -442,9 +445,9 @@ def test_post_v_flags_fused_into_v_sweep(sk, kw, exact):
     sa, sb = a.stats(), b.stats()
     assert sa["post_checked"] == sb["post_checked"] > 0
     assert sa["post_troubled"] == sb["post_troubled"] > 0
-    # the fused runs launched no v flag pass (one kernel less per step)
+    # the fused runs launched no flag pass (x1, v, x2: three kernels less per step)
     fused = exact or kw["k"] <= 3
-    assert b.launches() - a.launches() == (12 if fused else 0)
+    assert b.launches() - a.launches() == (36 if fused else 0)
 
 
 @pytest.mark.parametrize("kw", [
@@ -834,7 +837,9 @@ def test_injection_scenario(sk, ora, kw, exact, monkeypatch):
     for sp in (0, 1):
         assert not st.field(sp).download().any()
     # the fused path launches no separate source kernels: as many kernels per
-    # loop body as the blob scenario on the same grid (one more with a post limiter)
+    # loop body as the blob scenario on the same grid (with a post limiter two
+    # more: the second source half step, and the first x sweep, which carries
+    # the source, leaves its post flags to the separate pass)
     blob = sk.SimulationState(dataclasses.replace(cfg, scenario="blob"), exact=exact)
     l0, b0 = st.launches(), blob.launches()
     blob.run_step()
@@ -843,7 +848,7 @@ def test_injection_scenario(sk, ora, kw, exact, monkeypatch):
         st.run_step()
         if s == 0:
             extra = (st.launches() - l0) - (blob.launches() - b0)
-            assert extra == (1 if "+" in kw["limiter"] else 0), extra
+            assert extra == (2 if "+" in kw["limiter"] else 0), extra
         for sp in (0, 1):
             got, want = st.field(sp).download(), o.field(sp)
             if exact:
