@@ -77,6 +77,11 @@ struct sk_ctx {
     // limiter arithmetic), SK_EXACT_RHO (reference summation order of the charge
     // density), SK_EXACT_POISSON (reference dpbtrs order); SK_EXACT_ALL = all three
     int exact = 0;
+    // a fused charge density whose reduction waits for the post limiter X's
+    // fixes (enq_xsweep with rho_out and post_lim; enq_phase_a reduces)
+    bool rho_pending = false;
+    double* rho_pending_out = nullptr;
+    XSweepArgs rho_pending_args{};
     double* rho_fpart = nullptr;       // fused charge-density partials
     size_t rho_fpart_n = 0;
     unsigned long long* rho_corr = nullptr;
@@ -448,6 +453,11 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
         a.src_half = 0.5 * src->cfg.dt;
         a.src_t0 = src->cfg.t0;
     }
+    if (post_lim) {  // (caller checked post_x_fusable): the post limiter X's flags of the outputs
+        a.post_x = post_lim->indicator;
+        a.post = post_cfg(post_lim);
+        post_cfg_points(c->basis, a.post);
+    }
     if (rho_out) {  // fused charge density (both species in this launch)
         a.rho_fuse = 1;
         for (int i = 0; i < nspecies; ++i) {
@@ -478,11 +488,6 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
             c->launches += 1;
         }
     }
-    if (post_lim) {  // (caller checked post_x_fusable): the post limiter X's flags of the outputs
-        a.post_x = post_lim->indicator;
-        a.post = post_cfg(post_lim);
-        post_cfg_points(c->basis, a.post);
-    }
     if (inline_sldg || post_lim) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     CK(launch_xsweep(a, c->xtiles[c->grid.nblocks], c->stream));
     c->launches += 1;
@@ -492,7 +497,11 @@ sk_status enq_xsweep(sk_field** fs, int nspecies, int periodic, int inline_sldg,
         CK(launch_xfix(a, c->stream));
         c->launches += 1;
     }
-    if (rho_out) {
+    if (rho_out && post_lim) {  // reduced after the post limiter's fixes (their corrections)
+        c->rho_pending = true;
+        c->rho_pending_out = rho_out;
+        c->rho_pending_args = a;
+    } else if (rho_out) {
         CK(launch_rho_fused_reduce(a, rho_out, c->stream));
         c->launches += 1;
         if (fused_reduce) {
@@ -740,12 +749,24 @@ sk_status enq_post(sk_field** fs, int nspecies, int dir, const sk_limiter* lim, 
     a.fix_cap = c->fix_cap;
     a.fix_vals = c->fix_vals;
     a.flags_queued = flags_queued;  // (the sweep queued them: keep the list)
+    if (dir == SK_DIR_X && c->rho_pending) {  // the sweep before fused the charge density
+        a.rho_corr = c->rho_pending_args.rho_corr;
+        for (int i = 0; i < 2; ++i) {
+            a.charge_w[i] = c->rho_pending_args.charge_w[i];
+            a.vg[i] = c->rho_pending_args.vg[i];
+        }
+    }
     if (!a.flags_queued) CK(cudaMemsetAsync(c->fix_count, 0, sizeof(unsigned int), c->stream));
     if (dir == SK_DIR_X)
         CK(launch_post_x(a, c->ptiles[c->grid.nblocks], c->stream));
     else
         CK(launch_post_v(a, c->stream));
     c->launches += a.flags_queued ? 4 : 5;  // flag pass, overflow copy, fix, scatter, counter
+    if (dir == SK_DIR_X && c->rho_pending) {
+        c->rho_pending = false;
+        CK(launch_rho_fused_reduce(c->rho_pending_args, c->rho_pending_out, c->stream));
+        c->launches += 1;
+    }
     // in place: the field stays in its buffer
     return SK_OK;
 }
@@ -1528,6 +1549,13 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
         a.fma = 1;
         int g1 = xsweep_rho_groups(a);
         if (xsweep_fused_supported(c->P)) g1 = std::max(g1, xsweep_rho_groups(a, 1));  // fused boundaries
+        if (cfg->limiter.indicator) {  // the sweeps deciding the post limiter's X flags
+            a.post_x = cfg->limiter.indicator;
+            for (int fm = 0; fm < 2; ++fm) {
+                a.fma = fm;
+                g1 = std::max(g1, xsweep_rho_groups(a));
+            }
+        }
         const size_t need = (size_t)(g0 > g1 ? g0 : g1) * ne;
         if (need > c->rho_fpart_n) {
             if (c->rho_fpart) cudaFree(c->rho_fpart);
@@ -1630,6 +1658,13 @@ sk_status sk_state_create_shard(sk_ctx* c, const sk_run_config* cfg, int rank, i
         a.fma = 1;
         int g1 = xsweep_rho_groups(a);
         if (xsweep_fused_supported(c->P)) g1 = std::max(g1, xsweep_rho_groups(a, 1));  // fused boundaries
+        if (cfg->limiter.indicator) {  // the sweeps deciding the post limiter's X flags
+            a.post_x = cfg->limiter.indicator;
+            for (int fm = 0; fm < 2; ++fm) {
+                a.fma = fm;
+                g1 = std::max(g1, xsweep_rho_groups(a));
+            }
+        }
         const size_t need = (size_t)(g0 > g1 ? g0 : g1) * ne;
         if (need > c->rho_fpart_n) {
             if (c->rho_fpart) cudaFree(c->rho_fpart);
@@ -1814,11 +1849,12 @@ sk_status enq_phase_a(sk_state* s, bool fuse_in = false) {
     // x tables serve both x half-sweeps (same tau, same v grid within a step)
     if ((rc = mark(s, PH_XTAB)) || (rc = enq_xtab(fs, 2, half, s->sqrt_mu, inl, thr, -2, dt, -1)))
         return rc;
-    // the charge-density moment rides along the first x sweep unless a post
-    // limiter still has to modify f (or the parity mode wants the serial order)
-    const bool fuse = !post && !(c->exact & SK_EXACT_RHO);
-    // the post limiter X's flags ride in the x sweep where they can
+    // the charge-density moment rides along the first x sweep (unless the
+    // parity mode wants the serial order); with a post limiter only where the
+    // sweep also decides its X flags -- the fixes then correct the moment and
+    // it is reduced after them
     const bool px1 = !fuse_in && post_x_fusable(fs, lim, 0, src1);
+    const bool fuse = (!post || px1) && !(c->exact & SK_EXACT_RHO);
     {
         FixTimer ft(s, PH_X1_FIX);
         if ((rc = mark(s, PH_X1))) return rc;

@@ -753,8 +753,8 @@ __global__ void __launch_bounds__((XCfg<P>::NC + 1) * 32, XCfg<P>::MINB)
     // (profiles/r02_dmma_xsweep.txt).
     constexpr bool kDmma = kXsweepDmma && P == 4 && FMA && MODE == 0 && C::T % (C::NC * 8) == 0;
     if (halted(a.st)) return;
-    static_assert(MODE == 0 || MODE == 3 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
-    static_assert(MODE < 4 || SRC == 0, "fused post flags: no fused source");
+    static_assert(MODE == 0 || MODE >= 3 || (!INLINE && !RHO), "the flag pass has no sweep limiter or moment");
+    static_assert(MODE < 4 || (SRC == 0 && !INLINE), "fused post flags: no fused source, no inline limiter");
     // MODE 4 / 5: the x sweep deciding the post limiter's x flags (minmod /
     // mean error) of its own outputs -- summaries of the tile's cells in
     // shared memory, one consumer barrier, each cell's decision from its
@@ -3026,6 +3026,23 @@ __device__ __forceinline__ double* post_other(const PostArgs& a, int sp) {
     return const_cast<double*>(field_flipped(a.flip[sp]) ? a.src[sp] : a.dst[sp]);
 }
 
+// a modified cell's change to the charge density the x sweep fused (its
+// moment summed the unmodified values): exact integer corrections as the
+// sweep's clamp fixups add them (xfix_cell), same weight arithmetic
+template <int P>
+__device__ __forceinline__ void post_rho_corr(const PostArgs& a, int sp, int line, int cell, const double* o0,
+                                              const double* o) {
+    const int vn = line - (line / P) * P;
+    const double wdv = a.charge_w[sp] * a.basis.weights[vn] * a.vg[sp]->dx;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        if (o[q] == o0[q]) continue;
+        const double d = wdv * o[q] - wdv * o0[q];
+        rho_corr_add(a.rho_corr + (long long)(line % kRhoCorrCopies) * a.grid.ncells * P,
+                     (long long)kRhoCorrCopies * a.grid.ncells * P, (long long)cell * P + q, d);
+    }
+}
+
 // v flag pass: one thread per x dof walks kVChunk v cells (in place)
 template <int P, bool FAST, int IND>
 __global__ void __launch_bounds__(kVThreads) post_v_kernel(const __grid_constant__ PostArgs a) {
@@ -3134,6 +3151,7 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
         post_modify<P>(a.cfg, a.basis, um, u0, up, o);
         if (rescan) {
             double* out = post_live(a, sp);
+            if (DIR == 0 && a.rho_corr) post_rho_corr<P>(a, sp, row, col, u0, o);
 #pragma unroll
             for (int m = 0; m < P; ++m) out[at + m * ds] = o[m];
         } else {
@@ -3172,6 +3190,12 @@ __global__ void __launch_bounds__(128) post_scatter_kernel(const __grid_constant
         double* out = post_live(a, sp);
         const long long at = DIR == 0 ? ((long long)row * g.ncells + col) * P : (long long)row * P * a.ld + col;
         const long long ds = DIR == 0 ? 1 : a.ld;
+        if (DIR == 0 && a.rho_corr) {  // the sweep's fused moment summed the unmodified cell
+            double o0[P];
+#pragma unroll
+            for (int m = 0; m < P; ++m) o0[m] = out[at + m];
+            post_rho_corr<P>(a, sp, row, col, o0, a.fix_vals + i * P);
+        }
 #pragma unroll
         for (int m = 0; m < P; ++m) out[at + m * ds] = a.fix_vals[i * P + m];
     }
@@ -3331,11 +3355,11 @@ cudaError_t launch_xghost(const XSweepArgs& a, cudaStream_t s) {
 
 template <int P, bool INLINE, bool RHO, bool FMA>
 static cudaError_t launch_xsweep_s(const XSweepArgs& a, cudaStream_t s) {
-    if constexpr (!INLINE && !RHO)
+    if constexpr (!INLINE)
         if (a.post_x == 1 || a.post_x == 2) {  // (the host fuses only without a fused source)
             if (a.src_mode) return cudaErrorInvalidValue;
-            return a.post_x == 1 ? launch_xsweep_t<P, false, false, FMA, 4, 0>(a, s)
-                                 : launch_xsweep_t<P, false, false, FMA, 5, 0>(a, s);
+            return a.post_x == 1 ? launch_xsweep_t<P, false, RHO, FMA, 4, 0>(a, s)
+                                 : launch_xsweep_t<P, false, RHO, FMA, 5, 0>(a, s);
         }
     if (a.src_mode == 1) return launch_xsweep_t<P, INLINE, RHO, FMA, 0, 1>(a, s);
     if constexpr (!RHO)  // (the second source half step rides in the second x sweep: no moment)
@@ -3359,6 +3383,12 @@ static int rho_groups_t(const XSweepArgs& a) {
             e = xsweep_plan<P, INLINE, true, true, 3>(a, b, grid);
         else
             return 0;
+    } else if constexpr (MODE >= 4) {  // sweep + post flags (no inline limiter)
+        if constexpr (kHasFma<P>)
+            e = a.fma ? xsweep_plan<P, false, true, true, MODE>(a, b, grid)
+                      : xsweep_plan<P, false, true, false, MODE>(a, b, grid);
+        else
+            e = xsweep_plan<P, false, true, false, MODE>(a, b, grid);
     } else if constexpr (kHasFma<P>) {
         e = a.fma ? xsweep_plan<P, INLINE, true, true>(a, b, grid) : xsweep_plan<P, INLINE, true, false>(a, b, grid);
     } else {
@@ -3378,6 +3408,10 @@ int xsweep_rho_groups(const XSweepArgs& a, int fused) {
         }
     } else if (a.inline_sldg) {
         SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, true, 0>(a)))
+    } else if (a.post_x == 1) {
+        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, false, 4>(a)))
+    } else if (a.post_x == 2) {
+        SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, false, 5>(a)))
     } else {
         SK_DISPATCH_P(a.basis.p, return (rho_groups_t<PP, false, 0>(a)))
     }

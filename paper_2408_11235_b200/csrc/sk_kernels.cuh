@@ -239,6 +239,11 @@ struct PostArgs {
     unsigned int fix_cap;
     double* fix_vals;      // [fix_cap][P] modified values, scattered after all are computed
     int flags_queued;      // the sweep already queued the flags (VSweepArgs::post_v, XSweepArgs::post_x)
+    // x, after a sweep that fused the charge density: corrections of the
+    // modified cells (null: none)
+    unsigned long long* rho_corr;
+    double charge_w[2];
+    const DevVGrid* vg[2];
 };
 
 // launchers (P = k+1 dispatch inside)

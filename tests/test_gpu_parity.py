@@ -433,6 +433,9 @@ def test_post_flags_fused_into_sweeps(sk, kw, exact):
     a, b = sk.SimulationState(cfg, exact=exact), sk.SimulationState(cfg, exact=exact)
     a.ctx.set_post_fusion(True)
     b.ctx.set_post_fusion(False)
+    if not exact:  # the charge density in the reference order in both (its fusion: next test)
+        for st in (a, b):
+            st.ctx.set_exact_parts(st.ctx.EXACT_RHO)
     for st in (a, b):
         st.run_step()  # (eager body: first-step shrink)
         st.run_steps(11)
@@ -448,6 +451,39 @@ def test_post_flags_fused_into_sweeps(sk, kw, exact):
     # the fused runs launched no flag pass (x1, v, x2: three kernels less per step)
     fused = exact or kw["k"] <= 3
     assert b.launches() - a.launches() == (36 if fused else 0)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(k=3, nf=16, nc=32, m=1, nv=64, mu=1836.0, limiter="minmod+line"),
+    dict(k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter="meanerr+simple"),
+    dict(k=2, nf=16, nc=16, m=1, nv=48, limiter="meanerr+line")],
+    ids=["k3_minmod_line", "k3_meanerr_simple_m2", "k2_meanerr_line"])
+def test_post_limited_charge_density_fused(sk, ora, kw):
+    """Fast mode with a post limiter: the first x sweep, which decides the
+    post X flags, also sums the charge density; the fixes add the modified
+    cells' changes as exact integer corrections and the moment is reduced
+    after them. Against the separate charge-density pass (post fusion off)
+    over 3 steps: the same arithmetic grouped differently, so f and E agree
+    within the reference's rounding envelope, the counters and v_max
+    exactly; the fused run launches no rho pass (two kernels less per step:
+    rho partial + reduce -> one fused reduce; and three flag passes less)."""
+    cfg = cfg_of(sk, **kw)
+    a, b = sk.SimulationState(cfg), sk.SimulationState(cfg)
+    a.ctx.set_post_fusion(True)
+    b.ctx.set_post_fusion(False)
+    l0a, l0b = a.launches(), b.launches()
+    for _ in range(3):
+        a.run_step()
+        b.run_step()
+    assert (b.launches() - l0b) - (a.launches() - l0a) == 3 * (3 + 1)
+    ef, eE = _envelope(ora, cfg, 3)[3]
+    for sp in (0, 1):
+        assert a.field(sp).vmax() == b.field(sp).vmax()
+        fa, fb = a.field(sp).download(), b.field(sp).download()
+        assert rel(fa, fb) <= max(F_TOL, ENV_C * ef), f"sp{sp}"
+    Ea, Eb = a.E(), b.E()
+    assert np.abs(Ea - Eb).max() <= max(1e-12 * max(1.0, np.abs(Eb).max()), ENV_C * eE)
+    assert a.stats()["post_checked"] == b.stats()["post_checked"]
 
 
 @pytest.mark.parametrize("kw", [
@@ -839,7 +875,9 @@ def test_injection_scenario(sk, ora, kw, exact, monkeypatch):
     # the fused path launches no separate source kernels: as many kernels per
     # loop body as the blob scenario on the same grid (with a post limiter two
     # more: the second source half step, and the first x sweep, which carries
-    # the source, leaves its post flags to the separate pass)
+    # the source, leaves its post flags to the separate pass -- and in fast
+    # mode the charge density to its two-kernel pass, one more than blob's
+    # fused reduction)
     blob = sk.SimulationState(dataclasses.replace(cfg, scenario="blob"), exact=exact)
     l0, b0 = st.launches(), blob.launches()
     blob.run_step()
@@ -848,7 +886,7 @@ def test_injection_scenario(sk, ora, kw, exact, monkeypatch):
         st.run_step()
         if s == 0:
             extra = (st.launches() - l0) - (blob.launches() - b0)
-            assert extra == (2 if "+" in kw["limiter"] else 0), extra
+            assert extra == ((2 if exact else 3) if "+" in kw["limiter"] else 0), extra
         for sp in (0, 1):
             got, want = st.field(sp).download(), o.field(sp)
             if exact:
