@@ -631,6 +631,9 @@ struct PostCfg {
     double imt[SK_MAXP][SK_MAXP], imden[SK_MAXP];
     // fast mode: reciprocals of the denominators (and of evaluate()'s at 0, 1)
     double iprc[SK_MAXP], imrc[SK_MAXP], ev0rc, ev1rc;
+    // fast mode, mean error: each extension integral as one linear functional
+    // of the cell's nodes, sum_q w_q t[q][n] / den[q] folded on the host
+    double ipw[SK_MAXP], imw[SK_MAXP];
 };
 
 // host: fill PostCfg's evaluation points for a basis
@@ -651,6 +654,15 @@ inline void post_cfg_points(const Basis& b, PostCfg& c) {
     }
     c.ev0rc = 1.0 / b.ev0den;
     c.ev1rc = 1.0 / b.ev1den;
+    for (int n = 0; n < b.p; ++n) {
+        double wp = 0.0, wm = 0.0;
+        for (int q = 0; q < b.p; ++q) {
+            wp += b.weights[q] * c.ipt[q][n] / c.ipden[q];
+            wm += b.weights[q] * c.imt[q][n] / c.imden[q];
+        }
+        c.ipw[n] = wp;
+        c.imw[n] = wm;
+    }
 }
 
 // integrate(u, 1, 2) / integrate(u, -1, 0) with the precomputed points:
@@ -677,24 +689,13 @@ SK_HD double eval_end_fast(const Basis& b, const double* u, int one, double rc) 
     for (int n = 0; n < P; ++n) num = fma(one ? b.ev1[n] : b.ev0[n], u[n], num);
     return num * rc;
 }
-template <int P>
-SK_HD double integrate_fast(const Basis& b, const double (*t)[SK_MAXP], const double* rc, const double* u) {
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-        double num = 0.0;
-#pragma unroll
-        for (int n = 0; n < P; ++n) num = fma(t[q][n], u[n], num);
-        acc = fma(b.weights[q], num * rc[q], acc);
-    }
-    return acc;
-}
 // The post-limiter indicators split into a per-cell summary and a decision
 // from the three summaries of a stencil: indicator_minmod / indicator_meanerr
-// above with PostCfg's precomputed points (fast mode: DFMA sums and the
-// reciprocals), the same operations in the same order wherever a cell is
-// met, so a pass that meets every cell once (the v flags fused into the v
-// sweep) decides bitwise like the stencil passes.
+// above with PostCfg's precomputed points (fast mode: DFMA sums, the
+// reciprocals, each mean-error extension folded into one functional), the
+// same operations in the same order wherever a cell is met, so a pass that
+// meets every cell once (the flags fused into the sweeps) decides bitwise
+// like the stencil passes.
 // minmod: (mean, value at xi = 1, value at xi = 0); meanerr: (mean, the cell's
 // extension over its right neighbour, over its left neighbour).
 struct PostSum {
@@ -709,8 +710,14 @@ SK_HD PostSum post_summary(const Basis& b, const PostCfg& c, const double* u) {
             s.a = eval_end_fast<P>(b, u, 1, c.ev1rc);
             s.b = eval_end_fast<P>(b, u, 0, c.ev0rc);
         } else {
-            s.a = integrate_fast<P>(b, c.ipt, c.iprc, u);
-            s.b = integrate_fast<P>(b, c.imt, c.imrc, u);
+            double ea = 0.0, eb = 0.0;
+#pragma unroll
+            for (int n = 0; n < P; ++n) {
+                ea = fma(c.ipw[n], u[n], ea);
+                eb = fma(c.imw[n], u[n], eb);
+            }
+            s.a = ea;
+            s.b = eb;
         }
     } else {
         s.m = mean<P>(b, u);
