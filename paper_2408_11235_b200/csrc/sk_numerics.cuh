@@ -742,8 +742,16 @@ SK_HD bool post_decide(const PostCfg& c, const PostSum& sm, const PostSum& s0, c
             const double scale = fmax(fmax(fmax(fabs(sm.m), fabs(s0.m)), fmax(fabs(sp.m), fabs(u0_plus))),
                                       fmax(fmax(fabs(u0_minus), fabs(d_plus)), fabs(d_minus)));
             const double guard = 1e-13 * scale;
-            return (fabs(minmod(u0_plus, d_plus, d_minus) - u0_plus) > guard) |
-                   (fabs(minmod(u0_minus, d_plus, d_minus) - u0_minus) > guard);
+            // |minmod(a, d+, d-) - a| without forming minmod: |a| - min(|a|, |d+|, |d-|) when all
+            // three share a sign (the same rounding: fl(mn - |a|) = -fl(|a| - mn)), else |a|;
+            // the slopes' part is common to both ends
+            const double mbc = fmin(fabs(d_plus), fabs(d_minus));
+            const bool pos = (d_plus > 0) & (d_minus > 0), neg = (d_plus < 0) & (d_minus < 0);
+            auto dev = [&](double a) {
+                const double aa = fabs(a);
+                return ((pos & (a > 0)) | (neg & (a < 0))) ? aa - fmin(aa, mbc) : aa;
+            };
+            return (dev(u0_plus) > guard) | (dev(u0_minus) > guard);
         } else {
             double scale = fabs(sm.m);
             double v;
