@@ -739,9 +739,6 @@ SK_HD bool post_decide(const PostCfg& c, const PostSum& sm, const PostSum& s0, c
         const double d_plus = sp.m - s0.m;
         const double d_minus = s0.m - sm.m;
         if constexpr (FAST) {
-            const double scale = fmax(fmax(fmax(fabs(sm.m), fabs(s0.m)), fmax(fabs(sp.m), fabs(u0_plus))),
-                                      fmax(fmax(fabs(u0_minus), fabs(d_plus)), fabs(d_minus)));
-            const double guard = 1e-13 * scale;
             // |minmod(a, d+, d-) - a| without forming minmod: |a| - min(|a|, |d+|, |d-|) when all
             // three share a sign (the same rounding: fl(mn - |a|) = -fl(|a| - mn)), else |a|;
             // the slopes' part is common to both ends
@@ -751,7 +748,12 @@ SK_HD bool post_decide(const PostCfg& c, const PostSum& sm, const PostSum& s0, c
                 const double aa = fabs(a);
                 return ((pos & (a > 0)) | (neg & (a < 0))) ? aa - fmin(aa, mbc) : aa;
             };
-            return (dev(u0_plus) > guard) | (dev(u0_minus) > guard);
+            const double dp = dev(u0_plus), dm = dev(u0_minus);
+            if (!(dp > 0.0) && !(dm > 0.0)) return false;  // (a zero deviation never exceeds the guard)
+            const double scale = fmax(fmax(fmax(fabs(sm.m), fabs(s0.m)), fmax(fabs(sp.m), fabs(u0_plus))),
+                                      fmax(fmax(fabs(u0_minus), fabs(d_plus)), fabs(d_minus)));
+            const double guard = 1e-13 * scale;
+            return (dp > guard) | (dm > guard);
         } else {
             double scale = fabs(sm.m);
             double v;
