@@ -185,6 +185,7 @@ def config_dict(args, cfg):
                       else "parallel (two-pass moment, cyclic-reduction Poisson)",
         "l2": "inputs larger than L2 (no flush needed)"
               if 8 * cfg.dof_total > 126e6 else "state fits in L2 (parity config)",
+        **({"stress": "f *= 1 + 0.01 xi, xi ~ U(-1, 1)"} if getattr(args, "stress", False) else {}),
     }
 
 
@@ -197,6 +198,9 @@ def main():
     ap.add_argument("--limiter", default=None)
     ap.add_argument("--refinement", type=int, default=None,
                     help="sheath refinement ratio m of the three-block x mesh (default: the config's)")
+    ap.add_argument("--no-cutoff", action="store_true", help="velocity cut-off off (SURVEY.md §8d C5 variant)")
+    ap.add_argument("--stress", action="store_true",
+                    help="stress variant: f *= 1 + 0.01 xi, xi ~ U(-1, 1) (device hash RNG, seed 20240817)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -213,6 +217,8 @@ def main():
     over = {"limiter": args.limiter} if args.limiter else {}
     if args.refinement:
         over["refinement_ratio"] = args.refinement
+    if args.no_cutoff:
+        over["v_adjust"] = False
     cfg = sk.named_config(args.config, **over)
 
     if args.impl == "reference":
@@ -233,6 +239,9 @@ def main():
     torch.cuda.set_device(dev)
     st = sk.SimulationState(cfg, device=dev, exact=args.exact)
     st.ctx.set_eager_errors(False)
+    if args.stress:
+        for sp in (0, 1):
+            st.field(sp).perturb(20240817 + sp, 0.01)
     st.run_steps(args.warmup)
     st.prepare_steps(args.steps)  # graph captures outside the timed region
     st.ctx.synchronize()

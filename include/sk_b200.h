@@ -156,7 +156,8 @@ sk_status sk_ctx_check_guards(sk_ctx* ctx, long long* bad);
 /* Capacity of the deferred limiter-clamp list (troubled cells queued by the
  * sweeps, clamped by a fixup kernel); above it the fixup rescans the sweep.
  * Sized when a state is created: at least 4 Mi entries, cells/32 of a pass
- * for the inline limiter, cells/6 for the literature post limiters; cap may
+ * for the inline limiter, cells/6 for the literature post limiters (cells/3 where the
+ * device memory allows: rough data flag 15-25 % of a pass); cap may
  * only lower it (for testing the rescan path). */
 sk_status sk_ctx_set_fix_capacity(sk_ctx* ctx, unsigned int cap);
 sk_status sk_ctx_synchronize(sk_ctx* ctx); /* also reports device-side errors */
@@ -180,6 +181,11 @@ size_t sk_field_size(const sk_field* f);
 double* sk_field_data_dev(sk_field* f); /* current buffer (device) */
 sk_status sk_field_upload(sk_field* f, const double* host, size_t count);
 sk_status sk_field_download(sk_field* f, double* host, size_t count);
+/* Benchmark stress variant: f *= 1 + amp * xi, xi uniform in
+ * [-1, 1) from a counter-based hash of (seed, element index), on the device.
+ * Replaces the reference self-check's f * (1 + 0.01 xi) perturbation (not its
+ * mt19937_64 sequence). */
+sk_status sk_field_perturb(sk_field* f, unsigned long long seed, double amp);
 /* `height` runs of `width` doubles, `pitch` doubles apart, from element
  * `offset` of the field (layout field.hpp:71-73) into a packed host array:
  * one x line (offset = row * nx*p, width = nx*p, height = 1) or one v line

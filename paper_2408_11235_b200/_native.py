@@ -88,6 +88,7 @@ SIGNATURES = {
     "sk_field_data_dev": (_vp, [_vp]),
     "sk_field_upload": (_i, [_vp, _dp, _sz]),
     "sk_field_download": (_i, [_vp, _dp, _sz]),
+    "sk_field_perturb": (_i, [_vp, C.c_ulonglong, _d]),
     "sk_field_download_2d": (_i, [_vp, _dp, _sz, _sz, _sz, _sz]),
     "sk_field_upload_async": (_i, [_vp, _dp, _sz]),
     "sk_field_download_async": (_i, [_vp, _dp, _sz]),

@@ -1091,7 +1091,7 @@ sk_status sk_ctx_set_fix_capacity(sk_ctx* c, unsigned int cap) {
 
 namespace {
 // the deferred-limiter list must hold a pass's flagged cells: the sweeps flag
-// ~0.5 % of the cells, the literature post limiters ~5-10 % (outside capture)
+// ~0.5 % of the cells, the literature post limiters ~5-25 % (outside capture)
 sk_status ensure_fix_capacity(sk_ctx* c, size_t cells) {
     const size_t want = std::min<size_t>(cells, 0xffffffffu);
     if (want <= c->fix_alloc) return SK_OK;
@@ -1289,6 +1289,13 @@ sk_status sk_field_upload(sk_field* f, const double* host, size_t count) {
     CK(f->live_ptr(&live));
     CK(cudaMemcpyAsync(live, host, sizeof(double) * count, cudaMemcpyHostToDevice,
                        f->ctx->stream));
+    CK(cudaStreamSynchronize(f->ctx->stream));
+    return SK_OK;
+}
+sk_status sk_field_perturb(sk_field* f, unsigned long long seed, double amp) {
+    double* live = nullptr;
+    CK(f->live_ptr(&live));
+    CK(launch_perturb(live, f->n, seed, amp, f->ctx->stream));
     CK(cudaStreamSynchronize(f->ctx->stream));
     return SK_OK;
 }
@@ -1511,7 +1518,19 @@ sk_status sk_state_create(sk_ctx* c, const sk_run_config* cfg, sk_state** out) {
     {  // cells per pass, both species: room for the flagged ones (sLdG: ~0.5 %
        // troubled; a fused step boundary queues ~3x that, see xfix2_kernel)
         const size_t cells = 2 * (size_t)cfg->v_cells * c->P * c->grid.ncells;
-        if (sk_status rc = ensure_fix_capacity(c, cfg->limiter.indicator ? cells / 6 : cells / 32)) return rc;
+        size_t want = cfg->limiter.indicator ? cells / 6 : cells / 32;
+        if (cfg->limiter.indicator) {
+            // post limiters on rough data (the stress input) flag 15-25 % of a pass: a third keeps
+            // them in list mode (an overflow copies the field and rescans every cell) where the
+            // list (8 B) and the modified values (8P B) per entry fit beside the double-buffered
+            // fields with room to spare
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            const size_t fields = 2 * cells * c->P * sizeof(double);  // both buffers, both species
+            const size_t third = cells / 3 * (8 + 8 * (size_t)c->P);
+            if (free_b > fields + 2 * third + (8ull << 30)) want = cells / 3;
+        }
+        if (sk_status rc = ensure_fix_capacity(c, want)) return rc;
     }
     if (sk_status rc = ensure_xghost_cfg(c, cfg, cfg->v_cells * c->P)) return rc;
     if (cfg->limiter.indicator)

@@ -2976,9 +2976,16 @@ __global__ void copy_kernel(double* dst, const double* src, long long n) {
 // K3: literature post-limiters (limiters.cpp:254-345). Flags from pre-pass data
 // (out of place). X: tiles with a 1-cell halo (block ghosts via fill_ghost j=1).
 // ---------------------------------------------------------------------------
-template <int P>
+template <int P, bool FAST>
 __device__ __forceinline__ void post_modify(const PostCfg& cfg, const Basis& b, const double* um,
                                             const double* u0, const double* up, double* out) {
+    if constexpr (FAST) {  // (tolerance mode: precomputed functionals, see modify_simple_weno_fast)
+        if (cfg.modifier == 1)
+            modify_simple_weno_fast<P>(b, um, u0, up, cfg, out);
+        else
+            modify_line_weno_fast<P>(b, um, u0, up, cfg, out);
+        return;
+    }
     if (cfg.modifier == 1)
         modify_simple_weno<P>(b, um, u0, up, cfg, out);
     else
@@ -3148,7 +3155,7 @@ __global__ void __launch_bounds__(128) post_fix_kernel(const __grid_constant__ P
                 for (int m = 0; m < P; ++m) a.fix_vals[i * P + m] = u0[m];
             continue;
         }
-        post_modify<P>(a.cfg, a.basis, um, u0, up, o);
+        post_modify<P, FAST>(a.cfg, a.basis, um, u0, up, o);
         if (rescan) {
             double* out = post_live(a, sp);
             if (DIR == 0 && a.rho_corr) post_rho_corr<P>(a, sp, row, col, u0, o);
@@ -3877,6 +3884,29 @@ cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s) {
     int mask = 0;
     for (int i = 0; i < a.nspecies; ++i) mask |= 1 << (a.species0 + i);
     pdl_launch(post_v_count_kernel, 1, 1, 0, s, a.st, mask, (unsigned long long)a.nv * a.nxd);
+    return cudaGetLastError();
+}
+
+// stress variant of the benchmark input: f *= 1 + amp * xi,
+// xi uniform in [-1, 1) from a counter-based hash of (seed, index) -- the
+// same multiplicative noise as the reference's self-check perturbation, not
+// its mt19937_64 sequence
+namespace {
+__global__ void perturb_kernel(double* f, long long n, unsigned long long seed, double amp) {
+    pdl_enter();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        unsigned long long z = seed + 0x9e3779b97f4a7c15ull * (unsigned long long)(i + 1);  // splitmix64
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        const double xi = (double)(z >> 11) * 0x1p-52 - 1.0;  // [-1, 1)
+        f[i] *= 1.0 + amp * xi;
+    }
+}
+}  // namespace
+cudaError_t launch_perturb(double* f, size_t n, unsigned long long seed, double amp, cudaStream_t s) {
+    pdl_launch(perturb_kernel, 1184, 256, 0, s, f, (long long)n, seed, amp);
     return cudaGetLastError();
 }
 

@@ -308,5 +308,6 @@ cudaError_t launch_fill_separable(double* f, const double* gx, const double* gv,
 cudaError_t launch_post_x(const PostArgs& a, int ntiles, cudaStream_t s);
 cudaError_t launch_post_v(const PostArgs& a, cudaStream_t s);
 cudaError_t launch_scale_copy(double* dst, const double* src, size_t n, cudaStream_t s);
+cudaError_t launch_perturb(double* f, size_t n, unsigned long long seed, double amp, cudaStream_t s);
 
 }  // namespace sk

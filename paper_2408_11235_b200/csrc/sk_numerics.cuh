@@ -634,6 +634,11 @@ struct PostCfg {
     // fast mode, mean error: each extension integral as one linear functional
     // of the cell's nodes, sum_q w_q t[q][n] / den[q] folded on the host
     double ipw[SK_MAXP], imw[SK_MAXP];
+    // fast mode, simple WENO: the neighbours' polynomials at this cell's nodes,
+    // evaluate(u, 1 + xi_m) = sum_n evm[m][n] u[n] and evaluate(u, xi_m - 1) =
+    // sum_n evp[m][n] u[n] (the barycentric weights at fixed points, host)
+    double evm[SK_MAXP][SK_MAXP], evp[SK_MAXP][SK_MAXP];
+    double rg0;  // 1 / gamma_line[1]
 };
 
 // host: fill PostCfg's evaluation points for a basis
@@ -663,6 +668,17 @@ inline void post_cfg_points(const Basis& b, PostCfg& c) {
         c.ipw[n] = wp;
         c.imw[n] = wm;
     }
+    for (int m = 0; m < b.p; ++m)
+        for (int side = 0; side < 2; ++side) {
+            const double xi = side == 0 ? 1.0 + b.nodes[m] : b.nodes[m] - 1.0;
+            double den = 0.0, t[SK_MAXP];
+            for (int n = 0; n < b.p; ++n) {
+                t[n] = b.bary[n] / (xi - b.nodes[n]);  // (xi is never a node: |xi| > 1 off [0, 1])
+                den += t[n];
+            }
+            for (int n = 0; n < b.p; ++n) (side == 0 ? c.evm : c.evp)[m][n] = t[n] / den;
+        }
+    c.rg0 = 1.0 / c.gamma_line[1];
 }
 
 // integrate(u, 1, 2) / integrate(u, -1, 0) with the precomputed points:
@@ -812,6 +828,44 @@ SK_HD void modify_simple_weno(const Basis& b, const double* um, const double* u0
     }
 }
 
+// fast mode (tolerance): the same modification with the fixed-point
+// evaluations and extension integrals as precomputed linear functionals and
+// one reciprocal for the weight normalisation -- 4 divisions instead of ~90
+template <int P>
+SK_HD void modify_simple_weno_fast(const Basis& b, const double* um, const double* u0, const double* up,
+                                   const PostCfg& cfg, double* out) {
+    const double beta_m = smoothness_beta<P>(b, um);
+    const double beta_0 = smoothness_beta<P>(b, u0);
+    const double beta_p = smoothness_beta<P>(b, up);
+    const double eps = cfg.epsilon;
+    double wm = cfg.gamma_simple[0] / ((eps + beta_m) * (eps + beta_m));
+    double w0 = cfg.gamma_simple[1] / ((eps + beta_0) * (eps + beta_0));
+    double wp = cfg.gamma_simple[2] / ((eps + beta_p) * (eps + beta_p));
+    const double rs = 1.0 / (wm + w0 + wp);
+    wm *= rs;
+    w0 *= rs;
+    wp *= rs;
+    const double mean_0 = mean_f<P, true>(b, u0);
+    double ext_m = 0.0, ext_p = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+        ext_m = fma(cfg.ipw[n], um[n], ext_m);
+        ext_p = fma(cfg.imw[n], up[n], ext_p);
+    }
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        double em = 0.0, ep = 0.0;
+#pragma unroll
+        for (int n = 0; n < P; ++n) {
+            em = fma(cfg.evm[m][n], um[n], em);
+            ep = fma(cfg.evp[m][n], up[n], ep);
+        }
+        const double cand_m = em - ext_m + mean_0;
+        const double cand_p = ep - ext_p + mean_0;
+        out[m] = fma(wm, cand_m, fma(w0, u0[m], wp * cand_p));
+    }
+}
+
 template <int P>
 SK_HD void modify_line_weno(const Basis& b, const double* um, const double* u0, const double* up,
                             const PostCfg& cfg, double* out) {
@@ -844,6 +898,40 @@ SK_HD void modify_line_weno(const Basis& b, const double* um, const double* u0, 
     wp /= sum;
 #pragma unroll
     for (int m = 0; m < P; ++m) out[m] = wm * pm[m] + w0 * p0[m] + wp * pp[m];
+}
+
+template <int P>
+SK_HD void modify_line_weno_fast(const Basis& b, const double* um, const double* u0, const double* up,
+                                 const PostCfg& cfg, double* out) {
+    const double mean_m = mean_f<P, true>(b, um);
+    const double mean_0 = mean_f<P, true>(b, u0);
+    const double mean_p = mean_f<P, true>(b, up);
+    const double bm = mean_0 - mean_m, am = mean_0 - 0.5 * bm;
+    const double bp = mean_p - mean_0, ap = mean_0 - 0.5 * bp;
+    const double gm = cfg.gamma_line[0], g0 = cfg.gamma_line[1], gp = cfg.gamma_line[2];
+    double pm[P], pp[P], p0[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        const double xi = b.nodes[m];
+        pm[m] = fma(bm, xi, am);
+        pp[m] = fma(bp, xi, ap);
+        p0[m] = (u0[m] - gm * pm[m] - gp * pp[m]) * cfg.rg0;
+    }
+    const double beta_m = smoothness_beta<P>(b, um);
+    const double beta_0 = smoothness_beta<P>(b, u0);
+    const double beta_p = smoothness_beta<P>(b, up);
+    double tau = 0.5 * (fabs(beta_0 - beta_m) + fabs(beta_0 - beta_p));
+    tau *= tau;
+    const double eps = cfg.epsilon;
+    double wm = gm * (1.0 + tau / (eps + beta_m));
+    double w0 = g0 * (1.0 + tau / (eps + beta_0));
+    double wp = gp * (1.0 + tau / (eps + beta_p));
+    const double rs = 1.0 / (wm + w0 + wp);
+    wm *= rs;
+    w0 *= rs;
+    wp *= rs;
+#pragma unroll
+    for (int m = 0; m < P; ++m) out[m] = fma(wm, pm[m], fma(w0, p0[m], wp * pp[m]));
 }
 
 // ---------------- sheath-mesh transfer (adaptivity.cpp:132-156) ----------------

@@ -569,6 +569,10 @@ class NodalField:
                                          out.size))
         return out
 
+    def perturb(self, seed: int = 20240817, amp: float = 0.01):
+        """benchmark stress variant: f *= 1 + amp * xi, xi uniform in [-1, 1) (device hash RNG)"""
+        _check(N.lib().sk_field_perturb(self.h, int(seed), float(amp)))
+
     def fill_blob(self, sigma: float):
         _check(N.lib().sk_field_fill_blob(self.h, sigma))
 

@@ -1284,3 +1284,24 @@ def test_bench_sharded_one_rank_line(sk, monkeypatch, capsys):
     assert line["n_gpus"] == 1 and line["value"] > 0
     assert line["roofline"]["kernel"] in ("x_sweep_1", "x_sweep_2", "v_sweep")
     assert 0 < line["roofline"]["frac"] < 1.5
+
+
+def test_field_perturb_stress_input(sk):
+    """bench.py --stress (SURVEY.md §8d stress variant): f *= 1 + amp xi with
+    xi uniform in [-1, 1) from a device hash of (seed, index) -- bounded,
+    roughly zero-mean, reproducible for a seed, different across seeds."""
+    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=1, nv=64, mu=1836.0, limiter="sldg")
+    a, b = sk.SimulationState(cfg), sk.SimulationState(cfg)
+    f0 = a.field(0).download()
+    a.field(0).perturb(20240817, 0.01)
+    b.field(0).perturb(20240817, 0.01)
+    fa, fb = a.field(0).download(), b.field(0).download()
+    assert np.array_equal(fa, fb)
+    nz = f0 != 0
+    xi = (fa[nz] / f0[nz] - 1.0) / 0.01
+    assert xi.min() >= -1.0 - 1e-9 and xi.max() < 1.0 + 1e-9
+    assert abs(xi.mean()) < 0.05 and xi.std() > 0.5
+    b.field(1).perturb(1, 0.01)
+    assert not np.array_equal(b.field(1).download(), a.field(1).download())
+    a.run_steps(2)  # the perturbed state steps (limiter active)
+    assert np.isfinite(a.field(0).download()).all()
