@@ -2424,15 +2424,19 @@ __global__ void __launch_bounds__(1024) poisson_cluster_kernel(const __grid_cons
 // charge_density (poisson.cpp:194-216): per x dof, ions then electrons,
 // rows ascending, rho += ((sign*w_vn)*dv) * f. The sum is one sequential chain
 // per x dof (nx*p of them), so the parallelism for HBM is in the loads: each
-// thread streams its column through a kRhoRing-deep cp.async ring in shared
-// memory ([slot][thread]: a warp's slot is one coalesced 256-byte row piece),
-// keeping kRhoRing loads in flight while the adds retire in order.
-constexpr int kRhoThreads = 32, kRhoRing = 96;
+// thread streams its column through a cp.async ring in shared memory
+// ([slot][thread]: a warp's slot is one coalesced 256-byte row piece), one
+// commit group per v cell (P rows), kRhoRingCells cells in flight while the
+// adds retire in order. (Per-row groups cost ~140 cycles of issue overhead per
+// row, and a 96-row ring left C5's 2048 CTAs in two waves: C5 36.3 -> 18.4 ms,
+// C3 2.33 -> 1.32 ms.)
+constexpr int kRhoThreads = 32, kRhoRingCells = 12;  // 12.3 KB per CTA at P = 4: 18 CTAs/SM, C5 in one wave
 template <int P>
 __global__ void __launch_bounds__(kRhoThreads) rho_exact_kernel(const __grid_constant__ RhoArgs a) {
     pdl_enter();
     if (halted(a.st)) return;
-    __shared__ double ring[kRhoRing * kRhoThreads];
+    constexpr int RC = kRhoRingCells;
+    __shared__ double ring[RC * P * kRhoThreads];
     const int xd = blockIdx.x * blockDim.x + threadIdx.x;
     if (xd >= a.nxd) return;
     const double* fs[2];
@@ -2445,31 +2449,35 @@ __global__ void __launch_bounds__(kRhoThreads) rho_exact_kernel(const __grid_con
 #pragma unroll
         for (int vn = 0; vn < P; ++vn) wv[s][vn] = sign * a.basis.weights[vn] * dv;
     }
-    const long long nr = a.nrows, total = 2 * nr;
+    const long long nr = a.nrows;            // rows per species (a multiple of P)
+    const long long ncell = 2 * (nr / P);    // v cells of both species, ions first
     double* my = ring + threadIdx.x;
-    auto issue = [&](long long r, int slot) {
-        if (r < total) {
-            const int s = r >= nr;
-            cp_async8(my + slot * kRhoThreads, fs[s] + (r - s * nr) * a.ld, true);
+    auto issue = [&](long long g, int slot) {  // the P rows of v cell g
+        if (g < ncell) {
+            const long long r0 = g * P;
+            const int s = r0 >= nr;
+            const double* src = fs[s] + (r0 - s * nr) * a.ld;
+#pragma unroll
+            for (int vn = 0; vn < P; ++vn) cp_async8(my + (slot * P + vn) * kRhoThreads, src + vn * a.ld, true);
         }
         cp_commit();
     };
 #pragma unroll 1
-    for (int c = 0; c < kRhoRing - 1; ++c) issue(c, c);
+    for (int c = 0; c < RC - 1; ++c) issue(c, c);
     double acc = 0.0;
-    long long r = 0;
-    for (int s = 0; s < 2; ++s) {
-#pragma unroll 1
-        for (long long rr = 0; rr < nr; rr += P) {
 #pragma unroll
-            for (int vn = 0; vn < P; ++vn, ++r) {
-                const int slot = (int)(r % kRhoRing);
-                cp_wait<kRhoRing - 2>();
-                const double v = my[slot * kRhoThreads];
-                // refill the slot consumed one row ago (its value is in acc already)
-                issue(r + kRhoRing - 1, slot == 0 ? kRhoRing - 1 : slot - 1);
-                acc += wv[s][vn] * v;
-            }
+    for (int s = 0; s < 2; ++s) {  // (unrolled: the species' weights stay in registers)
+#pragma unroll 1
+        for (long long g = s * (ncell / 2); g < (s + 1) * (ncell / 2); ++g) {
+            const int slot = (int)(g % RC);
+            cp_wait<RC - 2>();
+            double v[P];
+#pragma unroll
+            for (int vn = 0; vn < P; ++vn) v[vn] = my[(slot * P + vn) * kRhoThreads];
+            // refill the slot consumed one cell ago (its values are in acc already)
+            issue(g + RC - 1, slot == 0 ? RC - 1 : slot - 1);
+#pragma unroll
+            for (int vn = 0; vn < P; ++vn) acc += wv[s][vn] * v[vn];
         }
     }
     cp_wait<0>();
