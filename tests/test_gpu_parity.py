@@ -1305,3 +1305,30 @@ def test_field_perturb_stress_input(sk):
     assert not np.array_equal(b.field(1).download(), a.field(1).download())
     a.run_steps(2)  # the perturbed state steps (limiter active)
     assert np.isfinite(a.field(0).download()).all()
+
+
+def test_bench_single_gpu_line_variants(sk):
+    """bench.py's single-GPU line end to end (C1, small): the contract keys,
+    e2e with its copied bytes, the CPU baseline, and the SURVEY.md §8(d)
+    variant switches (--stress, --no-cutoff) reflected in config."""
+    import json
+    import subprocess
+    import sys
+
+    base = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C1", "--steps", "3", "--warmup", "3"]
+    r = subprocess.run(base + ["--cpu-budget", "2", "--exact-steps", "2"], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks",
+                "gpu_launches", "exact_mode"):
+        assert key in line, key
+    assert line["steps"] == 3 and line["warmup"] == 3 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["cpu_baseline"]["value"] > 0
+    r = subprocess.run(base + ["--no-cpu", "--no-e2e", "--exact-steps", "0", "--stress", "--no-cutoff"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert "stress" in line["config"] and "cut-off off" in line["config"]["workload"]
