@@ -2502,6 +2502,10 @@ __global__ void __launch_bounds__(kRhoThreads) rho_exact_kernel(const __grid_con
 //    bit, and a pass with any mismatch is replayed with true divisions -- the
 //    result is the reference's either way.
 // The load and E = -phi' phases are parallel over dofs.
+#ifndef SK_PEX_UNROLL
+#define SK_PEX_UNROLL 4
+#endif
+constexpr int kPexUnroll = SK_PEX_UNROLL;  // exact Poisson: columns per unrolled step of the serial sweeps
 __device__ __forceinline__ double div_markstein(double a, double c, double r) {
     const double q = __dmul_rn(a, r);
     const double e = __fma_rn(-q, c, a);  // exact remainder
@@ -2560,16 +2564,20 @@ __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constan
             if (ch + 1 < nch) stage(ch + 1, b ^ 1, LD, false);
             if (threadIdx.x == 0) {
                 const int j0 = ch * CH, j1 = min(n, j0 + CH);
+                // (unrolled, branch-free: the column loads and the off-chain updates of
+                // the next columns overlap this column's division; a zero x[j] keeps
+                // every value through selects, as the reference's skip does)
+#pragma unroll kPexUnroll
                 for (int j = j0; j < j1; ++j) {
                     const double* col = &scol[b][(j - j0) * LD];
                     if (FAST) dvd[j] = w[0];
-                    if (w[0] != 0.0) {
-                        w[0] = FAST ? div_markstein(w[0], col[0], srcp[b][j - j0]) : w[0] / col[0];
-                        const double temp = w[0];
+                    const bool nz = w[0] != 0.0;
+                    const double q = FAST ? div_markstein(w[0], col[0], srcp[b][j - j0]) : w[0] / col[0];
+                    w[0] = nz ? q : w[0];
+                    const double temp = w[0];
 #pragma unroll
-                        for (int l = 1; l < LD; ++l)
-                            if (j + l < n) w[l] = w[l] - temp * col[l];
-                    }
+                    for (int l = 1; l < LD; ++l)
+                        if (j + l < n) w[l] = nz ? w[l] - temp * col[l] : w[l];
                     x[j] = w[0];
 #pragma unroll
                     for (int l = 0; l + 1 < LD; ++l) w[l] = w[l + 1];
@@ -2593,7 +2601,8 @@ __global__ void __launch_bounds__(256) poisson_exact_kernel(const __grid_constan
             if (ch > 0) stage(ch - 1, b ^ 1, 0, false);
             if (threadIdx.x == 0) {
                 const int j0 = ch * CH, j1 = min(n, j0 + CH);
-                for (int j = j1 - 1; j >= j0; --j) {
+#pragma unroll kPexUnroll
+                for (int j = j1 - 1; j >= j0; --j) {  // (unrolled: the chain's first KD - 1 terms overlap)
                     const double* col = &scol[b][(j - j0) * LD];
                     double temp = sx[b][j - j0];
 #pragma unroll
