@@ -1332,3 +1332,28 @@ def test_bench_single_gpu_line_variants(sk):
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert "stress" in line["config"] and "cut-off off" in line["config"]["workload"]
+
+
+def test_programmatic_dependent_launch_mode_same_bits(sk, tmp_path):
+    """SK_PDL=1 (launch attribute + early trigger; off by default, measured no
+    gain, profiles/r02_pdl.txt): every kernel waits for its predecessor's
+    completion at entry, so a run gives the same bits as without it."""
+    import subprocess
+    import sys
+
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2408_11235_b200 as sk\n"
+        "cfg = sk.RunConfig(k=3, fine_block_cells=16, coarse_block_cells=32, refinement_ratio=2, v_cells=64,"
+        " mu=1836.0, limiter='sldg')\n"
+        "st = sk.SimulationState(cfg)\n"
+        "st.run_steps(12)\n"
+        "np.save(sys.argv[1], np.concatenate([st.field(0).download(), st.field(1).download(), st.E()]))\n" % ROOT)
+    outs = []
+    for mode in ("0", "1"):
+        out = str(tmp_path / f"pdl{mode}.npy")
+        r = subprocess.run([sys.executable, "-c", script, out], capture_output=True, text=True, timeout=600,
+                           env={**os.environ, "SK_PDL": mode})
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
