@@ -239,6 +239,7 @@ def main():
     torch.cuda.set_device(dev)
     st = sk.SimulationState(cfg, device=dev, exact=args.exact)
     st.ctx.set_eager_errors(False)
+    fused = st.step_fusion()  # (auto: the C5-class states, sk_ctx_set_step_fusion)
     if args.stress:
         for sp in (0, 1):
             st.field(sp).perturb(20240817 + sp, 0.01)
@@ -285,10 +286,21 @@ def main():
     dom_share = phases[dom][0] / ms_phased
     dom_ms, dom_n = phases[dom]
     per_launch_ms = dom_ms / max(dom_n, 1)
+    traffic_key = dom
     if dom in sweep_phases or dom.startswith("post"):
         alg_bytes = BYTES_PER_DOF_SWEEP * cfg.dof_total
     else:
         alg_bytes = None
+    if fused and dom in ("x_sweep_1", "x_sweep_2"):
+        # fused step boundaries (sk_state_step_fusion): a step's two x half sweeps mostly run as ONE
+        # pass (xsweep_kernel MODE 3, timed in the x_sweep_2 phase; unfused where the cut-off may
+        # check). Both x phases together against the two half sweeps' algorithmic bytes per step
+        x_ms = phases["x_sweep_1"][0] + phases["x_sweep_2"][0]
+        dom = "x_sweeps (fused step boundaries)"
+        dom_share = x_ms / ms_phased
+        per_launch_ms = x_ms / max(phases["x_sweep_2"][1], 1)
+        alg_bytes = 2 * BYTES_PER_DOF_SWEEP * cfg.dof_total
+        traffic_key = "x_sweeps_fused"
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9 if alg_bytes else None
     step_bytes = 3 * BYTES_PER_DOF_SWEEP * cfg.dof_total
     step_gbs = step_bytes * args.steps / (ms / 1e3) / 1e9
@@ -296,7 +308,7 @@ def main():
     traffic = None
     try:
         with open(prof_path) as f:
-            traffic = json.load(f).get(args.config, {}).get(dom)
+            traffic = json.load(f).get(args.config, {}).get(traffic_key)
     except Exception:
         pass
 
@@ -310,7 +322,7 @@ def main():
                      "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes, "ms_per_launch": per_launch_ms,
-                     "share_of_step": dom_share,
+                     "share_of_step": dom_share, "fused_step_boundaries": fused,
                      "step_achieved_gbs": step_gbs, "step_frac": step_gbs / peak,
                      "timing": "kernel ms from per-phase CUDA events over a second K-step "
                                "window (eager enqueue, %.3f ms/step vs %.3f graphed)"

@@ -138,9 +138,12 @@ sk_status sk_ctx_set_exact_reductions(sk_ctx* ctx, int on);
 sk_status sk_ctx_set_exact_parts(sk_ctx* ctx, int mask);
 /* Fusion of step n's second and step n+1's first x half sweep inside
  * sk_run_steps: one pass over f instead of two (32 instead of 48 B/DoF per
- * step). Default off (SK_STEP_FUSION=1 in the environment turns it on): on
- * B200 each half sweep is issue-bound about as much as HBM-bound, so the fused
- * pass measures break-even at C5 and slower at C3. */
+ * step). on: 1 always, 0 never, -1 auto (the default; SK_STEP_FUSION=0/1 in
+ * the environment forces it): fused for states of at least 2^32 DoF, whose
+ * long steps run under the board power cap, where the lower traffic lifts the
+ * clock (C5 -1.5 %, C5 at k = 2 -10 %); not below, where the fused pass is
+ * compute-bound at full clock (C3 +8 %). Fast mode, blob scenario, no post
+ * limiter, uniform x mesh, one rank (sk_state_step_fusion tells). */
 sk_status sk_ctx_set_step_fusion(sk_ctx* ctx, int on);
 /* Post limiter V flags fused into the v sweep (default on; SK_POST_FUSION=0 in
  * the environment turns it off at context creation): in the step, on walls
@@ -328,6 +331,9 @@ sk_status sk_run_step(sk_state* s);
  * pass over f, unless the velocity cut-off may check at the end of step n
  * (then both sweeps run separately, decided on the device). */
 sk_status sk_run_steps(sk_state* s, int n);
+/* *on = 1 when sk_run_steps fuses this state's step boundaries (see
+ * sk_ctx_set_step_fusion). */
+sk_status sk_state_step_fusion(sk_state* s, int* on);
 /* Capture (without running) the CUDA graphs sk_run_steps(state, n) will
  * replay from the current state, so a later sk_run_steps(n) does no capture
  * inside a timed region. */

@@ -76,6 +76,7 @@ SIGNATURES = {
     "sk_ctx_set_exact_reductions": (_i, [_vp, _i]),
     "sk_ctx_set_exact_parts": (_i, [_vp, _i]),
     "sk_ctx_set_step_fusion": (_i, [_vp, _i]),
+    "sk_state_step_fusion": (_i, [_vp, C.POINTER(_i)]),
     "sk_ctx_set_post_fusion": (_i, [_vp, _i]),
     "sk_ctx_check_guards": (_i, [_vp, C.POINTER(C.c_longlong)]),
     "sk_ctx_set_fix_capacity": (_i, [_vp, C.c_uint]),

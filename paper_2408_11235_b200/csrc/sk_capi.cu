@@ -98,11 +98,12 @@ struct sk_ctx {
     // launch parameter baked into kernel arguments changes: states re-capture
     // their CUDA graphs when it differs from the generation they captured at
     unsigned long long gen = 0;
-    // step-boundary fusion of the x half sweeps (sk_ctx_set_step_fusion): off by
-    // default -- measured break-even at C5 and slower at C3, because each pass
-    // of the x sweep is issue-bound about as much as it is HBM-bound
-    // (profiles/r02_fused_xsweep.txt); SK_STEP_FUSION=1 turns it on
-    bool fuse_off = getenv("SK_STEP_FUSION") == nullptr || atoi(getenv("SK_STEP_FUSION")) == 0;
+    // step-boundary fusion of the x half sweeps (sk_ctx_set_step_fusion):
+    // -1 auto (default) = on for states of >= kFuseAutoDof DoF, whose long
+    // steps run under the board power cap, where 32 instead of 48 B/DoF per
+    // step lifts the clock (C5 -1.5 %, C5 k=2 -10 %); off below (C3 +8 %: the
+    // fused pass is compute-bound at full clock). SK_STEP_FUSION=0/1 forces it.
+    int fuse_mode = getenv("SK_STEP_FUSION") == nullptr ? -1 : (atoi(getenv("SK_STEP_FUSION")) != 0 ? 1 : 0);
     // out-of-bounds write detection (compute-sanitizer is unavailable on the
     // GPU pool): with SK_GUARD=1 the fields, tables, E, rho and phi get
     // kGuard-double guard zones of a sentinel pattern on both sides;
@@ -1148,7 +1149,7 @@ sk_status sk_ctx_check_guards(sk_ctx* c, long long* bad) {
 }
 
 sk_status sk_ctx_set_step_fusion(sk_ctx* c, int on) {
-    c->fuse_off = on == 0;
+    c->fuse_mode = on < 0 ? -1 : (on ? 1 : 0);
     ++c->gen;  // captured step graphs change
     return SK_OK;
 }
@@ -1834,9 +1835,12 @@ sk_status enq_source(sk_state* s, int second) {
 // can the loop bodies of this state fuse their x half sweeps across step
 // boundaries? (fast mode with the fused moment, sLdG or no limiter, no
 // injection source, one dx class, unsharded; sk_ctx_set_step_fusion turns it on)
+constexpr double kFuseAutoDof = 4294967296.0;  // 2^32 DoF (both species): C5-class states
 bool fusable(const sk_state* s) {
     const sk_ctx* c = s->ctx;
-    return !c->fuse_off && !(c->exact & (SK_EXACT_ARITH | SK_EXACT_RHO)) && s->cfg.limiter.indicator == 0 &&
+    const double dof = 2.0 * c->grid.ncells * c->P * (double)s->cfg.v_cells * c->P;
+    const bool want = c->fuse_mode == 1 || (c->fuse_mode < 0 && dof >= kFuseAutoDof);
+    return want && !(c->exact & (SK_EXACT_ARITH | SK_EXACT_RHO)) && s->cfg.limiter.indicator == 0 &&
            s->cfg.scenario != 1 && c->grid.nclass == 1 && s->nranks == 1 && xsweep_fused_supported(c->P);
 }
 
@@ -2263,6 +2267,11 @@ sk_status sk_state_phase_times(sk_state* s, double* ms, long* count, int n) {
 }
 
 long long sk_ctx_launch_count(sk_ctx* c) { return c->launches; }
+
+sk_status sk_state_step_fusion(sk_state* s, int* on) {
+    *on = fusable(s) ? 1 : 0;
+    return SK_OK;
+}
 
 sk_status sk_state_step_index(sk_state* s, long* step) {
     if (sk_status rc = collect_errors(s->ctx)) return rc;

@@ -475,9 +475,10 @@ class Context:
         _check(N.lib().sk_ctx_check_guards(self.h, C.byref(bad)))
         return bad.value
 
-    def set_step_fusion(self, on: bool):
-        """fuse step n's second and step n+1's first x half sweep in run_steps"""
-        _check(N.lib().sk_ctx_set_step_fusion(self.h, int(on)))
+    def set_step_fusion(self, on):
+        """fuse step n's second and step n+1's first x half sweep in run_steps
+        (True / False; None: auto, the default -- fused for states >= 2^32 DoF)"""
+        _check(N.lib().sk_ctx_set_step_fusion(self.h, -1 if on is None else int(bool(on))))
 
     def set_post_fusion(self, on: bool):
         """decide the post limiter V's flags inside the v sweep (default on)"""
@@ -783,6 +784,12 @@ class SimulationState:
 
     def launches(self) -> int:
         return int(N.lib().sk_ctx_launch_count(self.ctx.h))
+
+    def step_fusion(self) -> bool:
+        """whether run_steps fuses this state's step boundaries"""
+        on = C.c_int()
+        _check(N.lib().sk_state_step_fusion(self.h, C.byref(on)))
+        return bool(on.value)
 
     def step_index(self) -> int:
         s = C.c_long()
