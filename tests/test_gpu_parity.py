@@ -1357,3 +1357,29 @@ def test_programmatic_dependent_launch_mode_same_bits(sk, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(out))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_run_with_fused_step_boundaries(sk, ora, tmp_path, monkeypatch):
+    """run() (run.cpp:60-169) with the step boundaries fused (the default for
+    C5-class states, forced here on a small mesh): batches end at output
+    events and shrink-capable steps, so the flux rows land on the same steps
+    and times, the shrink events in run.log on the same steps with the same
+    v_max, and the values agree with the unfused run within the reference's
+    rounding envelope (the fused charge density is grouped differently)."""
+    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=1, nv=64, mu=1836.0, limiter="sldg")
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SK_STEP_FUSION", mode)
+        d = tmp_path / f"fuse{mode}"
+        out = sk.run(cfg, nsteps=24, cadence=4, snapshot_cadence=0, profile_cadence=0, out_dir=str(d))
+        assert out["exit_code"] == 0 and out["steps_done"] == 24
+        outs[mode] = (np.loadtxt(d / "flux.csv", delimiter=",", skiprows=1), (d / "run.log").read_text())
+    (fa, la), (fb, lb) = outs["1"], outs["0"]
+    assert fa.shape == fb.shape
+    assert np.array_equal(fa[:, 0], fb[:, 0])  # times
+    ef, eE = _envelope(ora, cfg, 24)[24]
+    scale = np.abs(fb[:, 1:]).max(axis=0)
+    assert (np.abs(fa[:, 1:] - fb[:, 1:]) <= np.maximum(1e-12, 20.0 * ENV_C * max(ef, eE)) * np.maximum(scale, 1e-300)).all()
+    sa = [ln.split("(mass delta")[0] for ln in la.splitlines() if "shrink" in ln.lower()]
+    sb = [ln.split("(mass delta")[0] for ln in lb.splitlines() if "shrink" in ln.lower()]
+    assert sa == sb and len(sa) >= 2
