@@ -205,7 +205,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--exact-steps", type=int, default=4,
                     help="steps of the exact-mode sub-measurement (0: skip)")
     ap.add_argument("--exact", action="store_true",
@@ -363,12 +363,12 @@ def main():
         k2 = args.e2e_steps
         torch.cuda.synchronize()
         w0 = time.perf_counter()
-        for _ in range(k2):
-            st.run_step_host(fe_np, fi_np)
+        st.run_steps_host(k2, fe_np, fi_np)  # every step: both species up, both results down
         w = time.perf_counter() - w0
         line["e2e"] = {"value": cfg.dof_total * k2 / w, "unit": UNIT,
                        "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n,
-                       "steps": k2, "api": "sk_run_step_host (include/sk_b200.h)"}
+                       "steps": k2, "api": "sk_run_steps_host (include/sk_b200.h): host copies of "
+                                           "consecutive steps pipelined over full-duplex PCIe"}
         del fe, fi
 
     # ---- CPU baseline: the reference on this host, bounded sample ----

@@ -353,6 +353,10 @@ sk_status sk_state_phase_times(sk_state* s, double* ms, long* count, int n);
 long long sk_ctx_launch_count(sk_ctx* ctx);
 /* drop-in strang_step over HOST NodalFields: upload, step, download */
 sk_status sk_run_step_host(sk_state* s, double* fe_host, double* fi_host, size_t count);
+/* n such steps with the host copies pipelined across steps (each step still
+ * uploads both species from and downloads both results into the host arrays;
+ * the next step's electron upload overlaps this step's ion download). */
+sk_status sk_run_steps_host(sk_state* s, int n, double* fe_host, double* fi_host, size_t count);
 
 #ifdef __cplusplus
 }

@@ -128,6 +128,7 @@ SIGNATURES = {
     "sk_state_step_index": (_i, [_vp, _lp]),
     "sk_state_shrinks": (_i, [_vp, _i, _ip, _lp]),
     "sk_run_step_host": (_i, [_vp, _dp, _dp, _sz]),
+    "sk_run_steps_host": (_i, [_vp, _i, _dp, _dp, _sz]),
     "sk_state_time": (_i, [_vp, _dp]),
     "sk_state_wall_flux": (_i, [_vp, _i, _i, _dp, _dp]),
     "sk_state_sample_fluxes": (_i, [_vp, C.POINTER(sk_flux_sample)]),

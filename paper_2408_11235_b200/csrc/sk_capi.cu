@@ -53,6 +53,9 @@ constexpr unsigned long long kGuardWord = 0x7ff4dead5a5a5a5aull;  // a NaN no ke
 struct sk_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // sk_run_steps_host: copy-in / copy-out streams and their events (created on first use)
+    cudaStream_t xs[2] = {nullptr, nullptr};
+    cudaEvent_t xev[5] = {};
     bool own_stream = true;
     bool eager = true;
     int k = 0, P = 1;
@@ -1065,6 +1068,10 @@ sk_status sk_ctx_destroy(sk_ctx* c) {
     cudaFree(c->fix_vals);
     cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->stream);
+    for (cudaStream_t x : c->xs)
+        if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t e : c->xev)
+        if (e) cudaEventDestroy(e);
     delete c;
     return SK_OK;
 }
@@ -2297,6 +2304,52 @@ sk_status sk_run_step_host(sk_state* s, double* fe, double* fi, size_t count) {
     return collect_errors(c);
 }
 
+// n drop-in steps over host arrays with the copies pipelined across steps:
+// each step still uploads both species and downloads both results, but the
+// copy-in of step k+1's electrons (host buffer final once step k's electron
+// download is done) runs during step k's ion download -- PCIe is full duplex,
+// so ~one species transfer per step is hidden (the dependencies are the host
+// arrays and the live device buffers; every wait is an event)
+sk_status sk_run_steps_host(sk_state* s, int n, double* fe, double* fi, size_t count) {
+    sk_ctx* c = s->ctx;
+    CK(cudaSetDevice(c->device));
+    if (n <= 0) return SK_OK;
+    if (count != s->f[0]->n || count != s->f[1]->n) return fail(SK_ERR_RUNTIME, "run_steps_host: size mismatch");
+    if (!c->xs[0]) {
+        for (auto& x : c->xs) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        for (auto& e : c->xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t up = c->xs[0], dn = c->xs[1];
+    cudaEvent_t dn_e = c->xev[0], dn_i = c->xev[1], up_e = c->xev[2], up_i = c->xev[3], done = c->xev[4];
+    const size_t bytes = sizeof(double) * count;
+    CK(cudaEventRecord(done, c->stream));  // after everything already queued
+    CK(cudaStreamWaitEvent(up, done, 0));
+    for (int k = 0; k < n; ++k) {
+        double *le = nullptr, *li = nullptr;
+        CK(s->f[0]->live_ptr(&le));
+        CK(s->f[1]->live_ptr(&li));
+        if (k > 0) CK(cudaStreamWaitEvent(up, dn_e, 0));  // fe holds step k-1's result, le is free
+        CK(cudaMemcpyAsync(le, fe, bytes, cudaMemcpyHostToDevice, up));
+        CK(cudaEventRecord(up_e, up));
+        if (k > 0) CK(cudaStreamWaitEvent(up, dn_i, 0));
+        CK(cudaMemcpyAsync(li, fi, bytes, cudaMemcpyHostToDevice, up));
+        CK(cudaEventRecord(up_i, up));
+        CK(cudaStreamWaitEvent(c->stream, up_e, 0));
+        CK(cudaStreamWaitEvent(c->stream, up_i, 0));
+        if (sk_status rc = enq_run_body(s)) return rc;
+        CK(cudaEventRecord(done, c->stream));
+        CK(s->f[0]->live_ptr(&le));  // (after the step: its buffer flips)
+        CK(s->f[1]->live_ptr(&li));
+        CK(cudaStreamWaitEvent(dn, done, 0));
+        CK(cudaMemcpyAsync(fe, le, bytes, cudaMemcpyDeviceToHost, dn));
+        CK(cudaEventRecord(dn_e, dn));
+        CK(cudaMemcpyAsync(fi, li, bytes, cudaMemcpyDeviceToHost, dn));
+        CK(cudaEventRecord(dn_i, dn));
+    }
+    CK(cudaStreamSynchronize(dn));
+    CK(cudaStreamWaitEvent(c->stream, dn_i, 0));  // later work on the main stream after the copies
+    return collect_errors(c);
+}
 
 // ---------------------------------------------------------------------------
 // diagnostics + output (diagnostics.cpp, run.cpp:60-169), SURVEY.md §8f N3

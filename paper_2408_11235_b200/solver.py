@@ -771,6 +771,13 @@ class SimulationState:
                                         fe.size))
         self.steps_enqueued += 1
 
+    def run_steps_host(self, n: int, fe: np.ndarray, fi: np.ndarray):
+        """n drop-in steps over host arrays (updated in place), copies pipelined across steps."""
+        pd = C.POINTER(C.c_double)
+        _check(N.lib().sk_run_steps_host(self.h, int(n), fe.ctypes.data_as(pd), fi.ctypes.data_as(pd),
+                                         fe.size))
+        self.steps_enqueued += n
+
     def set_phase_timing(self, on: bool):
         _check(N.lib().sk_state_set_phase_timing(self.h, int(on)))
 

@@ -1383,3 +1383,22 @@ def test_run_with_fused_step_boundaries(sk, ora, tmp_path, monkeypatch):
     sa = [ln.split("(mass delta")[0] for ln in la.splitlines() if "shrink" in ln.lower()]
     sb = [ln.split("(mass delta")[0] for ln in lb.splitlines() if "shrink" in ln.lower()]
     assert sa == sb and len(sa) >= 2
+
+
+def test_run_steps_host_pipelined_equals_single_steps(sk):
+    """sk_run_steps_host (bench.py's e2e leg): n drop-in steps over host arrays
+    with the copies of consecutive steps overlapped on two streams give the
+    same bits as n sk_run_step_host calls (the same bodies, every step's
+    inputs uploaded and results downloaded), through a shrink."""
+    cfg = cfg_of(sk, k=3, nf=16, nc=32, m=2, nv=64, mu=1836.0, limiter="sldg")
+    a, b = sk.SimulationState(cfg), sk.SimulationState(cfg)
+    fa = [a.f_e.download(), a.f_i.download()]
+    fb = [b.f_e.download(), b.f_i.download()]
+    a.run_steps_host(13, fa[0], fa[1])
+    for _ in range(13):
+        b.run_step_host(fb[0], fb[1])
+    assert np.array_equal(fa[0], fb[0]) and np.array_equal(fa[1], fb[1])
+    assert a.step_index() == b.step_index() == 13
+    assert a.shrinks(0) == b.shrinks(0)
+    # the host arrays hold the device state
+    assert np.array_equal(fa[0], a.f_e.download()) and np.array_equal(fa[1], a.f_i.download())
